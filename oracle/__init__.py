@@ -1,0 +1,226 @@
+"""oracle -- plain, slow fp64 CPU oracle of enforced-sparse ALS (arXiv 1510.05237).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  It shares no code with the CUDA path (paper_1510_05237_b200/); the
+two meet only in the seeded inputs from ``synth/``.
+
+The arithmetic lives in ``esnmf_oracle.c`` (fp64, OpenMP); this module only
+marshals arrays and strings the paper's steps together in the paper's order
+(Alg. 2, with per-column enforcement):
+
+    V  = A^T U (U^T U + eps I)^{-1}, clamp, keep t per column
+    U' = A V (V^T V + eps I)^{-1},   clamp, keep t per column
+    R  = ||U' - U||_F / ||U'||_F
+    E  = ||A - U' V^T||_F / ||A||_F  (trace identity)
+
+``oracle.bruteforce`` is a dense numpy twin used to pin this module on tiny
+inputs.  Parity status of every function: DESIGN.md section 4.
+"""
+from __future__ import annotations
+
+import ctypes
+import functools
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(HERE, "liboracle.so")
+RHO_DEFAULT = 1e-10   # ridge scale, reading C6
+
+
+def build(verbose: bool = False) -> None:
+    src = os.path.join(HERE, "esnmf_oracle.c")
+    cmd = ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", src, "-o", _SO, "-lm"]
+    subprocess.run(cmd, check=True, capture_output=not verbose)
+
+
+@functools.lru_cache(None)
+def _lib():
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(os.path.join(HERE, "esnmf_oracle.c")):
+        build()
+    lib = ctypes.CDLL(_SO)
+    i64, i32, u64, p, d = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_double
+    lib.or_u0.argtypes = [i64, i32, u64, p]
+    lib.or_splitmix64_pub.argtypes = [u64]
+    lib.or_splitmix64_pub.restype = u64
+    lib.or_gram.argtypes = [i64, i32, p, p]
+    lib.or_cholesky.argtypes = [i32, p, d, p, p]
+    lib.or_cholesky.restype = ctypes.c_int
+    lib.or_solve_rows.argtypes = [i64, i32, p, p, p]
+    lib.or_spmm.argtypes = [i64, i32, p, p, p, p, p]
+    lib.or_spmm_rows.argtypes = [i64, p, i32, p, p, p, p, p]
+    lib.or_clamp_top_t.argtypes = [i64, i32, i64, p, p]
+    lib.or_residual.argtypes = [i64, i32, p, p]
+    lib.or_residual.restype = d
+    lib.or_error.argtypes = [i64, i32, p, p, p, p, d]
+    lib.or_error.restype = d
+    lib.or_frob2_f32.argtypes = [i64, p]
+    lib.or_frob2_f32.restype = d
+    return lib
+
+
+def _p(a: np.ndarray) -> int:
+    assert a.flags.c_contiguous
+    return a.ctypes.data
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# ----------------------------------------------------------------- primitives
+
+def splitmix64(x: int) -> int:
+    return int(_lib().or_splitmix64_pub(x))
+
+
+def u0(n: int, k: int, seed: int = 0) -> np.ndarray:
+    """Initial guess U_0 (reading C10): dense uniform(0,1), fp32-exact."""
+    out = np.empty((n, k), np.float32)
+    _lib().or_u0(n, k, seed, _p(out))
+    return out
+
+
+def gram(F: np.ndarray) -> np.ndarray:
+    """F^T F in fp64."""
+    F = _c(F, np.float64)
+    rows, k = F.shape
+    G = np.empty((k, k), np.float64)
+    _lib().or_gram(rows, k, _p(F), _p(G))
+    return G
+
+
+def cholesky(G: np.ndarray, rho: float = RHO_DEFAULT):
+    """L with L L^T = G + eps I, eps = rho (tr G / k + 1) (C6).
+    Raises np.linalg.LinAlgError if not positive definite."""
+    G = _c(G, np.float64)
+    k = G.shape[0]
+    L = np.empty((k, k), np.float64)
+    eps = ctypes.c_double(0.0)
+    rc = _lib().or_cholesky(k, _p(G), rho, _p(L), ctypes.byref(eps))
+    if rc != 0:
+        raise np.linalg.LinAlgError("G + eps I is not positive definite")
+    return L, eps.value
+
+
+def solve_rows(L: np.ndarray, Y: np.ndarray) -> np.ndarray:
+    """X = Y (L L^T)^{-1}, row by row (two triangular solves)."""
+    Y = _c(Y, np.float64)
+    X = np.empty_like(Y)
+    _lib().or_solve_rows(Y.shape[0], Y.shape[1], _p(_c(L, np.float64)), _p(Y), _p(X))
+    return X
+
+
+def solve_gram(G: np.ndarray, rho: float = RHO_DEFAULT) -> np.ndarray:
+    """(G + eps I)^{-1} (SPEC solve_gram)."""
+    L, _ = cholesky(G, rho)
+    return solve_rows(L, np.eye(G.shape[0]))
+
+
+def spmm(ptr, idx, val, F: np.ndarray) -> np.ndarray:
+    """Y = T F with T in CSR (rows = output rows), F dense (P:63 A^T U, P:64 A V)."""
+    F = _c(F, np.float64)
+    rows_out = len(ptr) - 1
+    k = F.shape[1]
+    Y = np.empty((rows_out, k), np.float64)
+    _lib().or_spmm(rows_out, k, _p(_c(ptr, np.int64)), _p(_c(idx, np.int32)), _p(_c(val, np.float32)), _p(F), _p(Y))
+    return Y
+
+
+def spmm_rows(sel, ptr, idx, val, F: np.ndarray) -> np.ndarray:
+    """Rows ``sel`` of T F only (sampled parity at full size)."""
+    F = _c(F, np.float64)
+    sel = _c(sel, np.int64)
+    Y = np.empty((len(sel), F.shape[1]), np.float64)
+    _lib().or_spmm_rows(len(sel), _p(sel), F.shape[1], _p(_c(ptr, np.int64)), _p(_c(idx, np.int32)),
+                        _p(_c(val, np.float32)), _p(F), _p(Y))
+    return Y
+
+
+def clamp_top_t(X: np.ndarray, t: int | None):
+    """Projection + per-column enforcement (P:63 clamp; P:134,146 keep t largest;
+    P:304 per column; C4 ties -> lower row).  Returns (X', kept_per_column)."""
+    X = np.array(X, dtype=np.float64, order="C", copy=True)
+    rows, k = X.shape
+    kept = np.empty(k, np.int64)
+    _lib().or_clamp_top_t(rows, k, -1 if t is None else int(t), _p(X), _p(kept))
+    return X, kept
+
+
+def residual(Unew: np.ndarray, Uold: np.ndarray) -> float:
+    """R = ||U_i - U_{i-1}|| / ||U_i||.  ValueError if ||U_i|| = 0."""
+    a, b = _c(Unew, np.float64), _c(Uold, np.float64)
+    r = _lib().or_residual(a.shape[0], a.shape[1], _p(a), _p(b))
+    if r < 0:
+        raise ValueError("residual undefined: ||U_i||_F == 0")
+    return float(r)
+
+
+def error(U, AV, GU, GV, normA2: float) -> float:
+    """E = ||A - U V^T||_F / ||A||_F via the trace identity (BJ:5)."""
+    U, AV = _c(U, np.float64), _c(AV, np.float64)
+    return float(_lib().or_error(U.shape[0], U.shape[1], _p(U), _p(AV), _p(_c(GU, np.float64)),
+                                 _p(_c(GV, np.float64)), normA2))
+
+
+def frob2(val) -> float:
+    v = _c(val, np.float32)
+    return float(_lib().or_frob2_f32(len(v), _p(v)))
+
+
+# ------------------------------------------------------------------ the method
+
+def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFAULT) -> dict:
+    """One ALS half-step in the paper's order (P:133-134 for the V side with
+    T = A^T and F = U; P:135-136 for the U side with T = A and F = V):
+        G = F^T F; L L^T = G + eps I; Y = T F; LS = Y (G + eps I)^{-1};
+        F' = keep_top_t_per_column(max(LS, 0)).
+    All dense fp64."""
+    G = gram(F)
+    L, eps = cholesky(G, rho)
+    Y = spmm(ptr, idx, val, F)
+    LS = solve_rows(L, Y)
+    Fn, kept = clamp_top_t(LS, t)
+    return dict(G=G, eps=eps, L=L, Y=Y, LS=LS, F=Fn, kept=kept)
+
+
+def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float = RHO_DEFAULT,
+        U_init: np.ndarray | None = None, keep_states: bool = False) -> dict:
+    """Alg. 2 with per-column enforcement for ``iters`` iterations.
+    Returns the per-iteration records {it, R, E, nnz_u, nnz_v, dead_u, dead_v}
+    (IterationRecord) and the final dense U, V."""
+    n, m = inp["n"], inp["m"]
+    U = (u0(n, k, seed) if U_init is None else U_init).astype(np.float64)
+    normA2 = frob2(inp["a_val"])
+    recs, states = [], []
+    for it in range(1, iters + 1):
+        hv = half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, t, rho)
+        V = hv["F"]
+        hu = half_step(inp["a_ptr"], inp["a_col"], inp["a_val"], V, t, rho)
+        Un = hu["F"]
+        R = residual(Un, U)
+        GU = gram(Un)
+        E = error(Un, hu["Y"], GU, hu["G"], normA2)
+        recs.append(dict(it=it, R=R, E=E, nnz_u=int(np.count_nonzero(Un)), nnz_v=int(np.count_nonzero(V)),
+                         dead_u=int(np.sum(~Un.any(axis=0))), dead_v=int(np.sum(~V.any(axis=0)))))
+        if keep_states:
+            states.append(dict(U_prev=U, V=V, U=Un, LS_V=hv["LS"], LS_U=hu["LS"], G_U=hv["G"], G_V=hu["G"]))
+        U = Un
+    return dict(records=recs, U=U, V=V, states=states, normA2=normA2)
+
+
+# ------------------------------------------------------------- format helpers
+
+def dense_to_coo(F: np.ndarray):
+    """Canonical column-major COO (ascending column, then row)."""
+    rows, cols = np.nonzero(F.T)   # over F^T: first index = column of F
+    return cols.astype(np.int32), rows.astype(np.int32), F[cols, rows]
+
+
+def coo_to_dense(shape, row, col, val, dtype=np.float64) -> np.ndarray:
+    F = np.zeros(shape, dtype)
+    F[np.asarray(row, np.int64), np.asarray(col, np.int64)] = val
+    return F

@@ -1,0 +1,60 @@
+"""oracle.bruteforce -- dense numpy twin of the oracle, for tiny inputs only.
+
+TEST INFRASTRUCTURE ONLY.  Independent of ``esnmf_oracle.c``: it uses LAPACK
+solves (numpy.linalg.solve / pinv) instead of the oracle's Cholesky, a stable
+lexsort instead of qsort, and materialises A - U V^T instead of the trace
+identity.  Its job is to pin the oracle (tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def dense(ptr, idx, val, ncols: int) -> np.ndarray:
+    rows = len(ptr) - 1
+    D = np.zeros((rows, ncols), np.float64)
+    for r in range(rows):
+        s, e = int(ptr[r]), int(ptr[r + 1])
+        D[r, np.asarray(idx[s:e], np.int64)] = np.asarray(val[s:e], np.float64)
+    return D
+
+
+def ridge_eps(G: np.ndarray, rho: float) -> float:
+    return rho * (np.trace(G) / G.shape[0] + 1.0)
+
+
+def ls_step(T: np.ndarray, F: np.ndarray, rho: float) -> np.ndarray:
+    """T F (F^T F + eps I)^{-1}: the least-squares solve of Alg. 1 step 1/2."""
+    G = F.T @ F
+    Gr = G + ridge_eps(G, rho) * np.eye(G.shape[0])
+    return np.linalg.solve(Gr, (T @ F).T).T
+
+
+def top_t_per_column(X: np.ndarray, t: int | None) -> np.ndarray:
+    """clamp, then keep per column the t largest positives, ties -> lower row (C4, C5)."""
+    Y = np.where(X > 0, X, 0.0)
+    if t is None:
+        return Y
+    out = np.zeros_like(Y)
+    rows = np.arange(Y.shape[0])
+    for c in range(Y.shape[1]):
+        pos = rows[Y[:, c] > 0]
+        order = np.lexsort((pos, -Y[pos, c]))   # primary: value desc; secondary: row asc
+        keep = pos[order[:t]]
+        out[keep, c] = Y[keep, c]
+    return out
+
+
+def projected_als(A: np.ndarray, U0: np.ndarray, t: int | None, iters: int, rho: float):
+    """Alg. 2 (t given) / Alg. 1 (t None), per-column enforcement, dense."""
+    U = U0.astype(np.float64)
+    recs = []
+    nA = np.linalg.norm(A)
+    for _ in range(iters):
+        V = top_t_per_column(ls_step(A.T, U, rho), t)
+        Un = top_t_per_column(ls_step(A, V, rho), t)
+        R = np.linalg.norm(Un - U) / np.linalg.norm(Un)
+        E = np.linalg.norm(A - Un @ V.T) / nA
+        recs.append((R, E))
+        U = Un
+    return U, V, recs

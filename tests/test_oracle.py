@@ -1,0 +1,268 @@
+"""Pins for the fp64 oracle (oracle/), independent of the oracle itself.
+
+Each test fixes the oracle against something other than its own formula:
+published values (SPEC examples, the splitmix64 reference vector), closed
+forms (planted exact factorisations, 2x2 inverses, k = 1 division), library
+routines that implement a different algorithm (LAPACK solve / pinv, SVD,
+stable lexsort, materialised norms), brute force on tiny inputs, and
+invariants.  A dropped term, wrong sign / index or transposed operand in any
+oracle function fails at least one of these.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import bruteforce as bf
+import synth
+
+
+def csr(D):
+    D = np.asarray(D, np.float64)
+    ptr, idx, val = [0], [], []
+    for r in D:
+        nz = np.nonzero(r)[0]
+        idx += list(nz)
+        val += list(r[nz])
+        ptr.append(len(idx))
+    return np.array(ptr, np.int64), np.array(idx, np.int32), np.array(val, np.float32)
+
+
+def rand_sparse(rng, rows, cols, density, integer=False):
+    M = (rng.random((rows, cols)) < density) * (rng.integers(1, 5, (rows, cols)) if integer else rng.lognormal(0, 1, (rows, cols)))
+    return M.astype(np.float32).astype(np.float64)
+
+
+# ------------------------------------------------------------ published values
+
+def test_splitmix64_reference_vector():
+    # splitmix64 seeded with 0: first three outputs of the reference generator
+    assert oracle.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert oracle.splitmix64(0x9E3779B97F4A7C15) == 0x6E789E6AA1B965F4
+    assert oracle.splitmix64((2 * 0x9E3779B97F4A7C15) % 2**64) == 0x06C45D188009454F
+
+
+def test_u0_structure():
+    U = oracle.u0(1000, 7, 0)
+    assert U.dtype == np.float32 and U.shape == (1000, 7)
+    assert U.min() > 0 and U.max() < 1
+    s = U.astype(np.float64) * 2.0**24        # (2j+1) 2^-24: an odd integer
+    assert np.all(s == np.round(s)) and np.all(np.round(s) % 2 == 1)
+    assert abs(U.mean() - 0.5) < 0.02
+    assert np.array_equal(U, oracle.u0(1000, 7, 0))
+    assert not np.array_equal(U, oracle.u0(1000, 7, 1))
+    # counter layout: element (i, c) depends on i*k + c only
+    assert oracle.u0(10, 5, 3).ravel()[7] == oracle.u0(35, 1, 3)[7, 0]
+
+
+def test_spec_gram_examples():
+    assert np.array_equal(oracle.gram([[1, 2], [3, 4]]), [[10, 14], [14, 20]])
+    assert np.array_equal(oracle.gram(np.eye(2)), np.eye(2))
+    G = oracle.gram([[1, 0], [2, 0], [0, 0]])
+    assert G[1].tolist() == [0, 0] and G[:, 1].tolist() == [0, 0]
+
+
+def test_spec_solve_gram_examples():
+    assert np.allclose(oracle.solve_gram(np.array([[10.0, 14], [14, 20]]), 0.0), [[5, -3.5], [-3.5, 2.5]], rtol=1e-12)
+    assert np.allclose(oracle.solve_gram(np.diag([2.0, 4.0]), 0.0), np.diag([0.5, 0.25]), rtol=1e-15)
+    assert np.array_equal(oracle.solve_gram(np.eye(3), 0.0), np.eye(3))
+    # ridge reading C6: eps = rho (tr G / k + 1)
+    _, eps = oracle.cholesky(np.diag([2.0, 4.0]), 1e-3)
+    assert eps == pytest.approx(1e-3 * (3.0 + 1.0), rel=1e-15)
+    with pytest.raises(np.linalg.LinAlgError):
+        oracle.cholesky(np.zeros((2, 2)), 0.0)
+
+
+def test_spec_matmul_example():
+    ptr, idx, val = csr([[1, 2], [3, 4]])
+    Y = oracle.spmm(ptr, idx, val, np.array([[5.0, 6], [7, 8]]))
+    assert np.array_equal(Y, [[19, 22], [43, 50]])
+    ptr, idx, val = csr(np.eye(3))
+    F = np.arange(6.0).reshape(3, 2)
+    assert np.array_equal(oracle.spmm(ptr, idx, val, F), F)
+
+
+def test_spec_clamp_and_top_t_examples():
+    X, kept = oracle.clamp_top_t(np.array([[1.0, -2], [-3, 4]]), None)
+    assert np.array_equal(X, [[1, 0], [0, 4]]) and kept.tolist() == [1, 1]
+    X2, _ = oracle.clamp_top_t(X, None)
+    assert np.array_equal(X2, X)                                                       # idempotent
+    col = np.array([[3.0], [2.0], [1.0], [0.5]])
+    X, kept = oracle.clamp_top_t(col, 2)
+    assert X[:, 0].tolist() == [3, 2, 0, 0] and kept[0] == 2
+    X, _ = oracle.clamp_top_t(col, 10)
+    assert np.array_equal(X, col)
+    X, kept = oracle.clamp_top_t(col, 0)
+    assert not X.any() and kept[0] == 0
+    two = np.array([[5.0, 4], [1, 3], [0, 2]])
+    X, _ = oracle.clamp_top_t(two, 1)
+    assert X.tolist() == [[5, 4], [0, 0], [0, 0]]
+    g = np.array([[9.0, 1], [8, 0.5], [7, 0.25], [6, 0.125]])
+    X, kept = oracle.clamp_top_t(g, 2)
+    assert kept.tolist() == [2, 2] and X[:, 0].tolist() == [9, 8, 0, 0] and X[:, 1].tolist() == [1, 0.5, 0, 0]
+
+
+def test_spec_residual_examples():
+    U = np.array([[1.0, 0], [2, 3]])
+    assert oracle.residual(U, U) == 0.0
+    assert oracle.residual(U, np.zeros_like(U)) == 1.0
+    assert oracle.residual(U, 2 * U) == pytest.approx(1.0, rel=1e-15)
+    with pytest.raises(ValueError):
+        oracle.residual(np.zeros_like(U), U)
+
+
+def test_spec_als_step_v_identity():
+    ptr, idx, val = csr(np.diag([2.0, 3.0]))          # A^T = diag(2,3)
+    h = oracle.half_step(ptr, idx, val, np.eye(2), None, rho=0.0)
+    assert np.allclose(h["LS"], np.diag([2.0, 3.0]), rtol=1e-15)
+
+
+# ---------------------------------------------------- closed forms / library
+
+def test_gram_psd_and_against_numpy():
+    rng = np.random.default_rng(0)
+    F = rand_sparse(rng, 200, 9, 0.3)
+    G = oracle.gram(F)
+    assert np.allclose(G, F.T @ F, rtol=1e-13, atol=0)
+    assert np.array_equal(G, G.T)
+    assert np.linalg.eigvalsh(G).min() >= -1e-12 * np.trace(G)
+
+
+def test_solve_matches_lapack_and_pinv():
+    """V_ls = A^T pinv(U)^T for full-column-rank U (normal equations = pseudoinverse)."""
+    rng = np.random.default_rng(1)
+    A = rand_sparse(rng, 60, 40, 0.2)
+    U = rand_sparse(rng, 60, 4, 0.5) + 0.01 * rng.random((60, 4))
+    ptr, idx, val = csr(A.T)
+    h = oracle.half_step(ptr, idx, val, U, None, rho=0.0)
+    ref_pinv = A.T @ np.linalg.pinv(U).T
+    assert np.allclose(h["LS"], ref_pinv, rtol=1e-9, atol=1e-9 * np.abs(ref_pinv).max())
+    ref_solve = bf.ls_step(bf.dense(ptr, idx, val, 60), U, 0.0)
+    assert np.allclose(h["LS"], ref_solve, rtol=1e-11, atol=1e-12 * np.abs(ref_solve).max())
+    # with the ridge: LAPACK solve of (G + eps I)
+    h2 = oracle.half_step(ptr, idx, val, U, None, rho=1e-3)
+    ref2 = bf.ls_step(A.T, U, 1e-3)
+    assert np.allclose(h2["LS"], ref2, rtol=1e-11, atol=1e-12 * np.abs(ref2).max())
+
+
+def test_rank_one_is_a_division():
+    """k = 1: (u^T u + eps)^{-1} is a scalar division."""
+    rng = np.random.default_rng(2)
+    A = rand_sparse(rng, 30, 20, 0.3)
+    u = rng.random((30, 1)) + 0.1
+    ptr, idx, val = csr(A.T)
+    rho = 1e-6
+    h = oracle.half_step(ptr, idx, val, u, None, rho=rho)
+    g = float(u[:, 0] @ u[:, 0])
+    ref = (A.T @ u[:, 0]) / (g + rho * (g + 1.0))
+    assert np.allclose(h["LS"][:, 0], ref, rtol=1e-13)
+
+
+def test_error_trace_identity_vs_materialised():
+    rng = np.random.default_rng(3)
+    A = rand_sparse(rng, 25, 18, 0.3)
+    U = rand_sparse(rng, 25, 3, 0.5)
+    V = rand_sparse(rng, 18, 3, 0.5)
+    E = oracle.error(U, A @ V, U.T @ U, V.T @ V, float(np.sum(A * A)))
+    ref = np.linalg.norm(A - U @ V.T) / np.linalg.norm(A)
+    assert E == pytest.approx(ref, rel=1e-12)
+    assert oracle.error(np.zeros_like(U), A @ np.zeros_like(V), np.zeros((3, 3)), np.zeros((3, 3)),
+                        float(np.sum(A * A))) == pytest.approx(1.0, rel=1e-15)
+
+
+def test_planted_exact_factorisation_is_a_fixed_point():
+    """A = U* V*^T with sparse, non-negative, full-column-rank factors holding exactly
+    t entries per column: one iteration from U = U* returns V*, U*, so E = R = 0."""
+    rng = np.random.default_rng(4)
+    n, m, k, t = 40, 30, 3, 6
+    Us, Vs = np.zeros((n, k)), np.zeros((m, k))
+    for c in range(k):
+        Us[rng.choice(n, t, replace=False), c] = rng.integers(1, 5, t)
+        Vs[rng.choice(m, t, replace=False), c] = rng.integers(1, 5, t)
+    assert np.linalg.matrix_rank(Us) == k and np.linalg.matrix_rank(Vs) == k
+    A = Us @ Vs.T                                   # small integers: exact in fp32
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    inp = dict(n=n, m=m, a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+    r = oracle.run(inp, k, t, 1, U_init=Us)
+    assert np.allclose(r["V"], Vs, rtol=1e-8, atol=0)
+    assert np.allclose(r["U"], Us, rtol=1e-8, atol=0)
+    assert np.array_equal(r["V"] != 0, Vs != 0) and np.array_equal(r["U"] != 0, Us != 0)
+    assert r["records"][0]["E"] < 1e-7 and r["records"][0]["R"] < 1e-8
+
+
+def test_planted_block_corpus_converges():
+    """Heuristic convergence quorum: noise-free planted blocks, t >= the
+    planted column support -> E <= 1e-3 within 200 iterations for >= 8/10 seeds."""
+    k, terms, docs = 5, 10, 20
+    n, m = k * terms, k * docs
+    rng = np.random.default_rng(5)
+    A = np.zeros((n, m))
+    for c in range(k):
+        A[c * terms:(c + 1) * terms, c * docs:(c + 1) * docs] = np.outer(rng.integers(1, 4, terms), rng.integers(1, 4, docs))
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    inp = dict(n=n, m=m, a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+    ok = 0
+    for seed in range(10):
+        r = oracle.run(inp, k, docs, 200, seed=seed)
+        ok += min(x["E"] for x in r["records"]) <= 1e-3
+    assert ok >= 8
+
+
+# ---------------------------------------------------------- brute force (tiny)
+
+def test_top_t_invariants_and_ties():
+    rng = np.random.default_rng(6)
+    X = rng.normal(size=(300, 7))
+    X[10:20, 3] = 0.75          # forced exact ties inside column 3
+    X[:, 5] = -1.0              # all-negative column
+    for t in (0, 1, 5, 13, 50, 299, 1000):
+        Y, kept = oracle.clamp_top_t(X, t)
+        ref = bf.top_t_per_column(X, t)
+        assert np.array_equal(Y, ref)
+        for c in range(X.shape[1]):
+            pos = X[:, c] > 0
+            assert kept[c] == min(t, pos.sum()) == np.count_nonzero(Y[:, c])
+            kv, dv = Y[Y[:, c] > 0, c], X[pos & (Y[:, c] == 0), c]
+            if len(kv) and len(dv):
+                assert kv.min() >= dv.max()
+        assert np.array_equal(oracle.clamp_top_t(Y, t)[0], Y)                           # idempotent
+        assert np.all(Y >= 0)
+    Y, _ = oracle.clamp_top_t(X, 15)   # ties at 0.75 resolved by lower row first
+    col = X[:, 3]
+    above = np.sum(col > 0.75)
+    if 0 < 15 - above < 10:
+        kept_rows = np.nonzero(Y[10:20, 3])[0]
+        assert kept_rows.tolist() == list(range(15 - above))
+
+
+@pytest.mark.parametrize("t", [None, 4, 9])
+def test_oracle_run_matches_bruteforce(t):
+    rng = np.random.default_rng(7)
+    n, m, k = 40, 30, 3
+    A = rand_sparse(rng, n, m, 0.25)
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    inp = dict(n=n, m=m, a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+    rho = 1e-10
+    r = oracle.run(inp, k, t, 8, seed=3, rho=rho)
+    U0 = oracle.u0(n, k, 3)
+    U, V, recs = bf.projected_als(A, U0, t, 8, rho)
+    assert np.allclose(r["U"], U, rtol=1e-9, atol=1e-12 * np.abs(U).max())
+    assert np.allclose(r["V"], V, rtol=1e-9, atol=1e-12 * np.abs(V).max())
+    for rec, (R, E) in zip(r["records"], recs):
+        assert rec["R"] == pytest.approx(R, rel=1e-8, abs=1e-12)
+        assert rec["E"] == pytest.approx(E, rel=1e-10)
+        if t is not None:
+            assert rec["nnz_u"] <= k * t and rec["nnz_v"] <= k * t
+
+
+def test_oracle_tiny_config_records_sane():
+    cfg = synth.CONFIGS["tiny"]
+    g = synth.generate(cfg)
+    r = oracle.run(g, cfg.k, cfg.t, 5, seed=cfg.seed)
+    for x in r["records"]:
+        assert 0 <= x["E"] <= 1.0 + 1e-12
+        assert x["nnz_u"] <= cfg.k * cfg.t and x["nnz_v"] <= cfg.k * cfg.t
+    assert r["records"][0]["R"] > 0.5   # U_1 differs from the dense U_0
+    assert r["records"][-1]["E"] < r["records"][0]["E"]
