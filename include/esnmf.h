@@ -1,0 +1,197 @@
+/*
+ * esnmf.h -- C ABI of libesnmf.so: the B200 (sm_100a) hot path of
+ * enforced-sparse ALS NMF (Gavin, Gadepally, Kepner, arXiv 1510.05237).
+ *
+ * Citations: P:n = line n of the paper text; S:n = line n of the
+ * CPU-program spec (SPEC.md, interfaces only); readings C1..C16 are listed in
+ * DESIGN.md section 2.
+ *
+ * Problem: A in R^{n x m}, A >= 0 sparse (n terms x m documents,
+ * P:23); find U in R^{n x k}, V in R^{m x k}, U, V >= 0, A ~ U V^T.
+ * Method (Alg. 2, per-column enforcement P:304): starting
+ * from U = U_0, each iteration does
+ *   V side: V = A^T U (U^T U + eps I)^{-1}, negatives -> 0,
+ *                       keep the t largest entries of every column of V;
+ *   U side: U = A V (V^T V + eps I)^{-1},   negatives -> 0,
+ *                       keep the t largest entries of every column of U;
+ * with eps = ridge_scale * (tr(G)/k + 1) (reading C6), ties at the t-th value
+ * broken toward the lower row index so exactly min(t, #positive) entries
+ * survive (reading C4), and only strictly positive entries ever kept (C5).
+ * Metrics: R = ||U_i - U_{i-1}||_F / ||U_i||_F, computed by direct
+ * difference; E = ||A - U V^T||_F / ||A||_F via the trace identity
+ * ||A||^2 - 2 tr(U^T (A V)) + tr((U^T U)(V^T V)).
+ *
+ * Conventions for every entry point:
+ *  - Returns ESNMF_OK (0) or an error code; esnmf_last_error() gives a
+ *    message for the calling thread.  No entry point aborts the process.
+ *  - Matrices are 0-based.  CSR: row_ptr[rows+1] (int64, row_ptr[0] = 0,
+ *    non-decreasing, row_ptr[rows] = nnz), col_idx[nnz] (int32, strictly
+ *    increasing within a row), val[nnz] (fp32, finite, >= 0).
+ *  - Factor output is canonical column-major COO: ascending column, then
+ *    ascending row; values are the device fp32 values exactly.
+ *  - A handle is not thread-safe; distinct handles are independent.  All
+ *    device work is enqueued on the handle's stream; esnmf_iterate and
+ *    esnmf_half_step are asynchronous, every getter synchronises the stream.
+ *  - Asynchronous CUDA faults surface as ESNMF_ECUDA at the next
+ *    synchronising call.
+ */
+#ifndef ESNMF_H
+#define ESNMF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct esnmf esnmf_t; /* opaque; owns all of its device memory */
+
+typedef enum {
+  ESNMF_OK = 0,
+  ESNMF_EINVAL = 1,      /* bad argument or malformed CSR (message names it) */
+  ESNMF_ENOMEM = 2,      /* device or host allocation failed */
+  ESNMF_ECUDA = 3,       /* CUDA runtime error (including asynchronous faults) */
+  ESNMF_ECOMM = 4,       /* a collective callback returned non-zero */
+  ESNMF_ESINGULAR = 5,   /* G + eps I not positive definite / non-finite pivot */
+  ESNMF_EDEGENERATE = 6, /* ||U_i||_F == 0: residual undefined */
+  ESNMF_ESTATE = 7,      /* call-order violation (e.g. residual before iterate) */
+  ESNMF_ETRUNC = 8       /* caller buffer too small; *nnz holds the size needed */
+} esnmf_status;
+
+#define ESNMF_T_UNLIMITED (-1) /* Alg. 1, projected ALS: no truncation */
+#define ESNMF_SIDE_V 0         /* half-step 1: V <- A^T U */
+#define ESNMF_SIDE_U 1         /* half-step 2: U <- A V */
+#define ESNMF_MAX_K 256
+
+/*
+ * Collectives for world > 1 (one process per GPU, rows of A and A^T sharded
+ * across ranks).  Both callbacks are stream-ordered on `stream` and take
+ * DEVICE buffers; they return 0 on success.  The Python binding implements
+ * them with torch.distributed (NCCL on GPUs).
+ *   allgather: every rank contributes `bytes_per_rank` bytes from `send`;
+ *              `recv` receives world * bytes_per_rank bytes in rank order.
+ *   allreduce_sum_f64: in-place elementwise sum of `count` doubles.
+ */
+typedef struct {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes_per_rank, void* stream);
+  int (*allreduce_sum_f64)(void* ctx, double* buf, int64_t count, void* stream);
+} esnmf_comm;
+
+typedef struct {
+  uint64_t seed;        /* U_0 seed (reading C10), default 0 (BJ:7) */
+  double ridge_scale;   /* rho of eps = rho (tr G / k + 1), default 1e-10 (C6) */
+  int32_t device;       /* CUDA ordinal; -1 = current device (default) */
+  void* stream;         /* cudaStream_t to enqueue on; NULL = library-owned stream */
+  int32_t world, rank;  /* 1, 0 = single GPU (default) */
+  const esnmf_comm* comm; /* required when world > 1; must outlive the handle */
+  int32_t inputs_on_device; /* 1: every input pointer below and in create is a
+                               device pointer on `device`; 0 (default): host */
+  /* optional CSR(A^T) (m rows x n columns); NULL = built on the device */
+  const int64_t* at_row_ptr;
+  const int32_t* at_col_idx;
+  const float* at_val;
+  /* optional dense U_0 (n x k row-major fp32); NULL = reading C10 formula:
+     U0[i,c] = ((splitmix64(seed ^ 0x55305F494E495430 ^ (i*k + c)) >> 41) + 0.5) * 2^-23 */
+  const float* U0;
+} esnmf_options;
+
+typedef struct {
+  int32_t it;            /* 1-based iteration index */
+  double R;              /* relative residual of U after this iteration; -1 if undefined */
+  double E;              /* relative error after this iteration */
+  int64_t nnz_u, nnz_v;  /* stored entries of U and V ("NNZ") */
+  int32_t dead_u, dead_v;/* all-zero columns (dead topics, reading C6) */
+  int64_t active_u, active_v; /* rows holding at least one entry */
+} esnmf_record;
+
+/* Fill *opt with the defaults above.  Always ESNMF_OK (EINVAL if opt NULL). */
+esnmf_status esnmf_options_init(esnmf_options* opt);
+
+/*
+ * Create a solver for A (n x m, CSR by term rows) of rank k keeping t entries
+ * per topic column (t >= 0, or ESNMF_T_UNLIMITED).  1 <= k <= ESNMF_MAX_K,
+ * 1 <= n, m < 2^31, nnz >= 1.  Inputs are validated and copied (host->device
+ * when inputs_on_device == 0); the caller may free them on return.  Empty
+ * rows / columns are accepted.  Sets U = U_0 (reading C11).
+ * Errors: EINVAL (shape, non-monotone row_ptr, column out of range or not
+ * strictly increasing, negative or non-finite value, k or t out of range),
+ * ENOMEM, ECUDA.  On error *out is set to NULL.
+ */
+esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_t t,
+                          const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                          const esnmf_options* opt);
+
+/* Run `iters` >= 0 iterations {V side; U side} of Alg. 2, and
+ * record R and E for each.  Asynchronous on the handle's stream. */
+esnmf_status esnmf_iterate(esnmf_t* h, int32_t iters);
+
+/* One half-step only (side = ESNMF_SIDE_V or ESNMF_SIDE_U); test hook for
+ * per-half-step parity.  The V side reads the current U; the U side reads the
+ * current V and replaces U (the previous U is kept for R).  No record. */
+esnmf_status esnmf_half_step(esnmf_t* h, int32_t side);
+
+/* R of the last completed iteration (synchronises).  ESTATE before the first
+ * iteration; EDEGENERATE if ||U_i|| == 0. */
+esnmf_status esnmf_residual(esnmf_t* h, double* R);
+
+/* E of the last completed iteration (synchronises).  ESTATE before the first. */
+esnmf_status esnmf_error(esnmf_t* h, double* E);
+
+/* Copy out up to `cap` per-iteration records, oldest first; *count = number
+ * of records held.  ETRUNC if cap < *count (the first cap are written). */
+esnmf_status esnmf_records(esnmf_t* h, int64_t cap, int64_t* count, esnmf_record* out);
+
+/* Current U (n x k) / V (m x k) as canonical column-major COO (synchronises).
+ * Two-call pattern: if cap < nnz (or any array is NULL) returns ETRUNC with
+ * *nnz = entries needed; otherwise fills row/col/val and *nnz. */
+esnmf_status esnmf_get_U(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val);
+esnmf_status esnmf_get_V(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val);
+
+/* Replace U (side U) or V (side V) by a caller COO (host arrays, canonical
+ * order, values > 0, row < n or m, col < k).  Test hook: start a half-step
+ * from a given state.  Invalidates the stored records' "last" R/E. */
+esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32_t* row,
+                              const int32_t* col, const float* val);
+
+/* Pre-clamp least-squares rows of the last half-step of `side` for this
+ * rank's row shard, written row-major (rows_local x k) into `out` (host).
+ * *rows receives rows_local; *row0 the global index of the first row. */
+esnmf_status esnmf_get_ls(esnmf_t* h, int32_t side, int64_t* row0, int64_t* rows, float* out);
+
+/* Gram matrix (unregularised, k x k row-major fp64) used by the last
+ * half-step of `side` (side V: U^T U; side U: V^T V), and its eps. */
+esnmf_status esnmf_get_gram(esnmf_t* h, int32_t side, double* gram, double* eps);
+
+typedef struct {
+  int64_t n, m, nnz;
+  int32_t k;
+  int64_t t;
+  int32_t world, rank;
+  int64_t v_row0, v_rows;   /* this rank's document rows (V side) */
+  int64_t u_row0, u_rows;   /* this rank's term rows (U side) */
+  int64_t iterations;       /* completed iterations */
+  int64_t device_bytes;     /* device memory owned by the handle */
+  double normA2;            /* ||A||_F^2 */
+} esnmf_info;
+
+esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);
+
+/* Free all device memory of the handle (NULL is a no-op). */
+void esnmf_destroy(esnmf_t* h);
+
+const char* esnmf_strerror(esnmf_status s);
+const char* esnmf_last_error(void);
+
+/* Host-only helper (no GPU needed): nnz-balanced contiguous partition of
+ * `rows` rows into `world` ranges; bounds[world+1].  Used for the row shards
+ * of A; A^T rows are split in equal counts. */
+esnmf_status esnmf_partition_rows(int64_t rows, const int64_t* row_ptr, int32_t world, int64_t* bounds);
+
+/* Library version string (build id). */
+const char* esnmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESNMF_H */

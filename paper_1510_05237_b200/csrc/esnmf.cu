@@ -1,0 +1,928 @@
+// esnmf.cu -- libesnmf.so: C ABI (include/esnmf.h) and host orchestration of
+// the enforced-sparse ALS hot path on one B200 (sm_100a) per process.
+//
+// Per iteration (Alg. 2; per-column enforcement P:304):
+//   V side:  G_U = U^T U  -> W = (G_U + eps I)^{-1} -> Z = U W
+//            -> LS_V = A^T Z (k_spmm_tiled) -> clamp + top-t per column -> V
+//   U side:  G_V = V^T V  -> W -> Z = V W -> LS_U = A Z (k_spmm_items)
+//            -> clamp + top-t per column -> U
+//   R (direct difference) and E (trace identity).
+// Everything is enqueued on one stream; iterate never synchronises the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/esnmf.h"
+#include "common.cuh"
+#include "k_csr.cuh"
+#include "k_factor.cuh"
+#include "k_metrics.cuh"
+#include "k_select.cuh"
+#include "k_solve.cuh"
+#include "k_spmm.cuh"
+
+using namespace esk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  esnmf_status st;
+};
+
+[[noreturn]] void fail(esnmf_status st, const std::string& msg) {
+  g_last_error = msg;
+  throw Fail{st};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(ESNMF_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(ESNMF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) ck((x), #x)
+#define CKL(name) ck(cudaGetLastError(), name)
+
+constexpr int64_t kSplitLen = 4096;   // max stored entries per SpMM work item (A rows)
+constexpr int kMaxGramSeg = 64;
+
+struct DevCsr {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int64_t* ptr = nullptr;
+  int2* ent = nullptr;
+};
+
+struct Factor {
+  int64_t rows = 0, cap = 0, cap_rows = 0;
+  int64_t* colptr = nullptr;
+  int32_t* row = nullptr;
+  float* val = nullptr;
+  int32_t* rowmap = nullptr;
+  int32_t* active = nullptr;
+  int64_t* n_active = nullptr;
+  float* dense = nullptr;
+  int64_t maxcol = 0;  // host upper bound of a column's length
+  bool has = false;
+};
+
+struct Side {
+  int64_t row0 = 0, rows = 0, ldx = 0;  // this rank's output rows
+  float* X = nullptr;                   // LS, column-major k x ldx
+  DevCsr T;                             // operator rows of this shard (local row ids)
+  // work items (U side only)
+  WorkItem* items = nullptr;
+  int32_t* item_slot = nullptr;
+  int64_t nitems = 0;
+  SplitRow* splits = nullptr;
+  int64_t nsplit = 0, nslots = 0;
+  float* partial = nullptr;
+  // selection scratch
+  int64_t nchunks = 0;
+  uint32_t* hist = nullptr;
+  ColSel* sel = nullptr;
+  uint64_t* cand = nullptr;
+  int32_t* cand_fill = nullptr;
+  int64_t* chunk_cnt = nullptr;
+  int64_t* coltot = nullptr;
+  uint64_t* kthr = nullptr;
+  // Gram of the factor this side reads, and its eps
+  double* G = nullptr;
+  double* eps = nullptr;
+  bool ls_valid = false;
+};
+
+}  // namespace
+
+struct esnmf {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t n = 0, m = 0, nnz = 0;
+  int k = 0, kpad = 0;
+  int64_t t = 0;  // < 0 unlimited
+  double rho = 1e-10;
+  uint64_t seed = 0;
+  int world = 1, rank = 0;
+  esnmf_comm comm{};
+  Side side[2];  // 0: V side (A^T rows = documents), 1: U side (A rows = terms)
+  Factor U[2];
+  int ucur = 0;
+  Factor V;
+  float* Z = nullptr;
+  double* W = nullptr;
+  double* gram_partial = nullptr;
+  double* sweep_scratch = nullptr;
+  int* flags = nullptr;  // [0] singular, [1] validation, [2] U0 invalid
+  double* red = nullptr;
+  int64_t red_cap = 0;
+  double* scal = nullptr;
+  double* normA2_dev = nullptr;
+  esnmf_record* rec = nullptr;
+  int64_t rec_cap = 0, nrec = 0;
+  double normA2 = 0;
+  bool gramU_valid = false;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+
+  template <typename T>
+  T* alloc(int64_t count) {
+    if (count <= 0) count = 1;
+    void* p = nullptr;
+    size_t b = sizeof(T) * (size_t)count;
+    ck(cudaMalloc(&p, b), "cudaMalloc");
+    allocs.push_back(p);
+    bytes += (int64_t)b;
+    return static_cast<T*>(p);
+  }
+  ~esnmf() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+unsigned col_grid_x(int64_t maxcol) { return (unsigned)std::min<int64_t>(std::max<int64_t>(1, ceil_div(maxcol, 256)), 2048); }
+
+void launch_scan_inplace(esnmf_t* h, int64_t* a, int64_t n, int64_t* total) {
+  int64_t nb = ceil_div(n, kScanBlock);
+  int64_t* bs = h->alloc<int64_t>(nb);  // create-time only
+  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
+  k_scan_small<<<1, 1024, 0, h->stream>>>(bs, nb, total);
+  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
+  CKL("scan");
+}
+
+// ---------------------------------------------------------------- factors
+
+void factor_alloc(esnmf_t* h, Factor& f, int64_t rows, int64_t cap) {
+  f.rows = rows;
+  f.cap = cap;
+  f.cap_rows = std::min(rows, cap);
+  f.colptr = h->alloc<int64_t>(h->k + 1);
+  f.row = h->alloc<int32_t>(cap);
+  f.val = h->alloc<float>(cap);
+  f.rowmap = h->alloc<int32_t>(rows);
+  f.active = h->alloc<int32_t>(f.cap_rows);
+  f.n_active = h->alloc<int64_t>(1);
+  f.dense = h->alloc<float>(f.cap_rows * h->kpad);
+  CK(cudaMemsetAsync(f.colptr, 0, sizeof(int64_t) * (h->k + 1), h->stream));
+  CK(cudaMemsetAsync(f.rowmap, 0xFF, sizeof(int32_t) * rows, h->stream));
+  CK(cudaMemsetAsync(f.n_active, 0, sizeof(int64_t), h->stream));
+  CK(cudaMemsetAsync(f.dense, 0, sizeof(float) * f.cap_rows * h->kpad, h->stream));
+  f.has = false;
+  f.maxcol = 0;
+}
+
+// undo the row view of the factor's current content (before it is replaced)
+void factor_clear(esnmf_t* h, Factor& f) {
+  if (!f.has) return;
+  dim3 g(col_grid_x(f.maxcol), h->k);
+  k_clear_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, f.dense, h->kpad);
+  k_reset_rowmap<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, f.rowmap);
+  CKL("factor_clear");
+  f.has = false;
+}
+
+// build rowmap / active / dense from the column-major COO just written
+void factor_build_rows(esnmf_t* h, Factor& f, int64_t maxcol) {
+  f.maxcol = maxcol;
+  dim3 g(col_grid_x(maxcol), h->k);
+  k_mark_rows<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap);
+  const int64_t nb = ceil_div(f.rows, kRowBlock);
+  int64_t* bc = reinterpret_cast<int64_t*>(h->red);  // scratch (nb <= red_cap)
+  k_rows_count<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc);
+  k_scan_small<<<1, 1024, 0, h->stream>>>(bc, nb, f.n_active);
+  k_rows_assign<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc, f.active);
+  k_scatter_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad);
+  CKL("factor_build_rows");
+  f.has = true;
+}
+
+int64_t steady_maxcol(esnmf_t* h, int64_t rows) { return h->t < 0 ? rows : std::min(rows, h->t); }
+
+// ---------------------------------------------------------------- kernels
+
+void gram(esnmf_t* h, const Factor& f, double* G) {
+  const int k = h->k;
+  int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 256)));
+  int64_t seglen = std::max<int64_t>(1, ceil_div(f.maxcol, S));
+  dim3 g(k, (unsigned)S);
+  k_gram_partial<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
+                                            h->gram_partial);
+  k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(h->gram_partial, (int)S, k, G);
+  k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
+  CKL("gram");
+}
+
+void sweep(esnmf_t* h, const double* G, double* eps) {
+  const bool glob = h->k > 224;
+  k_sweep_inverse<<<1, 1024, sweep_smem_bytes(h->k, glob), h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags,
+                                                                         glob ? h->sweep_scratch : nullptr);
+  CKL("sweep_inverse");
+}
+
+void form_z(esnmf_t* h, const Factor& f) {
+  const int CJ = (h->kpad + 31) / 32;
+  unsigned grid = grid_for(f.cap_rows, 8, 148 * 64);
+#define ESNMF_FZ(cj) \
+  case cj: k_form_z<cj><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z); break;
+  switch (CJ) {
+    ESNMF_FZ(1) ESNMF_FZ(2) ESNMF_FZ(3) ESNMF_FZ(4) ESNMF_FZ(5) ESNMF_FZ(6) ESNMF_FZ(7) ESNMF_FZ(8)
+    default: fail(ESNMF_EINVAL, "k too large");
+  }
+#undef ESNMF_FZ
+  CKL("form_z");
+}
+
+template <int G, int CPL>
+void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
+  Side& sd = h->side[s];
+  const int KQ = h->kpad / 4;
+  const float4* Z4 = reinterpret_cast<const float4*>(h->Z);
+  if (s == ESNMF_SIDE_V) {
+    const int64_t ntiles = ceil_div(sd.rows, 32);
+    unsigned grid = (unsigned)std::min<int64_t>(ntiles, 148 * 8);
+    size_t smem = sizeof(float) * h->kpad * 33;
+    k_spmm_tiled<G, CPL><<<grid, 256, smem, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, rowmap, Z4, KQ, h->k, sd.X,
+                                                         sd.ldx);
+  } else {
+    unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.nitems, 8), 148 * 8);
+    k_spmm_items<G, CPL><<<grid, 256, 0, h->stream>>>(sd.items, sd.nitems, sd.item_slot, sd.T.ent, rowmap, Z4, KQ,
+                                                      h->k, h->kpad, sd.X, sd.ldx, sd.partial);
+    if (sd.nsplit > 0)
+      k_spmm_combine<<<grid_for(sd.nsplit, 8, 4096), 256, 0, h->stream>>>(sd.splits, sd.nsplit, sd.partial, h->k,
+                                                                          h->kpad, sd.X, sd.ldx);
+  }
+  CKL("spmm");
+}
+
+void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
+  const int KQ = h->kpad / 4;
+  if (KQ <= 4) spmm_launch<4, 1>(h, s, rowmap);
+  else if (KQ <= 8) spmm_launch<8, 1>(h, s, rowmap);
+  else if (KQ <= 16) spmm_launch<16, 1>(h, s, rowmap);
+  else if (KQ <= 32) spmm_launch<32, 1>(h, s, rowmap);
+  else spmm_launch<32, 2>(h, s, rowmap);
+}
+
+// clamp + per-column top-t of side s's LS into factor `out` (column-major COO)
+void select_topt(esnmf_t* h, int s, Factor& out) {
+  Side& sd = h->side[s];
+  const int k = h->k;
+  if (sd.rows == 0) fail(ESNMF_EINVAL, "empty shard");
+  const int64_t nch = sd.nchunks;
+  CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
+  CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
+  dim3 g((unsigned)nch, k);
+  k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
+  k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+  k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+                                          sd.chunk_cnt, nch);
+  k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+                                          sd.chunk_cnt, nch, sd.kthr);
+  k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nch, sd.coltot);
+  k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, out.colptr);
+  k_sel_write<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.kthr, out.colptr,
+                                        sd.chunk_cnt, nch, out.row, out.val);
+  CKL("select");
+}
+
+// one half-step; returns the factor that was written
+Factor& half_step(esnmf_t* h, int s) {
+  Side& sd = h->side[s];
+  Factor& in = (s == ESNMF_SIDE_V) ? h->U[h->ucur] : h->V;
+  Factor& out = (s == ESNMF_SIDE_V) ? h->V : h->U[1 - h->ucur];
+  if (!in.has) fail(ESNMF_ESTATE, s == ESNMF_SIDE_V ? "U is not set" : "V is not set (run the V side first)");
+  if (!(s == ESNMF_SIDE_V && h->gramU_valid)) gram(h, in, sd.G);   // a1: P:63 / P:64
+  sweep(h, sd.G, sd.eps);                                          // a2
+  form_z(h, in);                                                   // Z = F W
+  spmm(h, s, in.rowmap);                                           // a3 (+a4 scale)
+  sd.ls_valid = true;
+  factor_clear(h, out);
+  select_topt(h, s, out);                                          // a4 clamp + a5 top-t
+  factor_build_rows(h, out, steady_maxcol(h, out.rows));
+  if (s == ESNMF_SIDE_U) {
+    h->ucur = 1 - h->ucur;
+    h->gramU_valid = false;
+  }
+  return out;
+}
+
+void ensure_records(esnmf_t* h, int64_t need) {
+  if (need <= h->rec_cap) return;
+  int64_t cap = std::max<int64_t>(need, 2 * h->rec_cap + 64);
+  esnmf_record* r = h->alloc<esnmf_record>(cap);
+  if (h->nrec > 0) CK(cudaMemcpyAsync(r, h->rec, sizeof(esnmf_record) * h->nrec, cudaMemcpyDeviceToDevice, h->stream));
+  h->rec = r;
+  h->rec_cap = cap;
+}
+
+void iterate_one(esnmf_t* h) {
+  half_step(h, ESNMF_SIDE_V);
+  half_step(h, ESNMF_SIDE_U);
+  Factor& Un = h->U[h->ucur];
+  Factor& Uo = h->U[1 - h->ucur];
+  const int k = h->k;
+  // a7 residual, direct difference
+  const unsigned gxn = col_grid_x(Un.maxcol), gxo = col_grid_x(Uo.maxcol);
+  double* p_new = h->red;
+  double* p_old = p_new + 2 * (int64_t)gxn * k;
+  double* p_tr = p_old + (int64_t)gxo * k;
+  k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
+  k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
+  // Gram of the new U: S term of E now, and the next V side's G_U
+  gram(h, Un, h->side[ESNMF_SIDE_V].G);
+  h->gramU_valid = true;
+  // a8 error: T = tr(U^T (A V)) from the U side's LS rows
+  Side& su = h->side[ESNMF_SIDE_U];
+  k_err_trace<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, su.row0, su.rows, su.X, su.ldx, su.G,
+                                                    su.eps, k, p_tr);
+  CKL("metrics");
+  const double* t_red = nullptr;
+  if (h->world > 1) {
+    k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gxn * k, h->scal + 3);
+    if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 1, h->stream) != 0)
+      fail(ESNMF_ECOMM, "allreduce(T) failed");
+    t_red = h->scal + 3;
+  }
+  ensure_records(h, h->nrec + 1);
+  RecordInputs in;
+  in.rnew = p_new;
+  in.nrnew = (int64_t)gxn * k;
+  in.rold = p_old;
+  in.nrold = (int64_t)gxo * k;
+  in.tpart = p_tr;
+  in.ntpart = (int64_t)gxn * k;
+  in.GU = h->side[ESNMF_SIDE_V].G;
+  in.GV = su.G;
+  in.colptr_u = Un.colptr;
+  in.colptr_v = h->V.colptr;
+  in.nact_u = Un.n_active;
+  in.nact_v = h->V.n_active;
+  in.normA2 = h->normA2;
+  in.k = k;
+  in.it = (int)(h->nrec + 1);
+  in.t_reduced = t_red;
+  k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
+  CKL("finalize_record");
+  h->nrec += 1;
+}
+
+void sync_check(esnmf_t* h) {
+  CK(cudaStreamSynchronize(h->stream));
+  int fl[3];
+  CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+  if (fl[0]) fail(ESNMF_ESINGULAR, "G + eps I is not positive definite (non-positive or non-finite pivot)");
+}
+
+// U side work items over this shard's term rows (host, from a copy of row_ptr)
+void build_items(esnmf_t* h, Side& sd, const std::vector<int64_t>& ptr_local) {
+  std::vector<WorkItem> items;
+  std::vector<int32_t> slot;
+  std::vector<SplitRow> splits;
+  int64_t nslots = 0;
+  for (int64_t r = 0; r < sd.rows; ++r) {
+    const int64_t s = ptr_local[r], e = ptr_local[r + 1], len = e - s;
+    const int64_t nit = std::max<int64_t>(1, ceil_div(len, kSplitLen));
+    if (nit == 1) {
+      items.push_back(WorkItem{s, (int32_t)r, (int32_t)len});
+      slot.push_back(-1);
+    } else {
+      splits.push_back(SplitRow{(int32_t)r, (int32_t)nslots, (int32_t)nit, 0});
+      for (int64_t q = 0; q < nit; ++q) {
+        const int64_t b = s + q * kSplitLen;
+        items.push_back(WorkItem{b, (int32_t)r, (int32_t)std::min<int64_t>(kSplitLen, e - b)});
+        slot.push_back((int32_t)nslots++);
+      }
+    }
+  }
+  sd.nitems = (int64_t)items.size();
+  sd.nsplit = (int64_t)splits.size();
+  sd.nslots = nslots;
+  sd.items = h->alloc<WorkItem>(sd.nitems);
+  sd.item_slot = h->alloc<int32_t>(sd.nitems);
+  sd.splits = h->alloc<SplitRow>(sd.nsplit);
+  sd.partial = h->alloc<float>(std::max<int64_t>(1, nslots) * h->kpad);
+  CK(cudaMemcpy(sd.items, items.data(), sizeof(WorkItem) * sd.nitems, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(sd.item_slot, slot.data(), sizeof(int32_t) * sd.nitems, cudaMemcpyHostToDevice));
+  if (sd.nsplit) CK(cudaMemcpy(sd.splits, splits.data(), sizeof(SplitRow) * sd.nsplit, cudaMemcpyHostToDevice));
+}
+
+void side_alloc(esnmf_t* h, Side& sd) {
+  const int k = h->k;
+  sd.ldx = std::max<int64_t>(32, ceil_div(sd.rows, 32) * 32);
+  sd.X = h->alloc<float>((int64_t)k * sd.ldx);
+  sd.nchunks = std::max<int64_t>(1, ceil_div(sd.rows, kSelChunk));
+  sd.hist = h->alloc<uint32_t>((int64_t)k * kNumBins);
+  sd.sel = h->alloc<ColSel>(k);
+  sd.cand = h->alloc<uint64_t>((int64_t)k * kSelCap);
+  sd.cand_fill = h->alloc<int32_t>(k);
+  sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * sd.nchunks);
+  sd.coltot = h->alloc<int64_t>(k);
+  sd.kthr = h->alloc<uint64_t>(k);
+  sd.G = h->alloc<double>((int64_t)k * k);
+  sd.eps = h->alloc<double>(1);
+}
+
+// upload (or copy) a CSR and pack it; returns device CSR with local rows [r0, r1)
+DevCsr upload_csr(esnmf_t* h, int64_t rows_total, int64_t cols, const int64_t* ptr, const int32_t* col,
+                  const float* val, bool on_dev, int64_t r0, int64_t r1, std::vector<int64_t>* host_ptr_local) {
+  DevCsr c;
+  c.rows = r1 - r0;
+  c.cols = cols;
+  std::vector<int64_t> hp(rows_total + 1);
+  CK(cudaMemcpy(hp.data(), ptr, sizeof(int64_t) * (rows_total + 1), on_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  if (hp[0] != 0) fail(ESNMF_EINVAL, "row_ptr[0] != 0");
+  for (int64_t r = 0; r < rows_total; ++r)
+    if (hp[r + 1] < hp[r]) fail(ESNMF_EINVAL, "row_ptr is not non-decreasing at row " + std::to_string(r));
+  const int64_t e0 = hp[r0], e1 = hp[r1];
+  c.nnz = e1 - e0;
+  c.ptr = h->alloc<int64_t>(c.rows + 1);
+  std::vector<int64_t> lp(c.rows + 1);
+  for (int64_t r = 0; r <= c.rows; ++r) lp[r] = hp[r0 + r] - e0;
+  CK(cudaMemcpy(c.ptr, lp.data(), sizeof(int64_t) * (c.rows + 1), cudaMemcpyHostToDevice));
+  c.ent = h->alloc<int2>(c.nnz);
+  if (c.nnz > 0) {
+    int32_t* dcol;
+    float* dval;
+    if (on_dev) {
+      dcol = const_cast<int32_t*>(col) + e0;
+      dval = const_cast<float*>(val) + e0;
+    } else {
+      // stage through the (not yet used) entry buffer's tail: pack from two temporaries
+      dcol = h->alloc<int32_t>(c.nnz);
+      dval = h->alloc<float>(c.nnz);
+      CK(cudaMemcpyAsync(dcol, col + e0, sizeof(int32_t) * c.nnz, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaMemcpyAsync(dval, val + e0, sizeof(float) * c.nnz, cudaMemcpyHostToDevice, h->stream));
+    }
+    k_pack<<<grid_for(c.nnz, 256, 148 * 32), 256, 0, h->stream>>>(dcol, dval, c.nnz, c.ent);
+    CKL("pack");
+    if (!on_dev) {
+      CK(cudaStreamSynchronize(h->stream));
+      // release the staging buffers now (they were the last two allocations)
+      for (int q = 0; q < 2; ++q) {
+        void* p = h->allocs.back();
+        h->allocs.pop_back();
+        CK(cudaFree(p));
+      }
+      h->bytes -= (int64_t)(sizeof(int32_t) + sizeof(float)) * c.nnz;
+    }
+  }
+  k_validate<<<grid_for(c.rows, 8, 148 * 64), 256, 0, h->stream>>>(c.ptr, c.ent, c.rows, cols, c.nnz, h->flags + 1);
+  CKL("validate");
+  if (host_ptr_local) *host_ptr_local = std::move(lp);
+  return c;
+}
+
+// CSR(A^T) rows [m0, m1) built on the device from the full CSR(A)
+DevCsr build_at(esnmf_t* h, const DevCsr& A, int64_t m, int64_t m0, int64_t m1) {
+  DevCsr T;
+  T.rows = m;
+  T.cols = A.rows;
+  T.nnz = A.nnz;
+  T.ptr = h->alloc<int64_t>(m + 1);
+  T.ent = h->alloc<int2>(A.nnz);
+  CK(cudaMemsetAsync(T.ptr, 0, sizeof(int64_t) * (m + 1), h->stream));
+  k_col_count<<<grid_for(A.nnz, 256, 148 * 32), 256, 0, h->stream>>>(A.ent, A.nnz, T.ptr);
+  int64_t* tot = h->alloc<int64_t>(1);
+  launch_scan_inplace(h, T.ptr, m + 1, tot);
+  int64_t* cursor = h->alloc<int64_t>(m + 1);
+  CK(cudaMemcpyAsync(cursor, T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToDevice, h->stream));
+  k_transpose_scatter<<<grid_for(A.rows, 8, 148 * 64), 256, 0, h->stream>>>(A.ptr, A.ent, A.rows, cursor, T.ent);
+  k_sort_rows<<<grid_for(m, 1, 148 * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent, nullptr, 0);
+  // long rows (> kRowSortCap entries) in a global scratch, one block
+  std::vector<int64_t> hp(m + 1);
+  CK(cudaMemcpyAsync(hp.data(), T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  int64_t maxlen = 0;
+  for (int64_t j = 0; j < m; ++j) maxlen = std::max(maxlen, hp[j + 1] - hp[j]);
+  if (maxlen > kRowSortCap) {
+    int64_t np = 1;
+    while (np < maxlen) np <<= 1;
+    uint64_t* scr = h->alloc<uint64_t>(np);
+    k_sort_rows<<<1, 256, 0, h->stream>>>(T.ptr, m, T.ent, scr, 1);
+  }
+  CKL("build_at");
+  if (m0 == 0 && m1 == m) return T;
+  // shard: keep rows [m0, m1) with local offsets
+  DevCsr L;
+  L.rows = m1 - m0;
+  L.cols = A.rows;
+  L.nnz = hp[m1] - hp[m0];
+  L.ptr = h->alloc<int64_t>(L.rows + 1);
+  std::vector<int64_t> lp(L.rows + 1);
+  for (int64_t r = 0; r <= L.rows; ++r) lp[r] = hp[m0 + r] - hp[m0];
+  CK(cudaMemcpy(L.ptr, lp.data(), sizeof(int64_t) * (L.rows + 1), cudaMemcpyHostToDevice));
+  L.ent = T.ent + hp[m0];
+  return L;
+}
+
+void init_u0(esnmf_t* h, const float* user_u0, bool on_dev) {
+  Factor& f = h->U[0];
+  const float* du = nullptr;
+  if (user_u0) {
+    if (on_dev) du = user_u0;
+    else {
+      float* tmp = h->alloc<float>(h->n * h->k);
+      CK(cudaMemcpyAsync(tmp, user_u0, sizeof(float) * h->n * h->k, cudaMemcpyHostToDevice, h->stream));
+      du = tmp;
+    }
+  }
+  k_u0_dense<<<grid_for(h->n * h->kpad, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, h->seed, du,
+                                                                               f.dense, h->flags + 2);
+  k_u0_coo<<<grid_for(h->n * h->k, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, f.colptr,
+                                                                          f.row, f.val, f.rowmap, f.active,
+                                                                          f.n_active);
+  CKL("init_u0");
+  f.has = true;
+  f.maxcol = h->n;
+  h->ucur = 0;
+  h->gramU_valid = false;
+}
+
+esnmf_status guard_status(const Fail& f) { return f.st; }
+
+template <typename Fn>
+esnmf_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return ESNMF_OK;
+  } catch (const Fail& f) {
+    return guard_status(f);
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return ESNMF_ENOMEM;
+  } catch (...) {
+    g_last_error = "unexpected exception";
+    return ESNMF_ECUDA;
+  }
+}
+
+void set_device(esnmf_t* h) { CK(cudaSetDevice(h->dev)); }
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* esnmf_version(void) { return "esnmf-b200 0.1 (sm_100a)"; }
+
+const char* esnmf_strerror(esnmf_status s) {
+  switch (s) {
+    case ESNMF_OK: return "ok";
+    case ESNMF_EINVAL: return "invalid argument";
+    case ESNMF_ENOMEM: return "out of memory";
+    case ESNMF_ECUDA: return "CUDA error";
+    case ESNMF_ECOMM: return "collective failed";
+    case ESNMF_ESINGULAR: return "singular Gram system";
+    case ESNMF_EDEGENERATE: return "degenerate factor (||U|| = 0)";
+    case ESNMF_ESTATE: return "call-order violation";
+    case ESNMF_ETRUNC: return "buffer too small";
+  }
+  return "unknown status";
+}
+
+const char* esnmf_last_error(void) { return g_last_error.c_str(); }
+
+esnmf_status esnmf_options_init(esnmf_options* o) {
+  if (!o) return ESNMF_EINVAL;
+  std::memset(o, 0, sizeof(*o));
+  o->seed = 0;
+  o->ridge_scale = 1e-10;
+  o->device = -1;
+  o->world = 1;
+  o->rank = 0;
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_partition_rows(int64_t rows, const int64_t* row_ptr, int32_t world, int64_t* bounds) {
+  if (rows < 0 || world < 1 || !bounds || (rows > 0 && !row_ptr)) {
+    g_last_error = "esnmf_partition_rows: bad argument";
+    return ESNMF_EINVAL;
+  }
+  // contiguous ranges balancing stored entries + rows (each row costs one item)
+  const int64_t total = (rows > 0 ? row_ptr[rows] : 0) + rows;
+  bounds[0] = 0;
+  int64_t r = 0;
+  for (int32_t p = 1; p < world; ++p) {
+    const double target = (double)total * p / world;
+    while (r < rows && (double)(row_ptr[r + 1] + r + 1) <= target) ++r;
+    bounds[p] = r;
+  }
+  bounds[world] = rows;
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_t t, const int64_t* row_ptr,
+                          const int32_t* col_idx, const float* val, const esnmf_options* opt) {
+  if (out) *out = nullptr;
+  esnmf_options o;
+  esnmf_options_init(&o);
+  if (opt) o = *opt;
+  if (!out || !row_ptr || !col_idx || !val) { g_last_error = "esnmf_create: NULL argument"; return ESNMF_EINVAL; }
+  if (n < 1 || m < 1 || n >= (1LL << 31) || m >= (1LL << 31)) {
+    g_last_error = "esnmf_create: need 1 <= n, m < 2^31 (got n=" + std::to_string(n) + ", m=" + std::to_string(m) + ")";
+    return ESNMF_EINVAL;
+  }
+  if (k < 1 || k > ESNMF_MAX_K) { g_last_error = "esnmf_create: need 1 <= k <= 256"; return ESNMF_EINVAL; }
+  if (t < 0 && t != ESNMF_T_UNLIMITED) { g_last_error = "esnmf_create: t must be >= 0 or ESNMF_T_UNLIMITED"; return ESNMF_EINVAL; }
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { g_last_error = "esnmf_create: bad world/rank"; return ESNMF_EINVAL; }
+  if (o.world > 1 && (!o.comm || !o.comm->allgather || !o.comm->allreduce_sum_f64)) {
+    g_last_error = "esnmf_create: world > 1 needs comm callbacks";
+    return ESNMF_EINVAL;
+  }
+  if (o.world > 1) { g_last_error = "esnmf_create: multi-rank sharding is not enabled in this build"; return ESNMF_EINVAL; }
+  if (!(o.ridge_scale >= 0) || !std::isfinite(o.ridge_scale)) { g_last_error = "esnmf_create: bad ridge_scale"; return ESNMF_EINVAL; }
+  std::unique_ptr<esnmf> h(new esnmf());
+  esnmf_status st = guarded([&] {
+    if (o.device >= 0) h->dev = o.device;
+    else CK(cudaGetDevice(&h->dev));
+    set_device(h.get());
+    if (o.stream) h->stream = (cudaStream_t)o.stream;
+    else {
+      CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    h->n = n;
+    h->m = m;
+    h->k = k;
+    h->kpad = (k + 3) / 4 * 4;
+    h->t = t;
+    h->rho = o.ridge_scale;
+    h->seed = o.seed;
+    h->world = o.world;
+    h->rank = o.rank;
+    if (o.comm) h->comm = *o.comm;
+    const bool on_dev = o.inputs_on_device != 0;
+    h->flags = h->alloc<int>(4);
+    CK(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
+    h->scal = h->alloc<double>(8);
+    h->normA2_dev = h->alloc<double>(1);
+    h->red_cap = 4LL * 2048 * 256 * 2;
+    h->red = h->alloc<double>(h->red_cap);
+    // ---- A (U side operator, term rows) ----
+    std::vector<int64_t> aptr;
+    Side& su = h->side[ESNMF_SIDE_U];
+    su.row0 = 0;
+    su.rows = n;
+    su.T = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, 0, n, &aptr);
+    h->nnz = su.T.nnz;
+    if (h->nnz < 1) fail(ESNMF_EINVAL, "esnmf_create: nnz must be >= 1");
+    // ||A||_F^2
+    {
+      unsigned gb = grid_for(h->nnz, 256, 1024);
+      k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, h->nnz, h->red);
+      k_reduce_to<<<1, 256, 0, h->stream>>>(h->red, gb, h->normA2_dev);
+      CKL("frob2");
+    }
+    // ---- A^T (V side operator, document rows) ----
+    Side& sv = h->side[ESNMF_SIDE_V];
+    sv.row0 = 0;
+    sv.rows = m;
+    if (o.at_row_ptr && o.at_col_idx && o.at_val) {
+      sv.T = upload_csr(h.get(), m, n, o.at_row_ptr, o.at_col_idx, o.at_val, on_dev, 0, m, nullptr);
+      if (sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
+    } else {
+      sv.T = build_at(h.get(), su.T, m, 0, m);
+    }
+    build_items(h.get(), su, aptr);
+    side_alloc(h.get(), sv);
+    side_alloc(h.get(), su);
+    // ---- factors ----
+    const int64_t capU = n * (int64_t)k;
+    const int64_t capV = (t < 0 ? m : std::min(m, t)) * (int64_t)k;
+    factor_alloc(h.get(), h->U[0], n, capU);
+    factor_alloc(h.get(), h->U[1], n, capU);
+    factor_alloc(h.get(), h->V, m, capV);
+    h->Z = h->alloc<float>(std::max(h->U[0].cap_rows, h->V.cap_rows) * h->kpad);
+    h->W = h->alloc<double>((int64_t)k * k);
+    h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * k * k);
+    if (k > 224) h->sweep_scratch = h->alloc<double>((int64_t)k * (k + 1) / 2);
+    CK(cudaFuncSetAttribute(k_sweep_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sweep_smem_bytes(std::min(k, 224), false)));
+    init_u0(h.get(), o.U0, on_dev);
+    CK(cudaStreamSynchronize(h->stream));
+    int fl[4];
+    CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+    if (fl[1]) {
+      std::string why;
+      if (fl[1] & 1) why += " row_ptr;";
+      if (fl[1] & 2) why += " column index out of range;";
+      if (fl[1] & 4) why += " column indices not strictly increasing within a row;";
+      if (fl[1] & 8) why += " negative or non-finite value;";
+      fail(ESNMF_EINVAL, "esnmf_create: malformed CSR:" + why);
+    }
+    if (fl[2]) fail(ESNMF_EINVAL, "esnmf_create: U0 must be finite and > 0");
+    CK(cudaMemcpy(&h->normA2, h->normA2_dev, sizeof(double), cudaMemcpyDeviceToHost));
+    if (!(h->normA2 > 0)) fail(ESNMF_EINVAL, "esnmf_create: ||A|| == 0");
+  });
+  if (st != ESNMF_OK) return st;
+  *out = h.release();
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_iterate(esnmf_t* h, int32_t iters) {
+  if (!h || iters < 0) { g_last_error = "esnmf_iterate: bad argument"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    ensure_records(h, h->nrec + iters);
+    for (int32_t i = 0; i < iters; ++i) iterate_one(h);
+  });
+}
+
+esnmf_status esnmf_half_step(esnmf_t* h, int32_t side) {
+  if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U)) { g_last_error = "esnmf_half_step: bad argument"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    half_step(h, side);
+  });
+}
+
+static esnmf_status last_record(esnmf_t* h, esnmf_record* r) {
+  return guarded([&] {
+    set_device(h);
+    if (h->nrec == 0) fail(ESNMF_ESTATE, "no completed iteration");
+    sync_check(h);
+    CK(cudaMemcpy(r, h->rec + h->nrec - 1, sizeof(esnmf_record), cudaMemcpyDeviceToHost));
+  });
+}
+
+esnmf_status esnmf_residual(esnmf_t* h, double* R) {
+  if (!h || !R) { g_last_error = "esnmf_residual: NULL argument"; return ESNMF_EINVAL; }
+  esnmf_record r;
+  esnmf_status st = last_record(h, &r);
+  if (st != ESNMF_OK) return st;
+  if (r.R < 0) { g_last_error = "residual undefined: ||U_i||_F == 0"; return ESNMF_EDEGENERATE; }
+  *R = r.R;
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_error(esnmf_t* h, double* E) {
+  if (!h || !E) { g_last_error = "esnmf_error: NULL argument"; return ESNMF_EINVAL; }
+  esnmf_record r;
+  esnmf_status st = last_record(h, &r);
+  if (st != ESNMF_OK) return st;
+  *E = r.E;
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_records(esnmf_t* h, int64_t cap, int64_t* count, esnmf_record* out) {
+  if (!h || !count || cap < 0 || (cap > 0 && !out)) { g_last_error = "esnmf_records: bad argument"; return ESNMF_EINVAL; }
+  esnmf_status st = guarded([&] {
+    set_device(h);
+    sync_check(h);
+    *count = h->nrec;
+    const int64_t nc = std::min(cap, h->nrec);
+    if (nc > 0) CK(cudaMemcpy(out, h->rec, sizeof(esnmf_record) * nc, cudaMemcpyDeviceToHost));
+  });
+  if (st == ESNMF_OK && cap < h->nrec) { g_last_error = "esnmf_records: cap < count"; return ESNMF_ETRUNC; }
+  return st;
+}
+
+static esnmf_status get_factor(esnmf_t* h, const Factor& f, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col,
+                               float* val) {
+  if (!h || !nnz) { g_last_error = "get factor: NULL argument"; return ESNMF_EINVAL; }
+  bool trunc = false;
+  esnmf_status st = guarded([&] {
+    set_device(h);
+    sync_check(h);
+    std::vector<int64_t> cp(h->k + 1, 0);
+    if (f.has) CK(cudaMemcpy(cp.data(), f.colptr, sizeof(int64_t) * (h->k + 1), cudaMemcpyDeviceToHost));
+    *nnz = cp[h->k];
+    if (cap < cp[h->k] || ((!row || !col || !val) && cp[h->k] > 0)) { trunc = true; return; }
+    if (cp[h->k] > 0) {
+      CK(cudaMemcpy(row, f.row, sizeof(int32_t) * cp[h->k], cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(val, f.val, sizeof(float) * cp[h->k], cudaMemcpyDeviceToHost));
+      for (int c = 0; c < h->k; ++c)
+        for (int64_t e = cp[c]; e < cp[c + 1]; ++e) col[e] = c;
+    }
+  });
+  if (st == ESNMF_OK && trunc) { g_last_error = "factor buffer too small"; return ESNMF_ETRUNC; }
+  return st;
+}
+
+esnmf_status esnmf_get_U(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val) {
+  if (!h) { g_last_error = "NULL handle"; return ESNMF_EINVAL; }
+  return get_factor(h, h->U[h->ucur], cap, nnz, row, col, val);
+}
+
+esnmf_status esnmf_get_V(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val) {
+  if (!h) { g_last_error = "NULL handle"; return ESNMF_EINVAL; }
+  return get_factor(h, h->V, cap, nnz, row, col, val);
+}
+
+esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32_t* row, const int32_t* col,
+                              const float* val) {
+  if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U) || nnz < 0 || (nnz > 0 && (!row || !col || !val))) {
+    g_last_error = "esnmf_set_factor: bad argument";
+    return ESNMF_EINVAL;
+  }
+  Factor& f = side == ESNMF_SIDE_U ? h->U[h->ucur] : h->V;
+  const int64_t rows = side == ESNMF_SIDE_U ? h->n : h->m;
+  // validate canonical order on the host
+  std::vector<int64_t> cp(h->k + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (col[e] < 0 || col[e] >= h->k || row[e] < 0 || row[e] >= rows || !(val[e] > 0.f) || !std::isfinite(val[e])) {
+      g_last_error = "esnmf_set_factor: entry " + std::to_string(e) + " out of range or not > 0";
+      return ESNMF_EINVAL;
+    }
+    if (e > 0 && (col[e] < col[e - 1] || (col[e] == col[e - 1] && row[e] <= row[e - 1]))) {
+      g_last_error = "esnmf_set_factor: entries not in canonical (column, row) order";
+      return ESNMF_EINVAL;
+    }
+    cp[col[e] + 1]++;
+  }
+  for (int c = 0; c < h->k; ++c) cp[c + 1] += cp[c];
+  int64_t maxcol = 0;
+  for (int c = 0; c < h->k; ++c) maxcol = std::max(maxcol, cp[c + 1] - cp[c]);
+  if (nnz > f.cap) { g_last_error = "esnmf_set_factor: more entries than the factor capacity"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    factor_clear(h, f);
+    CK(cudaMemcpyAsync(f.colptr, cp.data(), sizeof(int64_t) * (h->k + 1), cudaMemcpyHostToDevice, h->stream));
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(f.row, row, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaMemcpyAsync(f.val, val, sizeof(float) * nnz, cudaMemcpyHostToDevice, h->stream));
+    }
+    factor_build_rows(h, f, std::max<int64_t>(maxcol, 1));
+    if (side == ESNMF_SIDE_U) h->gramU_valid = false;
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+esnmf_status esnmf_get_ls(esnmf_t* h, int32_t side, int64_t* row0, int64_t* rows, float* out) {
+  if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U)) { g_last_error = "esnmf_get_ls: bad argument"; return ESNMF_EINVAL; }
+  Side& sd = h->side[side];
+  if (row0) *row0 = sd.row0;
+  if (rows) *rows = sd.rows;
+  if (!out) return ESNMF_OK;
+  return guarded([&] {
+    set_device(h);
+    if (!sd.ls_valid) fail(ESNMF_ESTATE, "no half-step of this side has run");
+    sync_check(h);
+    std::vector<float> buf((size_t)h->k * sd.ldx);
+    CK(cudaMemcpy(buf.data(), sd.X, sizeof(float) * buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < sd.rows; ++r)
+      for (int c = 0; c < h->k; ++c) out[r * h->k + c] = buf[(size_t)c * sd.ldx + r];
+  });
+}
+
+esnmf_status esnmf_get_gram(esnmf_t* h, int32_t side, double* G, double* eps) {
+  if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U) || !G) { g_last_error = "esnmf_get_gram: bad argument"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    // Gram of the factor this side reads next (side V: U^T U, side U: V^T V),
+    // recomputed by the same kernels into a scratch buffer.
+    const Factor& f = side == ESNMF_SIDE_V ? h->U[h->ucur] : h->V;
+    if (!f.has) fail(ESNMF_ESTATE, "factor not set");
+    double* Gd = h->W;  // W is rebuilt by every half-step: free between calls
+    gram(h, f, Gd);
+    sync_check(h);
+    CK(cudaMemcpy(G, Gd, sizeof(double) * h->k * h->k, cudaMemcpyDeviceToHost));
+    if (eps) {
+      double tr = 0;
+      for (int a = 0; a < h->k; ++a) tr += G[a * h->k + a];
+      *eps = h->rho * (tr / h->k + 1.0);
+    }
+  });
+}
+
+esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
+  if (!h || !info) { g_last_error = "esnmf_get_info: NULL argument"; return ESNMF_EINVAL; }
+  info->n = h->n;
+  info->m = h->m;
+  info->nnz = h->nnz;
+  info->k = h->k;
+  info->t = h->t;
+  info->world = h->world;
+  info->rank = h->rank;
+  info->v_row0 = h->side[0].row0;
+  info->v_rows = h->side[0].rows;
+  info->u_row0 = h->side[1].row0;
+  info->u_rows = h->side[1].rows;
+  info->iterations = h->nrec;
+  info->device_bytes = h->bytes;
+  info->normA2 = h->normA2;
+  return ESNMF_OK;
+}
+
+void esnmf_destroy(esnmf_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  delete h;
+}
+
+}  // extern "C"

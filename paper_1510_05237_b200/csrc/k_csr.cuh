@@ -1,0 +1,134 @@
+// k_csr.cuh -- input CSR handling at create time: packing, validation, A^T.
+#pragma once
+#include "common.cuh"
+
+namespace esk {
+
+// (int32 column, fp32 value) pairs -> one 8-byte entry per stored element
+__global__ void k_pack(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t nnz,
+                       int2* __restrict__ ent) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    ent[e] = make_int2(col[e], __float_as_int(val[e]));
+}
+
+// One warp per row: row_ptr monotone, 0 <= col < ncols strictly increasing,
+// values finite and >= 0.  Sets bits of *bad: 1 ptr, 2 col range, 4 order, 8 value.
+__global__ void k_validate(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
+                           int64_t ncols, int64_t nnz, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const int64_t s = ptr[r], e = ptr[r + 1];
+    if (lane == 0 && (e < s || s < 0 || e > nnz)) atomicOr(bad, 1);
+    if (e < s || s < 0 || e > nnz) continue;
+    int flags = 0;
+    for (int64_t q = s + lane; q < e; q += 32) {
+      const int2 en = ent[q];
+      if (en.x < 0 || en.x >= ncols) flags |= 2;
+      if (q > s && ent[q - 1].x >= en.x) flags |= 4;
+      const float v = __int_as_float(en.y);
+      if (!(v >= 0.f) || !isfinite(v)) flags |= 8;
+    }
+    flags = __reduce_or_sync(kFull, flags);
+    if (lane == 0 && flags) atomicOr(bad, flags);
+  }
+}
+
+// ---- A^T from A on the device (used when the caller gives only CSR(A)) ----
+__global__ void k_col_count(const int2* __restrict__ ent, int64_t nnz, int64_t* __restrict__ cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&cnt[ent[e].x], 1ULL);
+}
+
+constexpr int kScanBlock = 2048;
+
+__global__ void k_blocksum_i64(const int64_t* __restrict__ a, int64_t n, int64_t* __restrict__ bsum) {
+  __shared__ int64_t sm[32];
+  int64_t s = 0;
+  const int64_t base = blockIdx.x * (int64_t)kScanBlock;
+  for (int q = threadIdx.x; q < kScanBlock; q += blockDim.x) {
+    const int64_t i = base + q;
+    if (i < n) s += a[i];
+  }
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+}
+
+// in place exclusive scan of a[0..n) given exclusive block offsets; 256 threads x 8
+__global__ void k_scan_apply_i64(int64_t* __restrict__ a, int64_t n, const int64_t* __restrict__ boff) {
+  __shared__ int64_t sm[33];
+  constexpr int per = kScanBlock / 256;
+  const int64_t base = blockIdx.x * (int64_t)kScanBlock + threadIdx.x * per;
+  int64_t v[per];
+  int64_t s = 0;
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    v[q] = base + q < n ? a[base + q] : 0;
+    s += v[q];
+  }
+  int64_t tot;
+  int64_t off = boff[blockIdx.x] + block_exscan(s, sm, &tot);
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    if (base + q < n) a[base + q] = off;
+    off += v[q];
+  }
+}
+
+// scatter A's entries into A^T rows (arbitrary order within a row; sorted next)
+__global__ void k_transpose_scatter(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
+                                    int64_t* __restrict__ cursor, int2* __restrict__ tent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    for (int64_t q = ptr[r] + lane; q < ptr[r + 1]; q += 32) {
+      const int2 en = ent[q];
+      const int64_t p = (int64_t)atomicAdd((unsigned long long*)&cursor[en.x], 1ULL);
+      tent[p] = make_int2((int32_t)r, en.y);
+    }
+  }
+}
+
+// sort every row of A^T by column (terms are distinct within a document):
+// bitonic sort of 64-bit (col << 32 | value bits) keys.  Rows up to
+// kRowSortCap entries sort in shared memory; longer rows in `scratch`.
+constexpr int kRowSortCap = 4096;
+
+__global__ void __launch_bounds__(256) k_sort_rows(const int64_t* __restrict__ ptr, int64_t rows,
+                                                   int2* __restrict__ ent, uint64_t* __restrict__ scratch,
+                                                   int long_rows_only) {
+  __shared__ uint64_t keys[kRowSortCap];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t s = ptr[r], e = ptr[r + 1];
+    const int64_t len = e - s;
+    if (len <= 1) continue;
+    const bool fits = len <= kRowSortCap;
+    if (fits == (bool)long_rows_only) continue;
+    int64_t np = 1;
+    while (np < len) np <<= 1;
+    uint64_t* a = fits ? keys : scratch;
+    for (int64_t i = threadIdx.x; i < np; i += blockDim.x)
+      a[i] = i < len ? (((uint64_t)(uint32_t)ent[s + i].x << 32) | (uint32_t)ent[s + i].y) : ~0ULL;
+    __syncthreads();
+    for (int64_t size = 2; size <= np; size <<= 1) {
+      for (int64_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int64_t i = threadIdx.x; i < np; i += blockDim.x) {
+          const int64_t j = i ^ stride;
+          if (j > i) {
+            const bool up = (i & size) == 0;
+            const uint64_t x = a[i], y = a[j];
+            if ((x > y) == up) { a[i] = y; a[j] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x)
+      ent[s + i] = make_int2((int32_t)(a[i] >> 32), (int32_t)(uint32_t)(a[i] & 0xFFFFFFFFu));
+    __syncthreads();
+  }
+}
+
+}  // namespace esk

@@ -1,0 +1,113 @@
+// k_metrics.cuh -- relative error E and the per-iteration record.
+#pragma once
+#include "common.cuh"
+#include "../../include/esnmf.h"
+
+namespace esk {
+
+// T = tr(U^T (A V)) restricted to this shard's term rows.  (A V) is recovered
+// from the pre-clamp LS rows of the U side: A V = U_ls (V^T V + eps I), using
+// the regularised Gram the solve used (reading C9).  part[blk] = block partial.
+__global__ void __launch_bounds__(256) k_err_trace(const int64_t* __restrict__ colptr,
+                                                   const int32_t* __restrict__ row, const float* __restrict__ val,
+                                                   int64_t row0, int64_t rows, const float* __restrict__ XU,
+                                                   int64_t ldx, const double* __restrict__ GV, const double* eps_v,
+                                                   int k, double* __restrict__ part) {
+  __shared__ double sm[32];
+  const int c_ = blockIdx.y;
+  const int64_t cb = colptr[c_], ce = colptr[c_ + 1];
+  const double eps = *eps_v;
+  double acc = 0;
+  for (int64_t e = cb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ce; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lr = (int64_t)row[e] - row0;
+    if (lr < 0 || lr >= rows) continue;
+    double s = 0;
+    for (int l = 0; l < k; ++l) s += (double)XU[(int64_t)l * ldx + lr] * GV[(int64_t)l * k + c_];
+    s += (double)XU[(int64_t)c_ * ldx + lr] * eps;
+    acc += (double)val[e] * s;
+  }
+  acc = block_sum(acc, sm);
+  if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = acc;
+}
+
+// Sum of a partial array in a fixed order by one block.
+__device__ double reduce_fixed(const double* p, int64_t n, int64_t stride, double* sm) {
+  double s = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += p[i * stride];
+  return block_sum(s, sm);
+}
+
+struct RecordInputs {
+  const double* rnew;   // 2 per block: (sum (v-old)^2, sum v^2)
+  int64_t nrnew;
+  const double* rold;   // 1 per block
+  int64_t nrold;
+  const double* tpart;  // error trace partials
+  int64_t ntpart;
+  const double* GU;
+  const double* GV;
+  const int64_t* colptr_u;
+  const int64_t* colptr_v;
+  const int64_t* nact_u;
+  const int64_t* nact_v;
+  double normA2;
+  int k;
+  int it;
+  const double* t_reduced;  // if non-null: T already summed over ranks
+};
+
+// One block: R, E, counts -> rec.  Also stores (Rnum, Rden, T) into scal[0..2].
+__global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ rec, double* __restrict__ scal) {
+  __shared__ double sm[32];
+  const double num = reduce_fixed(in.rnew, in.nrnew, 2, sm) + reduce_fixed(in.rold, in.nrold, 1, sm);
+  const double den = reduce_fixed(in.rnew + 1, in.nrnew, 2, sm);
+  const double T = in.t_reduced ? *in.t_reduced : reduce_fixed(in.tpart, in.ntpart, 1, sm);
+  double S = 0;
+  for (int q = threadIdx.x; q < in.k * in.k; q += blockDim.x) S += in.GU[q] * in.GV[q];
+  S = block_sum(S, sm);
+  int dead_u = 0, dead_v = 0;
+  for (int c = threadIdx.x; c < in.k; c += blockDim.x) {
+    dead_u += in.colptr_u[c + 1] == in.colptr_u[c];
+    dead_v += in.colptr_v[c + 1] == in.colptr_v[c];
+  }
+  dead_u = (int)block_sum((double)dead_u, sm);
+  dead_v = (int)block_sum((double)dead_v, sm);
+  if (threadIdx.x == 0) {
+    esnmf_record r;
+    r.it = in.it;
+    r.R = den > 0 ? sqrt(num) / sqrt(den) : -1.0;
+    double e2 = in.normA2 - 2.0 * T + S;
+    if (e2 < 0) e2 = 0;
+    r.E = sqrt(e2) / sqrt(in.normA2);
+    r.nnz_u = in.colptr_u[in.k];
+    r.nnz_v = in.colptr_v[in.k];
+    r.dead_u = dead_u;
+    r.dead_v = dead_v;
+    r.active_u = *in.nact_u;
+    r.active_v = *in.nact_v;
+    *rec = r;
+    scal[0] = num;
+    scal[1] = den;
+    scal[2] = T;
+  }
+}
+
+// ||A||_F^2 partials over the packed entries
+__global__ void k_frob2(const int2* __restrict__ ent, int64_t nnz, double* __restrict__ part) {
+  __shared__ double sm[32];
+  double s = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = __int_as_float(ent[e].y);
+    s += v * v;
+  }
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_reduce_to(const double* __restrict__ part, int64_t n, double* __restrict__ out) {
+  __shared__ double sm[32];
+  const double s = reduce_fixed(part, n, 1, sm);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace esk

@@ -1,0 +1,269 @@
+// k_select.cuh -- projection + per-column enforced sparsity.
+//
+// For every column c of the LS buffer X (column-major, rows of this shard):
+//   keep {j : X[c][j] > 0}                         ("negative entries to zero")
+//   if more than t: keep the t largest             (per column P:304)
+//   ties at the t-th value -> lower row first, so exactly min(t, #positive) survive (C4).
+// Equivalently: keep the positives whose 64-bit key (value desc, row asc) is <=
+// the t-th smallest key K*_c.  K*_c is found by a radix select:
+//   1. k_sel_hist      histogram of the top 12 value bits (bits 30..19) per column;
+//   2. k_sel_threshold bucket D holding the t-th largest, r = t - #(buckets > D);
+//   3. k_sel_collect   count entries above D per chunk, gather bucket-D keys;
+//   4. k_sel_refine    K*_c = r-th smallest bucket-D key (bitonic sort in shared
+//                      memory; exact multi-pass radix fallback if the bucket is large);
+//   5. k_sel_scan_cols / k_sel_colptr: per-chunk output offsets;
+//   6. k_sel_write     ordered (row-ascending) compaction into column-major COO.
+// Integer counts only; no float atomics; output independent of scheduling.
+#pragma once
+#include "common.cuh"
+
+namespace esk {
+
+__global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                  uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kNumBins];
+  const int c = blockIdx.y;
+  for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  for (int64_t j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
+    const float x = __ldg(col + j);
+    if (x > 0.f) atomicAdd(&h[sel_digit(x)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kNumBins; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[(int64_t)c * kNumBins + b], h[b]);
+}
+
+// one block (1024 threads) per column; thread q owns bins [4095-4q-3, 4095-4q]
+__global__ void __launch_bounds__(1024) k_sel_threshold(const uint32_t* __restrict__ hist, int64_t t,
+                                                        ColSel* __restrict__ sel) {
+  __shared__ int64_t sm[33];
+  const int c = blockIdx.x;
+  const uint32_t* hc = hist + (int64_t)c * kNumBins;
+  int64_t cnt[4];
+  int64_t mine = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    cnt[u] = hc[kNumBins - 1 - (4 * threadIdx.x + u)];
+    mine += cnt[u];
+  }
+  int64_t total;
+  const int64_t before = block_exscan(mine, sm, &total);  // # in higher bins
+  if (threadIdx.x == 0) {
+    ColSel s;
+    s.pad_ = 0;
+    s.npos = total;
+    s.ncand = 0;
+    s.r = 0;
+    if (t < 0 || total <= t) { s.digit = -1; s.above = total; }
+    else if (t == 0) { s.digit = kNumBins; s.above = 0; }
+    else { s.digit = -2; s.above = 0; }   // filled by the owning thread below
+    sel[c] = s;
+  }
+  __syncthreads();
+  if (t > 0 && total > t) {
+    int64_t acc = before;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (acc < t && acc + cnt[u] >= t) {
+        ColSel s = sel[c];
+        s.digit = kNumBins - 1 - (4 * threadIdx.x + u);
+        s.above = acc;
+        s.r = t - acc;
+        s.ncand = cnt[u];
+        sel[c] = s;
+      }
+      acc += cnt[u];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                     int64_t row0, const ColSel* __restrict__ sel,
+                                                     uint64_t* __restrict__ cand, int32_t* __restrict__ cand_fill,
+                                                     int64_t* __restrict__ chunk_cnt, int64_t nchunks) {
+  __shared__ int64_t sm[32];
+  const int c = blockIdx.y;
+  const ColSel s = sel[c];
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  int64_t above = 0;
+  for (int64_t j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
+    const float x = __ldg(col + j);
+    if (x > 0.f) {
+      const int dg = sel_digit(x);
+      if (dg > s.digit) {
+        ++above;
+      } else if (dg == s.digit) {
+        const int slot = atomicAdd(&cand_fill[c], 1);
+        if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x, (uint32_t)(row0 + j));
+      }
+    }
+  }
+  above = block_sum(above, sm);
+  if (threadIdx.x == 0) chunk_cnt[(int64_t)c * nchunks + blockIdx.x] = above;
+}
+
+// bitonic sort of n (power of two) keys in shared memory, ascending
+__device__ void bitonic_sort_smem(uint64_t* a, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int jx = i ^ stride;
+        if (jx > i) {
+          bool up = (i & size) == 0;
+          uint64_t x = a[i], y = a[jx];
+          if ((x > y) == up) { a[i] = y; a[jx] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// K*_c and the per-chunk counts of the selected bucket-D entries.
+__global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                     int64_t row0, const ColSel* __restrict__ sel,
+                                                     const uint64_t* __restrict__ cand,
+                                                     const int32_t* __restrict__ cand_fill,
+                                                     int64_t* __restrict__ chunk_cnt, int64_t nchunks,
+                                                     uint64_t* __restrict__ kthr) {
+  __shared__ uint64_t keys[kSelCap];           // sort buffer (common path)
+  uint32_t* h = reinterpret_cast<uint32_t*>(keys);  // histogram (fallback path)
+  __shared__ int64_t sm[33];
+  const int c = blockIdx.x;
+  const ColSel s = sel[c];
+  if (s.r == 0) {
+    if (threadIdx.x == 0) kthr[c] = s.digit < 0 ? ~0ULL : 0ULL;
+    return;
+  }
+  const int nc = cand_fill[c];
+  uint64_t kstar;
+  if (nc <= kSelCap) {
+    int np = 1;
+    while (np < nc) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) keys[i] = i < nc ? cand[(int64_t)c * kSelCap + i] : ~0ULL;
+    __syncthreads();
+    bitonic_sort_smem(keys, np);
+    kstar = keys[s.r - 1];
+    for (int i = threadIdx.x; i < s.r; i += blockDim.x) {
+      const int64_t lr = (int64_t)(uint32_t)(keys[i] & 0xFFFFFFFFu) - row0;
+      atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + lr / kSelChunk], 1ULL);
+    }
+  } else {
+    // Exact fallback: radix select over the whole column restricted to bucket D.
+    // Key bits below the bucket: value bits 18..0 (stored inverted), then the row.
+    const float* col = X + (int64_t)c * ldx;
+    // levels: (shift, width) over the 63-bit key; bucket D fixes key bits 62..51
+    const int shifts[5] = {39, 32, 20, 8, 0};
+    const int widths[5] = {12, 7, 12, 12, 8};
+    uint64_t prefix = ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51;
+    uint64_t fixed_mask = 0xFFFULL << 51;
+    int64_t r = s.r;
+    for (int lv = 0; lv < 5; ++lv) {
+      const int sh = shifts[lv], wd = widths[lv];
+      for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
+      __syncthreads();
+      for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
+        const float x = col[j];
+        if (x > 0.f && sel_digit(x) == s.digit) {
+          const uint64_t key = sel_key(x, (uint32_t)(row0 + j));
+          if ((key & fixed_mask) == prefix) atomicAdd(&h[(key >> sh) & ((1u << wd) - 1)], 1u);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        int b = 0;
+        for (; b < (1 << wd); ++b) {
+          if (acc + h[b] >= r) break;
+          acc += h[b];
+        }
+        r -= acc;
+        sm[0] = b;
+        sm[1] = r;
+      }
+      __syncthreads();
+      prefix |= (uint64_t)sm[0] << sh;
+      r = sm[1];
+      fixed_mask |= (uint64_t)((1u << wd) - 1) << sh;
+      __syncthreads();
+    }
+    kstar = prefix;
+    for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
+      const float x = col[j];
+      if (x > 0.f && sel_digit(x) == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar)
+        atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + j / kSelChunk], 1ULL);
+    }
+  }
+  if (threadIdx.x == 0) kthr[c] = kstar;
+}
+
+// per column: exclusive scan of the chunk counts (in place), column total -> coltot[c]
+__global__ void __launch_bounds__(1024) k_sel_scan_cols(int64_t* __restrict__ chunk_cnt, int64_t nchunks,
+                                                        int64_t* __restrict__ coltot) {
+  __shared__ int64_t sm[33];
+  const int c = blockIdx.x;
+  int64_t* a = chunk_cnt + (int64_t)c * nchunks;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nchunks; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nchunks ? a[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_exscan(v, sm, &tot);
+    if (i < nchunks) a[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) coltot[c] = carry;
+}
+
+// colptr[0..k] = exclusive scan of coltot (k <= 256: one block of 256)
+__global__ void k_sel_colptr(const int64_t* __restrict__ coltot, int k, int64_t* __restrict__ colptr) {
+  __shared__ int64_t sm[33];
+  const int64_t v = threadIdx.x < k ? coltot[threadIdx.x] : 0;
+  int64_t tot;
+  const int64_t ex = block_exscan(v, sm, &tot);
+  if (threadIdx.x < k) colptr[threadIdx.x] = ex;
+  if (threadIdx.x == 0) colptr[k] = tot;
+}
+
+__global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                   int64_t row0, const ColSel* __restrict__ sel,
+                                                   const uint64_t* __restrict__ kthr,
+                                                   const int64_t* __restrict__ colptr,
+                                                   const int64_t* __restrict__ chunk_off, int64_t nchunks,
+                                                   int32_t* __restrict__ out_row, float* __restrict__ out_val) {
+  __shared__ int64_t sm[33];
+  const int c = blockIdx.y;
+  const ColSel s = sel[c];
+  const uint64_t ks = kthr[c];
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  int64_t off = colptr[c] + chunk_off[(int64_t)c * nchunks + blockIdx.x];
+  for (int64_t base = r0; base < r1; base += blockDim.x) {
+    const int64_t j = base + threadIdx.x;
+    float x = 0.f;
+    bool keep = false;
+    if (j < r1) {
+      x = __ldg(col + j);
+      if (x > 0.f) {
+        const int dg = sel_digit(x);
+        keep = dg > s.digit || (dg == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= ks);
+      }
+    }
+    int64_t tot;
+    const int64_t ex = block_exscan((int64_t)keep, sm, &tot);
+    if (keep) {
+      out_row[off + ex] = (int32_t)(row0 + j);
+      out_val[off + ex] = x;
+    }
+    off += tot;
+  }
+}
+
+}  // namespace esk

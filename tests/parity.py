@@ -1,0 +1,88 @@
+"""Comparison rules for GPU-vs-oracle parity (BJ:5, reading C15).
+
+* products (pre-clamp LS rows): per column c,
+      max_j |gpu[j,c] - ref[j,c]| <= PROD_TOL * max_j |ref[j,c]|
+* retained factor entries: per entry |gpu - ref| <= ENTRY_TOL * |ref| + TIE_TOL * max_j |ref[j,c]|
+  (the second term matters only for entries near zero, which are kept only
+  when a column keeps all its positives: t >= #positive or t unlimited)
+* retained support: identical, except swaps between entries whose oracle
+  values differ by <= TIE_TOL * max_j |ref[j,c]| (near-ties)
+* trajectory: |E_gpu - E_ref| <= TRAJ_TOL * E_ref per iteration.
+"""
+import numpy as np
+
+PROD_TOL = 1e-5
+ENTRY_TOL = 1e-5
+TIE_TOL = 1e-6
+TRAJ_TOL = 1e-3
+
+
+def coo_dense(shape, row, col, val):
+    F = np.zeros(shape, np.float64)
+    F[np.asarray(row, np.int64), np.asarray(col, np.int64)] = val
+    return F
+
+
+def check_products(gpu: np.ndarray, ref: np.ndarray, tol: float = PROD_TOL) -> float:
+    """Returns the worst column-relative error; asserts it is <= tol."""
+    scale = np.abs(ref).max(axis=0)
+    scale[scale == 0] = 1.0
+    err = (np.abs(gpu.astype(np.float64) - ref) / scale).max()
+    assert err <= tol, f"LS column-relative error {err:.3e} > {tol:.0e}"
+    return float(err)
+
+
+def check_canonical(row, col, k):
+    row, col = np.asarray(row), np.asarray(col)
+    key = col.astype(np.int64) * (1 << 32) + row
+    assert np.all(np.diff(key) > 0), "factor COO not in canonical (column, row) order"
+    assert col.min(initial=0) >= 0 and col.max(initial=0) < k
+
+
+def check_selection(gpu_F: np.ndarray, ref_F: np.ndarray, ref_ls: np.ndarray, t: int | None):
+    """gpu_F, ref_F dense factors after clamp + top-t; ref_ls the oracle's pre-clamp LS."""
+    assert np.all(gpu_F >= 0)
+    swaps = 0
+    worst = 0.0
+    for c in range(ref_F.shape[1]):
+        scale = max(np.abs(ref_ls[:, c]).max(), 1e-300)
+        g, r = gpu_F[:, c] > 0, ref_F[:, c] > 0
+        if t is not None:
+            assert g.sum() <= t
+        assert g.sum() == r.sum(), f"column {c}: {g.sum()} kept vs oracle {r.sum()}"
+        only_g = np.nonzero(g & ~r)[0]
+        only_r = np.nonzero(r & ~g)[0]
+        if len(only_g):
+            # every swap must be a near-tie around the oracle's threshold
+            thr = ref_F[r, c].min()
+            assert np.all(np.abs(ref_ls[only_g, c] - thr) <= TIE_TOL * scale + 1e-300), f"column {c}: non-tie swap"
+            assert np.all(np.abs(ref_ls[only_r, c] - thr) <= TIE_TOL * scale + 1e-300), f"column {c}: non-tie swap"
+            swaps += len(only_g)
+        both = g & r
+        if both.any():
+            rel = np.abs(gpu_F[both, c] - ref_F[both, c]) / (ref_F[both, c] + (TIE_TOL / ENTRY_TOL) * scale)
+            worst = max(worst, float(rel.max()))
+    assert worst <= ENTRY_TOL, f"retained entry relative error {worst:.3e} > {ENTRY_TOL:.0e}"
+    return swaps, worst
+
+
+def check_topt_property(ls: np.ndarray, F: np.ndarray, t: int | None):
+    """Selection validity on the GPU's own LS values (any size): exactly
+    min(t, #positive) kept per column, kept values are the LS values, every
+    kept value >= every dropped positive, ties at the threshold -> lower rows."""
+    for c in range(ls.shape[1]):
+        x = ls[:, c]
+        pos = x > 0
+        kept = F[:, c] > 0
+        npos = int(pos.sum())
+        want = npos if t is None else min(t, npos)
+        assert kept.sum() == want, f"column {c}: kept {kept.sum()} want {want}"
+        assert np.all(F[kept, c] == x[kept])
+        dropped = pos & ~kept
+        if kept.any() and dropped.any():
+            kmin = x[kept].min()
+            assert kmin >= x[dropped].max()
+            tie_dropped = np.nonzero(dropped & (x == kmin))[0]
+            tie_kept = np.nonzero(kept & (x == kmin))[0]
+            if len(tie_dropped):
+                assert tie_kept.max() < tie_dropped.min(), f"column {c}: tie not broken toward lower rows"

@@ -1,0 +1,309 @@
+"""GPU parity: libesnmf.so (through the C ABI) against the fp64 oracle.
+
+Per-half-step checks start from the same state (the GPU's fp32 factor is read
+back and handed to the oracle), following reading C15:
+products within 1e-5 column-relative, retained entries within 1e-5 relative,
+supports identical except near-ties; trajectories within 1e-3 relative in E.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_1510_05237_b200 import ESNMF, ESNMF_SIDE_U, ESNMF_SIDE_V, ESNMFError
+from parity import (TRAJ_TOL, check_canonical, check_products, check_selection, check_topt_property,
+                    coo_dense)
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+TINY, MEDIUM, LARGE = synth.CONFIGS["tiny"], synth.CONFIGS["medium"], synth.CONFIGS["large"]
+
+
+def solver(cfg, g, t="cfg", k=None, **kw):
+    return ESNMF(cfg.n, cfg.m, k or cfg.k, cfg.t if t == "cfg" else t, g, seed=cfg.seed, **kw)
+
+
+def dense_U(s, n, k):
+    r, c, v = s.get_U()
+    check_canonical(r, c, k)
+    return coo_dense((n, k), r, c, v)
+
+
+def dense_V(s, m, k):
+    r, c, v = s.get_V()
+    check_canonical(r, c, k)
+    return coo_dense((m, k), r, c, v)
+
+
+def half_step_parity(s, g, n, m, k, t, side):
+    """Run one GPU half-step from the GPU's current state and compare with the oracle."""
+    if side == ESNMF_SIDE_V:
+        F = dense_U(s, n, k)
+        ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], F, t)
+        s.half_step(ESNMF_SIDE_V)
+        _, ls = s.get_ls(ESNMF_SIDE_V)
+        out = dense_V(s, m, k)
+    else:
+        F = dense_V(s, m, k)
+        ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], F, t)
+        s.half_step(ESNMF_SIDE_U)
+        _, ls = s.get_ls(ESNMF_SIDE_U)
+        out = dense_U(s, n, k)
+    err = check_products(ls, ref["LS"])
+    swaps, worst = check_selection(out, ref["F"], ref["LS"], t)
+    check_topt_property(ls, out, t)
+    return err, swaps, worst
+
+
+# ------------------------------------------------------------------ basics
+
+def test_u0_bitwise_equal_to_oracle():
+    g = synth.generate(TINY)
+    s = solver(TINY, g)
+    U = dense_U(s, TINY.n, TINY.k)
+    assert np.array_equal(U.astype(np.float32), oracle.u0(TINY.n, TINY.k, TINY.seed))
+    assert np.count_nonzero(U) == TINY.n * TINY.k
+
+
+def test_user_u0_is_used():
+    g = synth.generate(TINY)
+    U0 = np.random.default_rng(1).random((TINY.n, TINY.k)).astype(np.float32) + 0.01
+    s = solver(TINY, g, U0=U0)
+    assert np.array_equal(dense_U(s, TINY.n, TINY.k).astype(np.float32), U0)
+
+
+def test_gram_matches_oracle():
+    g = synth.generate(TINY)
+    s = solver(TINY, g)
+    G, eps = s.get_gram(ESNMF_SIDE_V)
+    Gr = oracle.gram(oracle.u0(TINY.n, TINY.k, TINY.seed).astype(np.float64))
+    assert np.allclose(G, Gr, rtol=1e-13, atol=0)
+    assert np.array_equal(G, G.T)
+    _, eps_r = oracle.cholesky(Gr)
+    assert eps == pytest.approx(eps_r, rel=1e-13)
+
+
+@pytest.mark.parametrize("cfg", [TINY, MEDIUM], ids=["tiny", "medium"])
+def test_first_iteration_half_steps(cfg):
+    g = synth.generate(cfg)
+    s = solver(cfg, g)
+    half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_V)
+    half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_U)
+
+
+@pytest.mark.parametrize("cfg,warm", [(TINY, 7), (MEDIUM, 6)], ids=["tiny", "medium"])
+def test_late_state_half_steps(cfg, warm):
+    g = synth.generate(cfg)
+    s = solver(cfg, g)
+    s.iterate(warm)
+    for _ in range(2):
+        half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_V)
+        half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_U)
+
+
+# ------------------------------------------------------------- trajectories
+
+def golden(tag):
+    path = os.path.join(HERE, "golden", f"traj_{tag}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    return json.load(open(path))
+
+
+def check_trajectory(s, gold):
+    recs = s.records()
+    assert len(recs) == len(gold["records"])
+    for a, b in zip(recs, gold["records"]):
+        assert abs(a["E"] - b["E"]) <= TRAJ_TOL * b["E"], (a["it"], a["E"], b["E"])
+        assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"], a["it"]
+        assert a["dead_u"] == b["dead_u"] and a["dead_v"] == b["dead_v"]
+        assert a["R"] >= 0
+    return recs
+
+
+@pytest.mark.parametrize("tag,cfg", [("tiny", TINY), ("medium", MEDIUM)])
+def test_trajectory_matches_golden(tag, cfg):
+    gold = golden(tag)
+    g = synth.generate(cfg)
+    s = solver(cfg, g)
+    s.iterate(cfg.iters)
+    recs = check_trajectory(s, gold)
+    assert s.error() == recs[-1]["E"] and s.residual() == recs[-1]["R"]
+
+
+@pytest.mark.parametrize("t", synth.SWEEP_T, ids=[str(t) for t in synth.SWEEP_T])
+def test_sweep_trajectory(t):
+    gold = golden(f"sweep_t{'inf' if t is None else t}")
+    g = synth.generate(MEDIUM)
+    s = solver(MEDIUM, g, t=t)
+    s.iterate(MEDIUM.iters)
+    check_trajectory(s, gold)
+
+
+def test_tiny_trajectory_live_oracle_R():
+    """R per iteration against a live oracle run (same U_0), 1e-3 relative."""
+    g = synth.generate(TINY)
+    r = oracle.run(g, TINY.k, TINY.t, 10, seed=TINY.seed)
+    s = solver(TINY, g)
+    s.iterate(10)
+    for a, b in zip(s.records(), r["records"]):
+        assert abs(a["R"] - b["R"]) <= 1e-3 * b["R"]
+
+
+def test_deterministic_bitwise():
+    g = synth.generate(TINY)
+    outs = []
+    for _ in range(2):
+        s = solver(TINY, g)
+        s.iterate(5)
+        outs.append((s.records(), s.get_U(), s.get_V()))
+    (r1, u1, v1), (r2, u2, v2) = outs
+    assert r1 == r2
+    for a, b in zip(u1 + v1, u2 + v2):
+        assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------- edge cases
+
+def small_inputs(A):
+    A = np.asarray(A, np.float32)
+
+    def csr(D):
+        ptr, idx, val = [0], [], []
+        for r in D:
+            nz = np.nonzero(r)[0]
+            idx += list(nz)
+            val += list(r[nz])
+            ptr.append(len(idx))
+        return np.array(ptr, np.int64), np.array(idx, np.int32), np.array(val, np.float32)
+
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    return dict(n=A.shape[0], m=A.shape[1], a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+
+
+@pytest.mark.parametrize("t", [1, 3, 37, 5000, None], ids=["t1", "t3", "t37", "t_ge_rows", "unlimited"])
+@pytest.mark.parametrize("k", [1, 4, 33])
+def test_edge_t_and_k(t, k):
+    g = synth.generate(TINY)
+    s = ESNMF(TINY.n, TINY.m, k, t, g, seed=3)
+    for _ in range(2):
+        half_step_parity(s, g, TINY.n, TINY.m, k, t, ESNMF_SIDE_V)
+        half_step_parity(s, g, TINY.n, TINY.m, k, t, ESNMF_SIDE_U)
+
+
+def test_exact_ties_break_to_lower_rows():
+    """Duplicated documents give identical LS rows: the kept set must take the lower rows."""
+    rng = np.random.default_rng(11)
+    base = (rng.random((60, 8)) < 0.3) * rng.integers(1, 5, (60, 8))
+    A = np.concatenate([base] * 5, axis=1)       # docs j, j+8, j+16, ... identical
+    A[:, 0] += 1                                   # no empty doc
+    inp = small_inputs(A)
+    n, m = A.shape
+    for t in (3, 7, 12):
+        s = ESNMF(n, m, 3, t, inp, seed=5)
+        half_step_parity(s, inp, n, m, 3, t, ESNMF_SIDE_V)
+        half_step_parity(s, inp, n, m, 3, t, ESNMF_SIDE_U)
+
+
+def test_without_transpose_input():
+    """A^T built on the device when the caller passes only CSR(A)."""
+    g = synth.generate(TINY)
+    s1 = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, use_at=False)
+    s2 = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g)
+    s1.iterate(3)
+    s2.iterate(3)
+    assert s1.records() == s2.records()
+
+
+def test_planted_fixed_point_on_gpu():
+    rng = np.random.default_rng(4)
+    n, m, k, t = 40, 30, 3, 6
+    Us, Vs = np.zeros((n, k)), np.zeros((m, k))
+    for c in range(k):
+        Us[rng.choice(n, t, replace=False), c] = rng.integers(1, 5, t)
+        Vs[rng.choice(m, t, replace=False), c] = rng.integers(1, 5, t)
+    A = Us @ Vs.T
+    A[:, ~A.any(axis=0)] = 0
+    inp = small_inputs(A)
+    s = ESNMF(n, m, k, t, inp)
+    row, col = np.nonzero(Us.T)[1], np.nonzero(Us.T)[0]
+    s.set_factor(ESNMF_SIDE_U, row, col, Us[row, col])
+    s.iterate(1)
+    V = dense_V(s, m, k)
+    U = dense_U(s, n, k)
+    assert np.array_equal(V > 0, Vs > 0) and np.array_equal(U > 0, Us > 0)
+    assert np.allclose(V, Vs, rtol=1e-5) and np.allclose(U, Us, rtol=1e-5)
+    rec = s.records()[0]
+    assert rec["E"] < 1e-3 and rec["R"] < 1e-5
+
+
+def test_errors_are_reported():
+    g = synth.generate(TINY)
+    with pytest.raises(ESNMFError) as e:
+        ESNMF(TINY.n, TINY.m, 0, 5, g)
+    assert e.value.status == 1
+    with pytest.raises(ESNMFError):
+        ESNMF(TINY.n, TINY.m, 300, 5, g)
+    bad = dict(g)
+    col = g["a_col"].copy()
+    s0, s1 = g["a_ptr"][0], g["a_ptr"][1]
+    if s1 - s0 >= 2:
+        col[s0], col[s0 + 1] = col[s0 + 1], col[s0]
+    else:
+        col[0] = TINY.m + 5
+    bad["a_col"] = col
+    with pytest.raises(ESNMFError) as e:
+        ESNMF(TINY.n, TINY.m, 4, 5, bad, use_at=False)
+    assert e.value.status == 1 and "malformed" in str(e.value)
+    bad = dict(g)
+    v = g["a_val"].copy()
+    v[3] = -1.0
+    bad["a_val"] = v
+    with pytest.raises(ESNMFError):
+        ESNMF(TINY.n, TINY.m, 4, 5, bad, use_at=False)
+    s = solver(TINY, g)
+    with pytest.raises(ESNMFError) as e:
+        s.residual()
+    assert e.value.status == 7
+
+
+# ---------------------------------------------------- full size, sampled
+
+@pytest.mark.slow
+def test_large_sampled_parity():
+    """Large at full size, the bench's launch configuration: sampled LS rows vs
+    the oracle computed row by row, and the selection property on every column."""
+    import torch
+
+    cfg = LARGE
+    gd = synth.generate_device(cfg)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, gd, seed=cfg.seed)
+    s.iterate(2)
+    g = synth.generate(cfg)
+    rng = np.random.default_rng(0)
+    for side in (ESNMF_SIDE_V, ESNMF_SIDE_U):
+        if side == ESNMF_SIDE_V:
+            F = dense_U(s, cfg.n, cfg.k)
+            ptr, idx, val, rows = g["at_ptr"], g["at_col"], g["at_val"], cfg.m
+        else:
+            F = dense_V(s, cfg.m, cfg.k)
+            ptr, idx, val, rows = g["a_ptr"], g["a_col"], g["a_val"], cfg.n
+        L, _ = oracle.cholesky(oracle.gram(F))
+        s.half_step(side)
+        _, ls = s.get_ls(side)
+        sel = np.sort(rng.choice(rows, 1500, replace=False))
+        if side == ESNMF_SIDE_U:
+            sel[:20] = np.arange(20)            # include the longest (head) term rows
+            sel = np.unique(sel)
+        ref = oracle.solve_rows(L, oracle.spmm_rows(sel, ptr, idx, val, F))
+        scale = np.abs(ls).max(axis=0).astype(np.float64)
+        err = (np.abs(ls[sel].astype(np.float64) - ref) / scale).max()
+        assert err <= 1e-5, err
+        out = dense_V(s, cfg.m, cfg.k) if side == ESNMF_SIDE_V else dense_U(s, cfg.n, cfg.k)
+        check_topt_property(ls, out, cfg.t)
+    del gd
+    torch.cuda.empty_cache()
