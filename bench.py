@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- enforced-sparse ALS iterations/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl ours|reference]
+
+A step is one full ALS iteration of the hot path (V side,
+U side, residual, error) on the Large config (BJ:9) in steady state, inputs
+resident in HBM.  Prints ONE JSON line on rank 0.  For N > 1 (torchrun) every
+rank runs an independent replica of the workload.
+
+--impl reference times the fp64 oracle (oracle/) on the host cores on a
+bounded, row-strided sample of the same workload (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "enforced-sparse ALS iterations/sec and achieved HBM GB/s vs ~8 TB/s"   # BASELINE.json metric
+UNIT = "iterations/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="large")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU time of the cpu_baseline sample")
+    return p.parse_args()
+
+
+def measured_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return dict(hbm_gbs=d["hbm_gbs"], src="MEASURED_PEAKS.json (measured copy)")
+    return dict(hbm_gbs=6650.0, src="fallback B200_PROFILING.md")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = None
+        self.p = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50", "-i", str(self.idx)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.15)
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# per-phase algorithmic bytes per launch (8 B per stored entry of
+# A or A^T per side, plus the row pointers)
+def algorithmic_bytes(phase: str, cfg) -> float | None:
+    if phase == "V.spmm":
+        return 8.0 * cfg.nnz + 8.0 * (cfg.m + 1)
+    if phase == "U.spmm":
+        return 8.0 * cfg.nnz + 8.0 * (cfg.n + 1)
+    if phase == "V.select":
+        return 4.0 * cfg.k * cfg.m      # one read of the LS rows
+    if phase == "U.select":
+        return 4.0 * cfg.k * cfg.n
+    return None
+
+
+def oracle_sample_step(g, U, V, cfg, frac: float) -> tuple[float, float]:
+    """One oracle iteration on a row-strided sample: the V half-step for every
+    (1/frac)-th document and the U half-step for every (1/frac)-th term, with the
+    full k x k Gram + Cholesky.  Returns (measured seconds, extrapolated seconds
+    for the full iteration)."""
+    import numpy as np
+
+    import oracle
+
+    def sub(ptr, idx, val, rows):
+        step = max(1, int(round(1.0 / frac)))
+        sel = np.arange(0, rows, step)
+        lens = ptr[sel + 1] - ptr[sel]
+        sptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        take = np.concatenate([np.arange(ptr[r], ptr[r + 1]) for r in sel]) if len(sel) else np.zeros(0, np.int64)
+        return sptr, idx[take], val[take], len(sel) / rows
+
+    tot = 0.0
+    extrap = 0.0
+    for (ptr, idx, val, rows, F) in ((g["at_ptr"], g["at_col"], g["at_val"], cfg.m, U),
+                                     (g["a_ptr"], g["a_col"], g["a_val"], cfg.n, V)):
+        sp, si, sv, f = sub(ptr, idx, val, rows)
+        t0 = time.perf_counter()
+        G = oracle.gram(F)
+        L, _ = oracle.cholesky(G)
+        t1 = time.perf_counter()
+        Y = oracle.spmm(sp, si, sv, F)
+        LS = oracle.solve_rows(L, Y)
+        oracle.clamp_top_t(LS, cfg.t)
+        t2 = time.perf_counter()
+        tot += t2 - t0
+        extrap += (t1 - t0) + (t2 - t1) / f
+    return tot, extrap
+
+
+def cpu_baseline(cfg, g_host, U, V, seconds: float) -> dict:
+    # calibrate the sample size so the measured CPU work is ~`seconds`
+    frac = 0.002
+    meas, ext = oracle_sample_step(g_host, U, V, cfg, frac)
+    if meas < seconds / 4:
+        frac = min(1.0, frac * seconds / max(meas, 1e-3))
+        meas, ext = oracle_sample_step(g_host, U, V, cfg, frac)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": 1.0 / ext, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"fp64 oracle, one iteration on a row-strided {frac:.3%} sample of documents (V side) and "
+                      f"terms (U side) of {cfg.name}, full k x k Gram + Cholesky; {meas:.1f} s measured, "
+                      f"extrapolated linearly in rows to {ext:.1f} s per full iteration"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_1510_05237_b200 import ESNMF
+
+    world, rank, local = dist_setup()
+    cfg = synth.CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    g = synth.generate_device(cfg, device=dev)
+    torch.cuda.synchronize()
+    # a dedicated (non-default) stream: the library enqueues on it and the
+    # timing events below are recorded on it too
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, stream=stream.cuda_stream, device=local)
+    s.iterate(args.warmup)
+    torch.cuda.synchronize()
+    s.profile(True)
+    l0 = s.info()["launches"]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record(stream)
+    s.iterate(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    launches = s.info()["launches"] - l0
+    phases = s.phase_times()
+    s.profile(False)
+    recs = s.records()
+    assert all(np.isfinite(r["E"]) for r in recs)
+    value = world * args.steps / (ms / 1e3)
+
+    # roofline of the dominant phase
+    peaks = measured_peaks()
+    dom = max(phases.items(), key=lambda kv: kv[1][1])
+    name, (calls, pms) = dom
+    per_launch_ms = pms / max(calls, 1)
+    ab = algorithmic_bytes(name, cfg)
+    roof = None
+    if ab is not None:
+        ach = ab / (per_launch_ms / 1e3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_src": peaks["src"],
+                "alg_bytes_per_launch": ab, "ms_per_launch": round(per_launch_ms, 4),
+                "share_of_step": round(pms / ms, 4)}
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            tr = json.load(open(tpath)).get(f"{cfg.name}:{name}")
+            if tr:
+                roof["traffic"] = tr["bytes_per_launch"]
+                roof["traffic_src"] = tr["source"]
+    phase_table = {k: {"calls": c, "ms_per_call": round(v / max(c, 1), 4), "share": round(v / ms, 4)}
+                   for k, (c, v) in phases.items() if c}
+    # whole-iteration algorithmic bytes: 16 nnz + 8 (n + m + 2) + 32 k t
+    it_bytes = 16.0 * cfg.nnz + 8.0 * (cfg.n + cfg.m + 2) + 32.0 * cfg.k * (cfg.t or cfg.m)
+    it_gbs = it_bytes / (ms / 1e3 / args.steps) / 1e9
+
+    # e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = {k: torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True) for k in ("a_ptr", "a_col", "a_val")}
+        for k in host:
+            host[k].copy_(g[k])
+        del g
+        torch.cuda.empty_cache()
+        times, d2h = [], 0
+        for _ in range(2):
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            e = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, host, seed=cfg.seed, stream=stream.cuda_stream, device=local)
+            e.iterate(cfg.iters)
+            rr = e.records()
+            u = e.get_U()
+            v = e.get_V()
+            t1 = time.perf_counter()
+            e.close()
+            times.append(max_over_ranks(t1 - t0, world))
+            d2h = 64 * len(rr) + sum(x.nbytes for x in u) + sum(x.nbytes for x in v)
+        best = min(times)
+        h2d = sum(x.numel() * x.element_size() for x in host.values())
+        e2e = {"value": round(world * cfg.iters / best, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d / cfg.iters), "d2h_bytes_per_step": int(d2h / cfg.iters),
+               "job": f"esnmf_create(host CSR(A), A^T built on device) + esnmf_iterate({cfg.iters}) + records + "
+                      f"get_U + get_V; best of 2 jobs, {best:.3f} s",
+               "unit_note": "iterations/s of the whole job; bytes per step = job bytes / iterations"}
+    else:
+        del g
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        g_host = synth.generate(cfg)
+        r_, c_, v_ = s.get_U()
+        U = np.zeros((cfg.n, cfg.k))
+        U[r_, c_] = v_
+        r_, c_, v_ = s.get_V()
+        V = np.zeros((cfg.m, cfg.k))
+        V[r_, c_] = v_
+        cpu = cpu_baseline(cfg, g_host, U, V, args.cpu_seconds)
+    s.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "nnz": cfg.nnz, "k": cfg.k, "t": cfg.t,
+                       "zipf_s": cfg.s, "sigma": cfg.sigma, "seed": cfg.seed,
+                       "state": f"steady state after {args.warmup} warm-up iterations from U0",
+                       "l2": "inputs larger than L2 (A and A^T 1.2 GB each), no flush",
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+            "iteration_gbs_algorithmic": round(it_gbs, 1),
+            "roofline": roof,
+            "phases": phase_table,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "E_last": recs[-1]["E"], "R_last": recs[-1]["R"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference arm: the fp64 oracle on the host cores, bounded samples."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    g = synth.generate(cfg)
+    U = oracle.u0(cfg.n, cfg.k, cfg.seed).astype(np.float64)
+    V = np.zeros((cfg.m, cfg.k))
+    rng = np.random.default_rng(0)
+    V[rng.integers(0, cfg.m, cfg.k * (cfg.t or 1)), np.repeat(np.arange(cfg.k), cfg.t or 1)] = 1.0
+    budget = 150.0 / max(1, args.steps + args.warmup)   # seconds per step: whole run within a few minutes
+    meas, ext = oracle_sample_step(g, U, V, cfg, 0.002)
+    frac = min(1.0, 0.002 * budget / max(meas, 1e-3))
+    for _ in range(args.warmup):
+        oracle_sample_step(g, U, V, cfg, frac)
+    exts, meass = [], []
+    for _ in range(args.steps):
+        m_, e_ = oracle_sample_step(g, U, V, cfg, frac)
+        meass.append(m_)
+        exts.append(e_)
+    per_it = statistics.mean(exts)
+    value = 1.0 / per_it
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_it * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "nnz": cfg.nnz, "k": cfg.k, "t": cfg.t},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: fp64 oracle iteration on a row-strided {frac:.3%} sample of "
+                                   f"documents and terms, full Gram + Cholesky, extrapolated linearly in rows; "
+                                   f"{statistics.mean(meass):.2f} s measured per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

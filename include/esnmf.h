@@ -173,9 +173,26 @@ typedef struct {
   int64_t iterations;       /* completed iterations */
   int64_t device_bytes;     /* device memory owned by the handle */
   double normA2;            /* ||A||_F^2 */
+  int64_t launches;         /* CUDA kernels enqueued by this handle so far */
 } esnmf_info;
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);
+
+/* Per-phase device timing with CUDA events on the handle's stream (the same
+ * stream the kernels run on).  esnmf_profile(h, 1) clears the accumulators and
+ * starts recording an event pair around every phase of every later half-step;
+ * esnmf_profile(h, 0) stops.  esnmf_phase_times synchronises and returns one
+ * entry per phase: "<side>.<phase>" with side V or U and phase one of gram,
+ * solve, form_z, spmm, select, rowview; plus "iter.metrics" (R, E, next Gram).
+ * ETRUNC if cap < *count. */
+typedef struct {
+  char name[32];
+  int64_t calls;  /* launches of the phase since profiling started */
+  double ms;      /* summed device time, milliseconds */
+} esnmf_phase;
+
+esnmf_status esnmf_profile(esnmf_t* h, int32_t enable);
+esnmf_status esnmf_phase_times(esnmf_t* h, int64_t cap, int64_t* count, esnmf_phase* out);
 
 /* Free all device memory of the handle (NULL is a no-op). */
 void esnmf_destroy(esnmf_t* h);

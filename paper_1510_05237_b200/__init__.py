@@ -23,6 +23,8 @@ from .esnmf import (  # noqa: F401
     esnmf_iterate,
     esnmf_options_init,
     esnmf_partition_rows,
+    esnmf_phase_times,
+    esnmf_profile,
     esnmf_records,
     esnmf_residual,
     esnmf_set_factor,

@@ -26,6 +26,8 @@
 #include "k_select.cuh"
 #include "k_solve.cuh"
 #include "k_spmm.cuh"
+#include "k_spmm_docs.cuh"
+#include "k_spmm_terms.cuh"
 
 using namespace esk;
 
@@ -117,9 +119,24 @@ struct esnmf {
   int ucur = 0;
   Factor V;
   float* Z = nullptr;
+  int zs = 0;                   // V-side Z row stride (floats), term-indexed rows
+  int32_t* zlist = nullptr;     // terms whose Z rows were written last
+  int64_t* zcount = nullptr;
+  uint32_t* tbits = nullptr;    // active-term bitmap of U
   double* W = nullptr;
   double* gram_partial = nullptr;
   double* sweep_scratch = nullptr;
+  // row-CSR of V for the U side
+  uint32_t* vbits = nullptr;  // [ceil(m/32)]
+  uint64_t* vmap = nullptr;   // [m]
+  int2* vent = nullptr;       // [V.cap]
+  int64_t* vrptr = nullptr;   // [V.cap_rows + 1]
+  int64_t* vcur = nullptr;    // [V.cap_rows + 1]
+  int64_t* vscan = nullptr;   // scan block sums
+  uint32_t* vmax = nullptr;   // bits of max(V) (fixed-point scale of the U side)
+  double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
+  int num_sms = 148;
+  int smem_optin = 227 * 1024;
   int* flags = nullptr;  // [0] singular, [1] validation, [2] U0 invalid
   double* red = nullptr;
   int64_t red_cap = 0;
@@ -129,6 +146,17 @@ struct esnmf {
   int64_t rec_cap = 0, nrec = 0;
   double normA2 = 0;
   bool gramU_valid = false;
+  int64_t nlaunch = 0;  // kernels enqueued by this handle (esnmf_get_info)
+  // per-phase CUDA-event profiling (esnmf_profile / esnmf_phase_times)
+  bool prof_on = false;
+  struct ProfRec {
+    int id;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[16] = {0};
+  int64_t prof_calls[16] = {0};
   std::vector<void*> allocs;
   int64_t bytes = 0;
 
@@ -144,6 +172,8 @@ struct esnmf {
   }
   ~esnmf() {
     if (stream) cudaStreamSynchronize(stream);
+    for (auto& r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -153,14 +183,64 @@ namespace {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// ---------------------------------------------------------------- profiling
+enum PhaseId { kVGram, kVSolve, kVFormZ, kVSpmm, kVSelect, kVRows, kUGram, kUSolve, kUFormZ, kUSpmm, kUSelect, kURows,
+               kMetrics, kNumPhases };
+const char* const kPhaseNames[kNumPhases] = {"V.gram",   "V.solve",  "V.form_z", "V.spmm",   "V.select",
+                                             "V.rowview", "U.gram",  "U.solve",  "U.form_z", "U.spmm",
+                                             "U.select", "U.rowview", "iter.metrics"};
+
+cudaEvent_t pool_event(esnmf_t* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// RAII event pair around one phase, recorded on the handle's stream
+struct Phase {
+  esnmf_t* h;
+  int id;
+  cudaEvent_t a = nullptr;
+  Phase(esnmf_t* h_, int id_) : h(h_), id(id_) {
+    if (h->prof_on) {
+      a = pool_event(h);
+      ck(cudaEventRecord(a, h->stream), "cudaEventRecord");
+    }
+  }
+  ~Phase() {
+    if (h->prof_on && a) {
+      cudaEvent_t b = pool_event(h);
+      cudaEventRecord(b, h->stream);
+      h->prof.push_back({id, a, b});
+    }
+  }
+};
+
+void prof_collect(esnmf_t* h) {
+  for (auto& r : h->prof) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+    h->prof_ms[r.id] += ms;
+    h->prof_calls[r.id] += 1;
+    h->ev_pool.push_back(r.a);
+    h->ev_pool.push_back(r.b);
+  }
+  h->prof.clear();
+}
+
 unsigned col_grid_x(int64_t maxcol) { return (unsigned)std::min<int64_t>(std::max<int64_t>(1, ceil_div(maxcol, 256)), 2048); }
 
 void launch_scan_inplace(esnmf_t* h, int64_t* a, int64_t n, int64_t* total) {
   int64_t nb = ceil_div(n, kScanBlock);
   int64_t* bs = h->alloc<int64_t>(nb);  // create-time only
-  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
-  k_scan_small<<<1, 1024, 0, h->stream>>>(bs, nb, total);
-  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
+  ++h->nlaunch; k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
+  ++h->nlaunch; k_scan_small<<<1, 1024, 0, h->stream>>>(bs, nb, total);
+  ++h->nlaunch; k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(a, n, bs);
   CKL("scan");
 }
 
@@ -189,8 +269,8 @@ void factor_alloc(esnmf_t* h, Factor& f, int64_t rows, int64_t cap) {
 void factor_clear(esnmf_t* h, Factor& f) {
   if (!f.has) return;
   dim3 g(col_grid_x(f.maxcol), h->k);
-  k_clear_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, f.dense, h->kpad);
-  k_reset_rowmap<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, f.rowmap);
+  ++h->nlaunch; k_clear_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, f.dense, h->kpad);
+  ++h->nlaunch; k_reset_rowmap<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, f.rowmap);
   CKL("factor_clear");
   f.has = false;
 }
@@ -199,13 +279,13 @@ void factor_clear(esnmf_t* h, Factor& f) {
 void factor_build_rows(esnmf_t* h, Factor& f, int64_t maxcol) {
   f.maxcol = maxcol;
   dim3 g(col_grid_x(maxcol), h->k);
-  k_mark_rows<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap);
+  ++h->nlaunch; k_mark_rows<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap);
   const int64_t nb = ceil_div(f.rows, kRowBlock);
   int64_t* bc = reinterpret_cast<int64_t*>(h->red);  // scratch (nb <= red_cap)
-  k_rows_count<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc);
-  k_scan_small<<<1, 1024, 0, h->stream>>>(bc, nb, f.n_active);
-  k_rows_assign<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc, f.active);
-  k_scatter_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad);
+  ++h->nlaunch; k_rows_count<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc);
+  ++h->nlaunch; k_scan_small<<<1, 1024, 0, h->stream>>>(bc, nb, f.n_active);
+  ++h->nlaunch; k_rows_assign<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc, f.active);
+  ++h->nlaunch; k_scatter_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad);
   CKL("factor_build_rows");
   f.has = true;
 }
@@ -219,62 +299,168 @@ void gram(esnmf_t* h, const Factor& f, double* G) {
   int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 256)));
   int64_t seglen = std::max<int64_t>(1, ceil_div(f.maxcol, S));
   dim3 g(k, (unsigned)S);
-  k_gram_partial<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
+  ++h->nlaunch; k_gram_partial<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
                                             h->gram_partial);
-  k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(h->gram_partial, (int)S, k, G);
-  k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
+  ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(h->gram_partial, (int)S, k, G);
+  ++h->nlaunch; k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
   CKL("gram");
 }
 
-void sweep(esnmf_t* h, const double* G, double* eps) {
+template <int JB, bool PACKED>
+void sweep_launch(esnmf_t* h, const double* G, double* eps) {
   const bool glob = h->k > 224;
-  k_sweep_inverse<<<1, 1024, sweep_smem_bytes(h->k, glob), h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags,
-                                                                         glob ? h->sweep_scratch : nullptr);
+  const size_t smem = sweep_smem_bytes(h->k, glob);
+  auto kern = k_sweep_inverse<JB, PACKED>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ++h->nlaunch;
+  kern<<<1, 1024, smem, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, glob ? h->sweep_scratch : nullptr);
   CKL("sweep_inverse");
 }
 
+void sweep(esnmf_t* h, const double* G, double* eps) {
+  const int JB = (h->k + 31) / 32;
+  const bool packed = sweep_packed(h->k);
+  if (JB <= 4) {  // register-resident matrix
+    ++h->nlaunch;
+    switch (JB) {
+      case 1: k_sweep_regs<1><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
+      case 2: k_sweep_regs<2><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
+      case 3: k_sweep_regs<3><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
+      default: k_sweep_regs<4><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
+    }
+    CKL("sweep_regs");
+    return;
+  }
+  switch (JB) {
+    case 5: packed ? sweep_launch<5, true>(h, G, eps) : sweep_launch<5, false>(h, G, eps); break;
+    case 6: sweep_launch<6, true>(h, G, eps); break;
+    case 7: sweep_launch<7, true>(h, G, eps); break;
+    default: sweep_launch<8, true>(h, G, eps); break;
+  }
+}
+
+// V side: Z = U W written term-indexed (stride zs); the rows written by the
+// previous call are zeroed first, and the active-term bitmap is rebuilt.
 void form_z(esnmf_t* h, const Factor& f) {
+  const int zq = h->zs / 4;
+  ++h->nlaunch;
+  k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+      h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq);
   const int CJ = (h->kpad + 31) / 32;
   unsigned grid = grid_for(f.cap_rows, 8, 148 * 64);
-#define ESNMF_FZ(cj) \
-  case cj: k_form_z<cj><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z); break;
+#define ESNMF_FZ(cj)                                                                                          \
+  case cj:                                                                                                    \
+    ++h->nlaunch;                                                                                             \
+    k_form_z<cj><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->zs, h->W, h->Z, \
+                                              h->zlist, h->zcount);                                           \
+    break;
   switch (CJ) {
     ESNMF_FZ(1) ESNMF_FZ(2) ESNMF_FZ(3) ESNMF_FZ(4) ESNMF_FZ(5) ESNMF_FZ(6) ESNMF_FZ(7) ESNMF_FZ(8)
     default: fail(ESNMF_EINVAL, "k too large");
   }
 #undef ESNMF_FZ
+  CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
+  ++h->nlaunch;
+  k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits);
   CKL("form_z");
+}
+
+// V-side lane-group layout: G lanes per gathered row, CPL float4 per lane
+void docs_layout(int kpad, int& G, int& CPL) {
+  const int KQ = kpad / 4;
+  CPL = 1;
+  if (KQ <= 4) G = 4;
+  else if (KQ <= 8) G = 8;
+  else if (KQ <= 16) G = 16;
+  else if (KQ <= 32) G = 32;
+  else { G = 32; CPL = 2; }
 }
 
 template <int G, int CPL>
 void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
+  (void)rowmap;
   Side& sd = h->side[s];
-  const int KQ = h->kpad / 4;
   const float4* Z4 = reinterpret_cast<const float4*>(h->Z);
-  if (s == ESNMF_SIDE_V) {
-    const int64_t ntiles = ceil_div(sd.rows, 32);
-    unsigned grid = (unsigned)std::min<int64_t>(ntiles, 148 * 8);
-    size_t smem = sizeof(float) * h->kpad * 33;
-    k_spmm_tiled<G, CPL><<<grid, 256, smem, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, rowmap, Z4, KQ, h->k, sd.X,
-                                                         sd.ldx);
-  } else {
-    unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.nitems, 8), 148 * 8);
-    k_spmm_items<G, CPL><<<grid, 256, 0, h->stream>>>(sd.items, sd.nitems, sd.item_slot, sd.T.ent, rowmap, Z4, KQ,
-                                                      h->k, h->kpad, sd.X, sd.ldx, sd.partial);
-    if (sd.nsplit > 0)
-      k_spmm_combine<<<grid_for(sd.nsplit, 8, 4096), 256, 0, h->stream>>>(sd.splits, sd.nsplit, sd.partial, h->k,
-                                                                          h->kpad, sd.X, sd.ldx);
-  }
+  const int64_t nwords = ceil_div(h->n, 32);
+  const bool smem_bits = nwords * 4 <= 96 * 1024;
+  const size_t smem = smem_bits ? nwords * 4 : 0;
+  auto kern = k_spmm_docs<G, CPL>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32), (int64_t)h->num_sms);
+  ++h->nlaunch;
+  kern<<<grid, kDocThreads, smem, h->stream>>>(
+      sd.T.ptr, sd.T.ent, sd.rows, h->tbits, smem_bits ? (int)nwords : 0, Z4, h->k, sd.X, sd.ldx);
   CKL("spmm");
 }
 
+// U side: paper order, fp64 (A V) from the sparse V rows, then (A V) W
+template <int CQ>
+void spmm_terms_launch(esnmf_t* h) {
+  Side& sd = h->side[ESNMF_SIDE_U];
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.nitems, 8), (int64_t)h->num_sms * 8);
+  auto* part = reinterpret_cast<unsigned long long*>(sd.partial);
+  ++h->nlaunch;
+  k_spmm_terms<CQ><<<grid, 256, 0, h->stream>>>(sd.items, sd.nitems, sd.item_slot, sd.T.ent, h->rsum, h->vbits,
+                                                h->vmap, h->vent, h->vmax, h->W, h->k, h->kpad, sd.X, sd.ldx, part);
+  if (sd.nsplit > 0) {
+    ++h->nlaunch;
+    k_terms_combine<CQ><<<grid_for(sd.nsplit, 8, 4096), 256, 0, h->stream>>>(sd.splits, sd.nsplit, part, h->rsum,
+                                                                             h->vmax, h->W, h->k, h->kpad, sd.X,
+                                                                             sd.ldx);
+  }
+  CKL("spmm_terms");
+}
+
 void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
+  if (s == ESNMF_SIDE_U) {
+    switch ((h->k + 31) / 32) {
+      case 1: spmm_terms_launch<1>(h); break;
+      case 2: spmm_terms_launch<2>(h); break;
+      case 3: spmm_terms_launch<3>(h); break;
+      case 4: spmm_terms_launch<4>(h); break;
+      case 5: spmm_terms_launch<5>(h); break;
+      case 6: spmm_terms_launch<6>(h); break;
+      case 7: spmm_terms_launch<7>(h); break;
+      default: spmm_terms_launch<8>(h); break;
+    }
+    return;
+  }
   const int KQ = h->kpad / 4;
   if (KQ <= 4) spmm_launch<4, 1>(h, s, rowmap);
   else if (KQ <= 8) spmm_launch<8, 1>(h, s, rowmap);
   else if (KQ <= 16) spmm_launch<16, 1>(h, s, rowmap);
   else if (KQ <= 32) spmm_launch<32, 1>(h, s, rowmap);
   else spmm_launch<32, 2>(h, s, rowmap);
+}
+
+// ---- V row-CSR for the U side (k_spmm_terms.cuh) ----
+void vrows_clear(esnmf_t* h) {
+  Factor& f = h->V;
+  if (!f.has) return;
+  ++h->nlaunch;
+  k_vrows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->vmap, h->vbits);
+  CKL("vrows_clear");
+}
+
+void vrows_build(esnmf_t* h) {
+  Factor& f = h->V;
+  const int64_t nr = f.cap_rows + 1;
+  CK(cudaMemsetAsync(h->vrptr, 0, sizeof(int64_t) * nr, h->stream));
+  dim3 g(col_grid_x(f.maxcol), h->k);
+  ++h->nlaunch;
+  k_vrows_count<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, h->vrptr);
+  const int64_t nb = ceil_div(nr, kScanBlock);
+  h->nlaunch += 3;
+  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->vrptr, nr, h->vscan);
+  k_scan_small<<<1, 1024, 0, h->stream>>>(h->vscan, nb, h->vscan + nb);
+  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->vrptr, nr, h->vscan);
+  CK(cudaMemcpyAsync(h->vcur, h->vrptr, sizeof(int64_t) * nr, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemsetAsync(h->vmax, 0, sizeof(uint32_t), h->stream));
+  h->nlaunch += 2;
+  k_vrows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->vcur, h->vent, h->vmax);
+  k_vrows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->vrptr, h->vent,
+                                                                         h->vmap, h->vbits);
+  CKL("vrows_build");
 }
 
 // clamp + per-column top-t of side s's LS into factor `out` (column-major COO)
@@ -286,15 +472,15 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
-  k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
-  k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
-  k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+  ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
+  ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+  ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nch);
-  k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+  ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nch, sd.kthr);
-  k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nch, sd.coltot);
-  k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, out.colptr);
-  k_sel_write<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.kthr, out.colptr,
+  ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nch, sd.coltot);
+  ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, out.colptr);
+  ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.kthr, out.colptr,
                                         sd.chunk_cnt, nch, out.row, out.val);
   CKL("select");
 }
@@ -305,14 +491,26 @@ Factor& half_step(esnmf_t* h, int s) {
   Factor& in = (s == ESNMF_SIDE_V) ? h->U[h->ucur] : h->V;
   Factor& out = (s == ESNMF_SIDE_V) ? h->V : h->U[1 - h->ucur];
   if (!in.has) fail(ESNMF_ESTATE, s == ESNMF_SIDE_V ? "U is not set" : "V is not set (run the V side first)");
-  if (!(s == ESNMF_SIDE_V && h->gramU_valid)) gram(h, in, sd.G);   // a1: P:63 / P:64
-  sweep(h, sd.G, sd.eps);                                          // a2
-  form_z(h, in);                                                   // Z = F W
-  spmm(h, s, in.rowmap);                                           // a3 (+a4 scale)
+  const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
+  if (!(s == ESNMF_SIDE_V && h->gramU_valid)) {                   // a1: P:63 / P:64
+    Phase ph(h, p0 + 0);
+    gram(h, in, sd.G);
+  }
+  { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                 // a2
+  if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
+  { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale)
   sd.ls_valid = true;
-  factor_clear(h, out);
-  select_topt(h, s, out);                                          // a4 clamp + a5 top-t
-  factor_build_rows(h, out, steady_maxcol(h, out.rows));
+  {
+    Phase ph(h, p0 + 4);
+    if (s == ESNMF_SIDE_V) vrows_clear(h);
+    factor_clear(h, out);
+    select_topt(h, s, out);                                        // a4 clamp + a5 top-t
+  }
+  {
+    Phase ph(h, p0 + 5);
+    factor_build_rows(h, out, steady_maxcol(h, out.rows));
+    if (s == ESNMF_SIDE_V) vrows_build(h);
+  }
   if (s == ESNMF_SIDE_U) {
     h->ucur = 1 - h->ucur;
     h->gramU_valid = false;
@@ -332,6 +530,7 @@ void ensure_records(esnmf_t* h, int64_t need) {
 void iterate_one(esnmf_t* h) {
   half_step(h, ESNMF_SIDE_V);
   half_step(h, ESNMF_SIDE_U);
+  Phase ph(h, kMetrics);
   Factor& Un = h->U[h->ucur];
   Factor& Uo = h->U[1 - h->ucur];
   const int k = h->k;
@@ -340,19 +539,19 @@ void iterate_one(esnmf_t* h) {
   double* p_new = h->red;
   double* p_old = p_new + 2 * (int64_t)gxn * k;
   double* p_tr = p_old + (int64_t)gxo * k;
-  k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
-  k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
+  ++h->nlaunch; k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
+  ++h->nlaunch; k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
   // Gram of the new U: S term of E now, and the next V side's G_U
   gram(h, Un, h->side[ESNMF_SIDE_V].G);
   h->gramU_valid = true;
   // a8 error: T = tr(U^T (A V)) from the U side's LS rows
   Side& su = h->side[ESNMF_SIDE_U];
-  k_err_trace<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, su.row0, su.rows, su.X, su.ldx, su.G,
+  ++h->nlaunch; k_err_trace<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, su.row0, su.rows, su.X, su.ldx, su.G,
                                                     su.eps, k, p_tr);
   CKL("metrics");
   const double* t_red = nullptr;
   if (h->world > 1) {
-    k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gxn * k, h->scal + 3);
+    ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gxn * k, h->scal + 3);
     if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 1, h->stream) != 0)
       fail(ESNMF_ECOMM, "allreduce(T) failed");
     t_red = h->scal + 3;
@@ -375,7 +574,7 @@ void iterate_one(esnmf_t* h) {
   in.k = k;
   in.it = (int)(h->nrec + 1);
   in.t_reduced = t_red;
-  k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
+  ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
   CKL("finalize_record");
   h->nrec += 1;
 }
@@ -414,7 +613,7 @@ void build_items(esnmf_t* h, Side& sd, const std::vector<int64_t>& ptr_local) {
   sd.items = h->alloc<WorkItem>(sd.nitems);
   sd.item_slot = h->alloc<int32_t>(sd.nitems);
   sd.splits = h->alloc<SplitRow>(sd.nsplit);
-  sd.partial = h->alloc<float>(std::max<int64_t>(1, nslots) * h->kpad);
+  sd.partial = reinterpret_cast<float*>(h->alloc<unsigned long long>(std::max<int64_t>(1, nslots) * h->kpad));
   CK(cudaMemcpy(sd.items, items.data(), sizeof(WorkItem) * sd.nitems, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(sd.item_slot, slot.data(), sizeof(int32_t) * sd.nitems, cudaMemcpyHostToDevice));
   if (sd.nsplit) CK(cudaMemcpy(sd.splits, splits.data(), sizeof(SplitRow) * sd.nsplit, cudaMemcpyHostToDevice));
@@ -467,7 +666,7 @@ DevCsr upload_csr(esnmf_t* h, int64_t rows_total, int64_t cols, const int64_t* p
       CK(cudaMemcpyAsync(dcol, col + e0, sizeof(int32_t) * c.nnz, cudaMemcpyHostToDevice, h->stream));
       CK(cudaMemcpyAsync(dval, val + e0, sizeof(float) * c.nnz, cudaMemcpyHostToDevice, h->stream));
     }
-    k_pack<<<grid_for(c.nnz, 256, 148 * 32), 256, 0, h->stream>>>(dcol, dval, c.nnz, c.ent);
+    ++h->nlaunch; k_pack<<<grid_for(c.nnz, 256, 148 * 32), 256, 0, h->stream>>>(dcol, dval, c.nnz, c.ent);
     CKL("pack");
     if (!on_dev) {
       CK(cudaStreamSynchronize(h->stream));
@@ -480,7 +679,7 @@ DevCsr upload_csr(esnmf_t* h, int64_t rows_total, int64_t cols, const int64_t* p
       h->bytes -= (int64_t)(sizeof(int32_t) + sizeof(float)) * c.nnz;
     }
   }
-  k_validate<<<grid_for(c.rows, 8, 148 * 64), 256, 0, h->stream>>>(c.ptr, c.ent, c.rows, cols, c.nnz, h->flags + 1);
+  ++h->nlaunch; k_validate<<<grid_for(c.rows, 8, 148 * 64), 256, 0, h->stream>>>(c.ptr, c.ent, c.rows, cols, c.nnz, h->flags + 1);
   CKL("validate");
   if (host_ptr_local) *host_ptr_local = std::move(lp);
   return c;
@@ -495,13 +694,13 @@ DevCsr build_at(esnmf_t* h, const DevCsr& A, int64_t m, int64_t m0, int64_t m1) 
   T.ptr = h->alloc<int64_t>(m + 1);
   T.ent = h->alloc<int2>(A.nnz);
   CK(cudaMemsetAsync(T.ptr, 0, sizeof(int64_t) * (m + 1), h->stream));
-  k_col_count<<<grid_for(A.nnz, 256, 148 * 32), 256, 0, h->stream>>>(A.ent, A.nnz, T.ptr);
+  ++h->nlaunch; k_col_count<<<grid_for(A.nnz, 256, 148 * 32), 256, 0, h->stream>>>(A.ent, A.nnz, T.ptr);
   int64_t* tot = h->alloc<int64_t>(1);
   launch_scan_inplace(h, T.ptr, m + 1, tot);
   int64_t* cursor = h->alloc<int64_t>(m + 1);
   CK(cudaMemcpyAsync(cursor, T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToDevice, h->stream));
-  k_transpose_scatter<<<grid_for(A.rows, 8, 148 * 64), 256, 0, h->stream>>>(A.ptr, A.ent, A.rows, cursor, T.ent);
-  k_sort_rows<<<grid_for(m, 1, 148 * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent, nullptr, 0);
+  ++h->nlaunch; k_transpose_scatter<<<grid_for(A.rows, 8, 148 * 64), 256, 0, h->stream>>>(A.ptr, A.ent, A.rows, cursor, T.ent);
+  ++h->nlaunch; k_sort_rows<<<grid_for(m, 1, 148 * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent, nullptr, 0);
   // long rows (> kRowSortCap entries) in a global scratch, one block
   std::vector<int64_t> hp(m + 1);
   CK(cudaMemcpyAsync(hp.data(), T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, h->stream));
@@ -512,7 +711,7 @@ DevCsr build_at(esnmf_t* h, const DevCsr& A, int64_t m, int64_t m0, int64_t m1) 
     int64_t np = 1;
     while (np < maxlen) np <<= 1;
     uint64_t* scr = h->alloc<uint64_t>(np);
-    k_sort_rows<<<1, 256, 0, h->stream>>>(T.ptr, m, T.ent, scr, 1);
+    ++h->nlaunch; k_sort_rows<<<1, 256, 0, h->stream>>>(T.ptr, m, T.ent, scr, 1);
   }
   CKL("build_at");
   if (m0 == 0 && m1 == m) return T;
@@ -540,9 +739,9 @@ void init_u0(esnmf_t* h, const float* user_u0, bool on_dev) {
       du = tmp;
     }
   }
-  k_u0_dense<<<grid_for(h->n * h->kpad, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, h->seed, du,
+  ++h->nlaunch; k_u0_dense<<<grid_for(h->n * h->kpad, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, h->seed, du,
                                                                                f.dense, h->flags + 2);
-  k_u0_coo<<<grid_for(h->n * h->k, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, f.colptr,
+  ++h->nlaunch; k_u0_coo<<<grid_for(h->n * h->k, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, f.colptr,
                                                                           f.row, f.val, f.rowmap, f.active,
                                                                           f.n_active);
   CKL("init_u0");
@@ -660,6 +859,8 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->m = m;
     h->k = k;
     h->kpad = (k + 3) / 4 * 4;
+    CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+    CK(cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
     h->t = t;
     h->rho = o.ridge_scale;
     h->seed = o.seed;
@@ -684,8 +885,8 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     // ||A||_F^2
     {
       unsigned gb = grid_for(h->nnz, 256, 1024);
-      k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, h->nnz, h->red);
-      k_reduce_to<<<1, 256, 0, h->stream>>>(h->red, gb, h->normA2_dev);
+      ++h->nlaunch; k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, h->nnz, h->red);
+      ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(h->red, gb, h->normA2_dev);
       CKL("frob2");
     }
     // ---- A^T (V side operator, document rows) ----
@@ -707,12 +908,33 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     factor_alloc(h.get(), h->U[0], n, capU);
     factor_alloc(h.get(), h->U[1], n, capU);
     factor_alloc(h.get(), h->V, m, capV);
-    h->Z = h->alloc<float>(std::max(h->U[0].cap_rows, h->V.cap_rows) * h->kpad);
+    {
+      int G, CPL;
+      docs_layout(h->kpad, G, CPL);
+      h->zs = 4 * G * CPL;  // term-indexed Z rows: whole 128-byte lines for k >= 32
+    }
+    h->Z = h->alloc<float>(n * (int64_t)h->zs);
+    CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * n * (int64_t)h->zs, h->stream));
+    h->zlist = h->alloc<int32_t>(n);
+    h->zcount = h->alloc<int64_t>(1);
+    CK(cudaMemsetAsync(h->zcount, 0, sizeof(int64_t), h->stream));
+    h->tbits = h->alloc<uint32_t>(ceil_div(n, 32));
+    h->vbits = h->alloc<uint32_t>(ceil_div(m, 32));
+    h->vmap = h->alloc<uint64_t>(m);
+    h->vent = h->alloc<int2>(h->V.cap);
+    h->vrptr = h->alloc<int64_t>(h->V.cap_rows + 1);
+    h->vcur = h->alloc<int64_t>(h->V.cap_rows + 1);
+    h->vscan = h->alloc<int64_t>(ceil_div(h->V.cap_rows + 1, kScanBlock) + 1);
+    h->vmax = h->alloc<uint32_t>(1);
+    h->rsum = h->alloc<double>(su.rows);
+    ++h->nlaunch;
+    k_rowsum<<<grid_for(su.rows, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(su.T.ptr, su.T.ent, su.rows,
+                                                                                   h->rsum);
+    CK(cudaMemsetAsync(h->vbits, 0, sizeof(uint32_t) * ceil_div(m, 32), h->stream));
+    CK(cudaMemsetAsync(h->vmap, 0, sizeof(uint64_t) * m, h->stream));
     h->W = h->alloc<double>((int64_t)k * k);
     h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * k * k);
     if (k > 224) h->sweep_scratch = h->alloc<double>((int64_t)k * (k + 1) / 2);
-    CK(cudaFuncSetAttribute(k_sweep_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sweep_smem_bytes(std::min(k, 224), false)));
     init_u0(h.get(), o.U0, on_dev);
     CK(cudaStreamSynchronize(h->stream));
     int fl[4];
@@ -851,6 +1073,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
   if (nnz > f.cap) { g_last_error = "esnmf_set_factor: more entries than the factor capacity"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
+    if (side == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, f);
     CK(cudaMemcpyAsync(f.colptr, cp.data(), sizeof(int64_t) * (h->k + 1), cudaMemcpyHostToDevice, h->stream));
     if (nnz > 0) {
@@ -858,6 +1081,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
       CK(cudaMemcpyAsync(f.val, val, sizeof(float) * nnz, cudaMemcpyHostToDevice, h->stream));
     }
     factor_build_rows(h, f, std::max<int64_t>(maxcol, 1));
+    if (side == ESNMF_SIDE_V) vrows_build(h);
     if (side == ESNMF_SIDE_U) h->gramU_valid = false;
     CK(cudaStreamSynchronize(h->stream));
   });
@@ -900,6 +1124,35 @@ esnmf_status esnmf_get_gram(esnmf_t* h, int32_t side, double* G, double* eps) {
   });
 }
 
+esnmf_status esnmf_profile(esnmf_t* h, int32_t enable) {
+  if (!h) { g_last_error = "esnmf_profile: NULL handle"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    CK(cudaStreamSynchronize(h->stream));
+    prof_collect(h);
+    for (int i = 0; i < kNumPhases; ++i) { h->prof_ms[i] = 0; h->prof_calls[i] = 0; }
+    h->prof_on = enable != 0;
+  });
+}
+
+esnmf_status esnmf_phase_times(esnmf_t* h, int64_t cap, int64_t* count, esnmf_phase* out) {
+  if (!h || !count || cap < 0 || (cap > 0 && !out)) { g_last_error = "esnmf_phase_times: bad argument"; return ESNMF_EINVAL; }
+  esnmf_status st = guarded([&] {
+    set_device(h);
+    CK(cudaStreamSynchronize(h->stream));
+    prof_collect(h);
+    *count = kNumPhases;
+    for (int i = 0; i < kNumPhases && i < cap; ++i) {
+      std::memset(out[i].name, 0, sizeof(out[i].name));
+      std::strncpy(out[i].name, kPhaseNames[i], sizeof(out[i].name) - 1);
+      out[i].calls = h->prof_calls[i];
+      out[i].ms = h->prof_ms[i];
+    }
+  });
+  if (st == ESNMF_OK && cap < kNumPhases) { g_last_error = "esnmf_phase_times: cap < count"; return ESNMF_ETRUNC; }
+  return st;
+}
+
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
   if (!h || !info) { g_last_error = "esnmf_get_info: NULL argument"; return ESNMF_EINVAL; }
   info->n = h->n;
@@ -916,6 +1169,7 @@ esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
   info->iterations = h->nrec;
   info->device_bytes = h->bytes;
   info->normA2 = h->normA2;
+  info->launches = h->nlaunch;
   return ESNMF_OK;
 }
 

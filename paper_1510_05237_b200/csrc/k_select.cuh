@@ -28,9 +28,18 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
   const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
   const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
-  for (int64_t j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
-    const float x = __ldg(col + j);
-    if (x > 0.f) atomicAdd(&h[sel_digit(x)], 1u);
+  for (int64_t j = r0 + 4 * threadIdx.x; j < r1; j += 4 * blockDim.x) {
+    float x[4];
+    if (j + 3 < r1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + u < r1 ? col[j + u] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x[u] > 0.f) atomicAdd(&h[sel_digit(x[u])], 1u);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kNumBins; b += blockDim.x)
@@ -92,15 +101,25 @@ __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X
   const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
   int64_t above = 0;
-  for (int64_t j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
-    const float x = __ldg(col + j);
-    if (x > 0.f) {
-      const int dg = sel_digit(x);
-      if (dg > s.digit) {
-        ++above;
-      } else if (dg == s.digit) {
-        const int slot = atomicAdd(&cand_fill[c], 1);
-        if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x, (uint32_t)(row0 + j));
+  for (int64_t j = r0 + 4 * threadIdx.x; j < r1; j += 4 * blockDim.x) {
+    float x[4];
+    if (j + 3 < r1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + u < r1 ? col[j + u] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (x[u] > 0.f) {
+        const int dg = sel_digit(x[u]);
+        if (dg > s.digit) {
+          ++above;
+        } else if (dg == s.digit) {
+          const int slot = atomicAdd(&cand_fill[c], 1);
+          if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
+        }
       }
     }
   }
@@ -137,8 +156,9 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
   __shared__ int64_t sm[33];
   const int c = blockIdx.x;
   const ColSel s = sel[c];
+  // kthr[c] = (tb << 32) | tr: keep x > 0 iff bits(x) > tb or (bits(x) == tb and row <= tr)
   if (s.r == 0) {
-    if (threadIdx.x == 0) kthr[c] = s.digit < 0 ? ~0ULL : 0ULL;
+    if (threadIdx.x == 0) kthr[c] = s.digit < 0 ? 0x00000000FFFFFFFFULL : 0xFFFFFFFF00000000ULL;
     return;
   }
   const int nc = cand_fill[c];
@@ -200,7 +220,8 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
         atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + j / kSelChunk], 1ULL);
     }
   }
-  if (threadIdx.x == 0) kthr[c] = kstar;
+  if (threadIdx.x == 0)
+    kthr[c] = ((uint64_t)(0x7FFFFFFFu - (uint32_t)(kstar >> 32)) << 32) | (kstar & 0xFFFFFFFFULL);
 }
 
 // per column: exclusive scan of the chunk counts (in place), column total -> coltot[c]
@@ -237,32 +258,68 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
                                                    const int64_t* __restrict__ colptr,
                                                    const int64_t* __restrict__ chunk_off, int64_t nchunks,
                                                    int32_t* __restrict__ out_row, float* __restrict__ out_val) {
-  __shared__ int64_t sm[33];
+  // each warp owns a contiguous kSelChunk/8-row segment, read as float4 (lane l
+  // holds rows 4l..4l+3 of a 128-row step): count, one block scan over the 8
+  // warp totals, then an in-order compaction with a warp scan of the per-lane
+  // counts (the second read of the segment hits L1)
+  (void)sel;
+  __shared__ int64_t wtot[8];
   const int c = blockIdx.y;
-  const ColSel s = sel[c];
   const uint64_t ks = kthr[c];
-  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
-  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const uint32_t tb = (uint32_t)(ks >> 32), tr = (uint32_t)ks;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kSeg = kSelChunk / 8;
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk + (int64_t)warp * kSeg;
+  const int64_t r1 = min(rows, r0 + kSeg);
   const float* col = X + (int64_t)c * ldx;
+  auto load4 = [&](int64_t j, float (&x)[4], unsigned& mask) {
+    mask = 0;
+    if (j + 3 < r1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + u < r1 ? col[j + u] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t b = __float_as_uint(x[u]);
+      const uint32_t gr = (uint32_t)(row0 + j + u);
+      const bool kp = x[u] > 0.f && (b > tb || (b == tb && gr <= tr));
+      mask |= (unsigned)kp << u;
+    }
+  };
+  int64_t cnt = 0;
+  for (int64_t base = r0; base < r1; base += 128) {
+    float x[4];
+    unsigned mk;
+    load4(base + 4 * lane, x, mk);
+    cnt += warp_sum((int64_t)__popc(mk));
+  }
+  if (lane == 0) wtot[warp] = cnt;
+  __syncthreads();
   int64_t off = colptr[c] + chunk_off[(int64_t)c * nchunks + blockIdx.x];
-  for (int64_t base = r0; base < r1; base += blockDim.x) {
-    const int64_t j = base + threadIdx.x;
-    float x = 0.f;
-    bool keep = false;
-    if (j < r1) {
-      x = __ldg(col + j);
-      if (x > 0.f) {
-        const int dg = sel_digit(x);
-        keep = dg > s.digit || (dg == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= ks);
+  for (int w = 0; w < warp; ++w) off += wtot[w];
+  for (int64_t base = r0; base < r1; base += 128) {
+    float x[4];
+    unsigned mk;
+    load4(base + 4 * lane, x, mk);
+    const int mine = __popc(mk);
+    int inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int64_t o = off + inc - mine;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((mk >> u) & 1u) {
+        out_row[o] = (int32_t)(row0 + base + 4 * lane + u);
+        out_val[o] = x[u];
+        ++o;
       }
-    }
-    int64_t tot;
-    const int64_t ex = block_exscan((int64_t)keep, sm, &tot);
-    if (keep) {
-      out_row[off + ex] = (int32_t)(row0 + j);
-      out_val[off + ex] = x;
-    }
-    off += tot;
+    off += __shfl_sync(kFull, inc, 31);
   }
 }
 

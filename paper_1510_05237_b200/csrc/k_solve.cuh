@@ -16,62 +16,144 @@ ESNMF_DEV int64_t pk_idx(int i, int j, int k) {  // i <= j, packed upper, row-ma
   return (int64_t)i * k - ((int64_t)i * (i - 1)) / 2 + (j - i);
 }
 
+inline bool sweep_packed(int k) { return (int64_t)k * k * 8 + k * 8 > 200 * 1024; }
+
+// k <= 128: the whole matrix lives in registers.  Thread (ty = warp, tx = lane)
+// owns elements (i, j) = (ty + 32a, tx + 32b), a, b < JB.  Per pivot the owner
+// warp of row p publishes it to shared memory (double-buffered, so one barrier
+// per pivot suffices), every thread updates its JB x JB block in registers.
+template <int JB>
+__global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ G, int k, double rho,
+                                                     double* __restrict__ W, double* __restrict__ eps_out,
+                                                     int* __restrict__ singular) {
+  __shared__ double vbuf[2][32 * JB];
+  __shared__ double red[32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double tr = 0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) tr += G[(int64_t)i * k + i];
+  tr = block_sum(tr, red);
+  const double eps = rho * (tr / k + 1.0);
+  double r[JB][JB];
+#pragma unroll
+  for (int a = 0; a < JB; ++a)
+#pragma unroll
+    for (int b = 0; b < JB; ++b) {
+      const int i = ty + 32 * a, j = tx + 32 * b;
+      r[a][b] = (i < k && j < k) ? G[(int64_t)i * k + j] + (i == j ? eps : 0.0) : 0.0;
+    }
+  bool bad = false;
+  for (int p = 0; p < k; ++p) {
+    double* v = vbuf[p & 1];
+    if (ty == (p & 31)) {  // owner warp publishes the old row p
+      const int ap = p >> 5;
+#pragma unroll
+      for (int a = 0; a < JB; ++a)
+        if (a == ap)
+#pragma unroll
+          for (int b = 0; b < JB; ++b) v[tx + 32 * b] = r[a][b];
+    }
+    __syncthreads();
+    double d = v[p];
+    if (!(d > 0.0) || !isfinite(d)) {
+      bad = true;
+      d = 1.0;
+    }
+    const double inv = 1.0 / d;
+    double vj[JB];
+#pragma unroll
+    for (int b = 0; b < JB; ++b) vj[b] = v[tx + 32 * b];
+#pragma unroll
+    for (int a = 0; a < JB; ++a) {
+      const int i = ty + 32 * a;
+      const double vi = v[i < 32 * JB ? i : 0] * inv;
+#pragma unroll
+      for (int b = 0; b < JB; ++b) {
+        const int j = tx + 32 * b;
+        if (i == p) r[a][b] = j == p ? -inv : vj[b] * inv;
+        else r[a][b] = j == p ? vi : fma(-vi, vj[b], r[a][b]);
+      }
+    }
+  }
+  if (bad && threadIdx.x == 0) atomicExch(singular, 1);
+#pragma unroll
+  for (int a = 0; a < JB; ++a)
+#pragma unroll
+    for (int b = 0; b < JB; ++b) {
+      const int i = ty + 32 * a, j = tx + 32 * b;
+      if (i < k && j < k) W[(int64_t)i * k + j] = -r[a][b];
+    }
+  if (threadIdx.x == 0) *eps_out = eps;
+}
+
+// 2-D thread layout (32 x 32 warps): warp ty updates rows i = ty + 32 a (so the
+// row-p test is warp-uniform), lane tx columns j = tx + 32 b, b < JB, with the
+// old pivot row held in registers -- ~5 instructions per element and pivot.
+template <int JB, bool PACKED>
 __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict__ G, int k, double rho,
                                                         double* __restrict__ W, double* __restrict__ eps_out,
                                                         int* __restrict__ singular, double* gscratch) {
   extern __shared__ double dsm[];
   __shared__ double red[32];
-  __shared__ double piv;
-  const int64_t np = (int64_t)k * (k + 1) / 2;
-  double* v = dsm;                              // old pivot row, k doubles
-  double* P = gscratch ? gscratch : dsm + k;    // packed matrix
+  double* v = dsm;                              // old pivot row
+  double* P = gscratch ? gscratch : dsm + k;    // full k x k, or packed upper triangle
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, nty = blockDim.x >> 5;
+  auto idx = [&](int i, int j) -> int64_t {
+    if (!PACKED) return (int64_t)i * k + j;
+    return i <= j ? pk_idx(i, j, k) : pk_idx(j, i, k);
+  };
   double tr = 0;
   for (int i = threadIdx.x; i < k; i += blockDim.x) tr += G[(int64_t)i * k + i];
   tr = block_sum(tr, red);
   const double eps = rho * (tr / k + 1.0);
-  for (int64_t q = threadIdx.x; q < (int64_t)k * k; q += blockDim.x) {
-    int i = (int)(q / k), j = (int)(q - (int64_t)i * k);
-    if (j >= i) P[pk_idx(i, j, k)] = G[q] + (i == j ? eps : 0.0);
-  }
+  for (int i = ty; i < k; i += nty)
+    for (int j = tx; j < k; j += 32)
+      if (!PACKED || j >= i) P[idx(i, j)] = G[(int64_t)i * k + j] + (i == j ? eps : 0.0);
   __syncthreads();
   for (int p = 0; p < k; ++p) {
-    for (int j = threadIdx.x; j < k; j += blockDim.x) v[j] = P[j <= p ? pk_idx(j, p, k) : pk_idx(p, j, k)];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) v[j] = P[idx(p, j)];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double d = v[p];
-      if (!(d > 0.0) || !isfinite(d)) {
-        atomicExch(singular, 1);
-        d = 1.0;
+    double d = v[p];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (threadIdx.x == 0) atomicExch(singular, 1);
+      d = 1.0;
+    }
+    const double inv = 1.0 / d;
+    double vj[JB];
+#pragma unroll
+    for (int b = 0; b < JB; ++b) {
+      const int j = tx + 32 * b;
+      vj[b] = j < k ? v[j] : 0.0;
+    }
+    for (int i = ty; i < k; i += nty) {
+      if (i == p) {  // the pivot row: a_pj <- a_pj / d, a_pp <- -1/d
+#pragma unroll
+        for (int b = 0; b < JB; ++b) {
+          const int j = tx + 32 * b;
+          if (j < k && (!PACKED || j >= i)) P[idx(i, j)] = j == p ? -inv : vj[b] * inv;
+        }
+      } else {
+        const double vi = v[i] * inv;
+#pragma unroll
+        for (int b = 0; b < JB; ++b) {
+          const int j = tx + 32 * b;
+          if (j < k && (!PACKED || j >= i)) {
+            const int64_t q = idx(i, j);
+            P[q] = j == p ? vi : fma(-vi, vj[b], P[q]);
+          }
+        }
       }
-      piv = d;
-    }
-    __syncthreads();
-    const double d = piv, inv = 1.0 / d;
-    for (int64_t q = threadIdx.x; q < np; q += blockDim.x) {
-      // recover (i, j) of packed index q (row i holds k - i entries)
-      int i = (int)((2.0 * k + 1.0 - sqrt((2.0 * k + 1.0) * (2.0 * k + 1.0) - 8.0 * (double)q)) * 0.5);
-      while (i > 0 && pk_idx(i, i, k) > q) --i;
-      while (i + 1 < k && pk_idx(i + 1, i + 1, k) <= q) ++i;
-      int j = i + (int)(q - pk_idx(i, i, k));
-      double a = P[q];
-      if (i == p && j == p) a = -inv;
-      else if (i == p) a = v[j] * inv;
-      else if (j == p) a = v[i] * inv;
-      else a = a - v[i] * v[j] * inv;
-      P[q] = a;
     }
     __syncthreads();
   }
-  for (int64_t q = threadIdx.x; q < (int64_t)k * k; q += blockDim.x) {
-    int i = (int)(q / k), j = (int)(q - (int64_t)i * k);
-    W[q] = -P[i <= j ? pk_idx(i, j, k) : pk_idx(j, i, k)];
-  }
+  for (int i = ty; i < k; i += nty)
+    for (int j = tx; j < k; j += 32) W[(int64_t)i * k + j] = -P[idx(i, j)];
   if (threadIdx.x == 0) *eps_out = eps;
 }
 
 inline size_t sweep_smem_bytes(int k, bool global_scratch) {
   size_t b = sizeof(double) * (size_t)k;
-  if (!global_scratch) b += sizeof(double) * (size_t)k * (k + 1) / 2;
+  if (!global_scratch)
+    b += sweep_packed(k) ? sizeof(double) * (size_t)k * (k + 1) / 2 : sizeof(double) * (size_t)k * k;
   return b;
 }
 
@@ -79,10 +161,15 @@ inline size_t sweep_smem_bytes(int k, bool global_scratch) {
 // The LS rows of a half-step are T (F W): the product with A^T (or A) is
 // reassociated onto Z (identical to (T F) W up to rounding).
 // One warp per active row; lanes own columns c = lane + 32 j.
+// Z row of active row r is written at Z[active[r] * zs] (term-indexed, stride
+// zs >= kpad floats, zero padded); zlist/zcount record the rows written so the
+// next call can zero them first (k_zrows_clear).
 template <int CJ>
 __global__ void __launch_bounds__(256) k_form_z(const float* __restrict__ dense, int kpad, int k,
                                                 const int64_t* __restrict__ n_active,
-                                                const double* __restrict__ W, float* __restrict__ Z) {
+                                                const int32_t* __restrict__ active, int zs,
+                                                const double* __restrict__ W, float* __restrict__ Z,
+                                                int32_t* __restrict__ zlist, int64_t* __restrict__ zcount) {
   const int lane = threadIdx.x & 31;
   const int64_t na = *n_active;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -112,12 +199,17 @@ __global__ void __launch_bounds__(256) k_form_z(const float* __restrict__ dense,
         }
       }
     }
+    const int32_t term = active[r];
+    float* zr = Z + (int64_t)term * zs;
 #pragma unroll
     for (int j = 0; j < CJ; ++j) {
       int c = lane + 32 * j;
-      if (c < kpad) Z[r * kpad + c] = c < k ? (float)acc[j] : 0.f;
+      if (c < zs) zr[c] = c < k ? (float)acc[j] : 0.f;
     }
+    for (int c = lane + 32 * CJ; c < zs; c += 32) zr[c] = 0.f;
+    if (lane == 0) zlist[r] = term;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *zcount = na;
 }
 
 }  // namespace esk

@@ -49,7 +49,11 @@ class esnmf_record(ctypes.Structure):
 class esnmf_info(ctypes.Structure):
     _fields_ = [("n", c_i64), ("m", c_i64), ("nnz", c_i64), ("k", c_i32), ("t", c_i64), ("world", c_i32),
                 ("rank", c_i32), ("v_row0", c_i64), ("v_rows", c_i64), ("u_row0", c_i64), ("u_rows", c_i64),
-                ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl)]
+                ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl), ("launches", c_i64)]
+
+
+class esnmf_phase(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("calls", c_i64), ("ms", c_dbl)]
 
 
 class ESNMFError(RuntimeError):
@@ -76,6 +80,8 @@ SIGNATURES = {
     "esnmf_get_ls": (ctypes.c_int, [c_p, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_p]),
     "esnmf_get_gram": (ctypes.c_int, [c_p, c_i32, c_p, ctypes.POINTER(c_dbl)]),
     "esnmf_get_info": (ctypes.c_int, [c_p, ctypes.POINTER(esnmf_info)]),
+    "esnmf_profile": (ctypes.c_int, [c_p, c_i32]),
+    "esnmf_phase_times": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(esnmf_phase)]),
     "esnmf_destroy": (None, [c_p]),
     "esnmf_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "esnmf_last_error": (ctypes.c_char_p, []),
@@ -228,6 +234,18 @@ def esnmf_get_info(h) -> dict:
     return {f: getattr(i, f) for f, _ in i._fields_}
 
 
+def esnmf_profile(h, enable: bool):
+    _check(lib().esnmf_profile(h, 1 if enable else 0), "esnmf_profile")
+
+
+def esnmf_phase_times(h) -> dict:
+    """{phase name: (calls, total ms)} since profiling was enabled."""
+    buf = (esnmf_phase * 32)()
+    cnt = c_i64()
+    _check(lib().esnmf_phase_times(h, 32, ctypes.byref(cnt), buf), "esnmf_phase_times")
+    return {buf[i].name.decode(): (buf[i].calls, buf[i].ms) for i in range(cnt.value)}
+
+
 def esnmf_destroy(h):
     if h:
         lib().esnmf_destroy(h)
@@ -304,6 +322,12 @@ class ESNMF:
 
     def info(self) -> dict:
         return esnmf_get_info(self.h)
+
+    def profile(self, enable: bool = True):
+        esnmf_profile(self.h, enable)
+
+    def phase_times(self) -> dict:
+        return esnmf_phase_times(self.h)
 
     def close(self):
         if self.h:
