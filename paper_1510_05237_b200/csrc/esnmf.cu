@@ -28,6 +28,7 @@
 #include "k_spmm.cuh"
 #include "k_spmm_docs.cuh"
 #include "k_spmm_terms.cuh"
+#include "k_uside_scatter.cuh"
 
 using namespace esk;
 
@@ -135,6 +136,8 @@ struct esnmf {
   int64_t* vscan = nullptr;   // scan block sums
   uint32_t* vmax = nullptr;   // bits of max(V) (fixed-point scale of the U side)
   double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
+  double* rsum_max = nullptr; // max_i rsum[i]
+  unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
   int num_sms = 148;
   int smem_optin = 227 * 1024;
   int* flags = nullptr;  // [0] singular, [1] validation, [2] U0 invalid
@@ -411,7 +414,34 @@ void spmm_terms_launch(esnmf_t* h) {
   CKL("spmm_terms");
 }
 
+// U side on one GPU: scatter from the active documents (k_uside_scatter.cuh)
+template <int CQ>
+void uside_scatter_launch(esnmf_t* h) {
+  Side& su = h->side[ESNMF_SIDE_U];
+  Side& sv = h->side[ESNMF_SIDE_V];
+  Factor& V = h->V;
+  h->nlaunch += 2;
+  k_uside_scatter<<<grid_for(V.cap_rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      V.active, V.n_active, h->vmap, h->vent, sv.T.ptr, sv.T.ent, h->rsum_max, h->vmax, h->kpad, h->Yq);
+  k_uside_finish<CQ><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      su.rows, h->rsum_max, h->vmax, h->W, h->k, h->kpad, h->Yq, su.X, su.ldx);
+  CKL("uside_scatter");
+}
+
 void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
+  if (s == ESNMF_SIDE_U && h->world == 1) {
+    switch ((h->k + 31) / 32) {
+      case 1: uside_scatter_launch<1>(h); break;
+      case 2: uside_scatter_launch<2>(h); break;
+      case 3: uside_scatter_launch<3>(h); break;
+      case 4: uside_scatter_launch<4>(h); break;
+      case 5: uside_scatter_launch<5>(h); break;
+      case 6: uside_scatter_launch<6>(h); break;
+      case 7: uside_scatter_launch<7>(h); break;
+      default: uside_scatter_launch<8>(h); break;
+    }
+    return;
+  }
   if (s == ESNMF_SIDE_U) {
     switch ((h->k + 31) / 32) {
       case 1: spmm_terms_launch<1>(h); break;
@@ -930,6 +960,13 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     ++h->nlaunch;
     k_rowsum<<<grid_for(su.rows, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(su.T.ptr, su.T.ent, su.rows,
                                                                                    h->rsum);
+    h->rsum_max = h->alloc<double>(1);
+    ++h->nlaunch;
+    k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);
+    if (h->world == 1) {
+      h->Yq = h->alloc<unsigned long long>(n * (int64_t)h->kpad);
+      CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * n * h->kpad, h->stream));
+    }
     CK(cudaMemsetAsync(h->vbits, 0, sizeof(uint32_t) * ceil_div(m, 32), h->stream));
     CK(cudaMemsetAsync(h->vmap, 0, sizeof(uint64_t) * m, h->stream));
     h->W = h->alloc<double>((int64_t)k * k);
