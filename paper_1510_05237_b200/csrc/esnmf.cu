@@ -389,7 +389,7 @@ void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
   const size_t smem = smem_bits ? nwords * 4 : 0;
   auto kern = k_spmm_docs<G, CPL>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32), (int64_t)h->num_sms);
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32 * 8), (int64_t)h->num_sms * 2);
   ++h->nlaunch;
   kern<<<grid, kDocThreads, smem, h->stream>>>(
       sd.T.ptr, sd.T.ent, sd.rows, h->tbits, smem_bits ? (int)nwords : 0, Z4, h->k, sd.X, sd.ldx);

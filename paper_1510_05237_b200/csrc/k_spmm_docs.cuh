@@ -45,10 +45,10 @@ __global__ void k_term_bits(const int32_t* __restrict__ active, const int64_t* _
   }
 }
 
-constexpr int kDocThreads = 1024;  // one CTA per SM: the bitmap is staged once per SM
+constexpr int kDocThreads = 512;  // two CTAs per SM (128 registers per thread for the 8-row results)
 
 template <int G, int CPL>
-__global__ void __launch_bounds__(kDocThreads, 1)
+__global__ void __launch_bounds__(kDocThreads, 2)
     k_spmm_docs(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
                 const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int k,
                 float* __restrict__ X, int64_t ldx) {
@@ -66,11 +66,19 @@ __global__ void __launch_bounds__(kDocThreads, 1)
   int2* st = stage[warp];
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nwarps) {
+  // each warp produces RG consecutive rows, kept in registers, then writes
+  // every LS column as one 32-byte segment (RG = 8 rows)
+  constexpr int RG = CPL == 1 ? 4 : 2;
+  const int64_t ngroups = (rows + RG - 1) / RG;
+  for (int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; grp < ngroups; grp += nwarps) {
+  float4 res[RG][CPL];
+#pragma unroll 1
+  for (int rr = 0; rr < RG; ++rr) {
+    const int64_t row = grp * RG + rr;
     float4 acc[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t s = ptr[row], e = ptr[row + 1];
+    const int64_t s = row < rows ? ptr[row] : 0, e = row < rows ? ptr[row + 1] : 0;
     for (int64_t base = s; base < e; base += 32) {
       const int64_t idx = base + lane;
       int2 en = make_int2(0, 0);
@@ -120,17 +128,36 @@ __global__ void __launch_bounds__(kDocThreads, 1)
         acc[j].w += __shfl_xor_sync(kFull, acc[j].w, o);
       }
     }
-    if (lane < G) {
+    // keep the row's result (dynamic index rr -> unrolled select keeps it in registers)
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const int c0 = 4 * (lg + j * G);
-        float* xo = X + (int64_t)c0 * ldx + row;
-        const float v[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+    for (int q = 0; q < RG; ++q)
+      if (q == rr)
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c0 + u < k) xo[(int64_t)u * ldx] = v[u];
+        for (int j = 0; j < CPL; ++j) res[q][j] = acc[j];
+  }
+  if (lane < G) {
+    const int64_t r0 = grp * RG;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c0 = 4 * (lg + j * G);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c0 + u >= k) continue;
+        float v[RG];
+#pragma unroll
+        for (int q = 0; q < RG; ++q) v[q] = u == 0 ? res[q][j].x : u == 1 ? res[q][j].y : u == 2 ? res[q][j].z : res[q][j].w;
+        float* xo = X + (int64_t)(c0 + u) * ldx + r0;
+        if (r0 + RG <= rows) {  // ldx and r0 are multiples of RG: one aligned vector store
+          if constexpr (RG == 4) *reinterpret_cast<float4*>(xo) = make_float4(v[0], v[1], v[2], v[3]);
+          else *reinterpret_cast<float2*>(xo) = make_float2(v[0], v[1]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < RG; ++q)
+            if (r0 + q < rows) xo[q] = v[q];
+        }
       }
     }
+  }
   }
 }
 
