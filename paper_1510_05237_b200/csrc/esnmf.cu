@@ -148,6 +148,7 @@ struct esnmf {
   double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
   double* rsum_max = nullptr; // max_i rsum[i]
   unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
+  float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish32
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -310,10 +311,11 @@ int64_t steady_maxcol(esnmf_t* h, int64_t rows) { return h->t < 0 ? rows : std::
 
 void gram(esnmf_t* h, const Factor& f, double* G) {
   const int k = h->k;
-  int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 256)));
+  int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 32)));
   int64_t seglen = std::max<int64_t>(1, ceil_div(f.maxcol, S));
   dim3 g(k, (unsigned)S);
-  ++h->nlaunch; k_gram_partial<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
+  const int gb = std::min(256, (k + 31) / 32 * 32);
+  ++h->nlaunch; k_gram_partial<<<g, gb, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
                                             h->gram_partial);
   ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(h->gram_partial, (int)S, k, G);
   ++h->nlaunch; k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
@@ -403,7 +405,8 @@ void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32 * 8), (int64_t)h->num_sms * 2);
   ++h->nlaunch;
   kern<<<grid, kDocThreads, smem, h->stream>>>(
-      sd.T.ptr, sd.T.ent, sd.rows, h->tbits, smem_bits ? (int)nwords : 0, Z4, h->k, sd.X, sd.ldx);
+      sd.T.ptr, sd.T.ent, sd.rows, h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4, h->k, sd.X,
+      sd.ldx);
   CKL("spmm");
 }
 
@@ -431,11 +434,25 @@ void uside_scatter_launch(esnmf_t* h) {
   Side& su = h->side[ESNMF_SIDE_U];
   Side& sv = h->side[ESNMF_SIDE_V];
   Factor& V = h->V;
-  h->nlaunch += 2;
+  h->nlaunch += 3;
   k_uside_scatter<<<grid_for(V.cap_rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
       V.active, V.n_active, h->vmap, h->vent, sv.T.ptr, sv.T.ent, h->rsum_max, h->vmax, h->kpad, h->Yq);
+  k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
+  // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
+  h->nlaunch += 3;
+  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, 100.0, h->flags + 3);
+  const size_t smem = sizeof(float) * h->k * h->kpad;
+  if (h->kpad <= 128) {
+    CK(cudaFuncSetAttribute(k_uside_finish32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_uside_finish32<1><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 4), 256, smem, h->stream>>>(
+        su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
+  } else {
+    CK(cudaFuncSetAttribute(k_uside_finish32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_uside_finish32<2><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 1), 256, smem, h->stream>>>(
+        su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
+  }
   k_uside_finish<CQ><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
-      su.rows, h->rsum_max, h->vmax, h->W, h->k, h->kpad, h->Yq, su.X, su.ldx);
+      su.rows, h->rsum_max, h->vmax, h->W, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
   CKL("uside_scatter");
 }
 
@@ -590,12 +607,23 @@ void iterate_one(esnmf_t* h) {
   h->gramU_valid = true;
   // a8 error: T = tr(U^T (A V)) from the U side's LS rows
   Side& su = h->side[ESNMF_SIDE_U];
-  ++h->nlaunch; k_err_trace<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, su.row0, su.rows, su.X, su.ldx, su.G,
-                                                    su.eps, k, p_tr);
+  const unsigned gtr = grid_for(Un.cap_rows, 8, (int64_t)h->num_sms * 8);
+  ++h->nlaunch;
+#define ESNMF_ET(cq)                                                                                              \
+  case cq:                                                                                                        \
+    k_err_trace_rows<cq><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0, su.rows, \
+                                                     su.X, su.ldx, su.G, su.eps, k, p_tr);                        \
+    break;
+  switch ((k + 31) / 32) {
+    ESNMF_ET(1) ESNMF_ET(2) ESNMF_ET(3) ESNMF_ET(4) ESNMF_ET(5) ESNMF_ET(6) ESNMF_ET(7)
+    default: k_err_trace_rows<8><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0,
+                                                             su.rows, su.X, su.ldx, su.G, su.eps, k, p_tr);
+  }
+#undef ESNMF_ET
   CKL("metrics");
   const double* t_red = nullptr;
   if (h->world > 1) {
-    ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gxn * k, h->scal + 3);
+    ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gtr, h->scal + 3);
     if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 1, h->stream) != 0)
       fail(ESNMF_ECOMM, "allreduce(T) failed");
     t_red = h->scal + 3;
@@ -607,7 +635,7 @@ void iterate_one(esnmf_t* h) {
   in.rold = p_old;
   in.nrold = (int64_t)gxo * k;
   in.tpart = p_tr;
-  in.ntpart = (int64_t)gxn * k;
+  in.ntpart = (int64_t)gtr;
   in.GU = h->side[ESNMF_SIDE_V].G;
   in.GV = su.G;
   in.colptr_u = Un.colptr;
@@ -1009,7 +1037,10 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     {
       int G, CPL;
       docs_layout(h->kpad, G, CPL);
-      h->zs = 4 * G * CPL;  // term-indexed Z rows: whole 128-byte lines for k >= 32
+      // term-indexed Z rows padded to whole 128-byte lines (measured: 2.73 ms vs
+      // 2.84 ms per V-side launch at Large for the packed stride kpad, ESNMF_ZPAD=0)
+      const char* zp = getenv("ESNMF_ZPAD");
+      h->zs = (zp && zp[0] == '0') ? h->kpad : 4 * G * CPL;
     }
     h->Z = h->alloc<float>(n * (int64_t)h->zs);
     CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * n * (int64_t)h->zs, h->stream));
@@ -1032,6 +1063,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     ++h->nlaunch;
     k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);
     if (h->world == 1) {
+      h->W32 = h->alloc<float>((int64_t)k * h->kpad);
       h->Yq = h->alloc<unsigned long long>(n * (int64_t)h->kpad);
       CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * n * h->kpad, h->stream));
     }

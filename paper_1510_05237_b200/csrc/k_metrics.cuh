@@ -30,6 +30,58 @@ __global__ void __launch_bounds__(256) k_err_trace(const int64_t* __restrict__ c
   if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = acc;
 }
 
+// Same T, one warp per active row i of U (row view: active list + dense rows):
+// lanes load the k LS values X_U[l][i] at once, then every lane forms
+// s_c = sum_l X_U[l][i] (G_V + eps I)[l][c] for its columns c = lane + 32 q and
+// adds U_ic s_c.  part[blk] = block partial (fixed-order reduction).
+template <int CQ>
+__global__ void __launch_bounds__(256) k_err_trace_rows(const int32_t* __restrict__ active,
+                                                        const int64_t* __restrict__ n_active,
+                                                        const float* __restrict__ dense, int kpad, int64_t row0,
+                                                        int64_t rows, const float* __restrict__ XU, int64_t ldx,
+                                                        const double* __restrict__ GV, const double* eps_v, int k,
+                                                        double* __restrict__ part) {
+  __shared__ double sm[32];
+  const int lane = threadIdx.x & 31;
+  const double eps = *eps_v;
+  const int64_t na = *n_active;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < na; r += nwarps) {
+    const int64_t lr = (int64_t)active[r] - row0;
+    if (lr < 0 || lr >= rows) continue;  // warp-uniform
+    double x[CQ], u[CQ];
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) {
+      const int l = lane + 32 * q;
+      x[q] = l < k ? (double)XU[(int64_t)l * ldx + lr] : 0.0;
+      u[q] = l < k ? (double)dense[r * kpad + l] : 0.0;
+    }
+    // only the columns c with U_ic != 0 contribute: s_c = sum_l x_l (G_V + eps I)[c][l]
+    // (G_V symmetric: row c is contiguous), reduced over the warp in a fixed tree
+#pragma unroll
+    for (int qc = 0; qc < CQ; ++qc) {
+      unsigned nz = __ballot_sync(kFull, u[qc] != 0.0);
+      while (nz) {
+        const int cl = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const int c = 32 * qc + cl;
+        const double uc = __shfl_sync(kFull, u[qc], cl);
+        double p = 0;
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+          const int l = lane + 32 * q;
+          if (l < k) p = fma(x[q], __ldg(GV + (int64_t)c * k + l) + (l == c ? eps : 0.0), p);
+        }
+        p = warp_sum(p);
+        acc += lane == 0 ? uc * p : 0.0;
+      }
+    }
+  }
+  acc = block_sum(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
 // Sum of a partial array in a fixed order by one block.
 __device__ double reduce_fixed(const double* p, int64_t n, int64_t stride, double* sm) {
   double s = 0;

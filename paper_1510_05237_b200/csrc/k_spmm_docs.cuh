@@ -50,10 +50,10 @@ constexpr int kDocThreads = 512;  // two CTAs per SM (128 registers per thread f
 template <int G, int CPL>
 __global__ void __launch_bounds__(kDocThreads, 2)
     k_spmm_docs(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
-                const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int k,
-                float* __restrict__ X, int64_t ldx) {
+                const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int zq, int kq,
+                int k, float* __restrict__ X, int64_t ldx) {
+  // zq: Z row stride in float4; kq: float4 chunks holding the k values
   constexpr int NG = 32 / G;
-  constexpr int ZQ = G * CPL;  // float4 chunks per Z row (row stride = 16 ZQ bytes)
   constexpr int U = 4;         // entries per lane group per step
   extern __shared__ uint32_t sbits_dyn[];              // [nwords] active-term bitmap
   __shared__ int2 stage[kDocThreads / 32][kDocStage];
@@ -98,14 +98,15 @@ __global__ void __launch_bounds__(kDocThreads, 2)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int2 ev = st[q0 + u * NG + g];
-          zr[u] = Z + (size_t)(uint32_t)ev.x * ZQ + lg;
+          zr[u] = Z + (size_t)(uint32_t)ev.x * (uint32_t)zq + lg;
           xv[u] = __int_as_float(ev.y);
         }
         float4 z[U][CPL];
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int j = 0; j < CPL; ++j) z[u][j] = __ldg(zr[u] + j * G);
+          for (int j = 0; j < CPL; ++j)
+            z[u][j] = (lg + j * G < kq) ? __ldg(zr[u] + j * G) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll

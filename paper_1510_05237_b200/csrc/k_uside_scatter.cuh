@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) k_uside_finish(int64_t rows, const double
                                                       const uint32_t* __restrict__ vmax,
                                                       const double* __restrict__ W, int k, int kpad,
                                                       unsigned long long* __restrict__ Yq, float* __restrict__ X,
-                                                      int64_t ldx) {
+                                                      int64_t ldx, const int* __restrict__ use_fp64) {
+  if (use_fp64 && !*use_fp64) return;  // the fp32 kernel handles this system
   const int lane = threadIdx.x & 31;
   const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -108,6 +109,137 @@ __global__ void __launch_bounds__(256) k_uside_finish(int64_t rows, const double
     for (int q = 0; q < CQ; ++q) {
       const int c = lane + 32 * q;
       if (c < k) X[(int64_t)c * ldx + i] = (float)o[q];
+    }
+  }
+}
+
+// kappa_inf(G + eps I) = ||G + eps I||_inf ||W||_inf (one block); *use_fp64 = kappa > kmax.
+// The fp32 product Y W is used only for well-conditioned systems (error ~ kappa * 2^-24);
+// near-singular Grams (e.g. two topics on the same single document) take the fp64 kernel.
+__global__ void k_cond_flag(const double* __restrict__ G, const double* __restrict__ W, const double* eps, int k,
+                            double kmax, int* __restrict__ use_fp64) {
+  __shared__ double sm[32];
+  double g = 0, w = 0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double sg = 0, sw = 0;
+    for (int j = 0; j < k; ++j) {
+      sg += fabs(G[(int64_t)i * k + j] + (i == j ? *eps : 0.0));
+      sw += fabs(W[(int64_t)i * k + j]);
+    }
+    g = fmax(g, sg);
+    w = fmax(w, sw);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    g = fmax(g, __shfl_xor_sync(kFull, g, o));
+    w = fmax(w, __shfl_xor_sync(kFull, w, o));
+  }
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = g;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gm = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) gm = fmax(gm, sm[q]);
+    sm[0] = gm;
+  }
+  __syncthreads();
+  const double gm = sm[0];
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double wm = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) wm = fmax(wm, sm[q]);
+    *use_fp64 = !(gm * wm <= kmax);
+  }
+}
+
+// W (fp64, k x k) -> fp32 rows of stride kpad (zero padded) for k_uside_finish32
+__global__ void k_w_to_f32(const double* __restrict__ W, int k, int kpad, float* __restrict__ W32) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < k * kpad; q += gridDim.x * blockDim.x) {
+    const int l = q / kpad, c = q - l * kpad;
+    W32[q] = c < k ? (float)W[(int64_t)l * k + c] : 0.f;
+  }
+}
+
+// LS row = (Y row) W in fp32 with W staged in shared memory: lane owns the 4
+// consecutive columns 4(lane + 32 j) .. +3 (float4 loads of W rows); Y is the
+// exact fixed-point row converted once to fp32.  One warp per term row; the
+// nonzero columns of Y are walked in order (deterministic).  The fp32 product
+// keeps the column-relative error ~1e-7.
+template <int CW>
+__global__ void __launch_bounds__(256) k_uside_finish32(int64_t rows, const double* __restrict__ bound,
+                                                        const uint32_t* __restrict__ vmax,
+                                                        const float* __restrict__ W32, int k, int kpad,
+                                                        unsigned long long* __restrict__ Yq, float* __restrict__ X,
+                                                        int64_t ldx, const int* __restrict__ use_fp64) {
+  if (*use_fp64) return;  // ill-conditioned: the fp64 kernel handles it
+  extern __shared__ float4 ws4[];  // [k][kpad/4]
+  const int kq = kpad / 4;
+  for (int q = threadIdx.x; q < k * kq; q += blockDim.x) ws4[q] = reinterpret_cast<const float4*>(W32)[q];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < rows; i += nwarps) {
+    unsigned long long* yr = Yq + i * kpad;
+    float y[CW][4];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int ch = lane + 32 * j;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[j][e] = 0.f;
+      if (ch < kq) {
+        const ulonglong2 a = reinterpret_cast<const ulonglong2*>(yr)[2 * ch];
+        const ulonglong2 b = reinterpret_cast<const ulonglong2*>(yr)[2 * ch + 1];
+        const unsigned long long q4[4] = {a.x, a.y, b.x, b.y};
+        bool nz = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          y[j][e] = (float)((double)q4[e] * unit);
+          nz |= q4[e] != 0ull;
+        }
+        if (nz) {  // clear for the next half-step
+          reinterpret_cast<ulonglong2*>(yr)[2 * ch] = make_ulonglong2(0ull, 0ull);
+          reinterpret_cast<ulonglong2*>(yr)[2 * ch + 1] = make_ulonglong2(0ull, 0ull);
+        }
+        any |= nz;
+      }
+    }
+    float4 o[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (__any_sync(kFull, any)) {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          unsigned nz = __ballot_sync(kFull, y[j][e] != 0.f);
+          while (nz) {
+            const int src = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const float yl = __shfl_sync(kFull, y[j][e], src);
+            const float4* wl = ws4 + (4 * (src + 32 * j) + e) * kq;
+#pragma unroll
+            for (int jj = 0; jj < CW; ++jj) {
+              const int ch = lane + 32 * jj;
+              if (ch < kq) {
+                const float4 w = wl[ch];
+                o[jj].x = fmaf(yl, w.x, o[jj].x);
+                o[jj].y = fmaf(yl, w.y, o[jj].y);
+                o[jj].z = fmaf(yl, w.z, o[jj].z);
+                o[jj].w = fmaf(yl, w.w, o[jj].w);
+              }
+            }
+          }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int c0 = 4 * (lane + 32 * j);
+      const float v[4] = {o[j].x, o[j].y, o[j].z, o[j].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (c0 + e < k) X[(int64_t)(c0 + e) * ldx + i] = v[e];
     }
   }
 }
