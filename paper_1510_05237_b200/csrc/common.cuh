@@ -42,6 +42,8 @@ constexpr int kSelBits = 12;             // first-level bucket: float bits 30..1
 constexpr int kNumBins = 1 << kSelBits;  // 4096
 constexpr int kSelShift = 31 - kSelBits; // 19
 constexpr int kSelChunk = 8192;          // rows per selection block
+constexpr int kSelSeg = 1024;            // rows per output segment (one warp in k_sel_write)
+constexpr int kSelSegs = kSelChunk / kSelSeg;
 constexpr int kSelCap = 4096;            // candidates sorted in shared memory
 
 ESNMF_DEV uint32_t f2u(float x) { return __float_as_uint(x); }

@@ -527,19 +527,20 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   const int k = h->k;
   if (sd.rows == 0) fail(ESNMF_EINVAL, "empty shard");
   const int64_t nch = sd.nchunks;
+  const int64_t nseg = nch * kSelSegs;  // per-(column, segment) output counts
   CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
   ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
   ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
   ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
-                                          sd.chunk_cnt, nch);
+                                          sd.chunk_cnt, nseg);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
-                                          sd.chunk_cnt, nch, sd.kthr);
-  ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nch, sd.coltot);
+                                          sd.chunk_cnt, nseg, sd.kthr);
+  ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.coltot);
   ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, out.colptr);
   ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.kthr, out.colptr,
-                                        sd.chunk_cnt, nch, out.row, out.val);
+                                        sd.chunk_cnt, nseg, out.row, out.val);
   CKL("select");
 }
 
@@ -700,7 +701,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.sel = h->alloc<ColSel>(k);
   sd.cand = h->alloc<uint64_t>((int64_t)k * kSelCap);
   sd.cand_fill = h->alloc<int32_t>(k);
-  sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * sd.nchunks);
+  sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * sd.nchunks * kSelSegs);
   sd.coltot = h->alloc<int64_t>(k);
   sd.kthr = h->alloc<uint64_t>(k);
   sd.G = h->alloc<double>((int64_t)k * k);

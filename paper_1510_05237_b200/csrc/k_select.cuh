@@ -93,15 +93,23 @@ __global__ void __launch_bounds__(1024) k_sel_threshold(const uint32_t* __restri
 __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X, int64_t ldx, int64_t rows,
                                                      int64_t row0, const ColSel* __restrict__ sel,
                                                      uint64_t* __restrict__ cand, int32_t* __restrict__ cand_fill,
-                                                     int64_t* __restrict__ chunk_cnt, int64_t nchunks) {
-  __shared__ int64_t sm[32];
+                                                     int64_t* __restrict__ chunk_cnt, int64_t nseg) {
+  // counts of strictly-above entries per kSelSeg-row segment: with 256 threads x
+  // float4 one loop iteration covers exactly one segment (1024 rows)
+  __shared__ int32_t sm[8][kSelSegs];
   const int c = blockIdx.y;
   const ColSel s = sel[c];
   const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
   const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
-  int64_t above = 0;
-  for (int64_t j = r0 + 4 * threadIdx.x; j < r1; j += 4 * blockDim.x) {
+  int32_t cnt[kSelSegs];
+#pragma unroll
+  for (int q = 0; q < kSelSegs; ++q) cnt[q] = 0;
+#pragma unroll
+  for (int q = 0; q < kSelSegs; ++q) {
+    const int64_t j = r0 + (int64_t)q * kSelSeg + 4 * threadIdx.x;
+    if (j >= r1) continue;
+    int32_t above = 0;
     float x[4];
     if (j + 3 < r1) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
@@ -122,9 +130,21 @@ __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X
         }
       }
     }
+    cnt[q] = above;
   }
-  above = block_sum(above, sm);
-  if (threadIdx.x == 0) chunk_cnt[(int64_t)c * nchunks + blockIdx.x] = above;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kSelSegs; ++q) {
+    const int32_t w = warp_sum(cnt[q]);
+    if (lane == 0) sm[warp][q] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x < kSelSegs) {
+    int64_t tot = 0;
+    for (int w = 0; w < 8; ++w) tot += sm[w][threadIdx.x];
+    const int64_t seg = (int64_t)blockIdx.x * kSelSegs + threadIdx.x;
+    if (seg < nseg) chunk_cnt[(int64_t)c * nseg + seg] = tot;
+  }
 }
 
 // bitonic sort of n (power of two) keys in shared memory, ascending
@@ -172,7 +192,7 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
     kstar = keys[s.r - 1];
     for (int i = threadIdx.x; i < s.r; i += blockDim.x) {
       const int64_t lr = (int64_t)(uint32_t)(keys[i] & 0xFFFFFFFFu) - row0;
-      atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + lr / kSelChunk], 1ULL);
+      atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + lr / kSelSeg], 1ULL);
     }
   } else {
     // Exact fallback: radix select over the whole column restricted to bucket D.
@@ -217,7 +237,7 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
     for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
       const float x = col[j];
       if (x > 0.f && sel_digit(x) == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar)
-        atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + j / kSelChunk], 1ULL);
+        atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + j / kSelSeg], 1ULL);
     }
   }
   if (threadIdx.x == 0)
@@ -258,19 +278,19 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
                                                    const int64_t* __restrict__ colptr,
                                                    const int64_t* __restrict__ chunk_off, int64_t nchunks,
                                                    int32_t* __restrict__ out_row, float* __restrict__ out_val) {
-  // each warp owns a contiguous kSelChunk/8-row segment, read as float4 (lane l
-  // holds rows 4l..4l+3 of a 128-row step): count, one block scan over the 8
-  // warp totals, then an in-order compaction with a warp scan of the per-lane
-  // counts (the second read of the segment hits L1)
+  // each warp owns one kSelSeg-row segment whose output offset is known from
+  // the per-segment counts (k_sel_collect + k_sel_refine, scanned by
+  // k_sel_scan_cols): one read of the segment as float4 (lane l holds rows
+  // 4l..4l+3 of a 128-row step) and an in-order compaction with a warp scan
   (void)sel;
-  __shared__ int64_t wtot[8];
   const int c = blockIdx.y;
   const uint64_t ks = kthr[c];
   const uint32_t tb = (uint32_t)(ks >> 32), tr = (uint32_t)ks;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kSeg = kSelChunk / 8;
-  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk + (int64_t)warp * kSeg;
-  const int64_t r1 = min(rows, r0 + kSeg);
+  const int64_t seg = (int64_t)blockIdx.x * kSelSegs + warp;
+  const int64_t r0 = seg * kSelSeg;
+  const int64_t r1 = min(rows, r0 + kSelSeg);
+  if (r0 >= rows) return;
   const float* col = X + (int64_t)c * ldx;
   auto load4 = [&](int64_t j, float (&x)[4], unsigned& mask) {
     mask = 0;
@@ -289,17 +309,7 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
       mask |= (unsigned)kp << u;
     }
   };
-  int64_t cnt = 0;
-  for (int64_t base = r0; base < r1; base += 128) {
-    float x[4];
-    unsigned mk;
-    load4(base + 4 * lane, x, mk);
-    cnt += warp_sum((int64_t)__popc(mk));
-  }
-  if (lane == 0) wtot[warp] = cnt;
-  __syncthreads();
-  int64_t off = colptr[c] + chunk_off[(int64_t)c * nchunks + blockIdx.x];
-  for (int w = 0; w < warp; ++w) off += wtot[w];
+  int64_t off = colptr[c] + chunk_off[(int64_t)c * nchunks + seg];
   for (int64_t base = r0; base < r1; base += 128) {
     float x[4];
     unsigned mk;
