@@ -94,6 +94,12 @@ typedef struct {
   /* optional dense U_0 (n x k row-major fp32); NULL = reading C10 formula:
      U0[i,c] = ((splitmix64(seed ^ 0x55305F494E495430 ^ (i*k + c)) >> 41) + 0.5) * 2^-23 */
   const float* U0;
+  /* V-side tensor-core head: the product A^T Z is split
+     by term; the `head_terms` most frequent terms (a multiple of 64, <= 1024)
+     run as a dense fp16-split GEMM on the tensor cores, the rest as a sparse
+     row gather.  -1 (default) = automatic (terms in >= 4 % of the documents),
+     0 = off.  The result is the same product to fp32 accuracy either way. */
+  int32_t head_terms;
 } esnmf_options;
 
 typedef struct {
@@ -174,6 +180,7 @@ typedef struct {
   int64_t device_bytes;     /* device memory owned by the handle */
   double normA2;            /* ||A||_F^2 */
   int64_t launches;         /* CUDA kernels enqueued by this handle so far */
+  int32_t head_terms;       /* V-side tensor-core head size (0 = none) */
 } esnmf_info;
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);

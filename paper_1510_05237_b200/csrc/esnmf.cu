@@ -30,6 +30,7 @@
 #include "k_spmm_docs.cuh"
 #include "k_spmm_terms.cuh"
 #include "k_uside_scatter.cuh"
+#include "k_vhead.cuh"
 
 using namespace esk;
 
@@ -149,6 +150,15 @@ struct esnmf {
   double* rsum_max = nullptr; // max_i rsum[i]
   unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
   float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish32
+  // V-side tensor-core head (k_vhead.cuh): h most frequent terms, dense fp16 hi/lo tiles
+  int head_h = 0, head_nchunks = 0, kn = 0, head_acc_cols = 0;
+  int64_t head_ntiles = 0;
+  int32_t* headterm = nullptr;   // [h] term of head slot s
+  int32_t* headslot = nullptr;   // [n] head slot of term i, -1 if not in the head
+  uint8_t* atile = nullptr;      // [tiles][chunks][32 KB] A^T head block
+  uint8_t* zhead = nullptr;      // [chunks][kn x 64 x 2 x 2 B] Z head rows, hi/lo
+  float* colscale = nullptr;     // [kn] 2^-(eA + eZ_c)
+  unsigned* amax_bits = nullptr; // max value of this rank's A^T shard (float bits)
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -200,10 +210,10 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---------------------------------------------------------------- profiling
 enum PhaseId { kVGram, kVSolve, kVFormZ, kVSpmm, kVSelect, kVRows, kUGram, kUSolve, kUFormZ, kUSpmm, kUSelect, kURows,
-               kMetrics, kNumPhases };
+               kMetrics, kVHead, kNumPhases };
 const char* const kPhaseNames[kNumPhases] = {"V.gram",   "V.solve",  "V.form_z", "V.spmm",   "V.select",
                                              "V.rowview", "U.gram",  "U.solve",  "U.form_z", "U.spmm",
-                                             "U.select", "U.rowview", "iter.metrics"};
+                                             "U.select", "U.rowview", "iter.metrics", "V.head"};
 
 cudaEvent_t pool_event(esnmf_t* h) {
   if (!h->ev_pool.empty()) {
@@ -378,6 +388,12 @@ void form_z(esnmf_t* h, const Factor& f) {
   CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
   ++h->nlaunch;
   k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits);
+  if (h->head_h > 0) {  // head terms go through the tensor cores (k_vhead.cuh), not the gather
+    h->nlaunch += 2;
+    k_head_bits_clear<<<(unsigned)ceil_div(h->head_h, 256), 256, 0, h->stream>>>(h->headterm, h->head_h, h->tbits);
+    k_zhead_prep<<<h->k, 256, 0, h->stream>>>(h->Z, h->zs, h->headterm, h->head_h, h->kn, h->amax_bits, h->zhead,
+                                              h->colscale);
+  }
   CKL("form_z");
 }
 
@@ -400,7 +416,7 @@ void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
   const int64_t nwords = ceil_div(h->n, 32);
   const bool smem_bits = nwords * 4 <= 96 * 1024;
   const size_t smem = smem_bits ? nwords * 4 : 0;
-  auto kern = k_spmm_docs<G, CPL>;
+  auto kern = h->head_h > 0 ? k_spmm_docs<G, CPL, true> : k_spmm_docs<G, CPL, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32 * 8), (int64_t)h->num_sms * 2);
   ++h->nlaunch;
@@ -546,6 +562,91 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
 
 void select_merge(esnmf_t* h, int s, Factor& out);
 
+// V side, head terms on the tensor cores: X += A^T[:, head] Z[head, :]
+int head_stages(int kn) {
+  const int sb = (int)((kHeadABytes + (uint32_t)kn * kHeadK * 4 + 1023u) & ~1023u);
+  return std::max(2, std::min(4, (200 * 1024) / sb));
+}
+
+template <int ST>
+void vhead_launch_st(esnmf_t* h) {
+  Side& sv = h->side[ESNMF_SIDE_V];
+  const int sb = (int)((kHeadABytes + (uint32_t)h->kn * kHeadK * 4 + 1023u) & ~1023u);
+  const int smem = ST * sb + 1024;
+  auto kern = k_vhead_tc<ST>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, h->num_sms);
+  ++h->nlaunch;
+  kern<<<grid, kHeadThreads, smem, h->stream>>>(h->atile, h->zhead, h->colscale, sv.rows, h->head_ntiles,
+                                                h->head_nchunks, h->k, h->kn, h->head_acc_cols, sv.X, sv.ldx);
+  CKL("vhead");
+}
+
+void vhead_launch(esnmf_t* h) {
+  switch (head_stages(h->kn)) {
+    case 2: vhead_launch_st<2>(h); break;
+    case 3: vhead_launch_st<3>(h); break;
+    default: vhead_launch_st<4>(h); break;
+  }
+}
+
+// Choose the head (create time): the terms of largest document frequency
+// (row lengths of A, global), at least `min_df` of the documents each, a
+// multiple of 64 terms, at most 1024; or `want` terms when want > 0.
+void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
+  if (want == 0) return;
+  const char* env = getenv("ESNMF_HEAD");
+  if (env && env[0]) want = atoi(env);
+  if (want == 0) return;
+  const int64_t n = h->n;
+  std::vector<int32_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return hptr[a + 1] - hptr[a] > hptr[b + 1] - hptr[b]; });
+  int64_t hh;
+  if (want > 0) {
+    hh = std::min<int64_t>(want, n);
+  } else {
+    double frac = 0.04;
+    const char* fe = getenv("ESNMF_HEAD_DF");
+    if (fe && fe[0]) frac = atof(fe);
+    const double min_df = std::max(1.0, frac * (double)h->m);
+    hh = 0;
+    while (hh < n && (double)(hptr[order[hh] + 1] - hptr[order[hh]]) >= min_df) ++hh;
+  }
+  hh = std::min<int64_t>(hh, 1024) / kHeadK * kHeadK;
+  if (hh < kHeadK) return;
+  Side& sv = h->side[ESNMF_SIDE_V];
+  h->kn = (h->k + 15) / 16 * 16;
+  h->head_acc_cols = h->kn <= 32 ? 32 : h->kn <= 64 ? 64 : h->kn <= 128 ? 128 : 256;
+  h->head_h = (int)hh;
+  h->head_nchunks = (int)(hh / kHeadK);
+  h->head_ntiles = ceil_div(std::max<int64_t>(sv.rows, 1), kHeadM);
+  std::vector<int32_t> slot(n, -1);
+  for (int64_t s = 0; s < hh; ++s) slot[order[s]] = (int32_t)s;
+  h->headterm = h->alloc<int32_t>(hh);
+  h->headslot = h->alloc<int32_t>(n);
+  CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
+  const size_t abytes = (size_t)h->head_ntiles * h->head_nchunks * kHeadABytes;
+  h->atile = h->alloc<uint8_t>((int64_t)abytes);
+  h->zhead = h->alloc<uint8_t>((int64_t)h->head_nchunks * h->kn * kHeadK * 4);
+  h->colscale = h->alloc<float>(h->kn);
+  h->amax_bits = h->alloc<unsigned>(1);
+  CK(cudaMemsetAsync(h->atile, 0, abytes, h->stream));
+  CK(cudaMemsetAsync(h->zhead, 0, (size_t)h->head_nchunks * h->kn * kHeadK * 4, h->stream));
+  CK(cudaMemsetAsync(h->colscale, 0, sizeof(float) * h->kn, h->stream));
+  CK(cudaMemsetAsync(h->amax_bits, 0, sizeof(unsigned), h->stream));
+  h->nlaunch += 2;
+  k_absmax_ent<<<grid_for(std::max<int64_t>(sv.T.nnz, 1), 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
+      sv.T.ent, sv.T.nnz, h->amax_bits);
+  k_head_build<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+      sv.T.ptr, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nchunks, h->atile);
+  CKL("head_setup");
+  // host vectors die here: make the async uploads complete first
+  CK(cudaStreamSynchronize(h->stream));
+}
+
 // one half-step; returns the factor that was written
 Factor& half_step(esnmf_t* h, int s) {
   Side& sd = h->side[s];
@@ -559,6 +660,7 @@ Factor& half_step(esnmf_t* h, int s) {
   }
   { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                 // a2
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
+  if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // head terms (TC)
   { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale)
   sd.ls_valid = true;
   {
@@ -912,6 +1014,7 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->device = -1;
   o->world = 1;
   o->rank = 0;
+  o->head_terms = -1;
   return ESNMF_OK;
 }
 
@@ -1028,6 +1131,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     if (h->world == 1 && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
     build_items(h.get(), su, aptr);
     side_alloc(h.get(), sv);
+    head_setup(h.get(), hptr, o.head_terms);
     side_alloc(h.get(), su);
     // ---- factors ----
     const int64_t capU = n * (int64_t)k;
@@ -1308,6 +1412,7 @@ esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
   info->device_bytes = h->bytes;
   info->normA2 = h->normA2;
   info->launches = h->nlaunch;
+  info->head_terms = h->head_h;
   return ESNMF_OK;
 }
 

@@ -15,7 +15,8 @@
 //    shared list (ballot + popc) padded with references to term 0 with value 0,
 //    then walks it U entries per lane group at a time: U independent loads in
 //    flight, then 4U FMAs -- branch-free.
-// Results go from registers straight to the column-major LS buffer.
+// Results go from registers straight to the column-major LS buffer (ACCUM:
+// added to the head part the tensor-core kernel stored there, k_vhead.cuh).
 // Accumulation order per row is fixed by the row's entry order (deterministic).
 #pragma once
 #include "common.cuh"
@@ -47,7 +48,7 @@ __global__ void k_term_bits(const int32_t* __restrict__ active, const int64_t* _
 
 constexpr int kDocThreads = 512;  // two CTAs per SM (128 registers per thread for the 8-row results)
 
-template <int G, int CPL>
+template <int G, int CPL, bool ACCUM>
 __global__ void __launch_bounds__(kDocThreads, 2)
     k_spmm_docs(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
                 const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int zq, int kq,
@@ -149,12 +150,25 @@ __global__ void __launch_bounds__(kDocThreads, 2)
         for (int q = 0; q < RG; ++q) v[q] = u == 0 ? res[q][j].x : u == 1 ? res[q][j].y : u == 2 ? res[q][j].z : res[q][j].w;
         float* xo = X + (int64_t)(c0 + u) * ldx + r0;
         if (r0 + RG <= rows) {  // ldx and r0 are multiples of RG: one aligned vector store
-          if constexpr (RG == 4) *reinterpret_cast<float4*>(xo) = make_float4(v[0], v[1], v[2], v[3]);
-          else *reinterpret_cast<float2*>(xo) = make_float2(v[0], v[1]);
+          if constexpr (RG == 4) {
+            float4 o = make_float4(v[0], v[1], v[2], v[3]);
+            if constexpr (ACCUM) {
+              const float4 p = *reinterpret_cast<const float4*>(xo);
+              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+            }
+            *reinterpret_cast<float4*>(xo) = o;
+          } else {
+            float2 o = make_float2(v[0], v[1]);
+            if constexpr (ACCUM) {
+              const float2 p = *reinterpret_cast<const float2*>(xo);
+              o.x += p.x; o.y += p.y;
+            }
+            *reinterpret_cast<float2*>(xo) = o;
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < RG; ++q)
-            if (r0 + q < rows) xo[q] = v[q];
+            if (r0 + q < rows) xo[q] = ACCUM ? xo[q] + v[q] : v[q];
         }
       }
     }

@@ -35,6 +35,7 @@ class esnmf_options(ctypes.Structure):
         ("world", c_i32), ("rank", c_i32), ("comm", ctypes.POINTER(esnmf_comm)),
         ("inputs_on_device", c_i32),
         ("at_row_ptr", c_p), ("at_col_idx", c_p), ("at_val", c_p), ("U0", c_p),
+        ("head_terms", c_i32),
     ]
 
 
@@ -49,7 +50,8 @@ class esnmf_record(ctypes.Structure):
 class esnmf_info(ctypes.Structure):
     _fields_ = [("n", c_i64), ("m", c_i64), ("nnz", c_i64), ("k", c_i32), ("t", c_i64), ("world", c_i32),
                 ("rank", c_i32), ("v_row0", c_i64), ("v_rows", c_i64), ("u_row0", c_i64), ("u_rows", c_i64),
-                ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl), ("launches", c_i64)]
+                ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl), ("launches", c_i64),
+                ("head_terms", c_i32)]
 
 
 class esnmf_phase(ctypes.Structure):
@@ -270,8 +272,10 @@ class ESNMF:
     at_ptr/at_col/at_val), numpy (host) or torch CUDA tensors (device)."""
 
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
-                 device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None):
+                 device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None,
+                 head_terms: int = -1):
         o = esnmf_options_init()
+        o.head_terms = head_terms
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device

@@ -1,0 +1,101 @@
+"""GPU parity of the V-side tensor-core head (csrc/k_vhead.cuh).
+
+The V-side product A^T Z is split by term: the `head_terms` most frequent terms
+run as a dense fp16-split GEMM on tcgen05, the rest as the sparse row gather.
+The split changes only the summation order, so every check here is the same
+oracle parity as tests/test_gpu_parity.py (reading C15: products 1e-5
+column-relative, near-tie-only support differences), for several head sizes,
+plus head-on versus head-off agreement on the same state.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_1510_05237_b200 import ESNMF, ESNMF_SIDE_U, ESNMF_SIDE_V
+from parity import PROD_TOL, check_canonical, check_products, check_selection, check_topt_property, coo_dense
+
+pytestmark = pytest.mark.gpu
+TINY, MEDIUM = synth.CONFIGS["tiny"], synth.CONFIGS["medium"]
+
+
+def dense(s, side, rows, k):
+    r, c, v = s.get_U() if side == ESNMF_SIDE_U else s.get_V()
+    check_canonical(r, c, k)
+    return coo_dense((rows, k), r, c, v)
+
+
+def v_side_parity(s, g, cfg, k, t):
+    F = dense(s, ESNMF_SIDE_U, cfg.n, k)
+    ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], F, t)
+    s.half_step(ESNMF_SIDE_V)
+    _, ls = s.get_ls(ESNMF_SIDE_V)
+    out = dense(s, ESNMF_SIDE_V, cfg.m, k)
+    err = check_products(ls, ref["LS"])
+    check_selection(out, ref["F"], ref["LS"], t)
+    check_topt_property(ls, out, t)
+    return err
+
+
+@pytest.mark.parametrize("head", [64, 192, 1024])
+def test_tiny_head_sizes_first_and_late(head):
+    g = synth.generate(TINY)
+    s = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, head_terms=head)
+    assert s.info()["head_terms"] == min(head, 1024)
+    v_side_parity(s, g, TINY, TINY.k, TINY.t)      # from dense U0
+    s.half_step(ESNMF_SIDE_U)
+    s.iterate(5)
+    v_side_parity(s, g, TINY, TINY.k, TINY.t)      # from a sparse late U
+
+
+@pytest.mark.parametrize("k", [1, 16, 33, 100])
+def test_tiny_head_odd_ranks(k):
+    """kn = k rounded up to 16: padding columns of the MMA must not leak."""
+    g = synth.generate(TINY)
+    s = ESNMF(TINY.n, TINY.m, k, 37, g, seed=TINY.seed, head_terms=128)
+    v_side_parity(s, g, TINY, k, 37)
+    s.half_step(ESNMF_SIDE_U)
+    v_side_parity(s, g, TINY, k, 37)
+
+
+def test_medium_auto_head_late_state():
+    g = synth.generate(MEDIUM)
+    s = ESNMF(MEDIUM.n, MEDIUM.m, MEDIUM.k, MEDIUM.t, g, seed=MEDIUM.seed)
+    assert s.info()["head_terms"] >= 64
+    s.iterate(4)
+    err = v_side_parity(s, g, MEDIUM, MEDIUM.k, MEDIUM.t)
+    assert err < PROD_TOL
+
+
+def test_head_on_off_agree():
+    """Same state, head on vs off: LS within fp32 rounding, identical trajectory."""
+    g = synth.generate(MEDIUM)
+    a = ESNMF(MEDIUM.n, MEDIUM.m, MEDIUM.k, MEDIUM.t, g, seed=MEDIUM.seed, head_terms=512)
+    b = ESNMF(MEDIUM.n, MEDIUM.m, MEDIUM.k, MEDIUM.t, g, seed=MEDIUM.seed, head_terms=0)
+    assert b.info()["head_terms"] == 0
+    a.iterate(3)
+    b.iterate(3)
+    ea = [r["E"] for r in a.records()]
+    eb = [r["E"] for r in b.records()]
+    assert np.allclose(ea, eb, rtol=1e-6, atol=0)
+    # same U in both, then one V side each
+    r, c, v = a.get_U()
+    b.set_factor(ESNMF_SIDE_U, r, c, v)
+    a.half_step(ESNMF_SIDE_V)
+    b.half_step(ESNMF_SIDE_V)
+    _, la = a.get_ls(ESNMF_SIDE_V)
+    _, lb = b.get_ls(ESNMF_SIDE_V)
+    check_products(la, lb.astype(np.float64), tol=5e-6)
+
+
+def test_head_deterministic():
+    g = synth.generate(TINY)
+    outs = []
+    for _ in range(2):
+        s = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, head_terms=192)
+        s.iterate(4)
+        _, ls = s.get_ls(ESNMF_SIDE_V)
+        outs.append((ls, s.get_U()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for x, y in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(x, y)
