@@ -31,6 +31,7 @@
 #include "k_spmm_terms.cuh"
 #include "k_uside_scatter.cuh"
 #include "k_vhead.cuh"
+#include "k_spmm_tail.cuh"
 
 using namespace esk;
 
@@ -159,6 +160,9 @@ struct esnmf {
   uint8_t* zhead = nullptr;      // [chunks][kn x 64 x 2 x 2 B] Z head rows, hi/lo
   float* colscale = nullptr;     // [kn] 2^-(eA + eZ_c)
   unsigned* amax_bits = nullptr; // max value of this rank's A^T shard (float bits)
+  int32_t* nh = nullptr;         // [v rows] head entries at the front of each A^T row
+  bool gather_docs = false;      // ESNMF_VGATHER=docs: the older batch-per-round gather
+  int tail_variant = 0;          // ESNMF_TAIL_VARIANT: alternative tail-gather instantiations
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -426,6 +430,36 @@ void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
   CKL("spmm");
 }
 
+// V side (default): k_spmm_tail over the non-head entries of every document
+// (G lanes per Z row) x (CPL float4 per lane) = Z row stride / 4
+void tail_layout(int kpad, int& G, int& CPL) {
+  const int KQ = kpad / 4;
+  if (KQ <= 4) { G = 4; CPL = 1; }
+  else if (KQ <= 8) { G = 8; CPL = 1; }
+  else if (KQ <= 16) { G = 8; CPL = 2; }
+  else if (KQ <= 32) { G = 32; CPL = 1; }
+  else { G = 32; CPL = 2; }
+}
+
+template <int G, int CPL, int U, int RG>
+void tail_launch(esnmf_t* h) {
+  Side& sd = h->side[ESNMF_SIDE_V];
+  const float4* Z4 = reinterpret_cast<const float4*>(h->Z);
+  const int64_t nwords = ceil_div(h->n, 32);
+  const bool smem_bits = nwords * 4 <= 64 * 1024;
+  const size_t smem = smem_bits ? nwords * 4 : 0;
+  if (h->zs != 4 * G * CPL) fail(ESNMF_EINVAL, "Z row stride does not match the tail gather layout");
+  auto kern = h->head_h > 0 ? k_spmm_tail<G, CPL, U, RG, true> : k_spmm_tail<G, CPL, U, RG, false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t groups = ceil_div(sd.rows, RG);
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * 3);
+  ++h->nlaunch;
+  kern<<<grid, kTailThreads, smem, h->stream>>>(sd.T.ptr, h->head_h > 0 ? h->nh : nullptr, sd.T.ent, sd.rows,
+                                                h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4,
+                                                h->k, sd.X, sd.ldx);
+  CKL("spmm_tail");
+}
+
 // U side: paper order, fp64 (A V) from the sparse V rows, then (A V) W
 template <int CQ>
 void spmm_terms_launch(esnmf_t* h) {
@@ -500,6 +534,22 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
     return;
   }
   const int KQ = h->kpad / 4;
+  if (!h->gather_docs) {  // layouts must match tail_layout()
+    if (KQ <= 4) tail_launch<4, 1, 2, 4>(h);
+    else if (KQ <= 8) tail_launch<8, 1, 2, 4>(h);
+    else if (KQ <= 16) tail_launch<8, 2, 2, 2>(h);
+    else if (KQ <= 32) {
+      switch (h->tail_variant) {  // ESNMF_TAIL_VARIANT (measurement only; same Z stride)
+        case 1: tail_launch<32, 1, 8, 4>(h); break;
+        case 2: tail_launch<16, 2, 4, 4>(h); break;
+        case 4: tail_launch<16, 2, 2, 4>(h); break;
+        case 6: tail_launch<32, 1, 6, 4>(h); break;
+        default: tail_launch<32, 1, 4, 4>(h); break;
+      }
+    }
+    else tail_launch<32, 2, 4, 2>(h);
+    return;
+  }
   if (KQ <= 4) spmm_launch<4, 1>(h, s, rowmap);
   else if (KQ <= 8) spmm_launch<8, 1>(h, s, rowmap);
   else if (KQ <= 16) spmm_launch<16, 1>(h, s, rowmap);
@@ -637,11 +687,25 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   CK(cudaMemsetAsync(h->zhead, 0, (size_t)h->head_nchunks * h->kn * kHeadK * 4, h->stream));
   CK(cudaMemsetAsync(h->colscale, 0, sizeof(float) * h->kn, h->stream));
   CK(cudaMemsetAsync(h->amax_bits, 0, sizeof(unsigned), h->stream));
+  // rows of A^T: head entries first (stable), so the tail gather skips them
+  h->nh = h->alloc<int32_t>(std::max<int64_t>(sv.rows, 1));
+  if (sv.T.nnz > 0) {
+    int2* tmp = nullptr;
+    CK(cudaMalloc(&tmp, sizeof(int2) * sv.T.nnz));
+    ++h->nlaunch;
+    k_reorder_head<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+        sv.T.ptr, sv.T.ent, sv.rows, h->headslot, tmp, h->nh);
+    CK(cudaMemcpyAsync(sv.T.ent, tmp, sizeof(int2) * sv.T.nnz, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaFree(tmp));
+  } else {
+    CK(cudaMemsetAsync(h->nh, 0, sizeof(int32_t) * std::max<int64_t>(sv.rows, 1), h->stream));
+  }
   h->nlaunch += 2;
   k_absmax_ent<<<grid_for(std::max<int64_t>(sv.T.nnz, 1), 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
       sv.T.ent, sv.T.nnz, h->amax_bits);
   k_head_build<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
-      sv.T.ptr, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nchunks, h->atile);
+      sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nchunks, h->atile);
   CKL("head_setup");
   // host vectors die here: make the async uploads complete first
   CK(cudaStreamSynchronize(h->stream));
@@ -1068,6 +1132,12 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     }
     h->n = n;
     h->m = m;
+    {
+      const char* vg = getenv("ESNMF_VGATHER");
+      h->gather_docs = vg && std::string(vg) == "docs";
+      const char* tv = getenv("ESNMF_TAIL_VARIANT");
+      h->tail_variant = tv ? atoi(tv) : 0;
+    }
     h->k = k;
     h->kpad = (k + 3) / 4 * 4;
     CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -1141,11 +1211,12 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     factor_alloc(h.get(), h->V, m, capV);
     {
       int G, CPL;
-      docs_layout(h->kpad, G, CPL);
-      // term-indexed Z rows padded to whole 128-byte lines (measured: 2.73 ms vs
-      // 2.84 ms per V-side launch at Large for the packed stride kpad, ESNMF_ZPAD=0)
-      const char* zp = getenv("ESNMF_ZPAD");
-      h->zs = (zp && zp[0] == '0') ? h->kpad : 4 * G * CPL;
+      if (h->gather_docs) docs_layout(h->kpad, G, CPL);
+      else tail_layout(h->kpad, G, CPL);
+
+      // term-indexed Z rows, zero-padded to the gather layout (whole 16-byte
+      // chunks per lane, no predicated loads)
+      h->zs = 4 * G * CPL;
     }
     h->Z = h->alloc<float>(n * (int64_t)h->zs);
     CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * n * (int64_t)h->zs, h->stream));

@@ -60,15 +60,17 @@ __global__ void k_absmax_ent(const int2* __restrict__ ent, int64_t nnz, unsigned
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
-// dense head tiles from the document rows (warp per row); buffer zeroed first
-__global__ void k_head_build(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
+// dense head tiles from the head prefix of the document rows (warp per row);
+// buffer zeroed first
+__global__ void k_head_build(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
+                             const int2* __restrict__ ent, int64_t rows,
                              const int32_t* __restrict__ headslot, const unsigned* __restrict__ amax_bits,
                              int nchunks, uint8_t* __restrict__ atile) {
   const int eA = head_exp(__uint_as_float(*amax_bits));
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-    const int64_t s = ptr[row], e = ptr[row + 1];
+    const int64_t s = ptr[row], e = s + nh[row];  // head entries lead the row (k_reorder_head)
     const int64_t tile = row / kHeadM;
     const int r = (int)(row % kHeadM);
     for (int64_t q = s + lane; q < e; q += 32) {
