@@ -99,6 +99,9 @@ struct Side {
   int64_t* chunk_cnt = nullptr;
   int64_t* coltot = nullptr;
   uint64_t* kthr = nullptr;
+  uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
+  int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
+  uint64_t* bucket = nullptr;     // [k][kSelCap] value keys of the threshold bucket
   // Gram of the factor this side reads, and its eps
   double* G = nullptr;
   double* eps = nullptr;
@@ -120,6 +123,12 @@ struct esnmf {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // second stream for work that overlaps the main chain (fork/join by events):
+  // the U side's Gram + solve run beside the active-document scatter, and the
+  // error/record kernels of iteration i beside the V side of iteration i+1
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_ufork = nullptr, ev_ujoin = nullptr, ev_mfork = nullptr, ev_mjoin = nullptr;
+  bool aux_pending = false;
   int64_t n = 0, m = 0, nnz = 0;
   int k = 0, kpad = 0;
   int64_t t = 0;  // < 0 unlimited
@@ -204,6 +213,10 @@ struct esnmf {
     for (auto& r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
+    if (aux) cudaStreamSynchronize(aux);
+    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin})
+      if (e) cudaEventDestroy(e);
+    if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -211,6 +224,31 @@ struct esnmf {
 namespace {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// enqueue on another stream for the lifetime of the object
+struct OnStream {
+  esnmf_t* h;
+  cudaStream_t saved;
+  OnStream(esnmf_t* h_, cudaStream_t s) : h(h_), saved(h_->stream) { h->stream = s; }
+  ~OnStream() { h->stream = saved; }
+};
+
+// main -> aux dependency (aux waits for everything enqueued on main so far)
+void fork_to_aux(esnmf_t* h, cudaEvent_t ev) {
+  ck(cudaEventRecord(ev, h->stream), "cudaEventRecord(fork)");
+  ck(cudaStreamWaitEvent(h->aux, ev, 0), "cudaStreamWaitEvent(fork)");
+}
+// aux -> main dependency
+void join_from_aux(esnmf_t* h, cudaEvent_t ev) {
+  ck(cudaEventRecord(ev, h->aux), "cudaEventRecord(join)");
+  ck(cudaStreamWaitEvent(h->stream, ev, 0), "cudaStreamWaitEvent(join)");
+}
+// the previous iteration's error/record kernels must finish before V is replaced
+void join_metrics(esnmf_t* h) {
+  if (!h->aux_pending) return;
+  join_from_aux(h, h->ev_mjoin);
+  h->aux_pending = false;
+}
 
 // ---------------------------------------------------------------- profiling
 enum PhaseId { kVGram, kVSolve, kVFormZ, kVSpmm, kVSelect, kVRows, kUGram, kUSolve, kUFormZ, kUSpmm, kUSelect, kURows,
@@ -478,27 +516,38 @@ void spmm_terms_launch(esnmf_t* h) {
   CKL("spmm_terms");
 }
 
+// fp32 copy of W and the conditioning flag choosing the fp32 or fp64 (Y W)
+void uside_w_prep(esnmf_t* h) {
+  Side& su = h->side[ESNMF_SIDE_U];
+  h->nlaunch += 2;
+  k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
+  // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
+  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, 100.0, h->flags + 3);
+  CKL("uside_w_prep");
+}
+
 // U side on one GPU: scatter from the active documents (k_uside_scatter.cuh)
 template <int CQ>
 void uside_scatter_launch(esnmf_t* h) {
   Side& su = h->side[ESNMF_SIDE_U];
   Side& sv = h->side[ESNMF_SIDE_V];
   Factor& V = h->V;
-  h->nlaunch += 3;
+  ++h->nlaunch;
   k_uside_scatter<<<grid_for(V.cap_rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
       V.active, V.n_active, h->vmap, h->vent, sv.T.ptr, sv.T.ent, h->rsum_max, h->vmax, h->kpad, h->Yq);
-  k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
-  // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
-  h->nlaunch += 3;
-  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, 100.0, h->flags + 3);
-  const size_t smem = sizeof(float) * h->k * h->kpad;
+  // Gram + solve + W prep (uside_w_prep) ran on the aux stream beside the scatter
+  join_from_aux(h, h->ev_ujoin);
+  h->nlaunch += 2;
+  // W32 staged in shared memory + per-warp transposed Y tiles (8 warps)
+  const size_t smem = sizeof(float) * h->k * h->kpad + sizeof(float) * 8 * h->kpad * kFinRT;
+  const int64_t rgroups = ceil_div(su.rows, kFinRT);
   if (h->kpad <= 128) {
-    CK(cudaFuncSetAttribute(k_uside_finish32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_uside_finish32<1><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 4), 256, smem, h->stream>>>(
+    CK(cudaFuncSetAttribute(k_uside_finish_rt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_uside_finish_rt<1><<<grid_for(rgroups, 8, (int64_t)h->num_sms * 3), 256, smem, h->stream>>>(
         su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
   } else {
-    CK(cudaFuncSetAttribute(k_uside_finish32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_uside_finish32<2><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 1), 256, smem, h->stream>>>(
+    CK(cudaFuncSetAttribute(k_uside_finish_rt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_uside_finish_rt<2><<<grid_for(rgroups, 8, (int64_t)h->num_sms * 1), 256, smem, h->stream>>>(
         su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
   }
   k_uside_finish<CQ><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
@@ -599,6 +648,22 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   dim3 g((unsigned)nch, k);
   ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
   ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+  if (sd.above) {  // two passes over X (k_sel_collect2 + k_sel_final)
+    CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
+    int32_t* bfill = sd.above_fill + k;
+    ++h->nlaunch;
+    k_sel_collect2<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(h->t, 1),
+                                             sd.above, sd.above_fill, sd.bucket, bfill);
+    ++h->nlaunch;
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, h->t, out.colptr);
+    CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
+    ++h->nlaunch;
+    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel,
+                                                       std::max<int64_t>(h->t, 1), sd.above, sd.above_fill,
+                                                       sd.bucket, bfill, out.colptr, out.row, out.val);
+    CKL("select2");
+    return;
+  }
   ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
@@ -718,17 +783,25 @@ Factor& half_step(esnmf_t* h, int s) {
   Factor& out = (s == ESNMF_SIDE_V) ? h->V : h->U[1 - h->ucur];
   if (!in.has) fail(ESNMF_ESTATE, s == ESNMF_SIDE_V ? "U is not set" : "V is not set (run the V side first)");
   const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
-  if (!(s == ESNMF_SIDE_V && h->gramU_valid)) {                   // a1: P:63 / P:64
-    Phase ph(h, p0 + 0);
-    gram(h, in, sd.G);
+  const bool overlap_u = s == ESNMF_SIDE_U && h->world == 1;    // Gram + solve on aux, beside the scatter
+  if (s == ESNMF_SIDE_U) join_metrics(h);  // (only pending after a bare half_step call)
+  if (overlap_u) fork_to_aux(h, h->ev_ufork);
+  {
+    OnStream os(h, overlap_u ? h->aux : h->stream);
+    if (!(s == ESNMF_SIDE_V && h->gramU_valid)) {                 // a1: P:63 / P:64
+      Phase ph(h, p0 + 0);
+      gram(h, in, sd.G);
+    }
+    { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }               // a2
+    if (overlap_u) uside_w_prep(h);
   }
-  { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                 // a2
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
   if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // head terms (TC)
   { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale)
   sd.ls_valid = true;
   {
     Phase ph(h, p0 + 4);
+    join_metrics(h);  // the previous iteration's record reads V
     if (s == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, out);
     if (h->world == 1) select_topt(h, s, out);                     // a4 clamp + a5 top-t
@@ -772,7 +845,12 @@ void iterate_one(esnmf_t* h) {
   // Gram of the new U: S term of E now, and the next V side's G_U
   gram(h, Un, h->side[ESNMF_SIDE_V].G);
   h->gramU_valid = true;
-  // a8 error: T = tr(U^T (A V)) from the U side's LS rows
+  // a8 error: T = tr(U^T (A V)) from the U side's LS rows.  On one GPU
+  // the trace and the record run on the aux stream, beside the next V side
+  // (joined before that V side replaces V, join_metrics).
+  const bool overlap_m = h->world == 1;
+  if (overlap_m) fork_to_aux(h, h->ev_mfork);
+  OnStream os(h, overlap_m ? h->aux : h->stream);
   Side& su = h->side[ESNMF_SIDE_U];
   const unsigned gtr = grid_for(Un.cap_rows, 8, (int64_t)h->num_sms * 8);
   ++h->nlaunch;
@@ -816,6 +894,7 @@ void iterate_one(esnmf_t* h) {
   ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
   CKL("finalize_record");
   h->nrec += 1;
+  if (overlap_m) h->aux_pending = true;
 }
 
 void sync_check(esnmf_t* h) {
@@ -870,6 +949,11 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * sd.nchunks * kSelSegs);
   sd.coltot = h->alloc<int64_t>(k);
   sd.kthr = h->alloc<uint64_t>(k);
+  if (h->t >= 0 && h->t <= kSelFastT) {
+    sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(h->t, 1));
+    sd.above_fill = h->alloc<int32_t>(2 * (int64_t)k);
+    sd.bucket = h->alloc<uint64_t>((int64_t)k * kSelCap);
+  }
   sd.G = h->alloc<double>((int64_t)k * k);
   sd.eps = h->alloc<double>(1);
   if (h->world > 1) {
@@ -1130,6 +1214,9 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
       h->own_stream = true;
     }
+    CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
     {
@@ -1275,6 +1362,7 @@ esnmf_status esnmf_iterate(esnmf_t* h, int32_t iters) {
     set_device(h);
     ensure_records(h, h->nrec + iters);
     for (int32_t i = 0; i < iters; ++i) iterate_one(h);
+    join_metrics(h);  // everything later on the caller's stream sees the records
   });
 }
 
@@ -1283,6 +1371,7 @@ esnmf_status esnmf_half_step(esnmf_t* h, int32_t side) {
   return guarded([&] {
     set_device(h);
     half_step(h, side);
+    join_metrics(h);
   });
 }
 

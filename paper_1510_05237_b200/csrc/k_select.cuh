@@ -333,4 +333,185 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-pass variant for t <= kSelFastT (every BASELINE config but Box and the
+// t = 10^4 / unlimited sweep points): after k_sel_hist + k_sel_threshold,
+//   k_sel_collect2  one pass over X appends every positive of bucket > D to a
+//                   per-column "above" list (row-keyed, < t of them) and every
+//                   positive of bucket D to a "bucket" list (value-keyed), with
+//                   warp-aggregated slot reservations;
+//   k_sel_final     one block per column: sort the bucket keys, keep the r
+//                   smallest (value desc, row asc), merge with the above list,
+//                   sort the kept entries by row and write the column.
+// The lists are filled in scheduling order but everything kept is sorted by a
+// total order, so the output is deterministic.  A bucket larger than
+// kSelCap falls back to an exact radix select over the column.
+constexpr int64_t kSelFastT = 4096;
+
+ESNMF_DEV uint64_t row_key(uint32_t row, float x) { return ((uint64_t)row << 32) | (uint64_t)f2u(x); }
+
+__global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                      int64_t row0, const ColSel* __restrict__ sel, int64_t t,
+                                                      uint64_t* __restrict__ above, int32_t* __restrict__ above_fill,
+                                                      uint64_t* __restrict__ bucket,
+                                                      int32_t* __restrict__ bucket_fill) {
+  const int c = blockIdx.y;
+  const ColSel s = sel[c];
+  if (s.digit >= kNumBins) return;  // t == 0: nothing kept
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t* ab = above + (int64_t)c * t;
+  uint64_t* bk = bucket + (int64_t)c * kSelCap;
+  // every thread runs the same trip count (the ballots need the full warp)
+  for (int64_t base = r0; base < r1; base += 4 * blockDim.x) {
+    const int64_t j = base + 4 * threadIdx.x;
+    float x[4];
+    if (j + 3 < r1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + u < r1 ? col[j + u] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool pos = x[u] > 0.f;
+      const int dg = pos ? sel_digit(x[u]) : -1;
+      const bool up = pos && dg > s.digit;
+      const bool eq = pos && dg == s.digit;
+      const unsigned mu = __ballot_sync(kFull, up), me = __ballot_sync(kFull, eq);
+      int bu = 0, be = 0;
+      if (lane == 0) {
+        if (mu) bu = atomicAdd(&above_fill[c], __popc(mu));
+        if (me) be = atomicAdd(&bucket_fill[c], __popc(me));
+      }
+      bu = __shfl_sync(kFull, bu, 0);
+      be = __shfl_sync(kFull, be, 0);
+      const uint32_t gr = (uint32_t)(row0 + j + u);
+      if (up) ab[bu + __popc(mu & lt)] = row_key(gr, x[u]);
+      if (eq) {
+        const int slot = be + __popc(me & lt);
+        if (slot < kSelCap) bk[slot] = sel_key(x[u], gr);
+      }
+    }
+  }
+}
+
+// colptr of the kept entries: min(t, #positive) per column (reading C4/C5)
+__global__ void k_sel_colptr_kept(const ColSel* __restrict__ sel, int k, int64_t t, int64_t* __restrict__ colptr) {
+  __shared__ int64_t sm[33];
+  int64_t v = 0;
+  if (threadIdx.x < k) {
+    const int64_t np = sel[threadIdx.x].npos;
+    v = t < 0 ? np : min(np, t);
+  }
+  int64_t tot;
+  const int64_t ex = block_exscan(v, sm, &tot);
+  if (threadIdx.x < k) colptr[threadIdx.x] = ex;
+  if (threadIdx.x == 0) colptr[k] = tot;
+}
+
+constexpr size_t kSelFinalSmem = sizeof(uint64_t) * (kSelCap + kSelFastT);
+
+__global__ void __launch_bounds__(1024) k_sel_final(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                    int64_t row0, const ColSel* __restrict__ sel, int64_t t,
+                                                    const uint64_t* __restrict__ above,
+                                                    const int32_t* __restrict__ above_fill,
+                                                    const uint64_t* __restrict__ bucket,
+                                                    const int32_t* __restrict__ bucket_fill,
+                                                    const int64_t* __restrict__ colptr, int32_t* __restrict__ out_row,
+                                                    float* __restrict__ out_val) {
+  extern __shared__ uint64_t fin_smem[];
+  uint64_t* kb = fin_smem;                                // [kSelCap] bucket keys
+  uint64_t* kept = fin_smem + kSelCap;                    // [kSelFastT] kept row keys
+  uint32_t* h = reinterpret_cast<uint32_t*>(kb);          // fallback histogram (aliases kb)
+  __shared__ int64_t sm[4];
+  __shared__ int nk_s;
+  const int c = blockIdx.x;
+  const ColSel s = sel[c];
+  if (s.digit >= kNumBins) return;
+  const int na = above_fill[c];  // == s.above (all positives when s.digit < 0)
+  const int nb = bucket_fill[c];
+  const int r = (int)s.r;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) kept[i] = above[(int64_t)c * t + i];
+  if (threadIdx.x == 0) nk_s = na;
+  __syncthreads();
+  if (r > 0) {
+    if (nb <= kSelCap) {
+      int np = 1;
+      while (np < nb) np <<= 1;
+      for (int i = threadIdx.x; i < np; i += blockDim.x) kb[i] = i < nb ? bucket[(int64_t)c * kSelCap + i] : ~0ULL;
+      __syncthreads();
+      bitonic_sort_smem(kb, np);
+      for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        const uint64_t key = kb[i];
+        const uint32_t row = (uint32_t)key;
+        const float x = __uint_as_float(0x7FFFFFFFu - (uint32_t)(key >> 32));
+        kept[na + i] = row_key(row, x);
+      }
+    } else {
+      // exact fallback: radix select of the r-th smallest key of bucket D over the column
+      const float* col = X + (int64_t)c * ldx;
+      const int shifts[5] = {39, 32, 20, 8, 0};
+      const int widths[5] = {12, 7, 12, 12, 8};
+      uint64_t prefix = ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51;
+      uint64_t fixed_mask = 0xFFFULL << 51;
+      int64_t rr = r;
+      for (int lv = 0; lv < 5; ++lv) {
+        const int sh = shifts[lv], wd = widths[lv];
+        for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
+        __syncthreads();
+        for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
+          const float x = col[j];
+          if (x > 0.f && sel_digit(x) == s.digit) {
+            const uint64_t key = sel_key(x, (uint32_t)(row0 + j));
+            if ((key & fixed_mask) == prefix) atomicAdd(&h[(key >> sh) & ((1u << wd) - 1)], 1u);
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int64_t acc = 0;
+          int b = 0;
+          for (; b < (1 << wd); ++b) {
+            if (acc + h[b] >= rr) break;
+            acc += h[b];
+          }
+          sm[0] = b;
+          sm[1] = rr - acc;
+        }
+        __syncthreads();
+        prefix |= (uint64_t)sm[0] << sh;
+        rr = sm[1];
+        fixed_mask |= (uint64_t)((1u << wd) - 1) << sh;
+        __syncthreads();
+      }
+      const uint64_t kstar = prefix;
+      for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
+        const float x = col[j];
+        if (x > 0.f && sel_digit(x) == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar) {
+          const int slot = atomicAdd(&nk_s, 1);
+          kept[slot] = row_key((uint32_t)(row0 + j), x);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int nk = na + r;
+  int np = 1;
+  while (np < nk) np <<= 1;
+  for (int i = nk + threadIdx.x; i < np; i += blockDim.x) kept[i] = ~0ULL;
+  __syncthreads();
+  bitonic_sort_smem(kept, np);
+  const int64_t o = colptr[c];
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+    const uint64_t key = kept[i];
+    out_row[o + i] = (int32_t)(key >> 32);
+    out_val[o + i] = __uint_as_float((uint32_t)key);
+  }
+}
+
 }  // namespace esk

@@ -244,6 +244,107 @@ __global__ void __launch_bounds__(256) k_uside_finish32(int64_t rows, const doub
   }
 }
 
+// Register-tiled variant of k_uside_finish32: a warp converts RT = 8 rows of
+// the fixed-point Y at a time into shared memory (transposed, ys[l][r]), clears
+// them, and computes the 8 x k block (Y W) with every W row read once from
+// shared memory per 8 rows (the one-row kernel re-read W per row and was bound
+// by shared-memory bandwidth).  Dense in l: Y's zeros are multiplied, not
+// skipped (the same fixed summation order for every row; deterministic).
+constexpr int kFinRT = 8;
+
+template <int CW>
+__global__ void __launch_bounds__(256) k_uside_finish_rt(int64_t rows, const double* __restrict__ bound,
+                                                         const uint32_t* __restrict__ vmax,
+                                                         const float* __restrict__ W32, int k, int kpad,
+                                                         unsigned long long* __restrict__ Yq, float* __restrict__ X,
+                                                         int64_t ldx, const int* __restrict__ use_fp64) {
+  if (*use_fp64) return;  // ill-conditioned: the fp64 kernel handles it
+  extern __shared__ float4 ws4[];  // [k][kpad/4] W, then per warp ys[kpad][kFinRT]
+  const int kq = kpad / 4;
+  for (int q = threadIdx.x; q < k * kq; q += blockDim.x) ws4[q] = reinterpret_cast<const float4*>(W32)[q];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* ys = reinterpret_cast<float*>(ws4 + k * kq) + warp * kpad * kFinRT;
+  __syncthreads();
+  const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ngroups = (rows + kFinRT - 1) / kFinRT;
+  for (int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; grp < ngroups; grp += nwarps) {
+    const int64_t i0 = grp * kFinRT;
+    // the RT rows are one contiguous block of Yq: every 16-byte load is issued
+    // before any is used (PER in flight per lane), then converted and cleared
+    constexpr int PER = CW * 16;  // >= kFinRT * kpad / 2 / 32 for kpad <= 128 CW
+    const int nch = (int)(min((int64_t)kFinRT, rows - i0) * kpad / 2);
+    ulonglong2* yg = reinterpret_cast<ulonglong2*>(Yq + i0 * kpad);
+    ulonglong2 buf[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = lane + 32 * u;
+      buf[u] = q < nch ? yg[q] : make_ulonglong2(0ull, 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = lane + 32 * u;
+      if (q < kFinRT * kpad / 2) {
+        const unsigned long long pr[2] = {buf[u].x, buf[u].y};
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int e = 2 * q + h2, r = e / kpad, c = e - r * kpad;
+          ys[c * kFinRT + r] = pr[h2] ? (float)((double)pr[h2] * unit) : 0.f;
+        }
+        if (q < nch && (buf[u].x | buf[u].y)) yg[q] = make_ulonglong2(0ull, 0ull);  // clear for the next half-step
+      }
+    }
+    __syncwarp();
+    float4 acc[kFinRT][CW];
+#pragma unroll
+    for (int r = 0; r < kFinRT; ++r)
+#pragma unroll
+      for (int j = 0; j < CW; ++j) acc[r][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int l = 0; l < k; ++l) {
+      const float4 y0 = *reinterpret_cast<const float4*>(ys + l * kFinRT);
+      const float4 y1 = *reinterpret_cast<const float4*>(ys + l * kFinRT + 4);
+      const float yv[kFinRT] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int ch = lane + 32 * j;
+        if (ch < kq) {
+          const float4 w = ws4[l * kq + ch];
+#pragma unroll
+          for (int r = 0; r < kFinRT; ++r) {
+            const float2 lo = __ffma2_rn(make_float2(yv[r], yv[r]), make_float2(w.x, w.y),
+                                         make_float2(acc[r][j].x, acc[r][j].y));
+            const float2 hi = __ffma2_rn(make_float2(yv[r], yv[r]), make_float2(w.z, w.w),
+                                         make_float2(acc[r][j].z, acc[r][j].w));
+            acc[r][j] = make_float4(lo.x, lo.y, hi.x, hi.y);
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int c0 = 4 * (lane + 32 * j);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (c0 + e >= k) continue;
+        float v[kFinRT];
+#pragma unroll
+        for (int r = 0; r < kFinRT; ++r)
+          v[r] = e == 0 ? acc[r][j].x : e == 1 ? acc[r][j].y : e == 2 ? acc[r][j].z : acc[r][j].w;
+        float* xo = X + (int64_t)(c0 + e) * ldx + i0;
+        if (i0 + kFinRT <= rows) {  // ldx and i0 are multiples of 8
+          reinterpret_cast<float4*>(xo)[0] = make_float4(v[0], v[1], v[2], v[3]);
+          reinterpret_cast<float4*>(xo)[1] = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < kFinRT; ++r)
+            if (i0 + r < rows) xo[r] = v[r];
+        }
+      }
+    }
+  }
+}
+
 // max_i rowsum_i(A) for the global fixed-point scale (one block)
 __global__ void k_max_to(const double* __restrict__ a, int64_t n, double* __restrict__ out) {
   __shared__ double sm[32];
