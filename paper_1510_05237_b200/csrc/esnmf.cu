@@ -27,7 +27,6 @@
 #include "k_select.cuh"
 #include "k_solve.cuh"
 #include "k_spmm.cuh"
-#include "k_spmm_docs.cuh"
 #include "k_spmm_terms.cuh"
 #include "k_uside_scatter.cuh"
 #include "k_vhead.cuh"
@@ -165,13 +164,14 @@ struct esnmf {
   int64_t head_ntiles = 0;
   int32_t* headterm = nullptr;   // [h] term of head slot s
   int32_t* headslot = nullptr;   // [n] head slot of term i, -1 if not in the head
-  uint8_t* atile = nullptr;      // [tiles][chunks][32 KB] A^T head block
   uint8_t* zhead = nullptr;      // [chunks][kn x 64 x 2 x 2 B] Z head rows, hi/lo
   float* colscale = nullptr;     // [kn] 2^-(eA + eZ_c)
   unsigned* amax_bits = nullptr; // max value of this rank's A^T shard (float bits)
   int32_t* nh = nullptr;         // [v rows] head entries at the front of each A^T row
-  bool gather_docs = false;      // ESNMF_VGATHER=docs: the older batch-per-round gather
-  int tail_variant = 0;          // ESNMF_TAIL_VARIANT: alternative tail-gather instantiations
+  int head_nd = 0;               // leading head chunks stored as dense tiles (atile)
+  uint8_t* atile = nullptr;      // [tiles][nd][32 KB] dense fp16 hi/lo tiles of those chunks
+  int64_t* hoff = nullptr;       // [tiles * sparse chunks + 1] segment offsets of the tiled head copy
+  int2* hseg = nullptr;          // head entries by (tile, chunk): (row in tile << 6 | slot, value)
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -439,36 +439,6 @@ void form_z(esnmf_t* h, const Factor& f) {
   CKL("form_z");
 }
 
-// V-side lane-group layout: G lanes per gathered row, CPL float4 per lane
-void docs_layout(int kpad, int& G, int& CPL) {
-  const int KQ = kpad / 4;
-  CPL = 1;
-  if (KQ <= 4) G = 4;
-  else if (KQ <= 8) G = 8;
-  else if (KQ <= 16) G = 16;
-  else if (KQ <= 32) G = 32;
-  else { G = 32; CPL = 2; }
-}
-
-template <int G, int CPL>
-void spmm_launch(esnmf_t* h, int s, const int32_t* rowmap) {
-  (void)rowmap;
-  Side& sd = h->side[s];
-  const float4* Z4 = reinterpret_cast<const float4*>(h->Z);
-  const int64_t nwords = ceil_div(h->n, 32);
-  const bool smem_bits = nwords * 4 <= 96 * 1024;
-  const size_t smem = smem_bits ? nwords * 4 : 0;
-  auto kern = h->head_h > 0 ? k_spmm_docs<G, CPL, true> : k_spmm_docs<G, CPL, false>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(sd.rows, kDocThreads / 32 * 8), (int64_t)h->num_sms * 2);
-  ++h->nlaunch;
-  kern<<<grid, kDocThreads, smem, h->stream>>>(
-      sd.T.ptr, sd.T.ent, sd.rows, h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4, h->k, sd.X,
-      sd.ldx);
-  CKL("spmm");
-}
-
-// V side (default): k_spmm_tail over the non-head entries of every document
 // (G lanes per Z row) x (CPL float4 per lane) = Z row stride / 4
 void tail_layout(int kpad, int& G, int& CPL) {
   const int KQ = kpad / 4;
@@ -487,7 +457,7 @@ void tail_launch(esnmf_t* h) {
   const bool smem_bits = nwords * 4 <= 64 * 1024;
   const size_t smem = smem_bits ? nwords * 4 : 0;
   if (h->zs != 4 * G * CPL) fail(ESNMF_EINVAL, "Z row stride does not match the tail gather layout");
-  auto kern = h->head_h > 0 ? k_spmm_tail<G, CPL, U, RG, true> : k_spmm_tail<G, CPL, U, RG, false>;
+  auto kern = k_spmm_tail<G, CPL, U, RG, false>;  // stores; the head kernel adds its part after
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t groups = ceil_div(sd.rows, RG);
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * 3);
@@ -583,27 +553,12 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
     return;
   }
   const int KQ = h->kpad / 4;
-  if (!h->gather_docs) {  // layouts must match tail_layout()
-    if (KQ <= 4) tail_launch<4, 1, 2, 4>(h);
-    else if (KQ <= 8) tail_launch<8, 1, 2, 4>(h);
-    else if (KQ <= 16) tail_launch<8, 2, 2, 2>(h);
-    else if (KQ <= 32) {
-      switch (h->tail_variant) {  // ESNMF_TAIL_VARIANT (measurement only; same Z stride)
-        case 1: tail_launch<32, 1, 8, 4>(h); break;
-        case 2: tail_launch<16, 2, 4, 4>(h); break;
-        case 4: tail_launch<16, 2, 2, 4>(h); break;
-        case 6: tail_launch<32, 1, 6, 4>(h); break;
-        default: tail_launch<32, 1, 4, 4>(h); break;
-      }
-    }
-    else tail_launch<32, 2, 4, 2>(h);
-    return;
-  }
-  if (KQ <= 4) spmm_launch<4, 1>(h, s, rowmap);
-  else if (KQ <= 8) spmm_launch<8, 1>(h, s, rowmap);
-  else if (KQ <= 16) spmm_launch<16, 1>(h, s, rowmap);
-  else if (KQ <= 32) spmm_launch<32, 1>(h, s, rowmap);
-  else spmm_launch<32, 2>(h, s, rowmap);
+  // layouts must match tail_layout() (the Z row stride)
+  if (KQ <= 4) tail_launch<4, 1, 2, 4>(h);
+  else if (KQ <= 8) tail_launch<8, 1, 2, 4>(h);
+  else if (KQ <= 16) tail_launch<8, 2, 2, 2>(h);
+  else if (KQ <= 32) tail_launch<32, 1, 4, 4>(h);
+  else tail_launch<32, 2, 4, 2>(h);
 }
 
 // ---- V row-CSR for the U side (k_spmm_terms.cuh) ----
@@ -678,22 +633,23 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
 void select_merge(esnmf_t* h, int s, Factor& out);
 
 // V side, head terms on the tensor cores: X += A^T[:, head] Z[head, :]
-int head_stages(int kn) {
-  const int sb = (int)((kHeadABytes + (uint32_t)kn * kHeadK * 4 + 1023u) & ~1023u);
-  return std::max(2, std::min(4, (200 * 1024) / sb));
+int head_stage_bytes_host(int kn) {
+  return (int)((kHeadABytes + (uint32_t)kn * kHeadK * 4 + kHeadRawBytes + 1023u) & ~1023u);
 }
+int head_stages(int kn) { return std::max(2, std::min(4, (220 * 1024) / head_stage_bytes_host(kn))); }
 
 template <int ST>
 void vhead_launch_st(esnmf_t* h) {
   Side& sv = h->side[ESNMF_SIDE_V];
-  const int sb = (int)((kHeadABytes + (uint32_t)h->kn * kHeadK * 4 + 1023u) & ~1023u);
-  const int smem = ST * sb + 1024;
-  auto kern = k_vhead_tc<ST>;
+  const int smem = ST * head_stage_bytes_host(h->kn) + 1024;
+  auto kern = k_vhead_otf<ST>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, h->num_sms);
   ++h->nlaunch;
-  kern<<<grid, kHeadThreads, smem, h->stream>>>(h->atile, h->zhead, h->colscale, sv.rows, h->head_ntiles,
-                                                h->head_nchunks, h->k, h->kn, h->head_acc_cols, sv.X, sv.ldx);
+  kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
+                                                   h->colscale,
+                                                   sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
+                                                   h->head_acc_cols, sv.X, sv.ldx);
   CKL("vhead");
 }
 
@@ -707,7 +663,7 @@ void vhead_launch(esnmf_t* h) {
 
 // Choose the head (create time): the terms of largest document frequency
 // (row lengths of A, global), at least `min_df` of the documents each, a
-// multiple of 64 terms, at most 1024; or `want` terms when want > 0.
+// multiple of 64 terms, at most kHeadMax; or `want` terms when want > 0.
 void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (want == 0) return;
   const char* env = getenv("ESNMF_HEAD");
@@ -722,14 +678,14 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (want > 0) {
     hh = std::min<int64_t>(want, n);
   } else {
-    double frac = 0.04;
+    double frac = 0.015;
     const char* fe = getenv("ESNMF_HEAD_DF");
     if (fe && fe[0]) frac = atof(fe);
     const double min_df = std::max(1.0, frac * (double)h->m);
     hh = 0;
     while (hh < n && (double)(hptr[order[hh] + 1] - hptr[order[hh]]) >= min_df) ++hh;
   }
-  hh = std::min<int64_t>(hh, 1024) / kHeadK * kHeadK;
+  hh = std::min<int64_t>(hh, kHeadMax) / kHeadK * kHeadK;
   if (hh < kHeadK) return;
   Side& sv = h->side[ESNMF_SIDE_V];
   h->kn = (h->k + 15) / 16 * 16;
@@ -743,12 +699,9 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   h->headslot = h->alloc<int32_t>(n);
   CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
-  const size_t abytes = (size_t)h->head_ntiles * h->head_nchunks * kHeadABytes;
-  h->atile = h->alloc<uint8_t>((int64_t)abytes);
   h->zhead = h->alloc<uint8_t>((int64_t)h->head_nchunks * h->kn * kHeadK * 4);
   h->colscale = h->alloc<float>(h->kn);
   h->amax_bits = h->alloc<unsigned>(1);
-  CK(cudaMemsetAsync(h->atile, 0, abytes, h->stream));
   CK(cudaMemsetAsync(h->zhead, 0, (size_t)h->head_nchunks * h->kn * kHeadK * 4, h->stream));
   CK(cudaMemsetAsync(h->colscale, 0, sizeof(float) * h->kn, h->stream));
   CK(cudaMemsetAsync(h->amax_bits, 0, sizeof(unsigned), h->stream));
@@ -766,11 +719,48 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   } else {
     CK(cudaMemsetAsync(h->nh, 0, sizeof(int32_t) * std::max<int64_t>(sv.rows, 1), h->stream));
   }
-  h->nlaunch += 2;
+  ++h->nlaunch;
   k_absmax_ent<<<grid_for(std::max<int64_t>(sv.T.nnz, 1), 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
       sv.T.ent, sv.T.nnz, h->amax_bits);
-  k_head_build<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
-      sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nchunks, h->atile);
+  // the densest chunks as dense tiles (bulk-copied as they are) ...
+  {
+    int nd = 4;
+    const char* de = getenv("ESNMF_HEAD_DENSE");
+    if (de && de[0]) nd = atoi(de);
+    h->head_nd = std::max(0, std::min(nd, h->head_nchunks));
+    if (h->head_nd > 0) {
+      const size_t ab = (size_t)h->head_ntiles * h->head_nd * kHeadABytes;
+      h->atile = h->alloc<uint8_t>((int64_t)ab);
+      CK(cudaMemsetAsync(h->atile, 0, ab, h->stream));
+      ++h->nlaunch;
+      k_head_dense<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+          sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nd, h->atile);
+    }
+  }
+  // ... and the others as a tiled copy of their entries: one run per (tile, chunk)
+  {
+    const int nsp = h->head_nchunks - h->head_nd;
+    const int64_t nseg = h->head_ntiles * nsp;
+    h->hoff = h->alloc<int64_t>(nseg + 1);
+    CK(cudaMemsetAsync(h->hoff, 0, sizeof(int64_t) * (nseg + 1), h->stream));
+    auto* cnt = reinterpret_cast<unsigned long long*>(h->hoff);
+    const unsigned g = grid_for(sv.rows, 8, (int64_t)h->num_sms * 32);
+    ++h->nlaunch;
+    k_head_count<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cnt);
+    launch_scan_inplace(h, h->hoff, nseg + 1, h->alloc<int64_t>(1));  // hoff[nseg] = total
+    int64_t nhe = 0;
+    CK(cudaMemcpyAsync(&nhe, h->hoff + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->hseg = h->alloc<int2>(std::max<int64_t>(nhe, 1));
+    unsigned long long* cursor = nullptr;
+    CK(cudaMalloc(&cursor, sizeof(int64_t) * (nseg + 1)));
+    CK(cudaMemcpyAsync(cursor, h->hoff, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToDevice, h->stream));
+    ++h->nlaunch;
+    k_head_fill<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cursor,
+                                         h->hseg);
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaFree(cursor));
+  }
   CKL("head_setup");
   // host vectors die here: make the async uploads complete first
   CK(cudaStreamSynchronize(h->stream));
@@ -796,8 +786,8 @@ Factor& half_step(esnmf_t* h, int s) {
     if (overlap_u) uside_w_prep(h);
   }
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
-  if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // head terms (TC)
-  { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale)
+  { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
+  if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
   sd.ls_valid = true;
   {
     Phase ph(h, p0 + 4);
@@ -1219,12 +1209,6 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
-    {
-      const char* vg = getenv("ESNMF_VGATHER");
-      h->gather_docs = vg && std::string(vg) == "docs";
-      const char* tv = getenv("ESNMF_TAIL_VARIANT");
-      h->tail_variant = tv ? atoi(tv) : 0;
-    }
     h->k = k;
     h->kpad = (k + 3) / 4 * 4;
     CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -1298,8 +1282,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     factor_alloc(h.get(), h->V, m, capV);
     {
       int G, CPL;
-      if (h->gather_docs) docs_layout(h->kpad, G, CPL);
-      else tail_layout(h->kpad, G, CPL);
+      tail_layout(h->kpad, G, CPL);
 
       // term-indexed Z rows, zero-padded to the gather layout (whole 16-byte
       // chunks per lane, no predicated loads)

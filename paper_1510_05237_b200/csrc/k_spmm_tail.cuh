@@ -31,8 +31,31 @@ constexpr int kTailThreads = 256;
 constexpr int kTailSub = 4;              // entries per lane per load round
 constexpr int kTailRound = 32 * kTailSub;
 
-// head entries (headslot >= 0) first, then the rest; both in their original
-// order (stable).  out-of-place; nh[row] = number of head entries.
+// zero the Z rows of the terms listed (the previous V side's active terms)
+__global__ void k_zrows_clear(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
+                              float4* __restrict__ Z, int zq) {
+  const int64_t cnt = *count;
+  const int64_t total = cnt * zq;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / zq;
+    Z[(int64_t)terms[r] * zq + (q - r * zq)] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// term bitmap of the active rows of U (all bits cleared by the caller first)
+__global__ void k_term_bits(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
+                            uint32_t* __restrict__ bits) {
+  const int64_t na = *n_active;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = active[r];
+    atomicOr(&bits[t >> 5], 1u << (t & 31));
+  }
+}
+
+// Head entries (headslot >= 0) first, then the rest; both in their original
+// order (stable).  Out-of-place; nh[row] = number of head entries.  The tensor
+// core kernel reads its own copy of the head entries (k_head_fill); the tail
+// gather reads [ptr + nh, ptr+1) and the U side reads whole rows.
 __global__ void k_reorder_head(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
                                const int32_t* __restrict__ headslot, int2* __restrict__ out,
                                int32_t* __restrict__ nh) {

@@ -3,12 +3,13 @@
 //
 // Split of the product by term.  The h most frequent terms ("head", chosen at
 // create time from the document frequencies of A) hold a dense-ish block of
-// A^T (Large: the 512 most frequent terms hold 44 % of the stored entries at
-// 13 % density), so their part of the product is a dense GEMM
+// A^T (Large: the 1024 most frequent terms hold 52 % of the stored entries at
+// 7.6 % density), so their part of the product is a GEMM
 //     LS_head[docs, :] = A^T[docs, head] * Z[head, :]
-// that runs on the 5th-generation tensor cores (tcgen05.mma, accumulator in
-// TMEM).  The remaining "tail" terms keep the row-gather kernel
-// (k_spmm_docs.cuh) with the head terms masked out of its active-term bitmap.
+// on the 5th-generation tensor cores (tcgen05.mma, accumulator in TMEM).  The
+// remaining "tail" terms keep the row-gather kernel (k_spmm_tail.cuh), which
+// reads only the tail part of every row (head entries are stored first, sorted
+// by head slot, with the slot in place of the term id: k_reorder_head).
 //
 // Precision (fp32-level, BJ:5 "relative 1e-5"): every operand is split into
 // two fp16 halves, x = x_hi + x_lo with x_hi = fp16(x), x_lo = fp16(x - x_hi)
@@ -18,16 +19,22 @@
 // a_lo z_hi in fp32 (the dropped a_lo z_lo is < 2^-22 relative); the epilogue
 // multiplies by the inverse power of two (exact).
 //
+// The A^T tiles are built ON CHIP from the sparse head entries (a dense copy
+// would cost 4 bytes per cell: 4 GB per pass at h = 1024 for 7.6 % density).
+// At create time the head entries are copied into per-(tile, chunk) segments
+// (k_head_count / k_head_fill): entry = (row in tile * 64 + slot in chunk,
+// value), so one chunk of one tile is one contiguous run.  Per chunk, 128
+// producer threads zero a shared-memory stage (one row each), read the run
+// coalesced and scatter it as fp16 hi/lo in the K-major layout, while one of
+// them bulk-copies (TMA engine) the matching Z chunk.
 // Layouts (K-major, no swizzle; core matrix = 8 rows x 16 bytes):
-//   head tiles  [tile of 128 documents][chunk of 64 head terms] -> 32 KB =
-//               hi block (128 x 64 fp16) then lo block, built once at create;
-//   Z chunks    [chunk][hi block (kn x 64 fp16), lo block], rebuilt per half-step.
-// Pipeline (one CTA per SM, persistent over document tiles): warp 0 issues
-// 1-D bulk copies (TMA engine) of a tile chunk and the matching Z chunk into a
-// STAGES-deep shared-memory ring; warp 1 (one thread) issues the MMAs into one
-// of two TMEM accumulators; warps 2-5 drain the other accumulator into the LS
-// buffer (column-major, coalesced stores); the gather kernel runs next and adds
-// the tail part (its read of X is cheap next to its k-wide gathers).
+//   A stage   hi block (128 x 64 fp16) then lo block      (32 KB)
+//   Z chunks  [chunk][hi block (kn x 64 fp16), lo block], rebuilt per half-step.
+// Roles (one CTA per SM, persistent over document tiles): a loader thread
+// bulk-copies runs + Z chunks STAGES ahead, warps 0-3 build A stages, warp 4
+// (one thread) issues the MMAs into one of two TMEM accumulators, warps 5-8
+// drain the other accumulator and add it to the LS buffer the tail gather wrote
+// (column-major: 32 consecutive rows per warp access, coalesced).
 #pragma once
 #include <cuda_fp16.h>
 
@@ -40,7 +47,7 @@ constexpr int kHeadK = 64;                                   // head terms per c
 constexpr int kHeadM = 128;                                  // documents per tile (MMA M)
 constexpr uint32_t kHeadABytes = kHeadM * kHeadK * 2 * 2;    // hi + lo fp16 = 32 KB
 constexpr uint32_t kHeadAHalf = kHeadM * kHeadK * 2;         // 16 KB
-constexpr int kHeadThreads = 192;                            // producer, MMA, 4 epilogue warps
+constexpr int kHeadMax = 4096;                               // largest head (terms)
 
 // exponent e such that x * 2^e lies in [2^14, 2^15) (0 for x == 0)
 ESNMF_DEV int head_exp(float x) {
@@ -58,34 +65,6 @@ __global__ void k_absmax_ent(const int2* __restrict__ ent, int64_t nnz, unsigned
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
-
-// dense head tiles from the head prefix of the document rows (warp per row);
-// buffer zeroed first
-__global__ void k_head_build(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
-                             const int2* __restrict__ ent, int64_t rows,
-                             const int32_t* __restrict__ headslot, const unsigned* __restrict__ amax_bits,
-                             int nchunks, uint8_t* __restrict__ atile) {
-  const int eA = head_exp(__uint_as_float(*amax_bits));
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-    const int64_t s = ptr[row], e = s + nh[row];  // head entries lead the row (k_reorder_head)
-    const int64_t tile = row / kHeadM;
-    const int r = (int)(row % kHeadM);
-    for (int64_t q = s + lane; q < e; q += 32) {
-      const int2 en = ent[q];
-      const int slot = headslot[en.x];
-      if (slot < 0) continue;
-      const float a = ldexpf(__int_as_float(en.y), eA);
-      const __half hi = __float2half_rn(a);
-      const __half lo = __float2half_rn(a - __half2float(hi));
-      uint8_t* b = atile + ((size_t)tile * nchunks + (slot / kHeadK)) * kHeadABytes;
-      const uint32_t off = tc::kmajor_off16(r, slot % kHeadK, kHeadK);
-      *reinterpret_cast<__half*>(b + off) = hi;
-      *reinterpret_cast<__half*>(b + kHeadAHalf + off) = lo;
-    }
-  }
 }
 
 // clear the head terms' bits from the gather kernel's active-term bitmap
@@ -132,27 +111,105 @@ __global__ void k_zhead_prep(const float* __restrict__ Z, int zs, const int32_t*
   }
 }
 
-ESNMF_DEV uint32_t head_stage_bytes(int kn) { return (kHeadABytes + (uint32_t)kn * kHeadK * 4 + 1023u) & ~1023u; }
+// dense A^T head tiles for the first nd chunks (the densest slots, where a run
+// would hold more entries than a stage can stage); warp per document
+__global__ void k_head_dense(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
+                             const int2* __restrict__ ent, int64_t rows, const int32_t* __restrict__ headslot,
+                             const unsigned* __restrict__ amax_bits, int nd, uint8_t* __restrict__ atile) {
+  const int eA = head_exp(__uint_as_float(*amax_bits));
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
+    const int64_t s = ptr[row], e = s + nh[row], tile = row / kHeadM;
+    const int r = (int)(row % kHeadM);
+    for (int64_t q = s + lane; q < e; q += 32) {
+      const int2 en = ent[q];
+      const int sl = headslot[en.x];
+      if (sl >= nd * kHeadK) continue;
+      const float a = ldexpf(__int_as_float(en.y), eA);
+      const __half hi = __float2half_rn(a);
+      const __half lo = __float2half_rn(a - __half2float(hi));
+      uint8_t* b = atile + ((size_t)tile * nd + sl / kHeadK) * kHeadABytes;
+      const uint32_t off = tc::kmajor_off16(r, sl % kHeadK, kHeadK);
+      *reinterpret_cast<__half*>(b + off) = hi;
+      *reinterpret_cast<__half*>(b + kHeadAHalf + off) = lo;
+    }
+  }
+}
 
-// X[c][row] = A^T[row, head] Z[head, c] for every document row of the shard (the
-// gather kernel then adds the tail terms: k_spmm_docs<.., ACCUM = true>)
+// per (tile, chunk) counts of head entries (warp per document; head entries
+// lead each row, k_reorder_head)
+__global__ void k_head_count(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
+                             const int2* __restrict__ ent, int64_t rows, const int32_t* __restrict__ headslot,
+                             int nd, int nsp, unsigned long long* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
+    const int64_t s = ptr[row], e = s + nh[row], tile = row / kHeadM;
+    for (int64_t q = s + lane; q < e; q += 32) {
+      const int ch = headslot[ent[q].x] / kHeadK - nd;  // sparse chunk index
+      if (ch >= 0) atomicAdd(&cnt[tile * nsp + ch], 1ull);
+    }
+  }
+}
+
+// scatter into the segments: (row in tile << 6 | slot in chunk, value); the
+// order inside a segment is irrelevant (each entry lands in its own cell)
+__global__ void k_head_fill(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
+                            const int2* __restrict__ ent, int64_t rows, const int32_t* __restrict__ headslot,
+                            int nd, int nsp, unsigned long long* __restrict__ cursor, int2* __restrict__ hseg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
+    const int64_t s = ptr[row], e = s + nh[row], tile = row / kHeadM;
+    const int r = (int)(row % kHeadM);
+    for (int64_t q = s + lane; q < e; q += 32) {
+      const int2 en = ent[q];
+      const int sl = headslot[en.x];
+      const int ch = sl / kHeadK - nd;
+      if (ch < 0) continue;
+      const unsigned long long pos = atomicAdd(&cursor[tile * nsp + ch], 1ull);
+      hseg[pos] = make_int2((r << 6) | (sl % kHeadK), en.y);
+    }
+  }
+}
+
+constexpr int kHeadProd = 128;                         // producer threads
+constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
+constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
+constexpr int kHeadOtfThreads = kHeadProd + 32 + 128 + 32;
+
+// stage = [A hi|lo 32 KB][Z chunk hi|lo][raw entries of the chunk's run]
+ESNMF_DEV uint32_t head_stage_bytes(int kn) {
+  return (kHeadABytes + (uint32_t)kn * kHeadK * 4 + kHeadRawBytes + 1023u) & ~1023u;
+}
+
+// X[c][row] += A^T[row, head] Z[head, c] for every document row of the shard
+// (the tail gather stored its part first: k_spmm_tail<.., ACCUM = false>).
+// Roles: warp 9 (one thread) bulk-copies each (tile, chunk) run of head
+// entries and the Z chunk into a stage (TMA engine, STAGES ahead); warps 0-3
+// zero the stage's A block and scatter the run into it; warp 4 (one thread)
+// issues the MMAs; warps 5-8 drain TMEM into X.
 template <int STAGES>
-__global__ void __launch_bounds__(kHeadThreads, 1)
-    k_vhead_tc(const uint8_t* __restrict__ atile, const uint8_t* __restrict__ zbuf,
-               const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
-               int acc_cols, float* __restrict__ X, int64_t ldx) {
+__global__ void __launch_bounds__(kHeadOtfThreads, 1)
+    k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
+                const int2* __restrict__ hseg, const unsigned* __restrict__ amax_bits, const uint8_t* __restrict__ zbuf,
+                const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
+                int acc_cols, float* __restrict__ X, int64_t ldx) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t zhalf = (uint32_t)kn * kHeadK * 2;
   const uint32_t zbytes = 2 * zhalf;
   const uint32_t stage_bytes = head_stage_bytes(kn);
+  const uint32_t raw_off = kHeadABytes + zbytes;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(&full_bar[s], 1);
+      tc::mbar_init(&raw_full[s], 1);
+      tc::mbar_init(&a_full[s], kHeadProd);
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -161,28 +218,81 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     }
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
+  if (warp == 4) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- producer: bulk copies into the smem ring ----
+  if (warp == 9) {
+    if (lane == 0) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int q = 0; q < nchunks; ++q) {
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = base + stage * stage_bytes;
-          tc::mbar_arrive_expect_tx(&full_bar[stage], kHeadABytes + zbytes);
-          tc::bulk_g2s(sa, atile + ((size_t)tile * nchunks + q) * kHeadABytes, kHeadABytes, &full_bar[stage]);
-          tc::bulk_g2s(sa + kHeadABytes, zbuf + (size_t)q * zbytes, zbytes, &full_bar[stage]);
+          uint8_t* st = base + stage * stage_bytes;
+          if (q < nd) {  // dense chunk: the A tile itself
+            tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + kHeadABytes);
+            tc::bulk_g2s(st, atile + ((size_t)tile * nd + q) * kHeadABytes, kHeadABytes, &raw_full[stage]);
+          } else {         // sparse chunk: its run of entries
+            const int64_t si = tile * (nchunks - nd) + (q - nd);
+            const int64_t sb = hoff[si], se = hoff[si + 1];
+            const int64_t a = sb & ~(int64_t)1;  // 16-byte aligned start
+            const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);  // even, capped
+            const uint32_t rb = (uint32_t)(b - a) * 8u;
+            tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + rb);
+            if (rb) tc::bulk_g2s(st + raw_off, hseg + a, rb, &raw_full[stage]);
+          }
+          tc::bulk_g2s(st + kHeadABytes, zbuf + (size_t)q * zbytes, zbytes, &raw_full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp < 4) {  // ---- producers: zero + scatter one tile chunk per stage ----
+    const int p = threadIdx.x;
+    const int eA = head_exp(__uint_as_float(*amax_bits));
+    int stage = 0;
+    uint32_t phase = 0;
+    auto put = [&](uint8_t* sa, int2 en) {
+      const float a = ldexpf(__int_as_float(en.y), eA);
+      const __half hi = __float2half_rn(a);
+      const __half lo = __float2half_rn(a - __half2float(hi));
+      const uint32_t off = tc::kmajor_off16(en.x >> 6, en.x & 63, kHeadK);
+      *reinterpret_cast<__half*>(sa + off) = hi;
+      *reinterpret_cast<__half*>(sa + kHeadAHalf + off) = lo;
+    };
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int q = 0; q < nchunks; ++q) {
+        uint8_t* sa = base + stage * stage_bytes;
+        tc::mbar_wait(&raw_full[stage], phase);  // also: the MMAs of this stage's last round are done
+        if (q < nd) {  // dense chunk: bulk-copied A tile, nothing to build
+          tc::mbar_arrive(&a_full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
+        const int64_t si = tile * (nchunks - nd) + (q - nd);
+        const int64_t sb = hoff[si], se = hoff[si + 1];
+        const int64_t a = sb & ~(int64_t)1;
+        const int64_t cap = a + (int64_t)kHeadRaw;  // staged: [a, min(se, cap)); the rest from global
+        const int2* raw = reinterpret_cast<const int2*>(sa + raw_off);
+        // zero row p of the A block (8 x 16 B in each of the hi and lo blocks)
+#pragma unroll
+        for (int j = 0; j < kHeadK / 8; ++j) {
+          const uint32_t off = (uint32_t)((p >> 3) * (kHeadK / 8) * 128 + j * 128 + (p & 7) * 16);
+          *reinterpret_cast<uint4*>(sa + off) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(sa + kHeadAHalf + off) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kHeadProd) : "memory");
+        const int64_t se_s = min(se, cap);
+        for (int64_t i = sb + p; i < se_s; i += kHeadProd) put(sa, raw[i - a]);
+        for (int64_t i = cap + p; i < se; i += kHeadProd) put(sa, __ldcs(hseg + i));  // long runs only
+        tc::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+        tc::mbar_arrive(&a_full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 4) {
     if (lane == 0) {  // ---- MMA issuer ----
       const uint32_t idesc = tc::make_idesc_f16(kHeadM, kn);
       int stage = 0, acc = 0;
@@ -192,7 +302,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         tc::fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * acc_cols);
         for (int q = 0; q < nchunks; ++q) {
-          tc::mbar_wait(&full_bar[stage], phase);
+          tc::mbar_wait(&a_full[stage], phase);
           tc::fence_after();
           const uint32_t ah = tc::smem_u32(base + stage * stage_bytes);
           const uint32_t al = ah + kHeadAHalf, zh = ah + kHeadABytes, zl = zh + zhalf;
@@ -205,7 +315,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             tc::mma_f16(d, dah, dzl, idesc, 1);
             tc::mma_f16(d, dal, dzh, idesc, 1);
           }
-          tc::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
+          tc::mma_commit(&empty_bar[stage]);  // frees the stage when these MMAs finish
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc::mma_commit(&tfull[acc]);          // accumulator ready for the epilogue
@@ -213,7 +323,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         if (acc == 0) aphase ^= 1;
       }
     }
-  } else {  // ---- epilogue: TMEM -> registers -> X += head part ----
+  } else {  // ---- epilogue (warps 5-8): TMEM -> registers -> X += ----
     const int lg = warp & 3;  // TMEM lanes 32*lg .. 32*lg+31
     int acc = 0;
     uint32_t aphase = 0;
@@ -226,11 +336,14 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();
-        if (row < rows) {
+        if (row < rows) {  // X += head part: 16 independent loads, then the stores
+          float x[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = c0 + j < k ? X[(int64_t)(c0 + j) * ldx + row] : 0.f;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int c = c0 + j;
-            if (c < k) X[(int64_t)c * ldx + row] = __uint_as_float(v[j]) * colscale[c];  // exact 2^-e scale
+            if (c < k) X[(int64_t)c * ldx + row] = fmaf(__uint_as_float(v[j]), colscale[c], x[j]);  // exact 2^-e
           }
         }
       }
@@ -242,7 +355,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 4) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 2 * acc_cols);
   }

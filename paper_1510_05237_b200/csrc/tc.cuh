@@ -137,6 +137,12 @@ ESNMF_DEV void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
                : "memory");
 }
 
+// add to the transaction count of the current phase without arriving
+ESNMF_DEV void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+               : "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA engine, no tensor map); completes `bytes`
 // of the mbarrier's transaction count.  16-byte aligned, bytes % 16 == 0.
 ESNMF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
