@@ -44,6 +44,15 @@ def parse():
     return p.parse_args()
 
 
+def measured_bf16_tflops():
+    """fp16 dense tensor peak = the measured bf16 one (same rate on B200)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("bf16_tflops", 2250.0), "MEASURED_PEAKS.json bf16_tflops (burst; fp16 runs at the bf16 rate)"
+    return 2250.0, "fallback B200_PROFILING.md (2.25 PFLOP/s dense bf16/fp16)"
+
+
 def measured_peaks() -> dict:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -132,10 +141,15 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # per-phase algorithmic bytes per launch (8 B per stored entry of
-# A or A^T per side, plus the row pointers)
-def algorithmic_bytes(phase: str, cfg) -> float | None:
-    if phase == "V.spmm":
-        return 8.0 * cfg.nnz + 8.0 * (cfg.m + 1)
+# A or A^T streamed, row pointers, the LS rows written).
+# `split` = (head terms, stored entries of A^T in head terms, dense head chunks)
+def algorithmic_bytes(phase: str, cfg, split) -> float | None:
+    h, head_nnz, nd = split
+    if phase == "V.spmm":   # tail gather: tail entries + row pointers + nh + LS stores
+        return 8.0 * (cfg.nnz - head_nnz) + 8.0 * (cfg.m + 1) + 4.0 * cfg.m + 4.0 * cfg.k * cfg.m
+    if phase == "V.head":   # head GEMM: dense tiles + tiled sparse head entries + LS read-modify-write
+        tiles = -(-cfg.m // 128)
+        return 32768.0 * tiles * nd + 8.0 * head_nnz + 8.0 * cfg.k * cfg.m
     if phase == "U.spmm":
         return 8.0 * cfg.nnz + 8.0 * (cfg.n + 1)
     if phase == "V.select":
@@ -143,6 +157,20 @@ def algorithmic_bytes(phase: str, cfg) -> float | None:
     if phase == "U.select":
         return 4.0 * cfg.k * cfg.n
     return None
+
+
+def head_split(g, cfg, h: int, nd_default: int = 4):
+    """Head size and the stored entries it covers (the library's rule: terms by
+    document frequency, descending, stable) -- for the roofline accounting only."""
+    import torch
+
+    if h <= 0:
+        return (0, 0, 0)
+    df = (g["a_ptr"][1:] - g["a_ptr"][:-1]).to(torch.int64)
+    order = torch.argsort(-df, stable=True)
+    head_nnz = int(df[order[:h]].sum().item())
+    nd = min(int(os.environ.get("ESNMF_HEAD_DENSE", nd_default)), h // 64)
+    return (h, head_nnz, nd)
 
 
 def oracle_sample_step(g, U, V, cfg, frac: float) -> tuple[float, float]:
@@ -240,27 +268,46 @@ def run_ours(args):
     assert all(np.isfinite(r["E"]) for r in recs)
     value = args.steps / (ms / 1e3)  # iterations of the ONE global factorisation per second
 
-    # roofline of the dominant phase
+    # roofline of the dominant phase (and of the tensor-core head kernel)
     peaks = measured_peaks()
-    dom = max(phases.items(), key=lambda kv: kv[1][1])
-    name, (calls, pms) = dom
-    per_launch_ms = pms / max(calls, 1)
-    ab = algorithmic_bytes(name, cfg)
-    if ab is not None:
+    split = head_split(g, cfg, s.info()["head_terms"])
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+
+    def roofline(name):
+        calls, pms = phases[name]
+        per_launch_ms = pms / max(calls, 1)
+        ab = algorithmic_bytes(name, cfg, split)
+        if ab is None:
+            return None
         ab /= world  # this rank's shard of the operator
-    roof = None
-    if ab is not None:
         ach = ab / (per_launch_ms / 1e3) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_src": peaks["src"],
-                "alg_bytes_per_launch": ab, "ms_per_launch": round(per_launch_ms, 4),
-                "share_of_step": round(pms / ms, 4)}
-        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
-            tr = json.load(open(tpath)).get(f"{cfg.name}:{name}")
-            if tr:
-                roof["traffic"] = tr["bytes_per_launch"]
-                roof["traffic_src"] = tr["source"]
+        r = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_src": peaks["src"],
+             "alg_bytes_per_launch": ab, "ms_per_launch": round(per_launch_ms, 4), "share_of_step": round(pms / ms, 4)}
+        tr = traffic.get(f"{cfg.name}:{name}")
+        if tr:
+            r["traffic"] = tr["bytes_per_launch"]
+            r["traffic_src"] = tr["source"]
+        return r
+
+    dom = max(phases.items(), key=lambda kv: kv[1][1])[0]
+    roof = roofline(dom)
+    kernels = {}
+    for nm in ("V.spmm", "V.head", "U.spmm", "V.select"):
+        if nm in phases and phases[nm][0]:
+            kernels[nm] = roofline(nm)
+    if split[0] > 0 and "V.head" in phases and phases["V.head"][0]:
+        # tensor view of the head GEMM: MMA flops issued (3 fp16 passes, M = 128-row tiles, N = k rounded to 16)
+        calls, pms = phases["V.head"]
+        tiles = -(-(cfg.m // world) // 128)
+        kn = -(-cfg.k // 16) * 16
+        fl = 3 * 2.0 * tiles * 128 * split[0] * kn
+        tf = fl / (pms / max(calls, 1) / 1e3) / 1e12
+        pk = measured_bf16_tflops()
+        kernels["V.head.tensor"] = {"bound": "tensor", "achieved": round(tf, 1), "peak": pk[0], "unit": "TFLOP/s",
+                                    "frac": round(tf / pk[0], 4), "peak_src": pk[1],
+                                    "flops_per_launch": fl, "head_terms": split[0], "head_nnz": split[1]}
     phase_table = {k: {"calls": c, "ms_per_call": round(v / max(c, 1), 4), "share": round(v / ms, 4)}
                    for k, (c, v) in phases.items() if c}
     # whole-iteration algorithmic bytes: 16 nnz + 8 (n + m + 2) + 32 k t
@@ -324,6 +371,7 @@ def run_ours(args):
                        f"{world} GPUs: A / A^T row-sharded, top-t candidates allgathered, T allreduced (NCCL)"},
             "iteration_gbs_algorithmic": round(it_gbs, 1),
             "roofline": roof,
+            "kernels": kernels,
             "phases": phase_table,
             "cpu_baseline": cpu,
             "e2e": e2e,
