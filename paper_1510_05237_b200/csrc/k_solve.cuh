@@ -21,7 +21,12 @@ inline bool sweep_packed(int k) { return (int64_t)k * k * 8 + k * 8 > 200 * 1024
 // k <= 128: the whole matrix lives in registers.  Thread (ty = warp, tx = lane)
 // owns elements (i, j) = (ty + 32a, tx + 32b), a, b < JB.  Per pivot the owner
 // warp of row p publishes it to shared memory (double-buffered, so one barrier
-// per pivot suffices), every thread updates its JB x JB block in registers.
+// per pivot suffices); every thread applies the rank-1 update
+//   a_ij <- a_ij - (a_ip / d) a_pj
+// to its whole block (which turns row p and column p into zeros) and then the
+// owners of row p / column p overwrite them with a_pj / d, a_ip / d, -1 / d.
+// Row blocks a with ty + 32a >= k hold only padding and are skipped (warp-
+// uniform).  ~1 DFMA per element and pivot instead of a select chain.
 template <int JB>
 __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ G, int k, double rho,
                                                      double* __restrict__ W, double* __restrict__ eps_out,
@@ -41,14 +46,17 @@ __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ 
       const int i = ty + 32 * a, j = tx + 32 * b;
       r[a][b] = (i < k && j < k) ? G[(int64_t)i * k + j] + (i == j ? eps : 0.0) : 0.0;
     }
+  int na = 0;  // live row blocks of this warp
+#pragma unroll
+  for (int a = 0; a < JB; ++a) na += (ty + 32 * a < k);
   bool bad = false;
   for (int p = 0; p < k; ++p) {
     double* v = vbuf[p & 1];
-    if (ty == (p & 31)) {  // owner warp publishes the old row p
-      const int ap = p >> 5;
+    const int pa = p >> 5, pl = p & 31;
+    if (ty == pl) {  // owner warp publishes the old row p
 #pragma unroll
       for (int a = 0; a < JB; ++a)
-        if (a == ap)
+        if (a == pa)
 #pragma unroll
           for (int b = 0; b < JB; ++b) v[tx + 32 * b] = r[a][b];
     }
@@ -59,19 +67,30 @@ __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ 
       d = 1.0;
     }
     const double inv = 1.0 / d;
-    double vj[JB];
+    double vj[JB], vi[JB];
 #pragma unroll
     for (int b = 0; b < JB; ++b) vj[b] = v[tx + 32 * b];
 #pragma unroll
-    for (int a = 0; a < JB; ++a) {
-      const int i = ty + 32 * a;
-      const double vi = v[i < 32 * JB ? i : 0] * inv;
+    for (int a = 0; a < JB; ++a) vi[a] = v[min(ty + 32 * a, 32 * JB - 1)] * inv;  // a_ip / d (symmetric)
 #pragma unroll
-      for (int b = 0; b < JB; ++b) {
-        const int j = tx + 32 * b;
-        if (i == p) r[a][b] = j == p ? -inv : vj[b] * inv;
-        else r[a][b] = j == p ? vi : fma(-vi, vj[b], r[a][b]);
-      }
+    for (int a = 0; a < JB; ++a)
+      if (a < na)
+#pragma unroll
+        for (int b = 0; b < JB; ++b) r[a][b] = fma(-vi[a], vj[b], r[a][b]);
+    // row p: a_pj / d (and -1/d on the diagonal); column p: a_ip / d
+    if (ty == pl) {
+#pragma unroll
+      for (int a = 0; a < JB; ++a)
+        if (a == pa)
+#pragma unroll
+          for (int b = 0; b < JB; ++b) r[a][b] = vj[b] * inv;
+    }
+    if (tx == pl) {
+#pragma unroll
+      for (int a = 0; a < JB; ++a)
+#pragma unroll
+        for (int b = 0; b < JB; ++b)
+          if (b == pa) r[a][b] = (ty + 32 * a == p) ? -inv : vi[a];
     }
   }
   if (bad && threadIdx.x == 0) atomicExch(singular, 1);
