@@ -515,13 +515,15 @@ void uside_scatter_launch(esnmf_t* h) {
     CK(cudaFuncSetAttribute(k_uside_finish_rt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_uside_finish_rt<1><<<grid_for(rgroups, 8, (int64_t)h->num_sms * 3), 256, smem, h->stream>>>(
         su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
-  } else {
+  } else if ((int)smem <= h->smem_optin) {
     CK(cudaFuncSetAttribute(k_uside_finish_rt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_uside_finish_rt<2><<<grid_for(rgroups, 8, (int64_t)h->num_sms * 1), 256, smem, h->stream>>>(
         su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
   }
+  // fp64 (Y W) for ill-conditioned systems -- and always when W does not fit in shared memory (k > ~224)
+  const bool fits = (int)smem <= h->smem_optin;
   k_uside_finish<CQ><<<grid_for(su.rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
-      su.rows, h->rsum_max, h->vmax, h->W, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
+      su.rows, h->rsum_max, h->vmax, h->W, h->k, h->kpad, h->Yq, su.X, su.ldx, fits ? h->flags + 3 : nullptr);
   CKL("uside_scatter");
 }
 

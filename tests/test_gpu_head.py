@@ -37,18 +37,20 @@ def v_side_parity(s, g, cfg, k, t):
     return err
 
 
-@pytest.mark.parametrize("head", [64, 192, 1024])
-def test_tiny_head_sizes_first_and_late(head):
+@pytest.mark.parametrize("head,dense", [(64, 0), (64, 1), (192, 4), (1024, 2), (1024, 0)])
+def test_tiny_head_sizes_first_and_late(head, dense, monkeypatch):
+    """dense = chunks stored as dense tiles (the rest built on chip from entry runs)."""
+    monkeypatch.setenv("ESNMF_HEAD_DENSE", str(dense))
     g = synth.generate(TINY)
     s = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, head_terms=head)
-    assert s.info()["head_terms"] == min(head, 1024)
+    assert s.info()["head_terms"] == head
     v_side_parity(s, g, TINY, TINY.k, TINY.t)      # from dense U0
     s.half_step(ESNMF_SIDE_U)
     s.iterate(5)
     v_side_parity(s, g, TINY, TINY.k, TINY.t)      # from a sparse late U
 
 
-@pytest.mark.parametrize("k", [1, 16, 33, 100])
+@pytest.mark.parametrize("k", [1, 16, 33, 100, 200, 256])
 def test_tiny_head_odd_ranks(k):
     """kn = k rounded up to 16: padding columns of the MMA must not leak."""
     g = synth.generate(TINY)
@@ -99,3 +101,14 @@ def test_head_deterministic():
     assert np.array_equal(outs[0][0], outs[1][0])
     for x, y in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(x, y)
+
+
+def test_large_k_paths_medium():
+    """k = 200 (Box's rank): 2-float4-per-lane tail gather, kn = 208 MMA with 256-column
+    accumulators, the packed fp64 sweep and the 2-chunk U-side register tiles."""
+    cfg = MEDIUM.with_(k=200, t=300)
+    g = synth.generate(MEDIUM)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed)
+    assert s.info()["head_terms"] >= 64
+    s.iterate(2)
+    v_side_parity(s, g, cfg, cfg.k, cfg.t)
