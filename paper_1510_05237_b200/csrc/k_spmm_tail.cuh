@@ -301,14 +301,17 @@ __global__ void __launch_bounds__(kTailThreads, 3)
           for (int q = 0; q < RG; ++q)
             v[q] = u == 0 ? res[q][j].x : u == 1 ? res[q][j].y : u == 2 ? res[q][j].z : res[q][j].w;
           float* xo = X + (int64_t)(c0 + u) * ldx + r0;
-          if (r0 + RG <= rows) {  // ldx and r0 are multiples of RG: one aligned vector access
-            if constexpr (RG == 4) {
-              float4 o = make_float4(v[0], v[1], v[2], v[3]);
-              if constexpr (ACCUM) {
-                const float4 pv = *reinterpret_cast<const float4*>(xo);
-                o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w;
+          if (r0 + RG <= rows) {  // ldx and r0 are multiples of RG: aligned vector accesses
+            if constexpr (RG % 4 == 0) {
+#pragma unroll
+              for (int q4 = 0; q4 < RG; q4 += 4) {
+                float4 o = make_float4(v[q4], v[q4 + 1], v[q4 + 2], v[q4 + 3]);
+                if constexpr (ACCUM) {
+                  const float4 pv = *reinterpret_cast<const float4*>(xo + q4);
+                  o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w;
+                }
+                *reinterpret_cast<float4*>(xo + q4) = o;
               }
-              *reinterpret_cast<float4*>(xo) = o;
             } else {
               float2 o = make_float2(v[0], v[1]);
               if constexpr (ACCUM) {

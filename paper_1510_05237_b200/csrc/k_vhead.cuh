@@ -178,6 +178,7 @@ constexpr int kHeadProd = 128;                         // producer threads
 constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
 constexpr int kHeadOtfThreads = kHeadProd + 32 + 128 + 32;
+constexpr int kHeadPf = 6;                             // rounds of L2 prefetch ahead of the copies
 
 // stage = [A hi|lo 32 KB][Z chunk hi|lo][raw entries of the chunk's run]
 ESNMF_DEV uint32_t head_stage_bytes(int kn) {
@@ -228,8 +229,28 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     if (lane == 0) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
       int stage = 0;
       uint32_t phase = 0;
+      // L2 prefetch kHeadPf rounds ahead of the copies: a stage's copy is issued
+      // only when the MMAs of the round STAGES earlier finish, so its latency is
+      // on the critical path; from L2 it is ~1/3 of the HBM latency.
+      int64_t pf_tile = blockIdx.x;
+      int pf_q = 0;
+      auto prefetch_next = [&]() {
+        if (pf_tile >= ntiles) return;
+        if (pf_q < nd) {
+          tc::bulk_prefetch_l2(atile + ((size_t)pf_tile * nd + pf_q) * kHeadABytes, kHeadABytes);
+        } else {
+          const int64_t si = pf_tile * (nchunks - nd) + (pf_q - nd);
+          const int64_t sb = hoff[si], se = hoff[si + 1];
+          const int64_t a = sb & ~(int64_t)1;
+          const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);
+          if (b > a) tc::bulk_prefetch_l2(hseg + a, (uint32_t)(b - a) * 8u);
+        }
+        if (++pf_q == nchunks) { pf_q = 0; pf_tile += gridDim.x; }
+      };
+      for (int i = 0; i < kHeadPf; ++i) prefetch_next();
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int q = 0; q < nchunks; ++q) {
+          prefetch_next();
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = base + stage * stage_bytes;
           if (q < nd) {  // dense chunk: the A tile itself

@@ -152,6 +152,11 @@ ESNMF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb
       : "memory");
 }
 
+// bulk prefetch of global memory into L2 (no completion mechanism)
+ESNMF_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // 16 consecutive fp32 columns of this thread's TMEM lane (no wait: call tmem_wait_ld)
 ESNMF_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
