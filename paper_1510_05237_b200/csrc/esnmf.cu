@@ -128,6 +128,7 @@ struct esnmf {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_ufork = nullptr, ev_ujoin = nullptr, ev_mfork = nullptr, ev_mjoin = nullptr;
   bool aux_pending = false;
+  bool u_prefork = false;        // the U side's Gram + solve already enqueued on aux (after V's row view)
   int64_t n = 0, m = 0, nnz = 0;
   int k = 0, kpad = 0;
   int64_t t = 0;  // < 0 unlimited
@@ -777,8 +778,8 @@ Factor& half_step(esnmf_t* h, int s) {
   const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
   const bool overlap_u = s == ESNMF_SIDE_U && h->world == 1;    // Gram + solve on aux, beside the scatter
   if (s == ESNMF_SIDE_U) join_metrics(h);  // (only pending after a bare half_step call)
-  if (overlap_u) fork_to_aux(h, h->ev_ufork);
-  {
+  if (!(overlap_u && h->u_prefork)) {
+    if (overlap_u) fork_to_aux(h, h->ev_ufork);
     OnStream os(h, overlap_u ? h->aux : h->stream);
     if (!(s == ESNMF_SIDE_V && h->gramU_valid)) {                 // a1: P:63 / P:64
       Phase ph(h, p0 + 0);
@@ -787,6 +788,7 @@ Factor& half_step(esnmf_t* h, int s) {
     { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }               // a2
     if (overlap_u) uside_w_prep(h);
   }
+  h->u_prefork = false;
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
   { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
   if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
@@ -802,6 +804,17 @@ Factor& half_step(esnmf_t* h, int s) {
   {
     Phase ph(h, p0 + 5);
     factor_build_rows(h, out, steady_maxcol(h, out.rows));
+    if (s == ESNMF_SIDE_V && h->world == 1) {
+      // the U side's a1 + a2 need only V's row view: start them now on aux,
+      // beside V's row-CSR build and the U side's scatter
+      fork_to_aux(h, h->ev_ufork);
+      OnStream os(h, h->aux);
+      Side& su = h->side[ESNMF_SIDE_U];
+      { Phase ph2(h, kUGram); gram(h, out, su.G); }
+      { Phase ph2(h, kUSolve); sweep(h, su.G, su.eps); }
+      uside_w_prep(h);
+      h->u_prefork = true;
+    }
     if (s == ESNMF_SIDE_V) vrows_build(h);
   }
   if (s == ESNMF_SIDE_U) {
@@ -1206,7 +1219,11 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
       h->own_stream = true;
     }
-    CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    {  // highest priority: its one-CTA solves must not queue behind the main stream's grids
+      int least = 0, greatest = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CK(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, greatest));
+    }
     for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
@@ -1357,6 +1374,7 @@ esnmf_status esnmf_half_step(esnmf_t* h, int32_t side) {
     set_device(h);
     half_step(h, side);
     join_metrics(h);
+    if (h->u_prefork) join_from_aux(h, h->ev_ujoin);  // callers may read G_V / W next
   });
 }
 
@@ -1460,6 +1478,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
   if (nnz > f.cap) { g_last_error = "esnmf_set_factor: more entries than the factor capacity"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
+    CK(cudaStreamSynchronize(h->aux));
     if (side == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, f);
     CK(cudaMemcpyAsync(f.colptr, cp.data(), sizeof(int64_t) * (h->k + 1), cudaMemcpyHostToDevice, h->stream));
@@ -1468,9 +1487,13 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
       CK(cudaMemcpyAsync(f.val, val, sizeof(float) * nnz, cudaMemcpyHostToDevice, h->stream));
     }
     factor_build_rows(h, f, std::max<int64_t>(maxcol, 1));
-    if (side == ESNMF_SIDE_V) vrows_build(h);
+    if (side == ESNMF_SIDE_V) {
+      vrows_build(h);
+      h->u_prefork = false;  // a pre-started U-side Gram belongs to the old V
+    }
     if (side == ESNMF_SIDE_U) h->gramU_valid = false;
     CK(cudaStreamSynchronize(h->stream));
+    CK(cudaStreamSynchronize(h->aux));
   });
 }
 
