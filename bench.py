@@ -159,7 +159,7 @@ def algorithmic_bytes(phase: str, cfg, split) -> float | None:
     return None
 
 
-def head_split(g, cfg, h: int, nd_default: int = 4):
+def head_split(g, cfg, h: int, nd: int):
     """Head size and the stored entries it covers (the library's rule: terms by
     document frequency, descending, stable) -- for the roofline accounting only."""
     import torch
@@ -169,7 +169,6 @@ def head_split(g, cfg, h: int, nd_default: int = 4):
     df = (g["a_ptr"][1:] - g["a_ptr"][:-1]).to(torch.int64)
     order = torch.argsort(-df, stable=True)
     head_nnz = int(df[order[:h]].sum().item())
-    nd = min(int(os.environ.get("ESNMF_HEAD_DENSE", nd_default)), h // 64)
     return (h, head_nnz, nd)
 
 
@@ -270,7 +269,7 @@ def run_ours(args):
 
     # roofline of the dominant phase (and of the tensor-core head kernel)
     peaks = measured_peaks()
-    split = head_split(g, cfg, s.info()["head_terms"])
+    split = head_split(g, cfg, s.info()["head_terms"], s.info()["head_dense"])
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
 

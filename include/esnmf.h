@@ -181,6 +181,7 @@ typedef struct {
   double normA2;            /* ||A||_F^2 */
   int64_t launches;         /* CUDA kernels enqueued by this handle so far */
   int32_t head_terms;       /* V-side tensor-core head size (0 = none) */
+  int32_t head_dense;       /* of its 64-term chunks, how many are stored as dense tiles */
 } esnmf_info;
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);

@@ -727,7 +727,9 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
       sv.T.ent, sv.T.nnz, h->amax_bits);
   // the densest chunks as dense tiles (bulk-copied as they are) ...
   {
-    int nd = 4;
+    // 8 dense chunks measured best at Large (0.62 ms vs 0.64 for 4, 0.77 for all 16);
+    // capped at 4 GB of dense tiles
+    int nd = (int)std::min<int64_t>(8, (int64_t)(4LL << 30) / std::max<int64_t>(1, h->head_ntiles * kHeadABytes));
     const char* de = getenv("ESNMF_HEAD_DENSE");
     if (de && de[0]) nd = atoi(de);
     h->head_nd = std::max(0, std::min(nd, h->head_nchunks));
@@ -1581,6 +1583,7 @@ esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
   info->normA2 = h->normA2;
   info->launches = h->nlaunch;
   info->head_terms = h->head_h;
+  info->head_dense = h->head_nd;
   return ESNMF_OK;
 }
 

@@ -32,7 +32,7 @@
 //   Z chunks  [chunk][hi block (kn x 64 fp16), lo block], rebuilt per half-step.
 // Roles (one CTA per SM, persistent over document tiles): a loader thread
 // bulk-copies runs + Z chunks STAGES ahead, warps 0-3 build A stages, warp 4
-// (one thread) issues the MMAs into one of two TMEM accumulators, warps 5-8
+// (one thread) issues the MMAs into one of two TMEM accumulators, warps 6-13
 // drain the other accumulator and add it to the LS buffer the tail gather wrote
 // (column-major: 32 consecutive rows per warp access, coalesced).
 #pragma once
@@ -177,7 +177,8 @@ __global__ void k_head_fill(const int64_t* __restrict__ ptr, const int32_t* __re
 constexpr int kHeadProd = 128;                         // producer threads
 constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
-constexpr int kHeadOtfThreads = kHeadProd + 32 + 128 + 32;
+constexpr int kHeadEpi = 256;                          // epilogue threads (2 warps per TMEM lane quadrant)
+constexpr int kHeadOtfThreads = kHeadProd + 32 + 32 + kHeadEpi;  // producers, MMA, loader, epilogue
 constexpr int kHeadPf = 6;                             // rounds of L2 prefetch ahead of the copies
 
 // stage = [A hi|lo 32 KB][Z chunk hi|lo][raw entries of the chunk's run]
@@ -187,10 +188,10 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 
 // X[c][row] += A^T[row, head] Z[head, c] for every document row of the shard
 // (the tail gather stored its part first: k_spmm_tail<.., ACCUM = false>).
-// Roles: warp 9 (one thread) bulk-copies each (tile, chunk) run of head
+// Roles: warp 5 (one thread) bulk-copies each (tile, chunk) run of head
 // entries and the Z chunk into a stage (TMA engine, STAGES ahead); warps 0-3
 // zero the stage's A block and scatter the run into it; warp 4 (one thread)
-// issues the MMAs; warps 5-8 drain TMEM into X.
+// issues the MMAs; warps 6-13 drain TMEM into X (two per lane quadrant).
 template <int STAGES>
 __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
+      tc::mbar_init(&tempty[a], kHeadEpi);
     }
     tc::fence_mbar_init();
   }
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 9) {
+  if (warp == 5) {
     if (lane == 0) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
       int stage = 0;
       uint32_t phase = 0;
@@ -344,8 +345,11 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         if (acc == 0) aphase ^= 1;
       }
     }
-  } else {  // ---- epilogue (warps 5-8): TMEM -> registers -> X += ----
+  } else {  // ---- epilogue (warps 6-13): TMEM -> registers -> X += ----
     const int lg = warp & 3;  // TMEM lanes 32*lg .. 32*lg+31
+    const int half = (warp - 6) >> 2;  // the two warps of a quadrant split the columns
+    const int cmid = ((kn / 16 + 1) / 2) * 16;
+    const int cbeg = half ? cmid : 0, cend = half ? kn : cmid;
     int acc = 0;
     uint32_t aphase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       tc::fence_after();
       const int64_t row = tile * kHeadM + lg * 32 + lane;
       const uint32_t ta = tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16);
-      for (int c0 = 0; c0 < kn; c0 += 16) {
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();

@@ -51,7 +51,7 @@ class esnmf_info(ctypes.Structure):
     _fields_ = [("n", c_i64), ("m", c_i64), ("nnz", c_i64), ("k", c_i32), ("t", c_i64), ("world", c_i32),
                 ("rank", c_i32), ("v_row0", c_i64), ("v_rows", c_i64), ("u_row0", c_i64), ("u_rows", c_i64),
                 ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl), ("launches", c_i64),
-                ("head_terms", c_i32)]
+                ("head_terms", c_i32), ("head_dense", c_i32)]
 
 
 class esnmf_phase(ctypes.Structure):
