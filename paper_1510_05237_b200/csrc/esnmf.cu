@@ -101,6 +101,11 @@ struct Side {
   uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
   int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
   uint64_t* bucket = nullptr;     // [k][kSelCap] value keys of the threshold bucket
+  // predicted-threshold candidates (the previous select's t-th value - 10 %)
+  uint32_t* pred = nullptr;       // [k] value bits; 0xFFFFFFFF = no prediction
+  uint64_t* pcand = nullptr;      // [k][pcap]
+  int32_t* pfill = nullptr;       // [k] then done [k]
+  int pcap = 0;
   // Gram of the factor this side reads, and its eps
   double* G = nullptr;
   double* eps = nullptr;
@@ -604,6 +609,37 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
+  if (sd.above && sd.pred) {
+    // one pass over X in steady state: histogram + candidates above the predicted
+    // threshold (k_sel_pred_final); columns whose prediction failed take the
+    // second pass (k_sel_collect2 + k_sel_final)
+    CK(cudaMemsetAsync(sd.pfill, 0, sizeof(int32_t) * k, h->stream));
+    ++h->nlaunch;
+    k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist, sd.pred, sd.row0, sd.pcand, sd.pfill,
+                                         sd.pcap);
+    ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+    ++h->nlaunch;
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, h->t, out.colptr);
+    int32_t* done = sd.pfill + k;
+    const size_t psm = sizeof(uint64_t) * kPredSort;
+    CK(cudaFuncSetAttribute(k_sel_pred_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    ++h->nlaunch;
+    k_sel_pred_final<<<k, 1024, psm, h->stream>>>(sd.sel, std::max<int64_t>(h->t, 1), sd.pcand, sd.pfill, sd.pcap,
+                                                  out.colptr, out.row, out.val, done, sd.pred);
+    CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
+    int32_t* bfill = sd.above_fill + k;
+    ++h->nlaunch;
+    k_sel_collect2<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(h->t, 1),
+                                             sd.above, sd.above_fill, sd.bucket, bfill, done);
+    CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
+    ++h->nlaunch;
+    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel,
+                                                       std::max<int64_t>(h->t, 1), sd.above, sd.above_fill,
+                                                       sd.bucket, bfill, out.colptr, out.row, out.val, done,
+                                                       sd.pred);
+    CKL("select2");
+    return;
+  }
   ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
   ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
   if (sd.above) {  // two passes over X (k_sel_collect2 + k_sel_final)
@@ -960,6 +996,15 @@ void side_alloc(esnmf_t* h, Side& sd) {
     sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(h->t, 1));
     sd.above_fill = h->alloc<int32_t>(2 * (int64_t)k);
     sd.bucket = h->alloc<uint64_t>((int64_t)k * kSelCap);
+    // predicted-threshold single pass: worth its extra kernel only when the LS
+    // buffer is large (V side of Large: 400 MB; its U side, 80 MB, keeps two passes)
+    if (sd.rows >= (1 << 19)) {
+      sd.pcap = (int)std::min<int64_t>(kPredSort, 2 * h->t + 2048);
+      sd.pred = h->alloc<uint32_t>(k);
+      CK(cudaMemsetAsync(sd.pred, 0xFF, sizeof(uint32_t) * k, h->stream));
+      sd.pcand = h->alloc<uint64_t>((int64_t)k * sd.pcap);
+      sd.pfill = h->alloc<int32_t>(2 * (int64_t)k);
+    }
   }
   sd.G = h->alloc<double>((int64_t)k * k);
   sd.eps = h->alloc<double>(1);

@@ -19,16 +19,26 @@
 
 namespace esk {
 
+// (pred != nullptr) also appends every positive with value bits >= pred[c] to a
+// per-column candidate list (row-keyed, capacity cap): pred[c] is the previous
+// select's t-th value lowered by ~10 %, so in steady state the list holds the
+// column's top t and the second pass over X is skipped (k_sel_pred_final).
 __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, int64_t ldx, int64_t rows,
-                                                  uint32_t* __restrict__ hist) {
+                                                  uint32_t* __restrict__ hist, const uint32_t* __restrict__ pred = nullptr,
+                                                  int64_t row0 = 0, uint64_t* __restrict__ pcand = nullptr,
+                                                  int32_t* __restrict__ pfill = nullptr, int pcap = 0) {
   __shared__ uint32_t h[kNumBins];
   const int c = blockIdx.y;
+  const uint32_t pb = pred ? pred[c] : 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
   const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
-  for (int64_t j = r0 + 4 * threadIdx.x; j < r1; j += 4 * blockDim.x) {
+  for (int64_t base = r0; base < r1; base += 4 * blockDim.x) {  // uniform trip count (ballots below)
+    const int64_t j = base + 4 * threadIdx.x;
     float x[4];
     if (j + 3 < r1) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
@@ -40,6 +50,20 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (x[u] > 0.f) atomicAdd(&h[sel_digit(x[u])], 1u);
+    if (pred) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool cd = x[u] > 0.f && f2u(x[u]) >= pb;
+        const unsigned m = __ballot_sync(kFull, cd);
+        if (m) {
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&pfill[c], __popc(m));
+          b0 = __shfl_sync(kFull, b0, 0);
+          const int slot = b0 + __popc(m & lt);
+          if (cd && slot < pcap) pcand[(int64_t)c * pcap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
+        }
+      }
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kNumBins; b += blockDim.x)
@@ -351,14 +375,23 @@ constexpr int64_t kSelFastT = 4096;
 
 ESNMF_DEV uint64_t row_key(uint32_t row, float x) { return ((uint64_t)row << 32) | (uint64_t)f2u(x); }
 
+// prediction for the next select: value bits 10 % below the kept minimum
+// (0 = every positive is a candidate)
+ESNMF_DEV uint32_t pred_of(uint32_t minbits) {
+  if (minbits == 0xFFFFFFFFu || minbits == 0u) return 0u;
+  return f2u(__uint_as_float(minbits) * 0.9f);
+}
+
 __global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ X, int64_t ldx, int64_t rows,
                                                       int64_t row0, const ColSel* __restrict__ sel, int64_t t,
                                                       uint64_t* __restrict__ above, int32_t* __restrict__ above_fill,
                                                       uint64_t* __restrict__ bucket,
-                                                      int32_t* __restrict__ bucket_fill) {
+                                                      int32_t* __restrict__ bucket_fill,
+                                                      const int32_t* __restrict__ done = nullptr) {
   const int c = blockIdx.y;
   const ColSel s = sel[c];
   if (s.digit >= kNumBins) return;  // t == 0: nothing kept
+  if (done && done[c]) return;      // selected from the predicted candidates
   const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
   const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
@@ -424,7 +457,9 @@ __global__ void __launch_bounds__(1024) k_sel_final(const float* __restrict__ X,
                                                     const uint64_t* __restrict__ bucket,
                                                     const int32_t* __restrict__ bucket_fill,
                                                     const int64_t* __restrict__ colptr, int32_t* __restrict__ out_row,
-                                                    float* __restrict__ out_val) {
+                                                    float* __restrict__ out_val,
+                                                    const int32_t* __restrict__ done = nullptr,
+                                                    uint32_t* __restrict__ pred_next = nullptr) {
   extern __shared__ uint64_t fin_smem[];
   uint64_t* kb = fin_smem;                                // [kSelCap] bucket keys
   uint64_t* kept = fin_smem + kSelCap;                    // [kSelFastT] kept row keys
@@ -433,7 +468,11 @@ __global__ void __launch_bounds__(1024) k_sel_final(const float* __restrict__ X,
   __shared__ int nk_s;
   const int c = blockIdx.x;
   const ColSel s = sel[c];
-  if (s.digit >= kNumBins) return;
+  if (s.digit >= kNumBins) {
+    if (pred_next && threadIdx.x == 0) pred_next[c] = 0xFFFFFFFFu;  // t == 0: no candidates
+    return;
+  }
+  if (done && done[c]) return;  // selected from the predicted candidates
   const int na = above_fill[c];  // == s.above (all positives when s.digit < 0)
   const int nb = bucket_fill[c];
   const int r = (int)s.r;
@@ -507,10 +546,97 @@ __global__ void __launch_bounds__(1024) k_sel_final(const float* __restrict__ X,
   __syncthreads();
   bitonic_sort_smem(kept, np);
   const int64_t o = colptr[c];
+  uint32_t mn = 0xFFFFFFFFu;
   for (int i = threadIdx.x; i < nk; i += blockDim.x) {
     const uint64_t key = kept[i];
     out_row[o + i] = (int32_t)(key >> 32);
     out_val[o + i] = __uint_as_float((uint32_t)key);
+    mn = min(mn, (uint32_t)key);
+  }
+  if (pred_next) {
+    mn = __reduce_min_sync(kFull, mn);
+    __shared__ uint32_t wmin[32];
+    if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t m = 0xFFFFFFFFu;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
+      // keep-all columns (s.digit < 0): predict 0 (every positive is a candidate)
+      pred_next[c] = s.digit < 0 ? 0u : pred_of(m);
+    }
+  }
+}
+
+// ---- predicted-threshold fast path ----------------------------------------
+
+// one block per column: if the candidates of the histogram pass contain the
+// column's top min(t, #pos) (#candidates >= that, no overflow), select from
+// them and mark the column done; else leave it to k_sel_collect2/k_sel_final.
+constexpr int kPredSort = 8192;  // keys sorted in shared memory (64 KB)
+
+__global__ void __launch_bounds__(1024) k_sel_pred_final(const ColSel* __restrict__ sel, int64_t t,
+                                                         const uint64_t* __restrict__ pcand,
+                                                         const int32_t* __restrict__ pfill, int pcap,
+                                                         const int64_t* __restrict__ colptr,
+                                                         int32_t* __restrict__ out_row, float* __restrict__ out_val,
+                                                         int32_t* __restrict__ done, uint32_t* __restrict__ pred_next) {
+  extern __shared__ uint64_t ps[];
+  __shared__ uint32_t wmin[32];
+  const int c = blockIdx.x;
+  const ColSel s = sel[c];
+  const int64_t need = min(t, s.npos);
+  const int nc = pfill[c];
+  const bool ok = s.digit < kNumBins && nc <= pcap && nc <= kPredSort && (int64_t)nc >= need && need > 0;
+  if (!ok) {
+    if (threadIdx.x == 0) {
+      done[c] = s.digit >= kNumBins || need == 0 ? 1 : 0;
+      if (need == 0) pred_next[c] = s.digit >= kNumBins ? 0xFFFFFFFFu : 0u;
+    }
+    return;
+  }
+  int np = 1;
+  while (np < nc) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) ps[i] = i < nc ? pcand[(int64_t)c * pcap + i] : ~0ULL;
+  __syncthreads();
+  bitonic_sort_smem(ps, np);  // (value desc, row asc)
+  // the first `need` keys, re-keyed by row, sorted again for the canonical order
+  const int nk = (int)need;
+  uint32_t mn = 0xFFFFFFFFu;
+  uint64_t rk[8];
+  int cnt = 0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    if (cnt < 8) {
+      if (i < nk) {
+        const uint64_t key = ps[i];
+        const uint32_t row = (uint32_t)key, bits = 0x7FFFFFFFu - (uint32_t)(key >> 32);
+        rk[cnt] = row_key(row, __uint_as_float(bits));
+        mn = min(mn, bits);
+      } else {
+        rk[cnt] = ~0ULL;
+      }
+      ++cnt;
+    }
+  }
+  __syncthreads();
+  cnt = 0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x)
+    if (cnt < 8) ps[i] = rk[cnt++];
+  __syncthreads();
+  bitonic_sort_smem(ps, np);
+  const int64_t o = colptr[c];
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+    const uint64_t key = ps[i];
+    out_row[o + i] = (int32_t)(key >> 32);
+    out_val[o + i] = __uint_as_float((uint32_t)key);
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t m = 0xFFFFFFFFu;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
+    done[c] = 1;
+    pred_next[c] = s.npos <= t ? 0u : pred_of(m);
   }
 }
 
