@@ -998,7 +998,9 @@ void side_alloc(esnmf_t* h, Side& sd) {
     sd.bucket = h->alloc<uint64_t>((int64_t)k * kSelCap);
     // predicted-threshold single pass: worth its extra kernel only when the LS
     // buffer is large (V side of Large: 400 MB; its U side, 80 MB, keeps two passes)
-    if (sd.rows >= (1 << 19)) {
+    int64_t min_rows = 1 << 19;
+    if (const char* pe = getenv("ESNMF_PRED_MIN_ROWS")) min_rows = atoll(pe);  // tests force it on small shards
+    if (sd.rows >= min_rows) {
       sd.pcap = (int)std::min<int64_t>(kPredSort, 2 * h->t + 2048);
       sd.pred = h->alloc<uint32_t>(k);
       CK(cudaMemsetAsync(sd.pred, 0xFF, sizeof(uint32_t) * k, h->stream));

@@ -311,3 +311,18 @@ def test_large_sampled_parity():
         check_topt_property(ls, out, cfg.t)
     del gd
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("tag,cfg", [("tiny", TINY), ("medium", MEDIUM)])
+def test_predicted_select_trajectory(tag, cfg, monkeypatch):
+    """The one-pass select (candidates above the previous t-th value - 10 %, with a
+    per-column fallback) forced on for every shard: the same trajectory as the oracle."""
+    monkeypatch.setenv("ESNMF_PRED_MIN_ROWS", "1")
+    gold = golden(tag)
+    g = synth.generate(cfg)
+    s = solver(cfg, g)
+    s.iterate(cfg.iters)
+    check_trajectory(s, gold)
+    # and a late half-step against the oracle from the same state
+    half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_V)
+    half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_U)
