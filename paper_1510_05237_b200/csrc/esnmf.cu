@@ -81,6 +81,7 @@ struct Factor {
 struct Side {
   int64_t row0 = 0, rows = 0, ldx = 0;  // this rank's output rows
   float* X = nullptr;                   // LS, column-major k x ldx
+  float* Xt = nullptr;                  // V side with a head: tail part, row-major rows x kpad
   DevCsr T;                             // operator rows of this shard (local row ids)
   // work items (U side only)
   WorkItem* items = nullptr;
@@ -463,14 +464,17 @@ void tail_launch(esnmf_t* h) {
   const bool smem_bits = nwords * 4 <= 64 * 1024;
   const size_t smem = smem_bits ? nwords * 4 : 0;
   if (h->zs != 4 * G * CPL) fail(ESNMF_EINVAL, "Z row stride does not match the tail gather layout");
-  auto kern = k_spmm_tail<G, CPL, U, RG, false>;  // stores; the head kernel adds its part after
+  // with a head: row-major staging (the head kernel adds its part and stores X);
+  // without: column-major straight into X
+  const bool trow = h->head_h > 0;
+  auto kern = trow ? k_spmm_tail<G, CPL, U, RG, true> : k_spmm_tail<G, CPL, U, RG, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t groups = ceil_div(sd.rows, RG);
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * 3);
   ++h->nlaunch;
   kern<<<grid, kTailThreads, smem, h->stream>>>(sd.T.ptr, h->head_h > 0 ? h->nh : nullptr, sd.T.ent, sd.rows,
                                                 h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4,
-                                                h->k, sd.X, sd.ldx);
+                                                h->k, trow ? sd.Xt : sd.X, trow ? (int64_t)h->kpad : sd.ldx);
   CKL("spmm_tail");
 }
 
@@ -688,7 +692,7 @@ void vhead_launch_st(esnmf_t* h) {
   kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
                                                    h->colscale,
                                                    sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
-                                                   h->head_acc_cols, sv.X, sv.ldx);
+                                                   h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad);
   CKL("vhead");
 }
 
@@ -739,6 +743,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
   h->zhead = h->alloc<uint8_t>((int64_t)h->head_nchunks * h->kn * kHeadK * 4);
+  sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);
   h->colscale = h->alloc<float>(h->kn);
   h->amax_bits = h->alloc<unsigned>(1);
   CK(cudaMemsetAsync(h->zhead, 0, (size_t)h->head_nchunks * h->kn * kHeadK * 4, h->stream));

@@ -104,7 +104,11 @@ ESNMF_DEV void ffma4(float4& acc, float x, const float4& z) {
 // G lanes per gathered Z row, CPL float4 per lane (Z rows are zs = G*CPL*4
 // floats, zero-padded, so every lane loads unconditionally), U entries per lane
 // group in flight, RG document rows per warp.
-template <int G, int CPL, int U, int RG, bool ACCUM>
+// TROW: store the rows ROW-MAJOR (stride ldx = kpad floats) into a staging
+// buffer that the tensor-core head kernel reads and adds to the column-major LS
+// buffer (400 contiguous bytes per row instead of 16-byte pieces of k columns);
+// otherwise store column-major into the LS buffer directly (no head).
+template <int G, int CPL, int U, int RG, bool TROW>
 __global__ void __launch_bounds__(kTailThreads, 3)
     k_spmm_tail(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh, const int2* __restrict__ ent,
                 int64_t rows, const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int zq,
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(kTailThreads, 3)
   const unsigned lt_mask = (1u << lane) - 1u;
   const char* zl = reinterpret_cast<const char*>(Z) + lg * 16;  // this lane's column chunk
   const uint32_t zrow = (uint32_t)zq * 16u;                      // bytes per Z row
-  (void)kq;
+
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t ngroups = (rows + RG - 1) / RG;
   // Software pipeline across groups: the next group's row bounds are loaded at
@@ -289,7 +293,16 @@ __global__ void __launch_bounds__(kTailThreads, 3)
           res[q][j].z += __shfl_xor_sync(kFull, res[q][j].z, o);
           res[q][j].w += __shfl_xor_sync(kFull, res[q][j].w, o);
         }
-    if (lane < G) {
+    if (TROW && lane < G) {
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int c4 = lg + j * G;
+        if (c4 < kq)
+#pragma unroll
+          for (int q = 0; q < RG; ++q)
+            if (r0 + q < rows) *reinterpret_cast<float4*>(X + (r0 + q) * ldx + 4 * c4) = res[q][j];
+      }
+    } else if (lane < G) {
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
         const int c0 = 4 * (lg + j * G);
@@ -304,26 +317,15 @@ __global__ void __launch_bounds__(kTailThreads, 3)
           if (r0 + RG <= rows) {  // ldx and r0 are multiples of RG: aligned vector accesses
             if constexpr (RG % 4 == 0) {
 #pragma unroll
-              for (int q4 = 0; q4 < RG; q4 += 4) {
-                float4 o = make_float4(v[q4], v[q4 + 1], v[q4 + 2], v[q4 + 3]);
-                if constexpr (ACCUM) {
-                  const float4 pv = *reinterpret_cast<const float4*>(xo + q4);
-                  o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w;
-                }
-                *reinterpret_cast<float4*>(xo + q4) = o;
-              }
+              for (int q4 = 0; q4 < RG; q4 += 4)
+                *reinterpret_cast<float4*>(xo + q4) = make_float4(v[q4], v[q4 + 1], v[q4 + 2], v[q4 + 3]);
             } else {
-              float2 o = make_float2(v[0], v[1]);
-              if constexpr (ACCUM) {
-                const float2 pv = *reinterpret_cast<const float2*>(xo);
-                o.x += pv.x; o.y += pv.y;
-              }
-              *reinterpret_cast<float2*>(xo) = o;
+              *reinterpret_cast<float2*>(xo) = make_float2(v[0], v[1]);
             }
           } else {
 #pragma unroll
             for (int q = 0; q < RG; ++q)
-              if (r0 + q < rows) xo[q] = ACCUM ? xo[q] + v[q] : v[q];
+              if (r0 + q < rows) xo[q] = v[q];
           }
         }
       }

@@ -33,8 +33,8 @@
 // Roles (one CTA per SM, persistent over document tiles): a loader thread
 // bulk-copies runs + Z chunks STAGES ahead, warps 0-3 build A stages, warp 4
 // (one thread) issues the MMAs into one of two TMEM accumulators, warps 6-13
-// drain the other accumulator and add it to the LS buffer the tail gather wrote
-// (column-major: 32 consecutive rows per warp access, coalesced).
+// drain the other accumulator, add the tail part the gather staged row-major,
+// and store the LS buffer column-major (32 consecutive rows per warp, coalesced).
 #pragma once
 #include <cuda_fp16.h>
 
@@ -186,8 +186,8 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
   return (kHeadABytes + (uint32_t)kn * kHeadK * 4 + kHeadRawBytes + 1023u) & ~1023u;
 }
 
-// X[c][row] += A^T[row, head] Z[head, c] for every document row of the shard
-// (the tail gather stored its part first: k_spmm_tail<.., ACCUM = false>).
+// X[c][row] = Xt[row][c] + A^T[row, head] Z[head, c] for every document row of
+// the shard (the tail gather stored its part row-major in Xt: k_spmm_tail<.., TROW>).
 // Roles: warp 5 (one thread) bulk-copies each (tile, chunk) run of head
 // entries and the Z chunk into a stage (TMA engine, STAGES ahead); warps 0-3
 // zero the stage's A block and scatter the run into it; warp 4 (one thread)
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
                 const int2* __restrict__ hseg, const unsigned* __restrict__ amax_bits, const uint8_t* __restrict__ zbuf,
                 const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
-                int acc_cols, float* __restrict__ X, int64_t ldx) {
+                int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
@@ -361,10 +361,15 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();
-        if (row < rows) {  // X += head part: 16 independent loads, then the stores
+        if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
           float x[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) x[j] = c0 + j < k ? X[(int64_t)(c0 + j) * ldx + row] : 0.f;
+          for (int v4 = 0; v4 < 4; ++v4) {
+            const int c = c0 + 4 * v4;
+            const float4 t4 = c < kpad ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[4 * v4] = t4.x; x[4 * v4 + 1] = t4.y; x[4 * v4 + 2] = t4.z; x[4 * v4 + 3] = t4.w;
+          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int c = c0 + j;
