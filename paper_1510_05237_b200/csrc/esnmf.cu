@@ -30,6 +30,7 @@
 #include "k_spmm_terms.cuh"
 #include "k_uside_scatter.cuh"
 #include "k_vhead.cuh"
+#include "k_uside_tc.cuh"
 #include "k_spmm_tail.cuh"
 
 using namespace esk;
@@ -165,7 +166,10 @@ struct esnmf {
   double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
   double* rsum_max = nullptr; // max_i rsum[i]
   unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
-  float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish32
+  float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish_rt
+  uint8_t* wtc = nullptr;            // W as the tensor-core B operand (fp16 hi/lo, k_uside_tc)
+  float* wtc_scale = nullptr;        // [kn] its per-column scales
+  int utc_kn = 0, utc_kk = 0;        // 0: k_uside_tc not used (kpad > 128)
   // V-side tensor-core head (k_vhead.cuh): h most frequent terms, dense fp16 hi/lo tiles
   int head_h = 0, head_nchunks = 0, kn = 0, head_acc_cols = 0;
   int64_t head_ntiles = 0;
@@ -503,6 +507,10 @@ void uside_w_prep(esnmf_t* h) {
   k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
   // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
   k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, 100.0, h->flags + 3);
+  if (h->utc_kn) {
+    ++h->nlaunch;
+    k_utc_wprep<<<h->k, 128, 0, h->stream>>>(h->W, h->k, h->utc_kn, h->utc_kk, h->wtc, h->wtc_scale);
+  }
   CKL("uside_w_prep");
 }
 
@@ -521,7 +529,15 @@ void uside_scatter_launch(esnmf_t* h) {
   // W32 staged in shared memory + per-warp transposed Y tiles (8 warps)
   const size_t smem = sizeof(float) * h->k * h->kpad + sizeof(float) * 8 * h->kpad * kFinRT;
   const int64_t rgroups = ceil_div(su.rows, kFinRT);
-  if (h->kpad <= 128) {
+  if (h->utc_kn) {  // tensor cores (k_uside_tc.cuh)
+    const size_t tsm = uside_tc_smem(h->utc_kn, h->utc_kk);
+    CK(cudaFuncSetAttribute(k_uside_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    const int64_t ntiles = ceil_div(su.rows, kUtcM);
+    const int acc = h->utc_kn <= 32 ? 32 : h->utc_kn <= 64 ? 64 : 128;
+    k_uside_tc<<<(unsigned)std::min<int64_t>(ntiles, h->num_sms), kUtcThreads, tsm, h->stream>>>(
+        su.rows, ntiles, h->rsum_max, h->vmax, h->wtc, h->wtc_scale, h->k, h->kpad, h->utc_kn, h->utc_kk, acc, h->Yq,
+        su.X, su.ldx, h->flags + 3);
+  } else if (h->kpad <= 128) {
     CK(cudaFuncSetAttribute(k_uside_finish_rt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_uside_finish_rt<1><<<grid_for(rgroups, 8, (int64_t)h->num_sms * 3), 256, smem, h->stream>>>(
         su.rows, h->rsum_max, h->vmax, h->W32, h->k, h->kpad, h->Yq, su.X, su.ldx, h->flags + 3);
@@ -1383,6 +1399,15 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);
     if (h->world == 1) {
       h->W32 = h->alloc<float>((int64_t)k * h->kpad);
+      if (h->kpad <= 128 && !getenv("ESNMF_UTC_OFF")) {  // tensor-core (Y W), k_uside_tc.cuh
+        h->utc_kn = (k + 15) / 16 * 16;
+        h->utc_kk = (h->kpad + 15) / 16 * 16;
+        const int64_t wb = (int64_t)h->utc_kn * h->utc_kk * 4;
+        h->wtc = h->alloc<uint8_t>(wb);
+        CK(cudaMemsetAsync(h->wtc, 0, wb, h->stream));
+        h->wtc_scale = h->alloc<float>(h->utc_kn);
+        CK(cudaMemsetAsync(h->wtc_scale, 0, sizeof(float) * h->utc_kn, h->stream));
+      }
       h->Yq = h->alloc<unsigned long long>(n * (int64_t)h->kpad);
       CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * n * h->kpad, h->stream));
     }

@@ -1,0 +1,243 @@
+// k_uside_tc.cuh -- U side, second half: LS_U = Y W on the tensor cores
+// ("U = A V (V^T V)^{-1}"), Y = A V the exact fixed-point accumulators of
+// k_uside_scatter, W = (V^T V + eps I)^{-1}.
+//
+// A dense (n x k) x (k x k) product: 200k x 100 x 100 at Large.  The SIMT
+// register-tiled kernel (k_uside_finish_rt) was bound by instruction issue;
+// here per 128-row tile:
+//   * 4 producer warps (32 rows each, lanes across columns, 4 rows in flight)
+//     convert the tile's fixed-point rows, find each row's maximum, scale the
+//     row by an exact power of two into [2^14, 2^15), split it into fp16 hi/lo
+//     (22 significant bits) in the K-major shared-memory layout, and clear the
+//     accumulator rows for the next half-step;
+//   * W is split the same way once per CTA (per-column power-of-two scales)
+//     and stays resident in shared memory as the B operand;
+//   * one thread issues kind::f16 MMAs (hi*hi + hi*lo + lo*hi) into TMEM;
+//   * 4 epilogue warps (thread = row) undo the two scales (exact) and store
+//     the LS rows column-major (coalesced).
+// Used when kappa_inf(G_V + eps I) <= 100 (device flag), like the fp32 SIMT
+// path it replaces; the fp64 kernel handles the rest.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace esk {
+
+constexpr int kUtcM = 128;
+constexpr int kUtcRows = 8;  // rows of a producer warp in flight
+constexpr int kUtcThreads = 128 + 32 + 128;  // producers, MMA, epilogue
+
+ESNMF_DEV int utc_exp(double x) {  // e with x 2^e in [2^14, 2^15), 0 for x == 0
+  if (!(x > 0.0)) return 0;
+  int ex;
+  frexp(x, &ex);
+  return 15 - ex;
+}
+
+// W (fp64 k x k) -> B operand [n = output column c][K = l] = W[l][c], fp16
+// hi/lo with per-column scales; wscale[c] = 2^-eW_c.  One block per column.
+__global__ void k_utc_wprep(const double* __restrict__ W, int k, int kn, int kk, uint8_t* __restrict__ wb,
+                            float* __restrict__ wscale) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  double mx = 0;
+  for (int l = threadIdx.x; l < k; l += blockDim.x) mx = fmax(mx, fabs(W[(int64_t)l * k + c]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    red[0] = m;
+  }
+  __syncthreads();
+  const int e = utc_exp(red[0]);
+  if (threadIdx.x == 0) wscale[c] = ldexpf(1.f, -e);
+  const uint32_t half = (uint32_t)kn * kk * 2;
+  for (int l = threadIdx.x; l < kk; l += blockDim.x) {
+    const float w = l < k ? (float)ldexp(W[(int64_t)l * k + c], e) : 0.f;
+    const __half hi = __float2half_rn(w);
+    const __half lo = __float2half_rn(w - __half2float(hi));
+    const uint32_t off = tc::kmajor_off16(c, l, kk);
+    *reinterpret_cast<__half*>(wb + off) = hi;
+    *reinterpret_cast<__half*>(wb + half + off) = lo;
+  }
+}
+
+// LS rows of tiles of 128 term rows; 2 A stages, W resident
+__global__ void __launch_bounds__(kUtcThreads, 1)
+    k_uside_tc(int64_t rows, int64_t ntiles, const double* __restrict__ bound, const uint32_t* __restrict__ vmax,
+               const uint8_t* __restrict__ wb, const float* __restrict__ wscale, int k, int kpad, int kn, int kk,
+               int acc_cols, unsigned long long* __restrict__ Yq, float* __restrict__ X, int64_t ldx,
+               const int* __restrict__ use_fp64) {
+  if (*use_fp64) return;  // ill-conditioned: the fp64 kernel handles it
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t wbar, afull[2], aempty[2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float rscale[2][kUtcM];
+  uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t wbytes = (uint32_t)kn * kk * 4;               // hi + lo
+  const uint32_t abytes = (uint32_t)kUtcM * kk * 4;            // hi + lo
+  uint8_t* ws = base;
+  uint8_t* as0 = base + ((wbytes + 1023u) & ~1023u);
+  const uint32_t astride = (abytes + 1023u) & ~1023u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&wbar, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&afull[s], 128);
+      tc::mbar_init(&aempty[s], 1);
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 4) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;  // fixed point -> value
+
+  if (warp < 4) {  // ---- producers: warp w converts rows 32w..32w+31 of a tile, lane-parallel per row ----
+    if (threadIdx.x == 0) {
+      tc::mbar_arrive_expect_tx(&wbar, wbytes);
+      tc::bulk_g2s(ws, wb, wbytes, &wbar);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t ahalf = (uint32_t)kUtcM * kk * 2;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      tc::mbar_wait(&aempty[stage], phase ^ 1);   // the MMAs of this stage's last tile are done
+      tc::mbar_wait(&tempty[stage], phase ^ 1);   // ... and its epilogue (rscale[stage] is free)
+      uint8_t* sa = as0 + stage * astride;
+      for (int rr = 0; rr < 32; rr += kUtcRows) {
+        // kUtcRows rows in flight: all loads issued before any use (the clearing
+        // stores come after, so they cannot serialise the loads)
+        unsigned long long qv[kUtcRows][4];
+#pragma unroll
+        for (int q = 0; q < kUtcRows; ++q) {
+          const int64_t row = tile * kUtcM + warp * 32 + rr + q;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = lane + 32 * j;
+            qv[q][j] = (row < rows && c < kpad) ? __ldcs(Yq + row * kpad + c) : 0ull;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kUtcRows; ++q) {
+          const int64_t row = tile * kUtcM + warp * 32 + rr + q;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (qv[q][j]) Yq[row * kpad + lane + 32 * j] = 0ull;  // clear for the next half-step
+        }
+#pragma unroll
+        for (int q = 0; q < kUtcRows; ++q) {
+          const int r = warp * 32 + rr + q;
+          float y[4];
+          float mx = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            y[j] = (float)((double)qv[q][j] * unit);
+            mx = fmaxf(mx, y[j]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+          int e = 0;
+          if (mx > 0.f) {
+            frexpf(mx, &e);
+            e = 15 - e;
+          }
+          const float sc = __int_as_float((127 + e) << 23);  // 2^e, exact
+          if (lane == 0) rscale[stage][r] = __int_as_float((127 - e) << 23);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = lane + 32 * j;
+            if (c < kk) {
+              const float v = y[j] * sc;
+              const __half hi = __float2half_rn(v);
+              const __half lo = __float2half_rn(v - __half2float(hi));
+              const uint32_t off = tc::kmajor_off16(r, c, kk);
+              *reinterpret_cast<__half*>(sa + off) = hi;
+              *reinterpret_cast<__half*>(sa + ahalf + off) = lo;
+            }
+          }
+        }
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&afull[stage]);
+      if (++stage == 2) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      tc::mbar_wait(&wbar, 0);
+      const uint32_t idesc = tc::make_idesc_f16(kUtcM, kn);
+      const uint32_t wh = tc::smem_u32(ws), wl = wh + (uint32_t)kn * kk * 2;
+      const uint32_t sbo = (uint32_t)(kk / 8) * 128;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        tc::mbar_wait(&tempty[stage], phase ^ 1);
+        tc::mbar_wait(&afull[stage], phase);
+        tc::fence_after();
+        const uint32_t ah = tc::smem_u32(as0 + stage * astride), al = ah + (uint32_t)kUtcM * kk * 2;
+        const uint32_t d = tmem + (uint32_t)(stage * acc_cols);
+        for (int s = 0; s < kk / 16; ++s) {
+          const uint32_t o = s * 256;
+          const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
+          const uint64_t dwh = tc::make_sdesc(wh + o, 128, sbo), dwl = tc::make_sdesc(wl + o, 128, sbo);
+          tc::mma_f16(d, dah, dwh, idesc, s != 0);
+          tc::mma_f16(d, dah, dwl, idesc, 1);
+          tc::mma_f16(d, dal, dwh, idesc, 1);
+        }
+        tc::mma_commit(&aempty[stage]);  // A stage free
+        tc::mma_commit(&tfull[stage]);   // accumulator ready
+        if (++stage == 2) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 5) {  // ---- epilogue (warps 5-8): thread = row ----
+    const int lg = warp & 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      tc::mbar_wait(&tfull[stage], phase);
+      tc::mbar_wait(&afull[stage], phase);  // acquire the producers' rscale writes
+      tc::fence_after();
+      const int r = lg * 32 + lane;
+      const int64_t row = tile * kUtcM + r;
+      const float rs = rscale[stage][r];
+      const uint32_t ta = tmem + (uint32_t)(stage * acc_cols) + ((uint32_t)(lg * 32) << 16);
+      for (int c0 = 0; c0 < kn; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(ta + (uint32_t)c0, v);
+        tc::tmem_wait_ld();
+        if (row < rows) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = c0 + j;
+            if (c < k) X[(int64_t)c * ldx + row] = __uint_as_float(v[j]) * rs * wscale[c];  // exact powers of two
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&tempty[stage]);
+      if (++stage == 2) { stage = 0; phase ^= 1; }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 2 * acc_cols);
+  }
+}
+
+inline size_t uside_tc_smem(int kn, int kk) {
+  return (((size_t)kn * kk * 4 + 1023) & ~(size_t)1023) + 2 * (((size_t)kUtcM * kk * 4 + 1023) & ~(size_t)1023) +
+         1024;
+}
+
+}  // namespace esk
