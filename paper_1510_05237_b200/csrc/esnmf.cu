@@ -641,7 +641,7 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
     ++h->nlaunch;
     k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, h->t, out.colptr);
     int32_t* done = sd.pfill + k;
-    const size_t psm = sizeof(uint64_t) * kPredSort;
+    const size_t psm = sizeof(uint64_t) * (kSelFastT + kSelCap);
     CK(cudaFuncSetAttribute(k_sel_pred_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
     ++h->nlaunch;
     k_sel_pred_final<<<k, 1024, psm, h->stream>>>(sd.sel, std::max<int64_t>(h->t, 1), sd.pcand, sd.pfill, sd.pcap,

@@ -572,7 +572,10 @@ __global__ void __launch_bounds__(1024) k_sel_final(const float* __restrict__ X,
 // one block per column: if the candidates of the histogram pass contain the
 // column's top min(t, #pos) (#candidates >= that, no overflow), select from
 // them and mark the column done; else leave it to k_sel_collect2/k_sel_final.
-constexpr int kPredSort = 8192;  // keys sorted in shared memory (64 KB)
+// Like k_sel_final: candidates above the threshold bucket D (from the full
+// histogram) are all kept, only bucket D's candidates are sorted by key, and
+// the kept entries are sorted by row for the canonical order.
+constexpr int kPredSort = 8192;  // candidate capacity (keys staged in shared memory)
 
 __global__ void __launch_bounds__(1024) k_sel_pred_final(const ColSel* __restrict__ sel, int64_t t,
                                                          const uint64_t* __restrict__ pcand,
@@ -580,13 +583,16 @@ __global__ void __launch_bounds__(1024) k_sel_pred_final(const ColSel* __restric
                                                          const int64_t* __restrict__ colptr,
                                                          int32_t* __restrict__ out_row, float* __restrict__ out_val,
                                                          int32_t* __restrict__ done, uint32_t* __restrict__ pred_next) {
-  extern __shared__ uint64_t ps[];
+  extern __shared__ uint64_t ps[];  // [kSelFastT] kept row keys, then [kSelCap] bucket keys
+  uint64_t* kept = ps;
+  uint64_t* bk = ps + kSelFastT;
+  __shared__ int nkept, nbk;
   __shared__ uint32_t wmin[32];
   const int c = blockIdx.x;
   const ColSel s = sel[c];
   const int64_t need = min(t, s.npos);
   const int nc = pfill[c];
-  const bool ok = s.digit < kNumBins && nc <= pcap && nc <= kPredSort && (int64_t)nc >= need && need > 0;
+  bool ok = s.digit < kNumBins && nc <= pcap && (int64_t)nc >= need && need > 0 && need <= kSelFastT;
   if (!ok) {
     if (threadIdx.x == 0) {
       done[c] = s.digit >= kNumBins || need == 0 ? 1 : 0;
@@ -594,40 +600,55 @@ __global__ void __launch_bounds__(1024) k_sel_pred_final(const ColSel* __restric
     }
     return;
   }
-  int np = 1;
-  while (np < nc) np <<= 1;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) ps[i] = i < nc ? pcand[(int64_t)c * pcap + i] : ~0ULL;
+  if (threadIdx.x == 0) {
+    nkept = 0;
+    nbk = 0;
+  }
   __syncthreads();
-  bitonic_sort_smem(ps, np);  // (value desc, row asc)
-  // the first `need` keys, re-keyed by row, sorted again for the canonical order
-  const int nk = (int)need;
-  uint32_t mn = 0xFFFFFFFFu;
-  uint64_t rk[8];
-  int cnt = 0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    if (cnt < 8) {
-      if (i < nk) {
-        const uint64_t key = ps[i];
-        const uint32_t row = (uint32_t)key, bits = 0x7FFFFFFFu - (uint32_t)(key >> 32);
-        rk[cnt] = row_key(row, __uint_as_float(bits));
-        mn = min(mn, bits);
-      } else {
-        rk[cnt] = ~0ULL;
-      }
-      ++cnt;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const uint64_t key = pcand[(int64_t)c * pcap + i];  // sel_key: (value desc, row asc)
+    const uint32_t bits = 0x7FFFFFFFu - (uint32_t)(key >> 32);
+    const int dg = (int)(bits >> kSelShift);
+    if (dg > s.digit) {
+      const int slot = atomicAdd(&nkept, 1);
+      if (slot < kSelFastT) kept[slot] = row_key((uint32_t)key, __uint_as_float(bits));
+    } else if (dg == s.digit) {
+      const int slot = atomicAdd(&nbk, 1);
+      if (slot < kSelCap) bk[slot] = key;
     }
   }
   __syncthreads();
-  cnt = 0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x)
-    if (cnt < 8) ps[i] = rk[cnt++];
+  const int na = nkept, nb = nbk;
+  const int r = (int)(need - na);  // from bucket D (s.digit < 0: every positive is "above")
+  if (na > kSelFastT || nb > kSelCap || r < 0 || r > nb) {  // cannot happen when the candidates are complete
+    if (threadIdx.x == 0) done[c] = 0;
+    return;
+  }
+  if (r > 0) {
+    int np = 1;
+    while (np < nb) np <<= 1;
+    for (int i = nb + threadIdx.x; i < np; i += blockDim.x) bk[i] = ~0ULL;
+    __syncthreads();
+    bitonic_sort_smem(bk, np);
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+      const uint64_t key = bk[i];
+      kept[na + i] = row_key((uint32_t)key, __uint_as_float(0x7FFFFFFFu - (uint32_t)(key >> 32)));
+    }
+  }
   __syncthreads();
-  bitonic_sort_smem(ps, np);
+  const int nk = (int)need;
+  int np = 1;
+  while (np < nk) np <<= 1;
+  for (int i = nk + threadIdx.x; i < np; i += blockDim.x) kept[i] = ~0ULL;
+  __syncthreads();
+  bitonic_sort_smem(kept, np);
   const int64_t o = colptr[c];
+  uint32_t mn = 0xFFFFFFFFu;
   for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-    const uint64_t key = ps[i];
+    const uint64_t key = kept[i];
     out_row[o + i] = (int32_t)(key >> 32);
     out_val[o + i] = __uint_as_float((uint32_t)key);
+    mn = min(mn, (uint32_t)key);
   }
   mn = __reduce_min_sync(kFull, mn);
   if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mn;

@@ -14,6 +14,6 @@ $C > gpurun_out/plain_l.log 2>&1 && \
 echo "launches=$?"
 C2="python bench.py --no-cpu --no-e2e --steps 1 --warmup 3"
 $C2 > gpurun_out/plain_f.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_spmm_tail|k_vhead_otf|k_uside" -s 8 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_spmm_tail|k_vhead_otf|k_uside_tc|k_uside_scatter" -s 8 -c 4 \
       -o gpurun_out/prof_full $C2 > gpurun_out/ncu_f.log 2>&1
 echo "full=$?"
