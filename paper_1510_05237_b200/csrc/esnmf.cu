@@ -474,7 +474,7 @@ void tail_launch(esnmf_t* h) {
   auto kern = trow ? k_spmm_tail<G, CPL, U, RG, true> : k_spmm_tail<G, CPL, U, RG, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t groups = ceil_div(sd.rows, RG);
-  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * 3);
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * kTailMinBlocks);
   ++h->nlaunch;
   kern<<<grid, kTailThreads, smem, h->stream>>>(sd.T.ptr, h->head_h > 0 ? h->nh : nullptr, sd.T.ent, sd.rows,
                                                 h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4,

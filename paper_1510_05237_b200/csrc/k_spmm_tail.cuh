@@ -28,6 +28,10 @@
 namespace esk {
 
 constexpr int kTailThreads = 256;
+#ifndef ESNMF_TAIL_MINB
+#define ESNMF_TAIL_MINB 3
+#endif
+constexpr int kTailMinBlocks = ESNMF_TAIL_MINB;
 constexpr int kTailSub = 4;              // entries per lane per load round
 constexpr int kTailRound = 32 * kTailSub;
 
@@ -109,7 +113,7 @@ ESNMF_DEV void ffma4(float4& acc, float x, const float4& z) {
 // buffer (400 contiguous bytes per row instead of 16-byte pieces of k columns);
 // otherwise store column-major into the LS buffer directly (no head).
 template <int G, int CPL, int U, int RG, bool TROW>
-__global__ void __launch_bounds__(kTailThreads, 3)
+__global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
     k_spmm_tail(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh, const int2* __restrict__ ent,
                 int64_t rows, const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int zq,
                 int kq, int k, float* __restrict__ X, int64_t ldx) {
