@@ -53,6 +53,7 @@ def _lib():
     lib.or_spmm.argtypes = [i64, i32, p, p, p, p, p]
     lib.or_spmm_rows.argtypes = [i64, p, i32, p, p, p, p, p]
     lib.or_clamp_top_t.argtypes = [i64, i32, i64, p, p]
+    lib.or_clamp_top_t_whole.argtypes = [i64, i32, i64, p, p]
     lib.or_residual.argtypes = [i64, i32, p, p]
     lib.or_residual.restype = d
     lib.or_error.argtypes = [i64, i32, p, p, p, p, d]
@@ -140,11 +141,17 @@ def spmm_rows(sel, ptr, idx, val, F: np.ndarray) -> np.ndarray:
     return Y
 
 
-def clamp_top_t(X: np.ndarray, t: int | None):
-    """Projection + per-column enforcement (P:63 clamp; P:134,146 keep t largest;
-    P:304 per column; C4 ties -> lower row).  Returns (X', kept_per_column)."""
+def clamp_top_t(X: np.ndarray, t: int | None, whole: bool = False):
+    """Projection + enforcement (P:63 clamp; P:134,146 keep t largest).
+    whole=False: per column (C4 ties -> lower row); returns (X', kept per column).
+    whole=True: of the whole matrix, Alg. 2 as printed (C17 ties ->
+    lower column, then row); returns (X', [kept total])."""
     X = np.array(X, dtype=np.float64, order="C", copy=True)
     rows, k = X.shape
+    if whole:
+        kept = np.empty(1, np.int64)
+        _lib().or_clamp_top_t_whole(rows, k, -1 if t is None else int(t), _p(X), _p(kept))
+        return X, kept
     kept = np.empty(k, np.int64)
     _lib().or_clamp_top_t(rows, k, -1 if t is None else int(t), _p(X), _p(kept))
     return X, kept
@@ -173,7 +180,7 @@ def frob2(val) -> float:
 
 # ------------------------------------------------------------------ the method
 
-def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFAULT) -> dict:
+def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFAULT, whole: bool = False) -> dict:
     """One ALS half-step in the paper's order (P:133-134 for the V side with
     T = A^T and F = U; P:135-136 for the U side with T = A and F = V):
         G = F^T F; L L^T = G + eps I; Y = T F; LS = Y (G + eps I)^{-1};
@@ -183,23 +190,32 @@ def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFA
     L, eps = cholesky(G, rho)
     Y = spmm(ptr, idx, val, F)
     LS = solve_rows(L, Y)
-    Fn, kept = clamp_top_t(LS, t)
+    Fn, kept = clamp_top_t(LS, t, whole)
     return dict(G=G, eps=eps, L=L, Y=Y, LS=LS, F=Fn, kept=kept)
 
 
+_SAME = object()
+
+
 def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float = RHO_DEFAULT,
-        U_init: np.ndarray | None = None, keep_states: bool = False) -> dict:
-    """Alg. 2 with per-column enforcement for ``iters`` iterations.
-    Returns the per-iteration records {it, R, E, nnz_u, nnz_v, dead_u, dead_v}
-    (IterationRecord) and the final dense U, V."""
+        U_init: np.ndarray | None = None, keep_states: bool = False, t_u=_SAME, t_v=_SAME,
+        whole: bool = False) -> dict:
+    """Alg. 2 for ``iters`` iterations: per-column enforcement
+    (BJ:5) or, whole=True, of the whole matrix (Alg. 2 as printed).
+    t_u / t_v (default t; None = unlimited) are the separate budgets of P:124
+    (U-only / V-only enforcement).  Returns the per-iteration records
+    {it, R, E, nnz_u, nnz_v, dead_u, dead_v} (IterationRecord, S:226-229) and
+    the final dense U, V."""
+    tu = t if t_u is _SAME else t_u
+    tv = t if t_v is _SAME else t_v
     n, m = inp["n"], inp["m"]
     U = (u0(n, k, seed) if U_init is None else U_init).astype(np.float64)
     normA2 = frob2(inp["a_val"])
     recs, states = [], []
     for it in range(1, iters + 1):
-        hv = half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, t, rho)   # P:133-134
+        hv = half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, tv, rho, whole)  # P:133-134
         V = hv["F"]
-        hu = half_step(inp["a_ptr"], inp["a_col"], inp["a_val"], V, t, rho)      # P:135-136
+        hu = half_step(inp["a_ptr"], inp["a_col"], inp["a_val"], V, tu, rho, whole)     # P:135-136
         Un = hu["F"]
         R = residual(Un, U)                                                      # P:160
         GU = gram(Un)

@@ -45,6 +45,20 @@ def top_t_per_column(X: np.ndarray, t: int | None) -> np.ndarray:
     return out
 
 
+def top_t_whole(X: np.ndarray, t: int | None) -> np.ndarray:
+    """clamp, then keep the t largest positives of the whole matrix, ties -> lower
+    column, then lower row (Alg. 2 as printed; reading C17)."""
+    Y = np.where(X > 0, X, 0.0)
+    if t is None:
+        return Y
+    r, c = np.nonzero(Y)
+    order = np.lexsort((r, c, -Y[r, c]))   # primary value desc, then column, then row
+    keep = order[:t]
+    out = np.zeros_like(Y)
+    out[r[keep], c[keep]] = Y[r[keep], c[keep]]
+    return out
+
+
 def projected_als(A: np.ndarray, U0: np.ndarray, t: int | None, iters: int, rho: float):
     """Alg. 2 (t given) / Alg. 1 (t None), per-column enforcement, dense."""
     U = U0.astype(np.float64)
@@ -56,5 +70,21 @@ def projected_als(A: np.ndarray, U0: np.ndarray, t: int | None, iters: int, rho:
         R = np.linalg.norm(Un - U) / np.linalg.norm(Un)
         E = np.linalg.norm(A - Un @ V.T) / nA
         recs.append((R, E))
+        U = Un
+    return U, V, recs
+
+
+def projected_als_budgets(A: np.ndarray, U0: np.ndarray, t_u: int | None, t_v: int | None, iters: int,
+                          rho: float, whole: bool):
+    """Alg. 2 as printed with separate budgets and whole-matrix or
+    per-column enforcement, dense."""
+    top = top_t_whole if whole else top_t_per_column
+    U = U0.astype(np.float64)
+    recs = []
+    nA = np.linalg.norm(A)
+    for _ in range(iters):
+        V = top(ls_step(A.T, U, rho), t_v)
+        Un = top(ls_step(A, V, rho), t_u)
+        recs.append((np.linalg.norm(Un - U) / np.linalg.norm(Un), np.linalg.norm(A - Un @ V.T) / nA))
         U = Un
     return U, V, recs

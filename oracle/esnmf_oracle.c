@@ -186,6 +186,44 @@ void or_clamp_top_t(int64_t rows, int32_t k, int64_t t, double* X, int64_t* kept
   }
 }
 
+/* ---- projection + WHOLE-MATRIX enforcement: Alg. 2 as printed ("keep
+ * the t_v largest values of V", P:136 for U; "find the t-th largest").
+ * Negatives and zeros -> 0; if more than t entries are positive, only the t
+ * largest of the whole matrix stay, ties ordered by lower column, then lower
+ * row (reading C17, the column-major order of the factor).  *kept receives the
+ * surviving count. ---- */
+typedef struct { double v; int64_t idx; } or_entry_w;  /* idx = c * rows + j */
+
+static int or_cmp_entry_w(const void* pa, const void* pb) {
+  const or_entry_w* a = (const or_entry_w*)pa;
+  const or_entry_w* b = (const or_entry_w*)pb;
+  if (a->v > b->v) return -1; /* value descending */
+  if (a->v < b->v) return 1;
+  return (a->idx < b->idx) ? -1 : (a->idx > b->idx); /* (column, row) ascending */
+}
+
+void or_clamp_top_t_whole(int64_t rows, int32_t k, int64_t t, double* X, int64_t* kept) {
+  int64_t npos = 0;
+  for (int64_t q = 0; q < rows * (int64_t)k; ++q) {
+    if (X[q] > 0.0) ++npos; else X[q] = 0.0;
+  }
+  if (t < 0 || npos <= t) { *kept = npos; return; }
+  or_entry_w* e = (or_entry_w*)malloc(sizeof(or_entry_w) * (size_t)npos);
+  int64_t p = 0;
+  for (int32_t c = 0; c < k; ++c)
+    for (int64_t j = 0; j < rows; ++j) {
+      double v = X[j * (int64_t)k + c];
+      if (v > 0.0) { e[p].v = v; e[p].idx = (int64_t)c * rows + j; ++p; }
+    }
+  qsort(e, (size_t)npos, sizeof(or_entry_w), or_cmp_entry_w);
+  for (int64_t q = t; q < npos; ++q) {
+    const int64_t c = e[q].idx / rows, j = e[q].idx % rows;
+    X[j * (int64_t)k + c] = 0.0;
+  }
+  *kept = t;
+  free(e);
+}
+
 /* ---- R = ||U_i - U_{i-1}||_F / ||U_i||_F by direct difference (C8) ----
  * returns -1 when ||U_i|| == 0 (degenerate). */
 double or_residual(int64_t rows, int32_t k, const double* Unew, const double* Uold) {

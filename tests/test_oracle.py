@@ -266,3 +266,59 @@ def test_oracle_tiny_config_records_sane():
         assert x["nnz_u"] <= cfg.k * cfg.t and x["nnz_v"] <= cfg.k * cfg.t
     assert r["records"][0]["R"] > 0.5   # U_1 differs from the dense U_0
     assert r["records"][-1]["E"] < r["records"][0]["E"]
+
+
+# ---- Alg. 2 as printed: whole-matrix enforcement, separate budgets (NEXT-1) ----
+
+def test_whole_matrix_top_t_against_bruteforce_and_invariants():
+    rng = np.random.default_rng(11)
+    X = rng.normal(size=(200, 6))
+    X[5:15, 2] = 0.5            # exact ties inside a column
+    X[5:15, 4] = 0.5            # ... and across columns
+    X[:, 1] = -1.0              # all-negative column
+    npos = int(np.sum(X > 0))
+    for t in (0, 1, 7, 40, 333, npos, npos + 10, None):
+        Y, kept = oracle.clamp_top_t(X, t, whole=True)
+        assert np.array_equal(Y, bf.top_t_whole(X, t))
+        want = npos if t is None else min(t, npos)
+        assert kept[0] == want == np.count_nonzero(Y)
+        kv, dv = Y[Y > 0], X[(X > 0) & (Y == 0)]
+        if len(kv) and len(dv):
+            assert kv.min() >= dv.max()                       # nothing dropped beats a kept entry
+        assert np.array_equal(oracle.clamp_top_t(Y, t, whole=True)[0], Y)   # idempotent
+    # ties at 0.5: lower column first, then lower row
+    above = int(np.sum(X > 0.5))
+    t = above + 12
+    Y, _ = oracle.clamp_top_t(X, t, whole=True)
+    assert np.count_nonzero(Y[5:15, 2]) == 10 and np.count_nonzero(Y[5:15, 4]) == 2
+    assert np.nonzero(Y[5:15, 4])[0].tolist() == [0, 1]
+
+
+def test_whole_matrix_reduces_to_per_column_for_one_column():
+    rng = np.random.default_rng(12)
+    X = rng.normal(size=(500, 1))
+    for t in (0, 3, 100, 499, None):
+        assert np.array_equal(oracle.clamp_top_t(X, t, whole=True)[0], oracle.clamp_top_t(X, t)[0])
+
+
+@pytest.mark.parametrize("t_u,t_v,whole", [(10, 25, True), (None, 6, False), (6, None, False), (15, None, True)])
+def test_oracle_budgets_match_bruteforce(t_u, t_v, whole):
+    """Separate t_u / t_v, U-only / V-only enforcement,
+    whole-matrix (Alg. 2 as printed) against the dense numpy twin."""
+    rng = np.random.default_rng(13)
+    n, m, k = 40, 30, 3
+    A = rand_sparse(rng, n, m, 0.25)
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    inp = dict(n=n, m=m, a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+    rho = 1e-10
+    r = oracle.run(inp, k, 999, 6, seed=5, rho=rho, t_u=t_u, t_v=t_v, whole=whole)
+    U, V, recs = bf.projected_als_budgets(A, oracle.u0(n, k, 5), t_u, t_v, 6, rho, whole)
+    assert np.allclose(r["U"], U, rtol=1e-9, atol=1e-12 * np.abs(U).max())
+    assert np.allclose(r["V"], V, rtol=1e-9, atol=1e-12 * np.abs(V).max())
+    for rec, (R, E) in zip(r["records"], recs):
+        assert rec["E"] == pytest.approx(E, rel=1e-10)
+        if whole and t_u is not None:
+            assert rec["nnz_u"] <= t_u
+        if whole and t_v is not None:
+            assert rec["nnz_v"] <= t_v
