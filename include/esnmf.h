@@ -59,6 +59,9 @@ typedef enum {
 } esnmf_status;
 
 #define ESNMF_T_UNLIMITED (-1) /* Alg. 1, projected ALS: no truncation */
+#define ESNMF_T_SAME (-2)      /* esnmf_options.t_u / t_v: use create's t */
+#define ESNMF_ENFORCE_COLUMN 0 /* keep the t largest of every topic column (BJ:5) */
+#define ESNMF_ENFORCE_MATRIX 1 /* keep the t largest of the whole factor: Alg. 2 as printed */
 #define ESNMF_SIDE_V 0         /* half-step 1: V <- A^T U */
 #define ESNMF_SIDE_U 1         /* half-step 2: U <- A V */
 #define ESNMF_MAX_K 256
@@ -100,6 +103,13 @@ typedef struct {
      row gather.  -1 (default) = automatic (terms in >= 4 % of the documents),
      0 = off.  The result is the same product to fp32 accuracy either way. */
   int32_t head_terms;
+  /* Separate budgets of Alg. 2 ("t_u, t_v"): ESNMF_T_SAME (default) = create's
+     t, ESNMF_T_UNLIMITED = no truncation of that factor (U-only / V-only
+     enforcement), >= 0 = that budget. */
+  int64_t t_u, t_v;
+  /* ESNMF_ENFORCE_COLUMN (default) or ESNMF_ENFORCE_MATRIX (whole-factor top-t,
+     ties -> lower column, then lower row; single GPU only: EINVAL with world > 1). */
+  int32_t enforce;
 } esnmf_options;
 
 typedef struct {

@@ -10,6 +10,9 @@ from .esnmf import (  # noqa: F401
     ESNMFError,
     ESNMF_SIDE_U,
     ESNMF_SIDE_V,
+    ESNMF_ENFORCE_COLUMN,
+    ESNMF_ENFORCE_MATRIX,
+    ESNMF_T_SAME,
     ESNMF_T_UNLIMITED,
     SIGNATURES,
     esnmf_create,

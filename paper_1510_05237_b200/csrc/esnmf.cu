@@ -138,7 +138,10 @@ struct esnmf {
   bool u_prefork = false;        // the U side's Gram + solve already enqueued on aux (after V's row view)
   int64_t n = 0, m = 0, nnz = 0;
   int k = 0, kpad = 0;
-  int64_t t = 0;  // < 0 unlimited
+  int64_t t = 0;  // < 0 unlimited (create's t)
+  int64_t tside[2] = {0, 0};  // budgets per side: [0] t_v (V side), [1] t_u (U side)
+  bool whole = false;         // whole-factor enforcement (Alg. 2 as printed)
+  int64_t* wcolptr = nullptr; // [2] colptr of the flat (one-column) selection
   double rho = 1e-10;
   uint64_t seed = 0;
   int world = 1, rank = 0;
@@ -368,7 +371,10 @@ void factor_build_rows(esnmf_t* h, Factor& f, int64_t maxcol) {
   f.has = true;
 }
 
-int64_t steady_maxcol(esnmf_t* h, int64_t rows) { return h->t < 0 ? rows : std::min(rows, h->t); }
+int64_t steady_maxcol(esnmf_t* h, int s, int64_t rows) {
+  const int64_t t = h->tside[s];
+  return t < 0 ? rows : std::min(rows, t);
+}
 
 // ---------------------------------------------------------------- kernels
 
@@ -620,73 +626,109 @@ void vrows_build(esnmf_t* h) {
 }
 
 // clamp + per-column top-t of side s's LS into factor `out` (column-major COO)
-void select_topt(esnmf_t* h, int s, Factor& out) {
-  Side& sd = h->side[s];
-  const int k = h->k;
-  if (sd.rows == 0) fail(ESNMF_EINVAL, "empty shard");
-  const int64_t nch = sd.nchunks;
+// the selection over a column-major buffer X (ldx x kc, `rows` rows used) into
+// (colptr_out[kc+1], row_out, val_out); per-column top-t, or with kc = 1 over a
+// flat view of the whole factor
+void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows, int kc, int64_t row0, int64_t t,
+                 bool use_pred, int64_t* colptr_out, int32_t* row_out, float* val_out) {
+  const int k = kc;
+  if (rows == 0) fail(ESNMF_EINVAL, "empty shard");
+  const int64_t nch = std::max<int64_t>(1, ceil_div(rows, kSelChunk));
   const int64_t nseg = nch * kSelSegs;  // per-(column, segment) output counts
   CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
-  if (sd.above && sd.pred) {
+  if (sd.above && sd.pred && use_pred) {
     // one pass over X in steady state: histogram + candidates above the predicted
     // threshold (k_sel_pred_final); columns whose prediction failed take the
     // second pass (k_sel_collect2 + k_sel_final)
     CK(cudaMemsetAsync(sd.pfill, 0, sizeof(int32_t) * k, h->stream));
     ++h->nlaunch;
-    k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist, sd.pred, sd.row0, sd.pcand, sd.pfill,
+    k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist, sd.pred, row0, sd.pcand, sd.pfill,
                                          sd.pcap);
-    ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+    ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
     ++h->nlaunch;
-    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, h->t, out.colptr);
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out);
     int32_t* done = sd.pfill + k;
     const size_t psm = sizeof(uint64_t) * (kSelFastT + kSelCap);
     CK(cudaFuncSetAttribute(k_sel_pred_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
     ++h->nlaunch;
-    k_sel_pred_final<<<k, 1024, psm, h->stream>>>(sd.sel, std::max<int64_t>(h->t, 1), sd.pcand, sd.pfill, sd.pcap,
-                                                  out.colptr, out.row, out.val, done, sd.pred);
+    k_sel_pred_final<<<k, 1024, psm, h->stream>>>(sd.sel, std::max<int64_t>(t, 1), sd.pcand, sd.pfill, sd.pcap,
+                                                  colptr_out, row_out, val_out, done, sd.pred);
     CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
     int32_t* bfill = sd.above_fill + k;
     ++h->nlaunch;
-    k_sel_collect2<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(h->t, 1),
+    k_sel_collect2<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, std::max<int64_t>(t, 1),
                                              sd.above, sd.above_fill, sd.bucket, bfill, done);
     CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
     ++h->nlaunch;
-    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel,
-                                                       std::max<int64_t>(h->t, 1), sd.above, sd.above_fill,
-                                                       sd.bucket, bfill, out.colptr, out.row, out.val, done,
+    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(X, ldx, rows, row0, sd.sel,
+                                                       std::max<int64_t>(t, 1), sd.above, sd.above_fill,
+                                                       sd.bucket, bfill, colptr_out, row_out, val_out, done,
                                                        sd.pred);
     CKL("select2");
     return;
   }
-  ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist);
-  ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, h->t, sd.sel);
+  ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist);
+  ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
   if (sd.above) {  // two passes over X (k_sel_collect2 + k_sel_final)
     CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
     int32_t* bfill = sd.above_fill + k;
     ++h->nlaunch;
-    k_sel_collect2<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(h->t, 1),
+    k_sel_collect2<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, std::max<int64_t>(t, 1),
                                              sd.above, sd.above_fill, sd.bucket, bfill);
     ++h->nlaunch;
-    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, h->t, out.colptr);
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out);
     CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
     ++h->nlaunch;
-    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel,
-                                                       std::max<int64_t>(h->t, 1), sd.above, sd.above_fill,
-                                                       sd.bucket, bfill, out.colptr, out.row, out.val);
+    k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(X, ldx, rows, row0, sd.sel,
+                                                       std::max<int64_t>(t, 1), sd.above, sd.above_fill,
+                                                       sd.bucket, bfill, colptr_out, row_out, val_out);
     CKL("select2");
     return;
   }
-  ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+  ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg);
-  ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.cand, sd.cand_fill,
+  ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg, sd.kthr);
   ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.coltot);
-  ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, out.colptr);
-  ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, sd.kthr, out.colptr,
-                                        sd.chunk_cnt, nseg, out.row, out.val);
+  ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, colptr_out);
+  ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.kthr, colptr_out,
+                                        sd.chunk_cnt, nseg, row_out, val_out);
   CKL("select");
+}
+
+// flat selection indices (c * ldx + row, ascending) -> rows in place + per-column colptr
+__global__ void k_whole_split(int32_t* __restrict__ idx, const int64_t* __restrict__ flat_colptr, int64_t ldx, int k,
+                              int64_t* __restrict__ colptr) {
+  const int64_t nnz = flat_colptr[1];
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) {  // first entry of column c (binary search)
+    int64_t lo = 0, hi = nnz;
+    const int64_t key = (int64_t)c * ldx;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)(uint32_t)idx[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    colptr[c] = lo;
+  }
+  __syncthreads();
+  for (int64_t q = threadIdx.x; q < nnz; q += blockDim.x) idx[q] = (int32_t)((int64_t)(uint32_t)idx[q] % ldx);
+}
+
+// clamp + top-t of side s's LS into factor `out` (column-major COO)
+void select_topt(esnmf_t* h, int s, Factor& out) {
+  Side& sd = h->side[s];
+  const int64_t t = h->tside[s];
+  if (!h->whole) {
+    select_core(h, sd, sd.X, sd.ldx, sd.rows, h->k, sd.row0, t, true, out.colptr, out.row, out.val);
+    return;
+  }
+  // Alg. 2 as printed: one selection over the flat k x ldx buffer (padding rows are 0)
+  select_core(h, sd, sd.X, (int64_t)h->k * sd.ldx, (int64_t)h->k * sd.ldx, 1, 0, t, false, h->wcolptr, out.row,
+              out.val);
+  ++h->nlaunch;
+  k_whole_split<<<1, 1024, 0, h->stream>>>(out.row, h->wcolptr, sd.ldx, h->k, out.colptr);
+  CKL("whole_split");
 }
 
 void select_merge(esnmf_t* h, int s, Factor& out);
@@ -862,7 +904,7 @@ Factor& half_step(esnmf_t* h, int s) {
   }
   {
     Phase ph(h, p0 + 5);
-    factor_build_rows(h, out, steady_maxcol(h, out.rows));
+    factor_build_rows(h, out, steady_maxcol(h, s, out.rows));
     if (s == ESNMF_SIDE_V && h->world == 1) {
       // the U side's a1 + a2 need only V's row view: start them now on aux,
       // beside V's row-CSR build and the U side's scatter
@@ -1005,16 +1047,18 @@ void side_alloc(esnmf_t* h, Side& sd) {
   const int k = h->k;
   sd.ldx = std::max<int64_t>(32, ceil_div(sd.rows, 32) * 32);
   sd.X = h->alloc<float>((int64_t)k * sd.ldx);
+  CK(cudaMemsetAsync(sd.X, 0, sizeof(float) * k * sd.ldx, h->stream));  // padding rows stay 0 (flat view)
   sd.nchunks = std::max<int64_t>(1, ceil_div(sd.rows, kSelChunk));
   sd.hist = h->alloc<uint32_t>((int64_t)k * kNumBins);
   sd.sel = h->alloc<ColSel>(k);
   sd.cand = h->alloc<uint64_t>((int64_t)k * kSelCap);
   sd.cand_fill = h->alloc<int32_t>(k);
-  sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * sd.nchunks * kSelSegs);
+  sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * (sd.nchunks + 1) * kSelSegs);  // (+1: the flat view)
   sd.coltot = h->alloc<int64_t>(k);
   sd.kthr = h->alloc<uint64_t>(k);
-  if (h->t >= 0 && h->t <= kSelFastT) {
-    sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(h->t, 1));
+  const int64_t ts = h->tside[&sd == &h->side[ESNMF_SIDE_V] ? 0 : 1];
+  if (ts >= 0 && ts <= kSelFastT) {
+    sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(ts, 1));
     sd.above_fill = h->alloc<int32_t>(2 * (int64_t)k);
     sd.bucket = h->alloc<uint64_t>((int64_t)k * kSelCap);
     // predicted-threshold single pass: worth its extra kernel only when the LS
@@ -1022,7 +1066,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
     int64_t min_rows = 1 << 19;
     if (const char* pe = getenv("ESNMF_PRED_MIN_ROWS")) min_rows = atoll(pe);  // tests force it on small shards
     if (sd.rows >= min_rows) {
-      sd.pcap = (int)std::min<int64_t>(kPredSort, 2 * h->t + 2048);
+      sd.pcap = (int)std::min<int64_t>(kPredSort, 2 * ts + 2048);
       sd.pred = h->alloc<uint32_t>(k);
       CK(cudaMemsetAsync(sd.pred, 0xFF, sizeof(uint32_t) * k, h->stream));
       sd.pcand = h->alloc<uint64_t>((int64_t)k * sd.pcap);
@@ -1033,7 +1077,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.eps = h->alloc<double>(1);
   if (h->world > 1) {
     const int64_t rows_max = (&sd == &h->side[ESNMF_SIDE_V]) ? h->v_rows_max : h->u_rows_max;
-    sd.cap_s = std::max<int64_t>(1, h->t < 0 ? rows_max : std::min(h->t, rows_max));
+    sd.cap_s = std::max<int64_t>(1, ts < 0 ? rows_max : std::min(ts, rows_max));
     sd.lcolptr = h->alloc<int64_t>(k + 1);
     sd.lrow = h->alloc<int32_t>((int64_t)k * sd.cap_s);
     sd.lval = h->alloc<float>((int64_t)k * sd.cap_s);
@@ -1062,8 +1106,9 @@ void select_merge(esnmf_t* h, int s, Factor& out) {
   if (h->comm.allgather(h->comm.ctx, sd.sendbuf, sd.recvbuf, (int64_t)sd.shard_bytes, h->stream) != 0)
     fail(ESNMF_ECOMM, "allgather(top-t candidates) failed");
   h->nlaunch += 2;
-  k_merge_counts<<<1, 256, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->t, out.colptr);
-  k_merge_topt<<<k, 1024, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->t, out.colptr,
+  k_merge_counts<<<1, 256, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->tside[s],
+                                           out.colptr);
+  k_merge_topt<<<k, 1024, 0, h->stream>>>(sd.recvbuf, sd.shard_bytes, h->world, k, sd.cap_s, h->tside[s], out.colptr,
                                           out.row, out.val, sd.mscratch);
   CKL("merge_topt");
 }
@@ -1238,6 +1283,9 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->world = 1;
   o->rank = 0;
   o->head_terms = -1;
+  o->t_u = ESNMF_T_SAME;
+  o->t_v = ESNMF_T_SAME;
+  o->enforce = ESNMF_ENFORCE_COLUMN;
   return ESNMF_OK;
 }
 
@@ -1272,6 +1320,19 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
   }
   if (k < 1 || k > ESNMF_MAX_K) { g_last_error = "esnmf_create: need 1 <= k <= 256"; return ESNMF_EINVAL; }
   if (t < 0 && t != ESNMF_T_UNLIMITED) { g_last_error = "esnmf_create: t must be >= 0 or ESNMF_T_UNLIMITED"; return ESNMF_EINVAL; }
+  if (opt && ((opt->t_u < 0 && opt->t_u != ESNMF_T_UNLIMITED && opt->t_u != ESNMF_T_SAME) ||
+              (opt->t_v < 0 && opt->t_v != ESNMF_T_UNLIMITED && opt->t_v != ESNMF_T_SAME))) {
+    g_last_error = "esnmf_create: t_u / t_v must be >= 0, ESNMF_T_UNLIMITED or ESNMF_T_SAME";
+    return ESNMF_EINVAL;
+  }
+  if (opt && opt->enforce != ESNMF_ENFORCE_COLUMN && opt->enforce != ESNMF_ENFORCE_MATRIX) {
+    g_last_error = "esnmf_create: enforce must be ESNMF_ENFORCE_COLUMN or ESNMF_ENFORCE_MATRIX";
+    return ESNMF_EINVAL;
+  }
+  if (opt && opt->enforce == ESNMF_ENFORCE_MATRIX && opt->world > 1) {
+    g_last_error = "esnmf_create: whole-matrix enforcement is single-GPU only";
+    return ESNMF_EINVAL;
+  }
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { g_last_error = "esnmf_create: bad world/rank"; return ESNMF_EINVAL; }
   if (o.world > 1 && (!o.comm || !o.comm->allgather || !o.comm->allreduce_sum_f64)) {
     g_last_error = "esnmf_create: world > 1 needs comm callbacks";
@@ -1303,6 +1364,12 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
     CK(cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
     h->t = t;
+    h->tside[0] = o.t_v == ESNMF_T_SAME ? t : o.t_v;
+    h->tside[1] = o.t_u == ESNMF_T_SAME ? t : o.t_u;
+    h->whole = o.enforce == ESNMF_ENFORCE_MATRIX;
+    if (h->whole && (int64_t)k * (std::max(n, m) + 32) >= (1LL << 31))
+      fail(ESNMF_EINVAL, "esnmf_create: whole-matrix enforcement needs k * rows < 2^31");
+    h->wcolptr = h->alloc<int64_t>(2);
     h->rho = o.ridge_scale;
     h->seed = o.seed;
     h->world = o.world;
@@ -1365,7 +1432,9 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     side_alloc(h.get(), su);
     // ---- factors ----
     const int64_t capU = n * (int64_t)k;
-    const int64_t capV = (t < 0 ? m : std::min(m, t)) * (int64_t)k;
+    const int64_t tv = h->tside[0];
+    const int64_t capV = h->whole ? (tv < 0 ? m * (int64_t)k : std::min(m * (int64_t)k, std::max<int64_t>(tv, 1)))
+                                  : (tv < 0 ? m : std::min(m, tv)) * (int64_t)k;
     factor_alloc(h.get(), h->U[0], n, capU);
     factor_alloc(h.get(), h->U[1], n, capU);
     factor_alloc(h.get(), h->V, m, capV);

@@ -19,6 +19,8 @@ c_i32, c_i64, c_u64, c_dbl, c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint6
 ESNMF_OK, ESNMF_EINVAL, ESNMF_ENOMEM, ESNMF_ECUDA, ESNMF_ECOMM = 0, 1, 2, 3, 4
 ESNMF_ESINGULAR, ESNMF_EDEGENERATE, ESNMF_ESTATE, ESNMF_ETRUNC = 5, 6, 7, 8
 ESNMF_T_UNLIMITED = -1
+ESNMF_T_SAME = -2
+ESNMF_ENFORCE_COLUMN, ESNMF_ENFORCE_MATRIX = 0, 1
 ESNMF_SIDE_V, ESNMF_SIDE_U = 0, 1
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_p, c_p, c_p, c_i64, c_p)
@@ -35,7 +37,7 @@ class esnmf_options(ctypes.Structure):
         ("world", c_i32), ("rank", c_i32), ("comm", ctypes.POINTER(esnmf_comm)),
         ("inputs_on_device", c_i32),
         ("at_row_ptr", c_p), ("at_col_idx", c_p), ("at_val", c_p), ("U0", c_p),
-        ("head_terms", c_i32),
+        ("head_terms", c_i32), ("t_u", c_i64), ("t_v", c_i64), ("enforce", c_i32),
     ]
 
 
@@ -273,9 +275,14 @@ class ESNMF:
 
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
                  device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None,
-                 head_terms: int = -1):
+                 head_terms: int = -1, t_u="same", t_v="same", whole: bool = False):
+        """t_u / t_v: separate budgets ("same" = t, None = unlimited); whole: whole-factor
+        enforcement (Alg. 2 as printed) instead of per column."""
         o = esnmf_options_init()
         o.head_terms = head_terms
+        o.t_u = ESNMF_T_SAME if t_u == "same" else (ESNMF_T_UNLIMITED if t_u is None else int(t_u))
+        o.t_v = ESNMF_T_SAME if t_v == "same" else (ESNMF_T_UNLIMITED if t_v is None else int(t_v))
+        o.enforce = ESNMF_ENFORCE_MATRIX if whole else ESNMF_ENFORCE_COLUMN
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device
