@@ -110,6 +110,10 @@ typedef struct {
   /* ESNMF_ENFORCE_COLUMN (default) or ESNMF_ENFORCE_MATRIX (whole-factor top-t,
      ties -> lower column, then lower row; single GPU only: EINVAL with world > 1). */
   int32_t enforce;
+  /* Sparse initial guess (P:289-298 vary the nnz of U_0; reading C18): 0 (default) =
+     dense U_0; > 0 = keep U0[i,c] only where splitmix64(seed ^ 0x55305F4D41534B30 ^
+     (i*k + c)) >> 11 < init_nnz * 2^53 / n (expected init_nnz entries per column). */
+  int64_t init_nnz;
 } esnmf_options;
 
 typedef struct {
@@ -119,6 +123,9 @@ typedef struct {
   int64_t nnz_u, nnz_v;  /* stored entries of U and V ("NNZ") */
   int32_t dead_u, dead_v;/* all-zero columns (dead topics, reading C6) */
   int64_t active_u, active_v; /* rows holding at least one entry */
+  int64_t peak_u, peak_v;     /* positive entries of the clamped least-squares factor before
+                                 truncation: the peak stored nnz of that half-step (P:289-298,
+                                 S:226-229 peak_nnz); this rank's share when world > 1 */
 } esnmf_record;
 
 /* Fill *opt with the defaults above.  Always ESNMF_OK (EINVAL if opt NULL). */
@@ -217,6 +224,15 @@ void esnmf_destroy(esnmf_t* h);
 
 const char* esnmf_strerror(esnmf_status s);
 const char* esnmf_last_error(void);
+
+/* Enforce-after: clamp and truncate the CURRENT
+ * factor of `side` once, in place -- the t largest entries per column
+ * (enforce = ESNMF_ENFORCE_COLUMN) or of the whole factor (ESNMF_ENFORCE_MATRIX),
+ * same tie rules as the iteration (C4, C17).  Typical use: create with t =
+ * ESNMF_T_UNLIMITED (Alg. 1), iterate, then truncate U and V.  Records are not
+ * changed.  Errors: EINVAL (side, t < 0), ESTATE (factor not set), ECUDA.
+ * Single GPU only (EINVAL with world > 1). */
+esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce);
 
 /* Host-only helper (no GPU needed): nnz-balanced contiguous partition of
  * `rows` rows into `world` ranges; bounds[world+1].  Used for the row shards

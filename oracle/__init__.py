@@ -44,6 +44,7 @@ def _lib():
     lib = ctypes.CDLL(_SO)
     i64, i32, u64, p, d = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_double
     lib.or_u0.argtypes = [i64, i32, u64, p]
+    lib.or_u0_sparsify.argtypes = [i64, i32, u64, i64, p]
     lib.or_splitmix64_pub.argtypes = [u64]
     lib.or_splitmix64_pub.restype = u64
     lib.or_gram.argtypes = [i64, i32, p, p]
@@ -78,10 +79,14 @@ def splitmix64(x: int) -> int:
     return int(_lib().or_splitmix64_pub(x))
 
 
-def u0(n: int, k: int, seed: int = 0) -> np.ndarray:
-    """Initial guess U_0 (reading C10): dense uniform(0,1), fp32-exact."""
+def u0(n: int, k: int, seed: int = 0, init_nnz: int = 0) -> np.ndarray:
+    """Initial guess U_0 (reading C10): dense uniform(0,1), fp32-exact.
+    init_nnz > 0: each entry kept with probability init_nnz / n by a hash draw
+    (reading C18; the nnz of U_0 varied in P:289-298)."""
     out = np.empty((n, k), np.float32)
     _lib().or_u0(n, k, seed, _p(out))
+    if init_nnz > 0:
+        _lib().or_u0_sparsify(n, k, seed, int(init_nnz), _p(out))
     return out
 
 
@@ -199,7 +204,7 @@ _SAME = object()
 
 def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float = RHO_DEFAULT,
         U_init: np.ndarray | None = None, keep_states: bool = False, t_u=_SAME, t_v=_SAME,
-        whole: bool = False) -> dict:
+        whole: bool = False, init_nnz: int = 0) -> dict:
     """Alg. 2 for ``iters`` iterations: per-column enforcement
     (BJ:5) or, whole=True, of the whole matrix (Alg. 2 as printed).
     t_u / t_v (default t; None = unlimited) are the separate budgets of P:124
@@ -209,7 +214,7 @@ def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float 
     tu = t if t_u is _SAME else t_u
     tv = t if t_v is _SAME else t_v
     n, m = inp["n"], inp["m"]
-    U = (u0(n, k, seed) if U_init is None else U_init).astype(np.float64)
+    U = (u0(n, k, seed, init_nnz) if U_init is None else U_init).astype(np.float64)
     normA2 = frob2(inp["a_val"])
     recs, states = [], []
     for it in range(1, iters + 1):
@@ -221,7 +226,8 @@ def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float 
         GU = gram(Un)
         E = error(Un, hu["Y"], GU, hu["G"], normA2)
         recs.append(dict(it=it, R=R, E=E, nnz_u=int(np.count_nonzero(Un)), nnz_v=int(np.count_nonzero(V)),
-                         dead_u=int(np.sum(~Un.any(axis=0))), dead_v=int(np.sum(~V.any(axis=0)))))
+                         dead_u=int(np.sum(~Un.any(axis=0))), dead_v=int(np.sum(~V.any(axis=0))),
+                         peak_u=int(np.sum(hu["LS"] > 0)), peak_v=int(np.sum(hv["LS"] > 0))))
         if keep_states:
             states.append(dict(U_prev=U, V=V, U=Un, LS_V=hv["LS"], LS_U=hu["LS"], G_U=hv["G"], G_V=hu["G"]))
         U = Un

@@ -52,6 +52,21 @@ void or_u0(int64_t n, int32_t k, uint64_t seed, float* out) {
     }
 }
 
+/* ---- sparse initial guess (P:289-298 vary the nnz of U_0; reading C18):
+ * U0[i,c] kept iff (splitmix64(seed ^ K_MASK ^ (i*k + c)) >> 11) < init_nnz 2^53 / n,
+ * i.e. an independent Bernoulli(init_nnz / n) draw per entry; others 0. ---- */
+#define OR_K_U0_MASK 0x55305F4D41534B30ULL /* "U0_MASK0" */
+void or_u0_sparsify(int64_t n, int32_t k, uint64_t seed, int64_t init_nnz, float* U) {
+  if (init_nnz <= 0) return;
+  const double p = (double)init_nnz / (double)n;
+  const uint64_t thr = p >= 1.0 ? UINT64_MAX : (uint64_t)(p * 0x1p53);
+  for (int64_t i = 0; i < n; ++i)
+    for (int32_t c = 0; c < k; ++c) {
+      uint64_t x = or_splitmix64(seed ^ OR_K_U0_MASK ^ (uint64_t)(i * (int64_t)k + c));
+      if ((x >> 11) >= thr) U[i * (int64_t)k + c] = 0.0f;
+    }
+}
+
 /* ---- Gram matrix F^T F ("U^T U", "V^T V") ---- */
 void or_gram(int64_t rows, int32_t k, const double* F, double* G) {
   for (int32_t a = 0; a < k; ++a)

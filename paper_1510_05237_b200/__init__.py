@@ -32,6 +32,7 @@ from .esnmf import (  # noqa: F401
     esnmf_records,
     esnmf_residual,
     esnmf_set_factor,
+    esnmf_truncate,
     esnmf_version,
     lib,
 )

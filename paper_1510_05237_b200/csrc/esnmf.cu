@@ -101,6 +101,7 @@ struct Side {
   int64_t* coltot = nullptr;
   uint64_t* kthr = nullptr;
   uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
+  int64_t above_t = -1;           // its t capacity per column
   int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
   uint64_t* bucket = nullptr;     // [k][kSelCap] value keys of the threshold bucket
   // predicted-threshold candidates (the previous select's t-th value - 10 %)
@@ -111,6 +112,7 @@ struct Side {
   // Gram of the factor this side reads, and its eps
   double* G = nullptr;
   double* eps = nullptr;
+  int64_t* peak = nullptr;  // positives of the clamped LS of the last select (record peak nnz)
   bool ls_valid = false;
   // multi-rank: local top-t, exchange buffers, merge scratch (k_merge.cuh)
   int64_t cap_s = 0;            // candidates per column per rank
@@ -141,6 +143,7 @@ struct esnmf {
   int64_t t = 0;  // < 0 unlimited (create's t)
   int64_t tside[2] = {0, 0};  // budgets per side: [0] t_v (V side), [1] t_u (U side)
   bool whole = false;         // whole-factor enforcement (Alg. 2 as printed)
+  int64_t init_nnz = 0;       // > 0: sparse U_0 (reading C18)
   int64_t* wcolptr = nullptr; // [2] colptr of the flat (one-column) selection
   double rho = 1e-10;
   uint64_t seed = 0;
@@ -630,7 +633,7 @@ void vrows_build(esnmf_t* h) {
 // (colptr_out[kc+1], row_out, val_out); per-column top-t, or with kc = 1 over a
 // flat view of the whole factor
 void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows, int kc, int64_t row0, int64_t t,
-                 bool use_pred, int64_t* colptr_out, int32_t* row_out, float* val_out) {
+                 bool use_pred, int64_t* colptr_out, int32_t* row_out, float* val_out, int64_t* peak_out) {
   const int k = kc;
   if (rows == 0) fail(ESNMF_EINVAL, "empty shard");
   const int64_t nch = std::max<int64_t>(1, ceil_div(rows, kSelChunk));
@@ -638,7 +641,9 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
-  if (sd.above && sd.pred && use_pred) {
+  // two-pass path: the [k][t] list must fit and the kept set of a column must fit k_sel_final's smem
+  const bool fast = sd.above && t >= 0 && t <= kSelFastT && t * kc <= sd.above_t * h->k;
+  if (fast && sd.pred && use_pred) {
     // one pass over X in steady state: histogram + candidates above the predicted
     // threshold (k_sel_pred_final); columns whose prediction failed take the
     // second pass (k_sel_collect2 + k_sel_final)
@@ -647,6 +652,7 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
     k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist, sd.pred, row0, sd.pcand, sd.pfill,
                                          sd.pcap);
     ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
+  if (peak_out) { ++h->nlaunch; k_sel_npos_sum<<<1, 256, 0, h->stream>>>(sd.sel, k, peak_out); }
     ++h->nlaunch;
     k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out);
     int32_t* done = sd.pfill + k;
@@ -671,7 +677,8 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   }
   ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist);
   ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
-  if (sd.above) {  // two passes over X (k_sel_collect2 + k_sel_final)
+  if (peak_out) { ++h->nlaunch; k_sel_npos_sum<<<1, 256, 0, h->stream>>>(sd.sel, k, peak_out); }
+  if (fast) {  // two passes over X (k_sel_collect2 + k_sel_final)
     CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
     int32_t* bfill = sd.above_fill + k;
     ++h->nlaunch;
@@ -720,12 +727,12 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   Side& sd = h->side[s];
   const int64_t t = h->tside[s];
   if (!h->whole) {
-    select_core(h, sd, sd.X, sd.ldx, sd.rows, h->k, sd.row0, t, true, out.colptr, out.row, out.val);
+    select_core(h, sd, sd.X, sd.ldx, sd.rows, h->k, sd.row0, t, true, out.colptr, out.row, out.val, sd.peak);
     return;
   }
   // Alg. 2 as printed: one selection over the flat k x ldx buffer (padding rows are 0)
   select_core(h, sd, sd.X, (int64_t)h->k * sd.ldx, (int64_t)h->k * sd.ldx, 1, 0, t, false, h->wcolptr, out.row,
-              out.val);
+              out.val, sd.peak);
   ++h->nlaunch;
   k_whole_split<<<1, 1024, 0, h->stream>>>(out.row, h->wcolptr, sd.ldx, h->k, out.colptr);
   CKL("whole_split");
@@ -993,6 +1000,8 @@ void iterate_one(esnmf_t* h) {
   in.colptr_v = h->V.colptr;
   in.nact_u = Un.n_active;
   in.nact_v = h->V.n_active;
+  in.peak_u = su.peak;
+  in.peak_v = h->side[ESNMF_SIDE_V].peak;
   in.normA2 = h->normA2;
   in.k = k;
   in.it = (int)(h->nrec + 1);
@@ -1059,6 +1068,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   const int64_t ts = h->tside[&sd == &h->side[ESNMF_SIDE_V] ? 0 : 1];
   if (ts >= 0 && ts <= kSelFastT) {
     sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(ts, 1));
+    sd.above_t = std::max<int64_t>(ts, 1);
     sd.above_fill = h->alloc<int32_t>(2 * (int64_t)k);
     sd.bucket = h->alloc<uint64_t>((int64_t)k * kSelCap);
     // predicted-threshold single pass: worth its extra kernel only when the LS
@@ -1074,6 +1084,8 @@ void side_alloc(esnmf_t* h, Side& sd) {
     }
   }
   sd.G = h->alloc<double>((int64_t)k * k);
+  sd.peak = h->alloc<int64_t>(1);
+  CK(cudaMemsetAsync(sd.peak, 0, sizeof(int64_t), h->stream));
   sd.eps = h->alloc<double>(1);
   if (h->world > 1) {
     const int64_t rows_max = (&sd == &h->side[ESNMF_SIDE_V]) ? h->v_rows_max : h->u_rows_max;
@@ -1219,6 +1231,24 @@ void init_u0(esnmf_t* h, const float* user_u0, bool on_dev) {
   }
   ++h->nlaunch; k_u0_dense<<<grid_for(h->n * h->kpad, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, h->seed, du,
                                                                                f.dense, h->flags + 2);
+  if (h->init_nnz > 0 && !du) {
+    // sparse U_0 (reading C18): mask the formula's entries, compact to COO, row view
+    const double p = (double)h->init_nnz / (double)h->n;
+    const uint64_t thr = p >= 1.0 ? ~0ULL : (uint64_t)(p * 0x1p53);
+    h->nlaunch += 4;
+    k_u0_mask<<<grid_for(h->n * h->k, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, h->seed, thr, f.dense);
+    int64_t* cnt = h->side[ESNMF_SIDE_U].coltot;  // k scratch
+    k_u0_compact<<<h->k, 1024, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, cnt, nullptr, f.row, f.val);
+    k_sel_colptr<<<1, 256, 0, h->stream>>>(cnt, h->k, f.colptr);
+    k_u0_compact<<<h->k, 1024, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, nullptr, f.colptr, f.row, f.val);
+    CK(cudaMemsetAsync(f.dense, 0, sizeof(float) * h->n * h->kpad, h->stream));  // rebuilt for the active rows
+    CKL("init_u0 sparse");
+    f.has = true;
+    factor_build_rows(h, f, h->n);
+    h->ucur = 0;
+    h->gramU_valid = false;
+    return;
+  }
   ++h->nlaunch; k_u0_coo<<<grid_for(h->n * h->k, 256, 148 * 32), 256, 0, h->stream>>>(h->n, h->k, h->kpad, f.dense, f.colptr,
                                                                           f.row, f.val, f.rowmap, f.active,
                                                                           f.n_active);
@@ -1286,6 +1316,7 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->t_u = ESNMF_T_SAME;
   o->t_v = ESNMF_T_SAME;
   o->enforce = ESNMF_ENFORCE_COLUMN;
+  o->init_nnz = 0;
   return ESNMF_OK;
 }
 
@@ -1367,6 +1398,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->tside[0] = o.t_v == ESNMF_T_SAME ? t : o.t_v;
     h->tside[1] = o.t_u == ESNMF_T_SAME ? t : o.t_u;
     h->whole = o.enforce == ESNMF_ENFORCE_MATRIX;
+    h->init_nnz = o.init_nnz;
     if (h->whole && (int64_t)k * (std::max(n, m) + 32) >= (1LL << 31))
       fail(ESNMF_EINVAL, "esnmf_create: whole-matrix enforcement needs k * rows < 2^31");
     h->wcolptr = h->alloc<int64_t>(2);
@@ -1642,6 +1674,42 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
     if (side == ESNMF_SIDE_U) h->gramU_valid = false;
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaStreamSynchronize(h->aux));
+  });
+}
+
+esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce) {
+  if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U) || t < 0 ||
+      (enforce != ESNMF_ENFORCE_COLUMN && enforce != ESNMF_ENFORCE_MATRIX)) {
+    g_last_error = "esnmf_truncate: bad argument";
+    return ESNMF_EINVAL;
+  }
+  if (h->world > 1) { g_last_error = "esnmf_truncate: single GPU only"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    CK(cudaStreamSynchronize(h->aux));
+    Factor& f = side == ESNMF_SIDE_U ? h->U[h->ucur] : h->V;
+    if (!f.has) fail(ESNMF_ESTATE, "esnmf_truncate: factor not set");
+    Side& sd = h->side[side];  // its LS buffer is the scratch
+    const int k = h->k;
+    CK(cudaMemsetAsync(sd.X, 0, sizeof(float) * k * sd.ldx, h->stream));
+    ++h->nlaunch;
+    k_coo_to_colmajor<<<dim3(col_grid_x(f.maxcol), k), 256, 0, h->stream>>>(f.colptr, f.row, f.val, sd.X, sd.ldx);
+    if (side == ESNMF_SIDE_V) vrows_clear(h);
+    factor_clear(h, f);
+    if (enforce == ESNMF_ENFORCE_COLUMN) {
+      select_core(h, sd, sd.X, sd.ldx, sd.rows, k, 0, t, false, f.colptr, f.row, f.val, nullptr);
+    } else {
+      select_core(h, sd, sd.X, (int64_t)k * sd.ldx, (int64_t)k * sd.ldx, 1, 0, t, false, h->wcolptr, f.row, f.val,
+                  nullptr);
+      ++h->nlaunch;
+      k_whole_split<<<1, 1024, 0, h->stream>>>(f.row, h->wcolptr, sd.ldx, k, f.colptr);
+    }
+    factor_build_rows(h, f, std::min<int64_t>(f.rows, std::max<int64_t>(t, 1)));
+    if (side == ESNMF_SIDE_V) vrows_build(h);
+    if (side == ESNMF_SIDE_U) h->gramU_valid = false;
+    h->u_prefork = false;
+    sd.ls_valid = false;  // the scratch overwrote the LS rows
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 

@@ -44,6 +44,43 @@ __global__ void k_u0_dense(int64_t n, int k, int kpad, uint64_t seed, const floa
   }
 }
 
+// sparse initial guess (reading C18): zero U0[i,c] unless the mask hash draw
+// (splitmix64(seed ^ K_MASK ^ (i*k + c)) >> 11) < thr = init_nnz 2^53 / n
+constexpr uint64_t kU0Mask = 0x55305F4D41534B30ULL;  // "U0_MASK0"
+
+__global__ void k_u0_mask(int64_t n, int k, int kpad, uint64_t seed, uint64_t thr, float* __restrict__ dense) {
+  const int64_t total = n * k;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / k;
+    const int c = (int)(q - i * k);
+    if ((splitmix64(seed ^ kU0Mask ^ (uint64_t)q) >> 11) >= thr) dense[i * kpad + c] = 0.f;
+  }
+}
+
+// compact the (masked) dense U_0 into canonical column-major COO: one block per
+// column, rows in order (block scan over chunks of blockDim rows).  Pass 1
+// (colptr == nullptr) counts into ccount[c]; pass 2 writes at colptr[c].
+__global__ void k_u0_compact(int64_t n, int k, int kpad, const float* __restrict__ dense,
+                             int64_t* __restrict__ ccount, const int64_t* __restrict__ colptr,
+                             int32_t* __restrict__ row, float* __restrict__ val) {
+  __shared__ int64_t sm[33];
+  const int c = blockIdx.x;
+  int64_t base = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const float v = i < n ? dense[i * kpad + c] : 0.f;
+    const int64_t on = v > 0.f;
+    int64_t tot;
+    const int64_t ex = block_exscan(on, sm, &tot);
+    if (on && colptr) {
+      row[colptr[c] + base + ex] = (int32_t)i;
+      val[colptr[c] + base + ex] = v;
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0 && !colptr) ccount[c] = base;
+}
+
 // every entry of the dense U_0 is stored (all are > 0)
 __global__ void k_u0_coo(int64_t n, int k, int kpad, const float* __restrict__ dense, int64_t* __restrict__ colptr,
                          int32_t* __restrict__ row, float* __restrict__ val, int32_t* __restrict__ rowmap,
@@ -69,6 +106,12 @@ __global__ void k_u0_coo(int64_t n, int k, int kpad, const float* __restrict__ d
   const int64_t cb_ = colptr[c_], ce_ = colptr[c_ + 1];                                            \
   for (int64_t e = cb_ + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ce_;                   \
        e += (int64_t)gridDim.x * blockDim.x)
+
+// factor entries -> column-major dense buffer X[c * ldx + row] (zeroed by the caller)
+__global__ void k_coo_to_colmajor(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
+                                  const float* __restrict__ val, float* __restrict__ X, int64_t ldx) {
+  ESNMF_FOR_COL_ENTRIES(colptr, e) { X[(int64_t)c_ * ldx + row[e]] = val[e]; }
+}
 
 // zero the dense cells of the factor's current entries (before it is replaced)
 __global__ void k_clear_dense(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,

@@ -102,6 +102,8 @@ struct RecordInputs {
   const int64_t* colptr_v;
   const int64_t* nact_u;
   const int64_t* nact_v;
+  const int64_t* peak_u;  // positives of the clamped LS before truncation (per side)
+  const int64_t* peak_v;
   double normA2;
   int k;
   int it;
@@ -137,6 +139,8 @@ __global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ re
     r.dead_v = dead_v;
     r.active_u = *in.nact_u;
     r.active_v = *in.nact_v;
+    r.peak_u = in.peak_u ? *in.peak_u : -1;
+    r.peak_v = in.peak_v ? *in.peak_v : -1;
     *rec = r;
     scal[0] = num;
     scal[1] = den;

@@ -434,6 +434,15 @@ __global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ 
   }
 }
 
+// positives of the clamped LS over all columns (the record's peak nnz)
+__global__ void k_sel_npos_sum(const ColSel* __restrict__ sel, int kc, int64_t* __restrict__ out) {
+  __shared__ int64_t sm[32];
+  int64_t v = 0;
+  for (int c = threadIdx.x; c < kc; c += blockDim.x) v += sel[c].npos;
+  v = block_sum(v, sm);
+  if (threadIdx.x == 0) *out = v;
+}
+
 // colptr of the kept entries: min(t, #positive) per column (reading C4/C5)
 __global__ void k_sel_colptr_kept(const ColSel* __restrict__ sel, int k, int64_t t, int64_t* __restrict__ colptr) {
   __shared__ int64_t sm[33];

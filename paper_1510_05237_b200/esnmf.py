@@ -37,13 +37,14 @@ class esnmf_options(ctypes.Structure):
         ("world", c_i32), ("rank", c_i32), ("comm", ctypes.POINTER(esnmf_comm)),
         ("inputs_on_device", c_i32),
         ("at_row_ptr", c_p), ("at_col_idx", c_p), ("at_val", c_p), ("U0", c_p),
-        ("head_terms", c_i32), ("t_u", c_i64), ("t_v", c_i64), ("enforce", c_i32),
+        ("head_terms", c_i32), ("t_u", c_i64), ("t_v", c_i64), ("enforce", c_i32), ("init_nnz", c_i64),
     ]
 
 
 class esnmf_record(ctypes.Structure):
     _fields_ = [("it", c_i32), ("R", c_dbl), ("E", c_dbl), ("nnz_u", c_i64), ("nnz_v", c_i64),
-                ("dead_u", c_i32), ("dead_v", c_i32), ("active_u", c_i64), ("active_v", c_i64)]
+                ("dead_u", c_i32), ("dead_v", c_i32), ("active_u", c_i64), ("active_v", c_i64),
+                ("peak_u", c_i64), ("peak_v", c_i64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -90,6 +91,7 @@ SIGNATURES = {
     "esnmf_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "esnmf_last_error": (ctypes.c_char_p, []),
     "esnmf_partition_rows": (ctypes.c_int, [c_i64, c_p, c_i32, c_p]),
+    "esnmf_truncate": (ctypes.c_int, [c_p, c_i32, c_i64, c_i32]),
     "esnmf_version": (ctypes.c_char_p, []),
 }
 
@@ -250,6 +252,11 @@ def esnmf_phase_times(h) -> dict:
     return {buf[i].name.decode(): (buf[i].calls, buf[i].ms) for i in range(cnt.value)}
 
 
+def esnmf_truncate(h, side: int, t: int, whole: bool = False):
+    _check(lib().esnmf_truncate(h, int(side), int(t), ESNMF_ENFORCE_MATRIX if whole else ESNMF_ENFORCE_COLUMN),
+           "esnmf_truncate")
+
+
 def esnmf_destroy(h):
     if h:
         lib().esnmf_destroy(h)
@@ -275,7 +282,7 @@ class ESNMF:
 
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
                  device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None,
-                 head_terms: int = -1, t_u="same", t_v="same", whole: bool = False):
+                 head_terms: int = -1, t_u="same", t_v="same", whole: bool = False, init_nnz: int = 0):
         """t_u / t_v: separate budgets ("same" = t, None = unlimited); whole: whole-factor
         enforcement (Alg. 2 as printed) instead of per column."""
         o = esnmf_options_init()
@@ -283,6 +290,7 @@ class ESNMF:
         o.t_u = ESNMF_T_SAME if t_u == "same" else (ESNMF_T_UNLIMITED if t_u is None else int(t_u))
         o.t_v = ESNMF_T_SAME if t_v == "same" else (ESNMF_T_UNLIMITED if t_v is None else int(t_v))
         o.enforce = ESNMF_ENFORCE_MATRIX if whole else ESNMF_ENFORCE_COLUMN
+        o.init_nnz = int(init_nnz)
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device
@@ -336,6 +344,9 @@ class ESNMF:
 
     def get_gram(self, side):
         return esnmf_get_gram(self.h, side)
+
+    def truncate(self, side: int, t: int, whole: bool = False):
+        esnmf_truncate(self.h, side, t, whole)
 
     def info(self) -> dict:
         return esnmf_get_info(self.h)

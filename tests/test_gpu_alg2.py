@@ -109,3 +109,51 @@ def test_bad_budgets_rejected():
     g = synth.generate(TINY)
     with pytest.raises(ESNMFError):
         ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, t_u=-5)
+
+
+# ---- NEXT-3: enforce-after, sparse initial guess, peak nnz telemetry ----
+
+@pytest.mark.parametrize("whole", [False, True])
+def test_enforce_after_truncation(whole):
+    """Alg. 1 (t unlimited) then one truncation of U and V: the
+    factors equal the oracle's truncation of the same (GPU) factors."""
+    cfg = TINY
+    g = synth.generate(cfg)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, None, g, seed=cfg.seed)
+    s.iterate(5)
+    U = factor(s, ESNMF_SIDE_U, cfg.n, cfg.k)
+    V = factor(s, ESNMF_SIDE_V, cfg.m, cfg.k)
+    t = 300 if whole else 40
+    s.truncate(ESNMF_SIDE_U, t, whole)
+    s.truncate(ESNMF_SIDE_V, t, whole)
+    Ut = factor(s, ESNMF_SIDE_U, cfg.n, cfg.k)
+    Vt = factor(s, ESNMF_SIDE_V, cfg.m, cfg.k)
+    assert np.array_equal(Ut, oracle.clamp_top_t(U, t, whole)[0])   # same values in, exact selection out
+    assert np.array_equal(Vt, oracle.clamp_top_t(V, t, whole)[0])
+    # the truncated state iterates on (the next V side starts from the truncated U)
+    s.half_step(ESNMF_SIDE_V)
+    ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], Ut, None)
+    _, ls = s.get_ls(ESNMF_SIDE_V)
+    check_products(ls, ref["LS"])
+
+
+@pytest.mark.parametrize("init_nnz", [50, 400])
+def test_sparse_initial_guess_and_peak_nnz(init_nnz):
+    """U_0 with ~init_nnz entries per column (reading C18) bitwise equal to the
+    oracle's, the trajectory from it, and the records' peak nnz (positives of the
+    clamped least-squares factor before truncation)."""
+    cfg = TINY
+    g = synth.generate(cfg)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, init_nnz=init_nnz)
+    U0 = factor(s, ESNMF_SIDE_U, cfg.n, cfg.k)
+    ref0 = oracle.u0(cfg.n, cfg.k, cfg.seed, init_nnz)
+    assert np.array_equal(U0.astype(np.float32), ref0)
+    assert abs(np.count_nonzero(U0) / cfg.k - init_nnz) < 5 * np.sqrt(init_nnz) + 5
+    ref = oracle.run(g, cfg.k, cfg.t, 8, seed=cfg.seed, init_nnz=init_nnz)
+    s.iterate(8)
+    for a, b in zip(s.records(), ref["records"]):
+        assert abs(a["E"] - b["E"]) <= TRAJ_TOL * b["E"], (a["it"], a["E"], b["E"])
+        assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"]
+        # a positive near zero may flip sign with rounding: allow 1e-4 relative
+        assert abs(a["peak_u"] - b["peak_u"]) <= 1e-4 * b["peak_u"] + 1
+        assert abs(a["peak_v"] - b["peak_v"]) <= 1e-4 * b["peak_v"] + 1

@@ -322,3 +322,23 @@ def test_oracle_budgets_match_bruteforce(t_u, t_v, whole):
             assert rec["nnz_u"] <= t_u
         if whole and t_v is not None:
             assert rec["nnz_v"] <= t_v
+
+
+def test_sparse_u0_mask():
+    """Reading C18: init_nnz >= n keeps the dense U_0; otherwise only zeroes are
+    introduced, each entry independently with probability init_nnz / n (binomial
+    count per column), and the kept values are U_0's."""
+    n, k = 4000, 6
+    dense = oracle.u0(n, k, 3)
+    assert np.array_equal(oracle.u0(n, k, 3, n), dense)
+    assert np.array_equal(oracle.u0(n, k, 3, 10 * n), dense)
+    for nnz in (10, 200, 1000):
+        s = oracle.u0(n, k, 3, nnz)
+        kept = s != 0
+        assert np.array_equal(s[kept], dense[kept])
+        p = nnz / n
+        cnt = kept.sum(axis=0)
+        sd = np.sqrt(n * p * (1 - p))
+        assert np.all(np.abs(cnt - nnz) <= 5 * sd + 1), (nnz, cnt)
+    # independent of the value stream: the same mask for another seed differs
+    assert not np.array_equal(oracle.u0(n, k, 3, 200) != 0, oracle.u0(n, k, 4, 200) != 0)
