@@ -234,6 +234,69 @@ def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float 
     return dict(records=recs, U=U, V=V, states=states, normA2=normA2)
 
 
+def seq_half_step(ptr, idx, val, F: np.ndarray, O1: np.ndarray, b0: int, k2: int, t: int | None,
+                  rho: float = RHO_DEFAULT, whole: bool = False) -> dict:
+    """One half-step of sequential ALS (Alg. 3) for the block columns
+    [b0, b0 + k2), in the order of Eq. (7) / Eq. (8):
+        V side (T = A^T, F = U, O1 = V_1):  V_2 = (A^T U_2 - V_1 U_1^T U_2)(U_2^T U_2)^{-1}
+        U side (T = A,   F = V, O1 = U_1):  U_2 = (A V_2 - U_1 V_1^T V_2)(V_2^T V_2)^{-1}
+    with F_1 = F[:, :b0] (converged topics), F_2 = F[:, b0:b0+k2], the ridge of
+    reading C6 on the block Gram (reading C19), then clamp and keep t per column
+    of the block (whole=True: t over the block, Alg. 3 step 2/4 as printed).
+    Returns LS2 (rows x k2, before the clamp) and F2 (after)."""
+    F = _c(F, np.float64)
+    F1, F2 = F[:, :b0], np.ascontiguousarray(F[:, b0:b0 + k2])
+    G22 = gram(F2)
+    L, eps = cholesky(G22, rho)
+    Y = spmm(ptr, idx, val, F2)                       # A^T U_2  /  A V_2
+    if b0 > 0:
+        Y = Y - _c(O1, np.float64) @ (F1.T @ F2)      # - V_1 (U_1^T U_2)  /  - U_1 (V_1^T V_2)
+    LS2 = solve_rows(L, Y)                            # (.)(F_2^T F_2 + eps I)^{-1}
+    F2n, kept = clamp_top_t(LS2, t, whole)
+    return dict(G22=G22, eps=eps, Y=Y, LS2=LS2, F2=F2n, kept=kept, peak=int(np.sum(LS2 > 0)))
+
+
+def run_sequential(inp: dict, k: int, k2: int, t: int | None, iters: int, seed: int = 0,
+                   rho: float = RHO_DEFAULT, t_u=_SAME, t_v=_SAME, whole: bool = False,
+                   init_nnz: int = 0) -> dict:
+    """Sequential ALS NMF (Alg. 3, P:330-352): eta = k / k2 blocks of k2 topics;
+    every block starts from U_2 = U_0 (n x k2; the same U_0 for every
+    block), runs ``iters`` iterations ("do until convergence", fixed count as
+    reading C12; the START block is Alg. 2 with U_0, which is this update with no
+    converged topics), then is appended to U_1, V_1.  One record per
+    iteration over the whole factors U = [U_1 U_2 0], V = [V_1 V_2 0]: R on the
+    full U (the block's first iteration compares with [U_1 U_0 0]), E the true
+    relative error of the current U V^T, peak = nnz(F_1) + positives of LS_2."""
+    tu = t if t_u is _SAME else t_u
+    tv = t if t_v is _SAME else t_v
+    n, m = inp["n"], inp["m"]
+    if k2 <= 0 or k % k2:
+        raise ValueError("k must be a multiple of k2")
+    U = np.zeros((n, k))
+    V = np.zeros((m, k))
+    U0 = u0(n, k2, seed, init_nnz).astype(np.float64)
+    normA2 = frob2(inp["a_val"])
+    recs = []
+    for b in range(k // k2):
+        b0 = b * k2
+        U[:, b0:b0 + k2] = U0                                              # P:336 Set U_2 = U_0
+        for _ in range(iters):
+            Uprev = U.copy()
+            hv = seq_half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, V[:, :b0], b0, k2, tv, rho, whole)
+            V[:, b0:b0 + k2] = hv["F2"]                                    # steps 1-2
+            hu = seq_half_step(inp["a_ptr"], inp["a_col"], inp["a_val"], V, U[:, :b0], b0, k2, tu, rho, whole)
+            U[:, b0:b0 + k2] = hu["F2"]                                    # steps 3-4
+            R = residual(U, Uprev)                                         # P:160 on the whole U
+            AV = spmm(inp["a_ptr"], inp["a_col"], inp["a_val"], V)
+            E = error(U, AV, gram(U), gram(V), normA2)                     # P:161 on the whole U V^T
+            recs.append(dict(it=len(recs) + 1, R=R, E=E, nnz_u=int(np.count_nonzero(U)),
+                             nnz_v=int(np.count_nonzero(V)), dead_u=int(np.sum(~U.any(axis=0))),
+                             dead_v=int(np.sum(~V.any(axis=0))),
+                             peak_u=int(np.count_nonzero(U[:, :b0])) + hu["peak"],
+                             peak_v=int(np.count_nonzero(V[:, :b0])) + hv["peak"], block=b))
+    return dict(records=recs, U=U, V=V, normA2=normA2)
+
+
 # ------------------------------------------------------------- format helpers
 
 def dense_to_coo(F: np.ndarray):

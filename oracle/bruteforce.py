@@ -88,3 +88,26 @@ def projected_als_budgets(A: np.ndarray, U0: np.ndarray, t_u: int | None, t_v: i
         recs.append((np.linalg.norm(Un - U) / np.linalg.norm(Un), np.linalg.norm(A - Un @ V.T) / nA))
         U = Un
     return U, V, recs
+
+
+def sequential_als(A: np.ndarray, U0: np.ndarray, k: int, t_u: int | None, t_v: int | None, iters: int,
+                   rho: float, whole: bool = False):
+    """Alg. 3, dense: the block of k2 = U0.shape[1] topics found by
+    Eq. (7) / (8) with the converged topics subtracted from A explicitly
+    (A - U_1 V_1^T, materialised), every block from U_0.  Returns U, V and
+    (R, E) per iteration over the whole factors."""
+    top = top_t_whole if whole else top_t_per_column
+    n, m = A.shape
+    k2 = U0.shape[1]
+    U, V = np.zeros((n, k)), np.zeros((m, k))
+    nA = np.linalg.norm(A)
+    recs = []
+    for b0 in range(0, k, k2):
+        U[:, b0:b0 + k2] = U0
+        R1 = A - U[:, :b0] @ V[:, :b0].T           # the residual the new topics fit
+        for _ in range(iters):
+            Uprev = U.copy()
+            V[:, b0:b0 + k2] = top(ls_step(R1.T, U[:, b0:b0 + k2], rho), t_v)
+            U[:, b0:b0 + k2] = top(ls_step(R1, V[:, b0:b0 + k2], rho), t_u)
+            recs.append((np.linalg.norm(U - Uprev) / np.linalg.norm(U), np.linalg.norm(A - U @ V.T) / nA))
+    return U, V, recs

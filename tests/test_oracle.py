@@ -342,3 +342,83 @@ def test_sparse_u0_mask():
         assert np.all(np.abs(cnt - nnz) <= 5 * sd + 1), (nnz, cnt)
     # independent of the value stream: the same mask for another seed differs
     assert not np.array_equal(oracle.u0(n, k, 3, 200) != 0, oracle.u0(n, k, 4, 200) != 0)
+
+
+# ---- NEXT-2: sequential ALS (Alg. 3) ----
+
+def _inp(A):
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    return dict(n=A.shape[0], m=A.shape[1], a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+
+
+@pytest.mark.parametrize("k,k2,t_u,t_v,whole", [(4, 1, 8, 10, False), (6, 2, None, 7, False), (6, 3, 9, 12, False),
+                                                 (4, 2, 15, 18, True)])
+def test_sequential_matches_bruteforce(k, k2, t_u, t_v, whole):
+    """Eq. (7)/(8) with the deflation term against the dense twin that fits the
+    materialised residual A - U_1 V_1^T (a dropped term, a wrong sign or a
+    transposed U_1^T U_2 fails here)."""
+    rng = np.random.default_rng(21)
+    n, m = 40, 30
+    A = rand_sparse(rng, n, m, 0.3)
+    rho = 1e-10
+    r = oracle.run_sequential(_inp(A), k, k2, 999, 5, seed=2, rho=rho, t_u=t_u, t_v=t_v, whole=whole)
+    U, V, recs = bf.sequential_als(A, oracle.u0(n, k2, 2).astype(np.float64), k, t_u, t_v, 5, rho, whole)
+    assert np.allclose(r["U"], U, rtol=1e-8, atol=1e-11 * np.abs(U).max())
+    assert np.allclose(r["V"], V, rtol=1e-8, atol=1e-11 * np.abs(V).max())
+    assert len(r["records"]) == len(recs) == 5 * (k // k2)
+    for rec, (R, E) in zip(r["records"], recs):
+        assert rec["R"] == pytest.approx(R, rel=1e-7, abs=1e-12)
+        assert rec["E"] == pytest.approx(E, rel=1e-9)
+
+
+def test_sequential_single_block_is_alg2():
+    """eta = 1 (k2 = k): Alg. 3 is its START step, i.e. Alg. 2 from U_0."""
+    cfg = synth.CONFIGS["tiny"]
+    g = synth.generate(cfg)
+    a = oracle.run(g, cfg.k, cfg.t, 4, seed=cfg.seed)
+    b = oracle.run_sequential(g, cfg.k, cfg.k, cfg.t, 4, seed=cfg.seed)
+    assert np.allclose(a["U"], b["U"], rtol=1e-12, atol=0) and np.allclose(a["V"], b["V"], rtol=1e-12, atol=0)
+    for x, y in zip(a["records"], b["records"]):
+        assert x["nnz_u"] == y["nnz_u"] and x["nnz_v"] == y["nnz_v"] and x["peak_u"] == y["peak_u"]
+        assert x["E"] == pytest.approx(y["E"], rel=1e-10) and x["R"] == pytest.approx(y["R"], rel=1e-10)
+
+
+def test_sequential_one_topic_is_a_division():
+    """k2 = 1: (U_2^T U_2)^{-1} is a scalar: the V side is
+    (A^T u - V_1 (U_1^T u)) / (u^T u + eps), written out by hand."""
+    rng = np.random.default_rng(22)
+    n, m = 30, 25
+    A = rand_sparse(rng, n, m, 0.3)
+    inp = _inp(A)
+    U = rng.random((n, 3))
+    V1 = rng.random((m, 2))
+    h = oracle.seq_half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, V1, 2, 1, None, rho=0.0)
+    u = U[:, 2]
+    want = (A.T @ u - V1 @ (U[:, :2].T @ u)) / (u @ u)
+    assert np.allclose(h["LS2"][:, 0], want, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(h["F2"][:, 0], np.maximum(h["LS2"][:, 0], 0))
+
+
+def test_sequential_planted_disjoint_topics_recovered():
+    """A = sum of k rank-one blocks with disjoint supports and distinct scales:
+    sequential rank-one ALS finds them one by one (power iteration on the
+    deflated residual), so the final error is ~0 and every U column is
+    supported on one planted block (t = the block's size)."""
+    k, terms, docs = 3, 8, 10
+    n, m = k * terms, k * docs
+    rng = np.random.default_rng(23)
+    A = np.zeros((n, m))
+    for c, s in enumerate((8.0, 4.0, 2.0)):
+        A[c * terms:(c + 1) * terms, c * docs:(c + 1) * docs] = s * np.outer(rng.integers(1, 4, terms),
+                                                                                rng.integers(1, 4, docs))
+    r = oracle.run_sequential(_inp(A), k, 1, None, 30, seed=1, t_u=terms, t_v=docs)
+    assert r["records"][-1]["E"] < 1e-6
+    u = oracle.run_sequential(_inp(A), k, 1, None, 30, seed=1)          # unlimited: same fit, up to decayed leakage
+    assert np.abs(u["U"] @ u["V"].T - A).max() <= 1e-6 * A.max()
+    for c in range(k):
+        blocks = {i // terms for i in np.nonzero(r["U"][:, c])[0]}
+        assert blocks == {c}    # largest block first (the top singular pair of the residual)
+    # the error drops as each block is appended
+    E = [x["E"] for x in r["records"]]
+    assert E[29] > E[59] > E[89]
