@@ -114,6 +114,17 @@ typedef struct {
      dense U_0; > 0 = keep U0[i,c] only where splitmix64(seed ^ 0x55305F4D41534B30 ^
      (i*k + c)) >> 11 < init_nnz * 2^53 / n (expected init_nnz entries per column). */
   int64_t init_nnz;
+  /* Sequential ALS (Alg. 3; NEXT-2): 0 (default) = off; k2 > 0 (dividing k)
+     = find the k topics in k / k2 blocks of k2.  Block b (columns [b k2, (b+1) k2))
+     starts from U_2 = U_0 (the reading C10 formula with k2 columns, index i*k2 + c;
+     masked per init_nnz) and runs `seq_iters` >= 1 iterations of Eq. (7) / (8)
+      with the converged columns held fixed; then the next block starts.
+     esnmf_iterate counts iterations over the whole schedule (k / k2 * seq_iters in
+     all; ESTATE after that).  E in the records is the true error of the current
+     U V^T.  Per-column t (enforce = ESNMF_ENFORCE_MATRIX only with k2 = 1, where it
+     is the same selection); single GPU; U0 must be NULL.  EINVAL otherwise. */
+  int32_t seq_k2;
+  int32_t seq_iters;
 } esnmf_options;
 
 typedef struct {

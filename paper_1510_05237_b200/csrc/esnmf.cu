@@ -32,6 +32,7 @@
 #include "k_vhead.cuh"
 #include "k_uside_tc.cuh"
 #include "k_spmm_tail.cuh"
+#include "k_seq.cuh"
 
 using namespace esk;
 
@@ -144,6 +145,10 @@ struct esnmf {
   int64_t tside[2] = {0, 0};  // budgets per side: [0] t_v (V side), [1] t_u (U side)
   bool whole = false;         // whole-factor enforcement (Alg. 2 as printed)
   int64_t init_nnz = 0;       // > 0: sparse U_0 (reading C18)
+  // sequential ALS (Alg. 3): blocks of seq_k2 topics, seq_iters iterations each
+  int seq_k2 = 0, seq_iters = 0, seq_b = 0, seq_i = 0;
+  double* seqG = nullptr;     // [k][k] block-restricted Gram (k_seq_gblock)
+  double* seqM = nullptr;     // [k][k2] G_12 W_22 (k_seq_m)
   int64_t* wcolptr = nullptr; // [2] colptr of the flat (one-column) selection
   double rho = 1e-10;
   uint64_t seed = 0;
@@ -425,6 +430,73 @@ void sweep(esnmf_t* h, const double* G, double* eps) {
     case 7: sweep_launch<7, true>(h, G, eps); break;
     default: sweep_launch<8, true>(h, G, eps); break;
   }
+}
+
+// a2: W = (G + eps I)^{-1}; in sequential mode the block inverse
+// (G_22 + eps I)^{-1}, zero outside block x block (k_seq.cuh)
+void solve_w(esnmf_t* h, const double* G, double* eps) {
+  if (!h->seq_k2) {
+    sweep(h, G, eps);
+    return;
+  }
+  const int b0 = h->seq_b * h->seq_k2;
+  const unsigned g = grid_for((int64_t)h->k * h->k, 256, 256);
+  ++h->nlaunch;
+  k_seq_gblock<<<g, 256, 0, h->stream>>>(G, h->k, b0, h->seq_k2, h->seqG);
+  sweep(h, h->seqG, eps);
+  ++h->nlaunch;
+  k_seq_wmask<<<g, 256, 0, h->stream>>>(h->W, h->k, b0, h->seq_k2);
+  CKL("solve_w seq");
+}
+
+// sequential mode, after the product: subtract O_1 (G_12 W_22) from the block
+// columns of side s's LS (Eq. (7) / (8)) and write the converged
+// columns of O back so the selection keeps them (k_seq.cuh)
+void seq_after_product(esnmf_t* h, int s) {
+  const int b0 = h->seq_b * h->seq_k2;
+  if (!h->seq_k2 || b0 == 0) return;
+  Side& sd = h->side[s];
+  Factor& O = s == ESNMF_SIDE_V ? h->V : h->U[h->ucur];
+  if (!O.has) fail(ESNMF_ESTATE, "sequential ALS: converged columns are not set");
+  const int k2 = h->seq_k2;
+  h->nlaunch += 3;
+  k_seq_m<<<grid_for((int64_t)b0 * k2, 256, 256), 256, 0, h->stream>>>(sd.G, h->W, h->k, b0, k2, h->seqM);
+  k_seq_deflate<<<grid_for(O.cap_rows * k2, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      O.active, O.n_active, O.dense, h->kpad, b0, k2, h->seqM, sd.X, sd.ldx, sd.row0, sd.rows);
+  k_coo_to_colmajor<<<dim3(col_grid_x(O.maxcol), b0), 256, 0, h->stream>>>(O.colptr, O.row, O.val, sd.X, sd.ldx);
+  CKL("seq_after_product");
+}
+
+void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows, int kc, int64_t row0, int64_t t,
+                 bool use_pred, int64_t* colptr_out, int32_t* row_out, float* val_out, int64_t* peak_out);
+
+// start block b: U = [U_1 | U_0 | 0] ("Set U_2 = U_0"), via the U side's LS
+// buffer and a keep-all selection into the current U
+void seq_begin_block(esnmf_t* h) {
+  join_metrics(h);
+  Side& su = h->side[ESNMF_SIDE_U];
+  Factor& Uc = h->U[h->ucur];
+  const int b0 = h->seq_b * h->seq_k2;
+  CK(cudaMemsetAsync(su.X, 0, sizeof(float) * su.ldx * h->k, h->stream));
+  if (b0 > 0) {
+    ++h->nlaunch;
+    k_coo_to_colmajor<<<dim3(col_grid_x(Uc.maxcol), b0), 256, 0, h->stream>>>(Uc.colptr, Uc.row, Uc.val, su.X,
+                                                                             su.ldx);
+  }
+  uint64_t thr = ~0ULL;
+  if (h->init_nnz > 0) {
+    const double p = (double)h->init_nnz / (double)h->n;
+    thr = p >= 1.0 ? ~0ULL : (uint64_t)(p * 0x1p53);
+  }
+  ++h->nlaunch;
+  k_seq_u0_block<<<grid_for(h->n * h->seq_k2, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+      h->n, h->seq_k2, h->seed, thr, b0, su.X, su.ldx);
+  CKL("seq_u0_block");
+  factor_clear(h, Uc);
+  select_core(h, su, su.X, su.ldx, su.rows, h->k, su.row0, -1, false, Uc.colptr, Uc.row, Uc.val, su.peak);
+  factor_build_rows(h, Uc, h->n);
+  h->gramU_valid = false;
+  su.ls_valid = false;
 }
 
 // V side: Z = U W written term-indexed (stride zs); the rows written by the
@@ -893,13 +965,14 @@ Factor& half_step(esnmf_t* h, int s) {
       Phase ph(h, p0 + 0);
       gram(h, in, sd.G);
     }
-    { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }               // a2
+    { Phase ph(h, p0 + 1); solve_w(h, sd.G, sd.eps); }             // a2
     if (overlap_u) uside_w_prep(h);
   }
   h->u_prefork = false;
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
   { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
   if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
+  seq_after_product(h, s);                                         // Alg. 3: Eq. (7) / (8)
   sd.ls_valid = true;
   {
     Phase ph(h, p0 + 4);
@@ -919,7 +992,7 @@ Factor& half_step(esnmf_t* h, int s) {
       OnStream os(h, h->aux);
       Side& su = h->side[ESNMF_SIDE_U];
       { Phase ph2(h, kUGram); gram(h, out, su.G); }
-      { Phase ph2(h, kUSolve); sweep(h, su.G, su.eps); }
+      { Phase ph2(h, kUSolve); solve_w(h, su.G, su.eps); }
       uside_w_prep(h);
       h->u_prefork = true;
     }
@@ -942,6 +1015,10 @@ void ensure_records(esnmf_t* h, int64_t need) {
 }
 
 void iterate_one(esnmf_t* h) {
+  if (h->seq_k2) {
+    if (h->seq_b * h->seq_k2 >= h->k) fail(ESNMF_ESTATE, "sequential ALS: all k / k2 blocks are done");
+    if (h->seq_i == 0) seq_begin_block(h);
+  }
   half_step(h, ESNMF_SIDE_V);
   half_step(h, ESNMF_SIDE_U);
   Phase ph(h, kMetrics);
@@ -972,7 +1049,11 @@ void iterate_one(esnmf_t* h) {
     k_err_trace_rows<cq><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0, su.rows, \
                                                      su.X, su.ldx, su.G, su.eps, k, p_tr);                        \
     break;
-  switch ((k + 31) / 32) {
+  if (h->seq_k2) {  // T = sum_ij a_ij (U_i . V_j) directly (k_seq.cuh)
+    const size_t smem = sizeof(float) * 8 * h->kpad;
+    k_err_trace_direct<<<gtr, 256, smem, h->stream>>>(Un.active, Un.n_active, Un.dense, su.T.ptr, su.T.ent,
+                                                       h->V.rowmap, h->V.dense, h->kpad, k, p_tr);
+  } else switch ((k + 31) / 32) {
     ESNMF_ET(1) ESNMF_ET(2) ESNMF_ET(3) ESNMF_ET(4) ESNMF_ET(5) ESNMF_ET(6) ESNMF_ET(7)
     default: k_err_trace_rows<8><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0,
                                                              su.rows, su.X, su.ldx, su.G, su.eps, k, p_tr);
@@ -1010,6 +1091,10 @@ void iterate_one(esnmf_t* h) {
   CKL("finalize_record");
   h->nrec += 1;
   if (overlap_m) h->aux_pending = true;
+  if (h->seq_k2 && ++h->seq_i == h->seq_iters) {  // block converged (fixed count): append, next block
+    h->seq_i = 0;
+    ++h->seq_b;
+  }
 }
 
 void sync_check(esnmf_t* h) {
@@ -1317,6 +1402,8 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->t_v = ESNMF_T_SAME;
   o->enforce = ESNMF_ENFORCE_COLUMN;
   o->init_nnz = 0;
+  o->seq_k2 = 0;
+  o->seq_iters = 0;
   return ESNMF_OK;
 }
 
@@ -1364,6 +1451,19 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     g_last_error = "esnmf_create: whole-matrix enforcement is single-GPU only";
     return ESNMF_EINVAL;
   }
+  if (o.seq_k2 != 0) {
+    const char* why = nullptr;
+    if (o.seq_k2 < 0 || k % o.seq_k2 != 0) why = "esnmf_create: seq_k2 must divide k";
+    else if (o.seq_iters < 1) why = "esnmf_create: seq_iters must be >= 1 with seq_k2";
+    else if (o.world > 1) why = "esnmf_create: sequential ALS is single-GPU only";
+    else if (o.enforce == ESNMF_ENFORCE_MATRIX && o.seq_k2 > 1)
+      why = "esnmf_create: sequential ALS enforces per column (whole-matrix only with seq_k2 = 1)";
+    else if (o.U0) why = "esnmf_create: sequential ALS draws its n x k2 U_0 itself (U0 must be NULL)";
+    if (why) {
+      g_last_error = why;
+      return ESNMF_EINVAL;
+    }
+  }
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { g_last_error = "esnmf_create: bad world/rank"; return ESNMF_EINVAL; }
   if (o.world > 1 && (!o.comm || !o.comm->allgather || !o.comm->allreduce_sum_f64)) {
     g_last_error = "esnmf_create: world > 1 needs comm callbacks";
@@ -1397,7 +1497,9 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->t = t;
     h->tside[0] = o.t_v == ESNMF_T_SAME ? t : o.t_v;
     h->tside[1] = o.t_u == ESNMF_T_SAME ? t : o.t_u;
-    h->whole = o.enforce == ESNMF_ENFORCE_MATRIX;
+    h->whole = o.enforce == ESNMF_ENFORCE_MATRIX && o.seq_k2 == 0;  // seq_k2 = 1: one column, same selection
+    h->seq_k2 = o.seq_k2;
+    h->seq_iters = o.seq_iters;
     h->init_nnz = o.init_nnz;
     if (h->whole && (int64_t)k * (std::max(n, m) + 32) >= (1LL << 31))
       fail(ESNMF_EINVAL, "esnmf_create: whole-matrix enforcement needs k * rows < 2^31");
@@ -1515,6 +1617,10 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     CK(cudaMemsetAsync(h->vbits, 0, sizeof(uint32_t) * ceil_div(m, 32), h->stream));
     CK(cudaMemsetAsync(h->vmap, 0, sizeof(uint64_t) * m, h->stream));
     h->W = h->alloc<double>((int64_t)k * k);
+    if (h->seq_k2) {
+      h->seqG = h->alloc<double>((int64_t)k * k);
+      h->seqM = h->alloc<double>((int64_t)k * h->seq_k2);
+    }
     h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * k * k);
     if (k > 224) h->sweep_scratch = h->alloc<double>((int64_t)k * (k + 1) / 2);
     init_u0(h.get(), o.U0, on_dev);
