@@ -120,9 +120,12 @@ typedef struct {
      masked per init_nnz) and runs `seq_iters` >= 1 iterations of Eq. (7) / (8)
       with the converged columns held fixed; then the next block starts.
      esnmf_iterate counts iterations over the whole schedule (k / k2 * seq_iters in
-     all; ESTATE after that).  E in the records is the true error of the current
-     U V^T.  Per-column t (enforce = ESNMF_ENFORCE_MATRIX only with k2 = 1, where it
-     is the same selection); single GPU; U0 must be NULL.  EINVAL otherwise. */
+     all; ESTATE after that).  Records cover the whole factors U = [U_1 U_2 0],
+     V = [V_1 V_2 0]; esnmf_get_U / _V return them (k columns).  The least-squares
+     buffer (esnmf_get_ls), the Gram, esnmf_set_factor and esnmf_truncate act on the
+     current block (k2 columns, info.ls_cols).  t_u / t_v bound each column of the
+     block (ESNMF_ENFORCE_COLUMN) or the whole block (ESNMF_ENFORCE_MATRIX, Alg. 3
+     steps 2 and 4 as printed).  Single GPU; U0 must be NULL.  EINVAL otherwise. */
   int32_t seq_k2;
   int32_t seq_iters;
 } esnmf_options;
@@ -210,6 +213,9 @@ typedef struct {
   int64_t launches;         /* CUDA kernels enqueued by this handle so far */
   int32_t head_terms;       /* V-side tensor-core head size (0 = none) */
   int32_t head_dense;       /* of its 64-term chunks, how many are stored as dense tiles */
+  int32_t ls_cols;          /* columns of esnmf_get_ls / esnmf_get_gram / esnmf_set_factor:
+                               k, or k2 (the current block) in sequential mode */
+  int32_t seq_block;        /* sequential mode: index of the current block (0-based) */
 } esnmf_info;
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);

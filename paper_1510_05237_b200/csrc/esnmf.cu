@@ -145,10 +145,14 @@ struct esnmf {
   int64_t tside[2] = {0, 0};  // budgets per side: [0] t_v (V side), [1] t_u (U side)
   bool whole = false;         // whole-factor enforcement (Alg. 2 as printed)
   int64_t init_nnz = 0;       // > 0: sparse U_0 (reading C18)
-  // sequential ALS (Alg. 3): blocks of seq_k2 topics, seq_iters iterations each
+  // sequential ALS (Alg. 3, k_seq.cuh): the pipeline above runs on the current
+  // block of k = seq_k2 columns; the ktot - k converged columns are in FU / FV
+  int ktot = 0, kpf = 0;       // all topics and their row stride (0: not sequential)
   int seq_k2 = 0, seq_iters = 0, seq_b = 0, seq_i = 0;
-  double* seqG = nullptr;     // [k][k] block-restricted Gram (k_seq_gblock)
-  double* seqM = nullptr;     // [k][k2] G_12 W_22 (k_seq_m)
+  Factor FU, FV;               // U_1, V_1: columns [0, seq_b k2) of ktot
+  double* seqC = nullptr;      // [ktot][k2] H_1^T H_2
+  double* seqM = nullptr;      // [ktot][k2] (H_1^T H_2) W_22
+  double* seqc = nullptr;      // [3] T_1, S_11, ||U_1||^2 (record constants of the block)
   int64_t* wcolptr = nullptr; // [2] colptr of the flat (one-column) selection
   double rho = 1e-10;
   uint64_t seed = 0;
@@ -335,46 +339,49 @@ void launch_scan_inplace(esnmf_t* h, int64_t* a, int64_t n, int64_t* total) {
 
 // ---------------------------------------------------------------- factors
 
-void factor_alloc(esnmf_t* h, Factor& f, int64_t rows, int64_t cap) {
+void factor_alloc(esnmf_t* h, Factor& f, int64_t rows, int64_t cap, int kk = 0, int kp = 0) {
+  if (!kk) kk = h->k, kp = h->kpad;
   f.rows = rows;
   f.cap = cap;
   f.cap_rows = std::min(rows, cap);
-  f.colptr = h->alloc<int64_t>(h->k + 1);
+  f.colptr = h->alloc<int64_t>(kk + 1);
   f.row = h->alloc<int32_t>(cap);
   f.val = h->alloc<float>(cap);
   f.rowmap = h->alloc<int32_t>(rows);
   f.active = h->alloc<int32_t>(f.cap_rows);
   f.n_active = h->alloc<int64_t>(1);
-  f.dense = h->alloc<float>(f.cap_rows * h->kpad);
-  CK(cudaMemsetAsync(f.colptr, 0, sizeof(int64_t) * (h->k + 1), h->stream));
+  f.dense = h->alloc<float>(f.cap_rows * kp);
+  CK(cudaMemsetAsync(f.colptr, 0, sizeof(int64_t) * (kk + 1), h->stream));
   CK(cudaMemsetAsync(f.rowmap, 0xFF, sizeof(int32_t) * rows, h->stream));
   CK(cudaMemsetAsync(f.n_active, 0, sizeof(int64_t), h->stream));
-  CK(cudaMemsetAsync(f.dense, 0, sizeof(float) * f.cap_rows * h->kpad, h->stream));
+  CK(cudaMemsetAsync(f.dense, 0, sizeof(float) * f.cap_rows * kp, h->stream));
   f.has = false;
   f.maxcol = 0;
 }
 
 // undo the row view of the factor's current content (before it is replaced)
-void factor_clear(esnmf_t* h, Factor& f) {
+void factor_clear(esnmf_t* h, Factor& f, int kk = 0, int kp = 0) {
   if (!f.has) return;
-  dim3 g(col_grid_x(f.maxcol), h->k);
-  ++h->nlaunch; k_clear_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, f.dense, h->kpad);
+  if (!kk) kk = h->k, kp = h->kpad;
+  dim3 g(col_grid_x(f.maxcol), kk);
+  ++h->nlaunch; k_clear_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, f.dense, kp);
   ++h->nlaunch; k_reset_rowmap<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, f.rowmap);
   CKL("factor_clear");
   f.has = false;
 }
 
 // build rowmap / active / dense from the column-major COO just written
-void factor_build_rows(esnmf_t* h, Factor& f, int64_t maxcol) {
+void factor_build_rows(esnmf_t* h, Factor& f, int64_t maxcol, int kk = 0, int kp = 0) {
+  if (!kk) kk = h->k, kp = h->kpad;
   f.maxcol = maxcol;
-  dim3 g(col_grid_x(maxcol), h->k);
+  dim3 g(col_grid_x(maxcol), kk);
   ++h->nlaunch; k_mark_rows<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap);
   const int64_t nb = ceil_div(f.rows, kRowBlock);
   int64_t* bc = reinterpret_cast<int64_t*>(h->red);  // scratch (nb <= red_cap)
   ++h->nlaunch; k_rows_count<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc);
   ++h->nlaunch; k_scan_small<<<1, 1024, 0, h->stream>>>(bc, nb, f.n_active);
   ++h->nlaunch; k_rows_assign<<<(unsigned)nb, 256, 0, h->stream>>>(f.rowmap, f.rows, bc, f.active);
-  ++h->nlaunch; k_scatter_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad);
+  ++h->nlaunch; k_scatter_dense<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp);
   CKL("factor_build_rows");
   f.has = true;
 }
@@ -386,15 +393,16 @@ int64_t steady_maxcol(esnmf_t* h, int s, int64_t rows) {
 
 // ---------------------------------------------------------------- kernels
 
-void gram(esnmf_t* h, const Factor& f, double* G) {
-  const int k = h->k;
+void gram(esnmf_t* h, const Factor& f, double* G, int kk = 0, int kp = 0, double* partial = nullptr) {
+  if (!kk) kk = h->k, kp = h->kpad, partial = h->gram_partial;
+  const int k = kk;
   int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 32)));
   int64_t seglen = std::max<int64_t>(1, ceil_div(f.maxcol, S));
   dim3 g(k, (unsigned)S);
   const int gb = std::min(256, (k + 31) / 32 * 32);
-  ++h->nlaunch; k_gram_partial<<<g, gb, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, h->kpad, k, seglen,
-                                            h->gram_partial);
-  ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(h->gram_partial, (int)S, k, G);
+  ++h->nlaunch; k_gram_partial<<<g, gb, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k, seglen,
+                                            partial);
+  ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(partial, (int)S, k, G);
   ++h->nlaunch; k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
   CKL("gram");
 }
@@ -432,71 +440,61 @@ void sweep(esnmf_t* h, const double* G, double* eps) {
   }
 }
 
-// a2: W = (G + eps I)^{-1}; in sequential mode the block inverse
-// (G_22 + eps I)^{-1}, zero outside block x block (k_seq.cuh)
-void solve_w(esnmf_t* h, const double* G, double* eps) {
-  if (!h->seq_k2) {
-    sweep(h, G, eps);
-    return;
-  }
+// sequential mode, after the block's product T H_2 W_22: subtract O_1 (H_1^T H_2) W_22
+// (Eq. (7) / (8); k_seq.cuh).  V side: H = U, O = V; U side: H = V, O = U.
+void seq_deflate(esnmf_t* h, int s) {
   const int b0 = h->seq_b * h->seq_k2;
-  const unsigned g = grid_for((int64_t)h->k * h->k, 256, 256);
-  ++h->nlaunch;
-  k_seq_gblock<<<g, 256, 0, h->stream>>>(G, h->k, b0, h->seq_k2, h->seqG);
-  sweep(h, h->seqG, eps);
-  ++h->nlaunch;
-  k_seq_wmask<<<g, 256, 0, h->stream>>>(h->W, h->k, b0, h->seq_k2);
-  CKL("solve_w seq");
-}
-
-// sequential mode, after the product: subtract O_1 (G_12 W_22) from the block
-// columns of side s's LS (Eq. (7) / (8)) and write the converged
-// columns of O back so the selection keeps them (k_seq.cuh)
-void seq_after_product(esnmf_t* h, int s) {
-  const int b0 = h->seq_b * h->seq_k2;
-  if (!h->seq_k2 || b0 == 0) return;
+  if (!h->ktot || b0 == 0) return;
   Side& sd = h->side[s];
-  Factor& O = s == ESNMF_SIDE_V ? h->V : h->U[h->ucur];
-  if (!O.has) fail(ESNMF_ESTATE, "sequential ALS: converged columns are not set");
-  const int k2 = h->seq_k2;
+  const Factor& H2 = s == ESNMF_SIDE_V ? h->U[h->ucur] : h->V;
+  const Factor& H1 = s == ESNMF_SIDE_V ? h->FU : h->FV;
+  const Factor& O1 = s == ESNMF_SIDE_V ? h->FV : h->FU;
+  const int k2 = h->k;
   h->nlaunch += 3;
-  k_seq_m<<<grid_for((int64_t)b0 * k2, 256, 256), 256, 0, h->stream>>>(sd.G, h->W, h->k, b0, k2, h->seqM);
-  k_seq_deflate<<<grid_for(O.cap_rows * k2, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
-      O.active, O.n_active, O.dense, h->kpad, b0, k2, h->seqM, sd.X, sd.ldx, sd.row0, sd.rows);
-  k_coo_to_colmajor<<<dim3(col_grid_x(O.maxcol), b0), 256, 0, h->stream>>>(O.colptr, O.row, O.val, sd.X, sd.ldx);
-  CKL("seq_after_product");
+  k_seq_cross<<<dim3(b0, k2), 256, 0, h->stream>>>(H1.colptr, H1.row, H1.val, H2.rowmap, H2.dense, h->kpad, k2,
+                                                   h->seqC);
+  k_seq_m<<<grid_for((int64_t)b0 * k2, 256, 256), 256, 0, h->stream>>>(h->seqC, h->W, b0, k2, h->seqM);
+  k_seq_deflate<<<grid_for(O1.cap_rows * k2, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      O1.active, O1.n_active, O1.dense, h->kpf, b0, k2, h->seqM, sd.X, sd.ldx, sd.row0, sd.rows);
+  CKL("seq_deflate");
 }
 
-void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows, int kc, int64_t row0, int64_t t,
-                 bool use_pred, int64_t* colptr_out, int32_t* row_out, float* val_out, int64_t* peak_out);
+void init_u0(esnmf_t* h, const float* user_u0, bool on_dev);
 
-// start block b: U = [U_1 | U_0 | 0] ("Set U_2 = U_0"), via the U side's LS
-// buffer and a keep-all selection into the current U
-void seq_begin_block(esnmf_t* h) {
+// block b is done (its seq_iters iterations, reading C12): append U_2, V_2 to
+// U_1, V_1, refresh the record constants, restart from U_2 = U_0
+void seq_next_block(esnmf_t* h) {
   join_metrics(h);
-  Side& su = h->side[ESNMF_SIDE_U];
-  Factor& Uc = h->U[h->ucur];
-  const int b0 = h->seq_b * h->seq_k2;
-  CK(cudaMemsetAsync(su.X, 0, sizeof(float) * su.ldx * h->k, h->stream));
+  const int b0 = h->seq_b * h->seq_k2, k2 = h->k;
+  const Factor& U2 = h->U[h->ucur];
+  // record constants first (they need the old U_1, V_1): C_U, C_V into seqC / seqM
   if (b0 > 0) {
-    ++h->nlaunch;
-    k_coo_to_colmajor<<<dim3(col_grid_x(Uc.maxcol), b0), 256, 0, h->stream>>>(Uc.colptr, Uc.row, Uc.val, su.X,
-                                                                             su.ldx);
+    h->nlaunch += 2;
+    k_seq_cross<<<dim3(b0, k2), 256, 0, h->stream>>>(h->FU.colptr, h->FU.row, h->FU.val, U2.rowmap, U2.dense,
+                                                     h->kpad, k2, h->seqC);
+    k_seq_cross<<<dim3(b0, k2), 256, 0, h->stream>>>(h->FV.colptr, h->FV.row, h->FV.val, h->V.rowmap, h->V.dense,
+                                                     h->kpad, k2, h->seqM);
   }
-  uint64_t thr = ~0ULL;
-  if (h->init_nnz > 0) {
-    const double p = (double)h->init_nnz / (double)h->n;
-    thr = p >= 1.0 ? ~0ULL : (uint64_t)(p * 0x1p53);
-  }
+  // G_U2 = side V's G (the metrics' Gram of the final U_2), G_V2 = side U's G
   ++h->nlaunch;
-  k_seq_u0_block<<<grid_for(h->n * h->seq_k2, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
-      h->n, h->seq_k2, h->seed, thr, b0, su.X, su.ldx);
-  CKL("seq_u0_block");
-  factor_clear(h, Uc);
-  select_core(h, su, su.X, su.ldx, su.rows, h->k, su.row0, -1, false, Uc.colptr, Uc.row, Uc.val, su.peak);
-  factor_build_rows(h, Uc, h->n);
-  h->gramU_valid = false;
-  su.ls_valid = false;
+  k_seq_consts<<<1, 256, 0, h->stream>>>(h->seqC, h->seqM, b0 * k2, h->scal + 2, h->side[ESNMF_SIDE_V].G,
+                                         h->side[ESNMF_SIDE_U].G, k2, h->seqc);
+  for (int q = 0; q < 2; ++q) {
+    Factor& F = q == 0 ? h->FU : h->FV;
+    const Factor& B = q == 0 ? U2 : h->V;
+    factor_clear(h, F, h->ktot, h->kpf);
+    h->nlaunch += 2;
+    k_seq_append_entries<<<grid_for(B.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
+        B.colptr, B.row, B.val, k2, b0, F.colptr, F.row, F.val);
+    k_seq_append_colptr<<<1, 256, 0, h->stream>>>(B.colptr, k2, b0, h->ktot, F.colptr);
+    factor_build_rows(h, F, std::max(F.maxcol, B.maxcol), h->ktot, h->kpf);
+  }
+  CKL("seq_next_block");
+  ++h->seq_b;
+  h->seq_i = 0;
+  factor_clear(h, h->U[0]);
+  factor_clear(h, h->U[1]);
+  init_u0(h, nullptr, false);  // U_2 = U_0 (k2 columns), ucur = 0
 }
 
 // V side: Z = U W written term-indexed (stride zs); the rows written by the
@@ -965,14 +963,14 @@ Factor& half_step(esnmf_t* h, int s) {
       Phase ph(h, p0 + 0);
       gram(h, in, sd.G);
     }
-    { Phase ph(h, p0 + 1); solve_w(h, sd.G, sd.eps); }             // a2
+    { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }               // a2
     if (overlap_u) uside_w_prep(h);
   }
   h->u_prefork = false;
   if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
   { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
   if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
-  seq_after_product(h, s);                                         // Alg. 3: Eq. (7) / (8)
+  seq_deflate(h, s);                                               // Alg. 3: Eq. (7) / (8)
   sd.ls_valid = true;
   {
     Phase ph(h, p0 + 4);
@@ -992,7 +990,7 @@ Factor& half_step(esnmf_t* h, int s) {
       OnStream os(h, h->aux);
       Side& su = h->side[ESNMF_SIDE_U];
       { Phase ph2(h, kUGram); gram(h, out, su.G); }
-      { Phase ph2(h, kUSolve); solve_w(h, su.G, su.eps); }
+      { Phase ph2(h, kUSolve); sweep(h, su.G, su.eps); }
       uside_w_prep(h);
       h->u_prefork = true;
     }
@@ -1015,9 +1013,9 @@ void ensure_records(esnmf_t* h, int64_t need) {
 }
 
 void iterate_one(esnmf_t* h) {
-  if (h->seq_k2) {
-    if (h->seq_b * h->seq_k2 >= h->k) fail(ESNMF_ESTATE, "sequential ALS: all k / k2 blocks are done");
-    if (h->seq_i == 0) seq_begin_block(h);
+  if (h->ktot && h->seq_i == h->seq_iters) {
+    if ((h->seq_b + 1) * h->seq_k2 >= h->ktot) fail(ESNMF_ESTATE, "sequential ALS: all k / k2 blocks are done");
+    seq_next_block(h);
   }
   half_step(h, ESNMF_SIDE_V);
   half_step(h, ESNMF_SIDE_U);
@@ -1049,11 +1047,7 @@ void iterate_one(esnmf_t* h) {
     k_err_trace_rows<cq><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0, su.rows, \
                                                      su.X, su.ldx, su.G, su.eps, k, p_tr);                        \
     break;
-  if (h->seq_k2) {  // T = sum_ij a_ij (U_i . V_j) directly (k_seq.cuh)
-    const size_t smem = sizeof(float) * 8 * h->kpad;
-    k_err_trace_direct<<<gtr, 256, smem, h->stream>>>(Un.active, Un.n_active, Un.dense, su.T.ptr, su.T.ent,
-                                                       h->V.rowmap, h->V.dense, h->kpad, k, p_tr);
-  } else switch ((k + 31) / 32) {
+  switch ((k + 31) / 32) {
     ESNMF_ET(1) ESNMF_ET(2) ESNMF_ET(3) ESNMF_ET(4) ESNMF_ET(5) ESNMF_ET(6) ESNMF_ET(7)
     default: k_err_trace_rows<8><<<gtr, 256, 0, h->stream>>>(Un.active, Un.n_active, Un.dense, h->kpad, su.row0,
                                                              su.rows, su.X, su.ldx, su.G, su.eps, k, p_tr);
@@ -1087,14 +1081,18 @@ void iterate_one(esnmf_t* h) {
   in.k = k;
   in.it = (int)(h->nrec + 1);
   in.t_reduced = t_red;
+  if (h->ktot) {  // whole-factor records: the converged columns' constant terms
+    in.seqc = h->seqc;
+    in.fcolptr_u = h->FU.colptr;
+    in.fcolptr_v = h->FV.colptr;
+    in.ktot = h->ktot;
+    in.b0 = h->seq_b * h->seq_k2;
+  }
   ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
   CKL("finalize_record");
   h->nrec += 1;
   if (overlap_m) h->aux_pending = true;
-  if (h->seq_k2 && ++h->seq_i == h->seq_iters) {  // block converged (fixed count): append, next block
-    h->seq_i = 0;
-    ++h->seq_b;
-  }
+  if (h->ktot) ++h->seq_i;  // after seq_iters: the next iterate appends the block (seq_next_block)
 }
 
 void sync_check(esnmf_t* h) {
@@ -1456,8 +1454,6 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     if (o.seq_k2 < 0 || k % o.seq_k2 != 0) why = "esnmf_create: seq_k2 must divide k";
     else if (o.seq_iters < 1) why = "esnmf_create: seq_iters must be >= 1 with seq_k2";
     else if (o.world > 1) why = "esnmf_create: sequential ALS is single-GPU only";
-    else if (o.enforce == ESNMF_ENFORCE_MATRIX && o.seq_k2 > 1)
-      why = "esnmf_create: sequential ALS enforces per column (whole-matrix only with seq_k2 = 1)";
     else if (o.U0) why = "esnmf_create: sequential ALS draws its n x k2 U_0 itself (U0 must be NULL)";
     if (why) {
       g_last_error = why;
@@ -1490,18 +1486,23 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
-    h->k = k;
-    h->kpad = (k + 3) / 4 * 4;
+    h->k = o.seq_k2 ? o.seq_k2 : k;  // sequential ALS: the pipeline works on one block
+    h->kpad = (h->k + 3) / 4 * 4;
+    const int32_t kb = h->k;  // columns of the pipeline (k, or k2 in sequential mode)
+    if (o.seq_k2) {
+      h->ktot = k;
+      h->kpf = (k + 3) / 4 * 4;
+      h->seq_k2 = o.seq_k2;
+      h->seq_iters = o.seq_iters;
+    }
     CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
     CK(cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
     h->t = t;
     h->tside[0] = o.t_v == ESNMF_T_SAME ? t : o.t_v;
     h->tside[1] = o.t_u == ESNMF_T_SAME ? t : o.t_u;
-    h->whole = o.enforce == ESNMF_ENFORCE_MATRIX && o.seq_k2 == 0;  // seq_k2 = 1: one column, same selection
-    h->seq_k2 = o.seq_k2;
-    h->seq_iters = o.seq_iters;
+    h->whole = o.enforce == ESNMF_ENFORCE_MATRIX;
     h->init_nnz = o.init_nnz;
-    if (h->whole && (int64_t)k * (std::max(n, m) + 32) >= (1LL << 31))
+    if (h->whole && (int64_t)kb * (std::max(n, m) + 32) >= (1LL << 31))
       fail(ESNMF_EINVAL, "esnmf_create: whole-matrix enforcement needs k * rows < 2^31");
     h->wcolptr = h->alloc<int64_t>(2);
     h->rho = o.ridge_scale;
@@ -1565,10 +1566,10 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     head_setup(h.get(), hptr, o.head_terms);
     side_alloc(h.get(), su);
     // ---- factors ----
-    const int64_t capU = n * (int64_t)k;
+    const int64_t capU = n * (int64_t)kb;
     const int64_t tv = h->tside[0];
-    const int64_t capV = h->whole ? (tv < 0 ? m * (int64_t)k : std::min(m * (int64_t)k, std::max<int64_t>(tv, 1)))
-                                  : (tv < 0 ? m : std::min(m, tv)) * (int64_t)k;
+    const int64_t capV = h->whole ? (tv < 0 ? m * (int64_t)kb : std::min(m * (int64_t)kb, std::max<int64_t>(tv, 1)))
+                                  : (tv < 0 ? m : std::min(m, tv)) * (int64_t)kb;
     factor_alloc(h.get(), h->U[0], n, capU);
     factor_alloc(h.get(), h->U[1], n, capU);
     factor_alloc(h.get(), h->V, m, capV);
@@ -1601,9 +1602,9 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     ++h->nlaunch;
     k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);
     if (h->world == 1) {
-      h->W32 = h->alloc<float>((int64_t)k * h->kpad);
+      h->W32 = h->alloc<float>((int64_t)kb * h->kpad);
       if (h->kpad <= 128 && !getenv("ESNMF_UTC_OFF")) {  // tensor-core (Y W), k_uside_tc.cuh
-        h->utc_kn = (k + 15) / 16 * 16;
+        h->utc_kn = (kb + 15) / 16 * 16;
         h->utc_kk = (h->kpad + 15) / 16 * 16;
         const int64_t wb = (int64_t)h->utc_kn * h->utc_kk * 4;
         h->wtc = h->alloc<uint8_t>(wb);
@@ -1616,13 +1617,18 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     }
     CK(cudaMemsetAsync(h->vbits, 0, sizeof(uint32_t) * ceil_div(m, 32), h->stream));
     CK(cudaMemsetAsync(h->vmap, 0, sizeof(uint64_t) * m, h->stream));
-    h->W = h->alloc<double>((int64_t)k * k);
-    if (h->seq_k2) {
-      h->seqG = h->alloc<double>((int64_t)k * k);
-      h->seqM = h->alloc<double>((int64_t)k * h->seq_k2);
+    h->W = h->alloc<double>((int64_t)kb * kb);
+    if (h->ktot) {  // converged columns (all blocks but the current one) and scratch
+      const int eta = h->ktot / h->k;
+      factor_alloc(h.get(), h->FU, n, h->U[0].cap * eta, h->ktot, h->kpf);
+      factor_alloc(h.get(), h->FV, m, h->V.cap * eta, h->ktot, h->kpf);
+      h->seqC = h->alloc<double>((int64_t)h->ktot * h->k);
+      h->seqM = h->alloc<double>((int64_t)h->ktot * h->k);
+      h->seqc = h->alloc<double>(4);
+      CK(cudaMemsetAsync(h->seqc, 0, sizeof(double) * 4, h->stream));
     }
-    h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * k * k);
-    if (k > 224) h->sweep_scratch = h->alloc<double>((int64_t)k * (k + 1) / 2);
+    h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * kb * kb);
+    if (kb > 224) h->sweep_scratch = h->alloc<double>((int64_t)kb * (kb + 1) / 2);
     init_u0(h.get(), o.U0, on_dev);
     CK(cudaStreamSynchronize(h->stream));
     int fl[4];
@@ -1705,22 +1711,34 @@ esnmf_status esnmf_records(esnmf_t* h, int64_t cap, int64_t* count, esnmf_record
   return st;
 }
 
+// the factor's COO; in sequential mode the frozen columns [0, b0) (F1) first,
+// then the block's k columns shifted to [b0, b0 + k)
 static esnmf_status get_factor(esnmf_t* h, const Factor& f, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col,
-                               float* val) {
+                               float* val, const Factor* F1 = nullptr) {
   if (!h || !nnz) { g_last_error = "get factor: NULL argument"; return ESNMF_EINVAL; }
   bool trunc = false;
   esnmf_status st = guarded([&] {
     set_device(h);
     sync_check(h);
+    const int b0 = F1 ? h->seq_b * h->seq_k2 : 0;
+    std::vector<int64_t> fp(b0 + 1, 0);
+    if (b0 > 0) CK(cudaMemcpy(fp.data(), F1->colptr, sizeof(int64_t) * (b0 + 1), cudaMemcpyDeviceToHost));
     std::vector<int64_t> cp(h->k + 1, 0);
     if (f.has) CK(cudaMemcpy(cp.data(), f.colptr, sizeof(int64_t) * (h->k + 1), cudaMemcpyDeviceToHost));
-    *nnz = cp[h->k];
-    if (cap < cp[h->k] || ((!row || !col || !val) && cp[h->k] > 0)) { trunc = true; return; }
+    const int64_t nf = fp[b0], total = nf + cp[h->k];
+    *nnz = total;
+    if (cap < total || ((!row || !col || !val) && total > 0)) { trunc = true; return; }
+    if (nf > 0) {
+      CK(cudaMemcpy(row, F1->row, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(val, F1->val, sizeof(float) * nf, cudaMemcpyDeviceToHost));
+      for (int c = 0; c < b0; ++c)
+        for (int64_t e = fp[c]; e < fp[c + 1]; ++e) col[e] = c;
+    }
     if (cp[h->k] > 0) {
-      CK(cudaMemcpy(row, f.row, sizeof(int32_t) * cp[h->k], cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(val, f.val, sizeof(float) * cp[h->k], cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(row + nf, f.row, sizeof(int32_t) * cp[h->k], cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(val + nf, f.val, sizeof(float) * cp[h->k], cudaMemcpyDeviceToHost));
       for (int c = 0; c < h->k; ++c)
-        for (int64_t e = cp[c]; e < cp[c + 1]; ++e) col[e] = c;
+        for (int64_t e = cp[c]; e < cp[c + 1]; ++e) col[nf + e] = b0 + c;
     }
   });
   if (st == ESNMF_OK && trunc) { g_last_error = "factor buffer too small"; return ESNMF_ETRUNC; }
@@ -1729,12 +1747,12 @@ static esnmf_status get_factor(esnmf_t* h, const Factor& f, int64_t cap, int64_t
 
 esnmf_status esnmf_get_U(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val) {
   if (!h) { g_last_error = "NULL handle"; return ESNMF_EINVAL; }
-  return get_factor(h, h->U[h->ucur], cap, nnz, row, col, val);
+  return get_factor(h, h->U[h->ucur], cap, nnz, row, col, val, h->ktot ? &h->FU : nullptr);
 }
 
 esnmf_status esnmf_get_V(esnmf_t* h, int64_t cap, int64_t* nnz, int32_t* row, int32_t* col, float* val) {
   if (!h) { g_last_error = "NULL handle"; return ESNMF_EINVAL; }
-  return get_factor(h, h->V, cap, nnz, row, col, val);
+  return get_factor(h, h->V, cap, nnz, row, col, val, h->ktot ? &h->FV : nullptr);
 }
 
 esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32_t* row, const int32_t* col,
@@ -1890,7 +1908,9 @@ esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {
   info->n = h->n;
   info->m = h->m;
   info->nnz = h->nnz;
-  info->k = h->k;
+  info->k = h->ktot ? h->ktot : h->k;
+  info->ls_cols = h->k;
+  info->seq_block = h->seq_b;
   info->t = h->t;
   info->world = h->world;
   info->rank = h->rank;

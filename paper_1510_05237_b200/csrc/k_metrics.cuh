@@ -108,6 +108,13 @@ struct RecordInputs {
   int k;
   int it;
   const double* t_reduced;  // if non-null: T already summed over ranks
+  // sequential ALS (Alg. 3): the record covers U = [U_1 U_2 0], V = [V_1 V_2 0]; the
+  // pipeline's factors are the block (k columns), U_1 / V_1 the frozen columns
+  // [0, b0) of ktot.  seqc = {T_1, S_11, ||U_1||^2}; null otherwise.
+  const double* seqc = nullptr;
+  const int64_t* fcolptr_u = nullptr;
+  const int64_t* fcolptr_v = nullptr;
+  int ktot = 0, b0 = 0;
 };
 
 // One block: R, E, counts -> rec.  Also stores (Rnum, Rden, T) into scal[0..2].
@@ -124,23 +131,41 @@ __global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ re
     dead_u += in.colptr_u[c + 1] == in.colptr_u[c];
     dead_v += in.colptr_v[c + 1] == in.colptr_v[c];
   }
+  int64_t fnnz_u = 0, fnnz_v = 0;
+  double seq_T = 0, seq_S = 0, seq_N = 0;
+  if (in.seqc) {
+    // E^2 ||A||^2 = ||A||^2 - 2 T_1 - 2 T_2' + S_11 + S_22: the cross terms
+    // 2 tr(U_1^T U_2 V_2^T V_1) of ||U V^T||^2 and of T_2 = T_2' + that (A V_2
+    // recovered from the deflated LS, reading C9) cancel
+    for (int c = threadIdx.x; c < in.b0; c += blockDim.x) {
+      dead_u += in.fcolptr_u[c + 1] == in.fcolptr_u[c];
+      dead_v += in.fcolptr_v[c + 1] == in.fcolptr_v[c];
+    }
+    const int future = in.ktot - in.b0 - in.k;  // blocks not started: zero columns
+    if (threadIdx.x == 0) dead_u += future, dead_v += future;
+    fnnz_u = in.fcolptr_u[in.ktot];
+    fnnz_v = in.fcolptr_v[in.ktot];
+    seq_T = in.seqc[0];
+    seq_S = in.seqc[1];
+    seq_N = in.seqc[2];
+  }
   dead_u = (int)block_sum((double)dead_u, sm);
   dead_v = (int)block_sum((double)dead_v, sm);
   if (threadIdx.x == 0) {
     esnmf_record r;
     r.it = in.it;
-    r.R = den > 0 ? sqrt(num) / sqrt(den) : -1.0;
-    double e2 = in.normA2 - 2.0 * T + S;
+    r.R = den + seq_N > 0 ? sqrt(num) / sqrt(den + seq_N) : -1.0;
+    double e2 = in.normA2 - 2.0 * (T + seq_T) + S + seq_S;
     if (e2 < 0) e2 = 0;
     r.E = sqrt(e2) / sqrt(in.normA2);
-    r.nnz_u = in.colptr_u[in.k];
-    r.nnz_v = in.colptr_v[in.k];
+    r.nnz_u = in.colptr_u[in.k] + fnnz_u;
+    r.nnz_v = in.colptr_v[in.k] + fnnz_v;
     r.dead_u = dead_u;
     r.dead_v = dead_v;
     r.active_u = *in.nact_u;
     r.active_v = *in.nact_v;
-    r.peak_u = in.peak_u ? *in.peak_u : -1;
-    r.peak_v = in.peak_v ? *in.peak_v : -1;
+    r.peak_u = in.peak_u ? *in.peak_u + fnnz_u : -1;
+    r.peak_v = in.peak_v ? *in.peak_v + fnnz_v : -1;
     *rec = r;
     scal[0] = num;
     scal[1] = den;

@@ -1,60 +1,56 @@
 // k_seq.cuh -- sequential ALS (Alg. 3).
 //
-// Block b of k2 topics occupies columns [b0, b0 + k2) of the k-column
-// factors; the columns < b0 are the converged topics U_1, V_1.  The update of
-// Eq. (7) / Eq. (8),
+// The handle runs the k2-column pipeline on the current block (U_2, V_2); the
+// converged topics U_1, V_1 (the first b0 = b k2 of the k columns) live in
+// separate "frozen" factors FU, FV.  The update of Eq. (7) / Eq. (8)
+// (P:322-326),
 //     F_2 = (T H_2 - O_1 H_1^T H_2)(H_2^T H_2 + eps I)^{-1}
-// (V side: T = A^T, H = U, O = V; U side: T = A, H = V, O = U), runs through
-// the k-column pipeline unchanged with three additions:
-//   * W is the block inverse: (G_22 + eps I)^{-1} in the block, 0 elsewhere
-//     (k_seq_gblock + the sweep + k_seq_wmask), so the product T H W writes
-//     T H_2 W_22 into the block columns and 0 into the others;
-//   * k_seq_deflate subtracts O_1 (G_12 W_22), G_12 = H_1^T H_2, from the block
-//     columns (M = G_12 W_22 from k_seq_m);
-//   * the converged columns of O are written back into the LS buffer before
-//     the selection (k_coo_to_colmajor), which keeps them (<= t entries each).
+// (V side: T = A^T, H = U, O = V; U side: T = A, H = V, O = U), is the block's
+// own product T H_2 W_22 minus O_1 M with M = (H_1^T H_2) W_22:
+//   k_seq_cross   C = H_1^T H_2  (b0 x k2, fp64, one block per (c, d))
+//   k_seq_m       M = C W_22
+//   k_seq_deflate X[:, d] -= O_1 M[:, d] over O_1's active rows
+// Appending a finished block to FU / FV and updating the constants of the
+// whole-factor records (T_1 = tr(U_1^T A V_1), S_11 = tr(G_U1 G_V1), ||U_1||^2)
+// are the other kernels here.
 #pragma once
 #include "common.cuh"
 
 namespace esk {
 
-// Gs = G on the block, (tr G_22 / k2) on the other diagonal entries, 0 elsewhere:
-// the sweep's eps = rho (tr Gs / k + 1) is then rho (tr G_22 / k2 + 1), reading C6
-// on the block Gram (reading C19), and its inverse is block-diagonal.
-__global__ void k_seq_gblock(const double* __restrict__ G, int k, int b0, int k2, double* __restrict__ Gs) {
-  double tr = 0;
-  for (int d = 0; d < k2; ++d) tr += G[(int64_t)(b0 + d) * k + b0 + d];
-  const double mean = tr / k2;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)k * k; q += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q / k), j = (int)(q - (int64_t)i * k);
-    const bool bi = i >= b0 && i < b0 + k2, bj = j >= b0 && j < b0 + k2;
-    Gs[q] = (bi && bj) ? G[q] : (i == j ? mean : 0.0);
+// C[c][d] = sum over the entries (i, v) of column c of H_1 of v * H_2[i][d]
+// (H_2 through its row view: rowmap + dense rows of stride kpad)
+__global__ void __launch_bounds__(256) k_seq_cross(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
+                                                   const float* __restrict__ val, const int32_t* __restrict__ rowmap,
+                                                   const float* __restrict__ dense, int kpad, int k2,
+                                                   double* __restrict__ C) {
+  __shared__ double sm[32];
+  const int c = blockIdx.x, d = blockIdx.y;
+  double s = 0;
+  for (int64_t e = colptr[c] + threadIdx.x; e < colptr[c + 1]; e += blockDim.x) {
+    const int32_t r = rowmap[row[e]];
+    if (r >= 0) s = fma((double)val[e], (double)dense[(int64_t)r * kpad + d], s);
   }
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) C[(int64_t)c * k2 + d] = s;
 }
 
-// zero W outside block x block
-__global__ void k_seq_wmask(double* __restrict__ W, int k, int b0, int k2) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)k * k; q += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q / k), j = (int)(q - (int64_t)i * k);
-    if (!(i >= b0 && i < b0 + k2 && j >= b0 && j < b0 + k2)) W[q] = 0.0;
-  }
-}
-
-// M[c][d] = sum_e G[c][b0+e] W[b0+e][b0+d] for c < b0, d < k2 (fp64)
-__global__ void k_seq_m(const double* __restrict__ G, const double* __restrict__ W, int k, int b0, int k2,
+// M[c][d] = sum_e C[c][e] W[e][d]  (c < b0, d < k2; W is the block's k2 x k2 inverse)
+__global__ void k_seq_m(const double* __restrict__ C, const double* __restrict__ W, int b0, int k2,
                         double* __restrict__ M) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)b0 * k2; q += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(q / k2), d = (int)(q - (int64_t)c * k2);
     double s = 0;
-    for (int e = 0; e < k2; ++e) s = fma(G[(int64_t)c * k + b0 + e], W[(int64_t)(b0 + e) * k + b0 + d], s);
+    for (int e = 0; e < k2; ++e) s = fma(C[(int64_t)c * k2 + e], W[(int64_t)e * k2 + d], s);
     M[q] = s;
   }
 }
 
-// X[b0+d][i] -= sum_{c < b0} O[i][c] M[c][d] for every active row i of O (rows
-// of O that are empty have nothing to subtract).  One thread per (row, d).
+// X[d][i] -= sum_{c < b0} O[i][c] M[c][d] for every active row i of O (rows of
+// O that are empty have nothing to subtract).  One thread per (row, d); O's
+// dense rows have stride kpf.
 __global__ void k_seq_deflate(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
-                              const float* __restrict__ dense, int kpad, int b0, int k2,
+                              const float* __restrict__ dense, int kpf, int b0, int k2,
                               const double* __restrict__ M, float* __restrict__ X, int64_t ldx, int64_t row0,
                               int64_t rows) {
   const int64_t total = *n_active * k2;
@@ -63,70 +59,60 @@ __global__ void k_seq_deflate(const int32_t* __restrict__ active, const int64_t*
     const int d = (int)(q - r * k2);
     const int64_t lr = (int64_t)active[r] - row0;
     if (lr < 0 || lr >= rows) continue;
-    const float* o = dense + r * kpad;
+    const float* o = dense + r * kpf;
     double s = 0;
     for (int c = 0; c < b0; ++c) {
       const float oc = o[c];
       if (oc != 0.f) s = fma((double)oc, M[(int64_t)c * k2 + d], s);
     }
-    float* x = X + (int64_t)(b0 + d) * ldx + lr;
+    float* x = X + (int64_t)d * ldx + lr;
     *x = (float)((double)*x - s);
   }
 }
 
-// U_0 block ("Set U_2 = U_0", U_0 in R^{n x k2}): the reading C10 formula
-// with k2 columns (index i*k2 + c), masked as reading C18 when thr != ~0,
-// written into columns [b0, b0 + k2) of the column-major buffer X.
-__global__ void k_seq_u0_block(int64_t n, int k2, uint64_t seed, uint64_t thr, int b0, float* __restrict__ X,
-                               int64_t ldx) {
-  const int64_t total = n * k2;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q / k2;
-    const int c = (int)(q - i * k2);
-    const uint64_t x = splitmix64(seed ^ kU0Stream ^ (uint64_t)q);
-    float v = (float)(((double)(x >> 41) + 0.5) * 0x1p-23);
-    if (thr != ~0ULL && (splitmix64(seed ^ kU0Mask ^ (uint64_t)q) >> 11) >= thr) v = 0.f;
-    X[(int64_t)(b0 + c) * ldx + i] = v;
+// append the block's COO (k2 columns) as columns [b0, b0 + k2) of the frozen
+// factor F (ktot columns, canonical column-major): entries first ...
+__global__ void k_seq_append_entries(const int64_t* __restrict__ bcolptr, const int32_t* __restrict__ brow,
+                                     const float* __restrict__ bval, int k2, int b0,
+                                     const int64_t* __restrict__ fcolptr, int32_t* __restrict__ frow,
+                                     float* __restrict__ fval) {
+  const int64_t base = fcolptr[b0], nb = bcolptr[k2];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nb; e += (int64_t)gridDim.x * blockDim.x) {
+    frow[base + e] = brow[e];
+    fval[base + e] = bval[e];
   }
 }
 
-// E's trace term without the LS recovery (the deflated, block-masked LS of
-// Alg. 3 no longer gives A V): T = tr(U^T A V) = sum over the entries a_ij of
-// the active term rows i of U of a_ij (U_i . V_j), V_j from V's row view.
-// One warp per active U row, U_i staged in shared memory, lanes over entries;
-// fixed-order per-block partials.
-__global__ void __launch_bounds__(256) k_err_trace_direct(const int32_t* __restrict__ active,
-                                                          const int64_t* __restrict__ n_active,
-                                                          const float* __restrict__ udense,
-                                                          const int64_t* __restrict__ aptr,
-                                                          const int2* __restrict__ aent,
-                                                          const int32_t* __restrict__ vrowmap,
-                                                          const float* __restrict__ vdense, int kpad, int k,
-                                                          double* __restrict__ part) {
-  extern __shared__ float su[];  // [8 warps][kpad]
+// ... then the column pointers (one block; colptr[c] for c > b0 + k2 = new total)
+__global__ void k_seq_append_colptr(const int64_t* __restrict__ bcolptr, int k2, int b0, int ktot,
+                                    int64_t* __restrict__ fcolptr) {
+  const int64_t base = fcolptr[b0];
+  __syncthreads();
+  for (int c = b0 + 1 + threadIdx.x; c <= ktot; c += blockDim.x) fcolptr[c] = base + bcolptr[min(c - b0, k2)];
+}
+
+// record constants when block (U_2, V_2) joins U_1, V_1 (one block): with
+// C_U = U_1^T U_2, C_V = V_1^T V_2 (old U_1, V_1) and X = sum C_U o C_V,
+//   T_1   += tr(U_2^T A V_2) = T_2' + X    (T_2' = the last record's LS-recovered
+//                                          trace, scal[2]; A V_2 = LS_2 (G + eps I) + U_1 C_V)
+//   S_11  += 2 X + tr(G_U2 G_V2)          (the Gram of [U_1 U_2] is [[G_11, C_U], [C_U^T, G_22]])
+//   |U_1|^2 += tr G_U2
+__global__ void k_seq_consts(const double* __restrict__ CU, const double* __restrict__ CV, int ncross,
+                             const double* __restrict__ T2, const double* __restrict__ GU2,
+                             const double* __restrict__ GV2, int k2, double* __restrict__ c) {
   __shared__ double sm[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* ur = su + w * kpad;
-  const int64_t na = *n_active;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double acc = 0;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < na; r += nwarps) {
-    for (int c = lane; c < kpad; c += 32) ur[c] = udense[r * kpad + c];
-    __syncwarp();
-    const int64_t i = active[r];
-    for (int64_t e = aptr[i] + lane; e < aptr[i + 1]; e += 32) {
-      const int2 en = aent[e];
-      const int32_t vr = vrowmap[en.x];
-      if (vr < 0) continue;
-      const float* v = vdense + (int64_t)vr * kpad;
-      double s = 0;
-      for (int c = 0; c < k; ++c) s = fma((double)ur[c], (double)v[c], s);
-      acc = fma((double)__int_as_float(en.y), s, acc);
-    }
-    __syncwarp();
+  double X = 0, S = 0, tr = 0;
+  for (int q = threadIdx.x; q < ncross; q += blockDim.x) X += CU[q] * CV[q];
+  for (int q = threadIdx.x; q < k2 * k2; q += blockDim.x) S += GU2[q] * GV2[q];
+  for (int d = threadIdx.x; d < k2; d += blockDim.x) tr += GU2[(int64_t)d * k2 + d];
+  X = block_sum(X, sm);
+  S = block_sum(S, sm);
+  tr = block_sum(tr, sm);
+  if (threadIdx.x == 0) {
+    c[0] += *T2 + X;
+    c[1] += 2.0 * X + S;
+    c[2] += tr;
   }
-  acc = block_sum(acc, sm);
-  if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
 }  // namespace esk

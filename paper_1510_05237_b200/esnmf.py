@@ -55,7 +55,8 @@ class esnmf_info(ctypes.Structure):
     _fields_ = [("n", c_i64), ("m", c_i64), ("nnz", c_i64), ("k", c_i32), ("t", c_i64), ("world", c_i32),
                 ("rank", c_i32), ("v_row0", c_i64), ("v_rows", c_i64), ("u_row0", c_i64), ("u_rows", c_i64),
                 ("iterations", c_i64), ("device_bytes", c_i64), ("normA2", c_dbl), ("launches", c_i64),
-                ("head_terms", c_i32), ("head_dense", c_i32)]
+                ("head_terms", c_i32), ("head_dense", c_i32),
+                ("ls_cols", c_i32), ("seq_block", c_i32)]
 
 
 class esnmf_phase(ctypes.Structure):
@@ -221,14 +222,14 @@ def esnmf_get_ls(h, side: int):
     """(row0, LS rows x k float32) of this rank's shard for the last half-step of `side`."""
     r0, rows = c_i64(), c_i64()
     _check(lib().esnmf_get_ls(h, int(side), ctypes.byref(r0), ctypes.byref(rows), None), "esnmf_get_ls")
-    k = esnmf_get_info(h)["k"]
+    k = esnmf_get_info(h)["ls_cols"]   # k, or k2 (the current block) in sequential mode
     out = np.empty((rows.value, k), np.float32)
     _check(lib().esnmf_get_ls(h, int(side), ctypes.byref(r0), ctypes.byref(rows), out.ctypes.data), "esnmf_get_ls")
     return r0.value, out
 
 
 def esnmf_get_gram(h, side: int):
-    k = esnmf_get_info(h)["k"]
+    k = esnmf_get_info(h)["ls_cols"]
     G = np.empty((k, k), np.float64)
     eps = c_dbl()
     _check(lib().esnmf_get_gram(h, int(side), G.ctypes.data, ctypes.byref(eps)), "esnmf_get_gram")
