@@ -101,6 +101,7 @@ struct Side {
   int64_t* chunk_cnt = nullptr;
   int64_t* coltot = nullptr;
   uint64_t* kthr = nullptr;
+  SelLvl* lvl = nullptr;          // [k] multi-block radix fallback state
   uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
   int64_t above_t = -1;           // its t capacity per column
   int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
@@ -712,7 +713,8 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   CK(cudaMemsetAsync(sd.cand_fill, 0, sizeof(int32_t) * k, h->stream));
   dim3 g((unsigned)nch, k);
   // two-pass path: the [k][t] list must fit and the kept set of a column must fit k_sel_final's smem
-  const bool fast = sd.above && t >= 0 && t <= kSelFastT && t * kc <= sd.above_t * h->k;
+  // (not for the flat whole-factor view, rows > ldx: its one column would run k_sel_final in one block)
+  const bool fast = sd.above && t >= 0 && t <= kSelFastT && t * kc <= sd.above_t * h->k && rows <= sd.ldx;
   if (fast && sd.pred && use_pred) {
     // one pass over X in steady state: histogram + candidates above the predicted
     // threshold (k_sel_pred_final); columns whose prediction failed take the
@@ -768,6 +770,18 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
                                           sd.chunk_cnt, nseg);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg, sd.kthr);
+  {  // columns whose threshold bucket overflowed kSelCap: grid-wide radix levels
+    CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
+    ++h->nlaunch; k_sel_lvl_init<<<1, 256, 0, h->stream>>>(sd.sel, sd.cand_fill, k, sd.lvl);
+    const int shifts[5] = {39, 32, 20, 8, 0}, widths[5] = {12, 7, 12, 12, 8};
+    for (int lv = 0; lv < 5; ++lv) {
+      h->nlaunch += 2;
+      k_sel_lvl_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.lvl, shifts[lv], widths[lv], sd.hist);
+      k_sel_lvl_pick<<<k, 256, 0, h->stream>>>(sd.hist, shifts[lv], widths[lv], lv == 4, sd.lvl);
+    }
+    ++h->nlaunch; k_sel_lvl_count<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.lvl, sd.chunk_cnt, nseg,
+                                                            sd.kthr);
+  }
   ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.coltot);
   ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, colptr_out);
   ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.kthr, colptr_out,
@@ -1148,6 +1162,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * (sd.nchunks + 1) * kSelSegs);  // (+1: the flat view)
   sd.coltot = h->alloc<int64_t>(k);
   sd.kthr = h->alloc<uint64_t>(k);
+  sd.lvl = h->alloc<SelLvl>(k);
   const int64_t ts = h->tside[&sd == &h->side[ESNMF_SIDE_V] ? 0 : 1];
   if (ts >= 0 && ts <= kSelFastT) {
     sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(ts, 1));

@@ -144,14 +144,20 @@ __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (x[u] > 0.f) {
-        const int dg = sel_digit(x[u]);
-        if (dg > s.digit) {
-          ++above;
-        } else if (dg == s.digit) {
-          const int slot = atomicAdd(&cand_fill[c], 1);
-          if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
-        }
+      const int dg = x[u] > 0.f ? sel_digit(x[u]) : -1;
+      above += dg > s.digit;
+      // bucket-D candidates: one atomic per warp (a flat whole-factor column can
+      // put millions of entries into the bucket)
+      const bool cd = x[u] > 0.f && dg == s.digit;
+      const unsigned m = __ballot_sync(__activemask(), cd);
+      if (cd) {
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(m) - 1;
+        int b0 = 0;
+        if (lane == leader) b0 = atomicAdd(&cand_fill[c], __popc(m));
+        b0 = __shfl_sync(m, b0, leader);
+        const int slot = b0 + __popc(m & ((1u << lane) - 1u));
+        if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
       }
     }
     cnt[q] = above;
@@ -219,53 +225,147 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
       atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + lr / kSelSeg], 1ULL);
     }
   } else {
-    // Exact fallback: radix select over the whole column restricted to bucket D.
-    // Key bits below the bucket: value bits 18..0 (stored inverted), then the row.
-    const float* col = X + (int64_t)c * ldx;
-    // levels: (shift, width) over the 63-bit key; bucket D fixes key bits 62..51
-    const int shifts[5] = {39, 32, 20, 8, 0};
-    const int widths[5] = {12, 7, 12, 12, 8};
-    uint64_t prefix = ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51;
-    uint64_t fixed_mask = 0xFFFULL << 51;
-    int64_t r = s.r;
-    for (int lv = 0; lv < 5; ++lv) {
-      const int sh = shifts[lv], wd = widths[lv];
-      for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
-      __syncthreads();
-      for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
-        const float x = col[j];
-        if (x > 0.f && sel_digit(x) == s.digit) {
-          const uint64_t key = sel_key(x, (uint32_t)(row0 + j));
-          if ((key & fixed_mask) == prefix) atomicAdd(&h[(key >> sh) & ((1u << wd) - 1)], 1u);
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        int b = 0;
-        for (; b < (1 << wd); ++b) {
-          if (acc + h[b] >= r) break;
-          acc += h[b];
-        }
-        r -= acc;
-        sm[0] = b;
-        sm[1] = r;
-      }
-      __syncthreads();
-      prefix |= (uint64_t)sm[0] << sh;
-      r = sm[1];
-      fixed_mask |= (uint64_t)((1u << wd) - 1) << sh;
-      __syncthreads();
-    }
-    kstar = prefix;
-    for (int64_t j = threadIdx.x; j < rows; j += blockDim.x) {
-      const float x = col[j];
-      if (x > 0.f && sel_digit(x) == s.digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar)
-        atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nchunks + j / kSelSeg], 1ULL);
-    }
+    return;  // bucket larger than kSelCap: exact multi-block radix select (k_sel_lvl_*)
   }
   if (threadIdx.x == 0)
     kthr[c] = ((uint64_t)(0x7FFFFFFFu - (uint32_t)(kstar >> 32)) << 32) | (kstar & 0xFFFFFFFFULL);
+}
+
+// ---- exact fallback for a threshold bucket larger than kSelCap ----------------
+// Radix select over the column restricted to bucket D, every level a grid-wide
+// pass (a whole-factor selection is one column of k x rows entries: one block
+// would take ~100 ms).  Key bits below the bucket: value bits 18..0 (stored
+// inverted), then the row; levels (shift, width) = (39,12) (32,7) (20,12) (8,12)
+// (0,8).  A level whose chosen bin is taken whole ends the search (lower bits
+// set to ones), so without exact value ties two levels suffice.
+struct SelLvl {
+  uint64_t prefix, mask;
+  int64_t r;
+  int32_t active, done;
+};
+
+__global__ void k_sel_lvl_init(const ColSel* __restrict__ sel, const int32_t* __restrict__ cand_fill, int k,
+                               SelLvl* __restrict__ lvl) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const ColSel s = sel[c];
+    SelLvl L;
+    L.active = s.r > 0 && cand_fill[c] > kSelCap;
+    L.done = !L.active;
+    L.prefix = L.active ? ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51 : 0;
+    L.mask = 0xFFFULL << 51;
+    L.r = s.r;
+    lvl[c] = L;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sel_lvl_hist(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                      int64_t row0, const ColSel* __restrict__ sel,
+                                                      const SelLvl* __restrict__ lvl, int sh, int wd,
+                                                      uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kNumBins];
+  const int c = blockIdx.y;
+  const SelLvl L = lvl[c];
+  if (L.done) return;
+  const int digit = sel[c].digit;
+  const int nb = 1 << wd;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  for (int64_t j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
+    const float x = col[j];
+    if (x > 0.f && sel_digit(x) == digit) {
+      const uint64_t key = sel_key(x, (uint32_t)(row0 + j));
+      if ((key & L.mask) == L.prefix) atomicAdd(&h[(key >> sh) & (nb - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (h[b]) atomicAdd(&ghist[(int64_t)c * kNumBins + b], h[b]);
+}
+
+// one block of 256 per column: bin of the r-th key, narrow the prefix; clears the histogram
+__global__ void __launch_bounds__(256) k_sel_lvl_pick(uint32_t* __restrict__ ghist, int sh, int wd, bool last,
+                                                      SelLvl* __restrict__ lvl) {
+  __shared__ int64_t sm[33];
+  __shared__ int64_t res[2];
+  const int c = blockIdx.x;
+  SelLvl L = lvl[c];
+  if (L.done) return;
+  uint32_t* hc = ghist + (int64_t)c * kNumBins;
+  const int nb = 1 << wd, per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  int64_t mine = 0;
+  for (int b = b0; b < min(nb, b0 + per); ++b) mine += hc[b];
+  int64_t tot;
+  const int64_t before = block_exscan(mine, sm, &tot);
+  if (before < L.r && before + mine >= L.r) {  // exactly one thread
+    int64_t acc = before;
+    int b = b0;
+    for (; b < b0 + per - 1; ++b) {
+      if (acc + hc[b] >= L.r) break;
+      acc += hc[b];
+    }
+    res[0] = b;
+    res[1] = L.r - acc;
+    res[1] |= (int64_t)(res[1] == (int64_t)hc[b]) << 62;  // the whole bin is taken
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) hc[b] = 0;
+  if (threadIdx.x == 0) {
+    const bool whole = (res[1] >> 62) & 1;
+    L.r = res[1] & ((1LL << 62) - 1);
+    L.prefix |= (uint64_t)res[0] << sh;
+    L.mask |= (uint64_t)(nb - 1) << sh;
+    if (whole || last) {
+      if (whole) L.prefix |= (1ULL << sh) - 1;  // every key of the bin is <= K*
+      L.done = 1;
+    }
+    lvl[c] = L;
+  }
+}
+
+// per-segment counts of the kept bucket-D keys (key <= K*), and kthr of the column
+__global__ void __launch_bounds__(256) k_sel_lvl_count(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                                       int64_t row0, const ColSel* __restrict__ sel,
+                                                       const SelLvl* __restrict__ lvl,
+                                                       int64_t* __restrict__ chunk_cnt, int64_t nseg,
+                                                       uint64_t* __restrict__ kthr) {
+  __shared__ int32_t sm[8][kSelSegs];
+  const int c = blockIdx.y;
+  const SelLvl L = lvl[c];
+  if (!L.active) return;
+  const uint64_t kstar = L.prefix;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    kthr[c] = ((uint64_t)(0x7FFFFFFFu - (uint32_t)(kstar >> 32)) << 32) | (kstar & 0xFFFFFFFFULL);
+  const int digit = sel[c].digit;
+  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
+  const int64_t r1 = min(rows, r0 + kSelChunk);
+  const float* col = X + (int64_t)c * ldx;
+  int32_t cnt[kSelSegs];
+#pragma unroll
+  for (int q = 0; q < kSelSegs; ++q) {
+    cnt[q] = 0;
+    for (int64_t j = r0 + (int64_t)q * kSelSeg + threadIdx.x; j < min(r1, r0 + (int64_t)(q + 1) * kSelSeg);
+         j += blockDim.x) {
+      const float x = col[j];
+      cnt[q] += x > 0.f && sel_digit(x) == digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kSelSegs; ++q) {
+    const int32_t w = warp_sum(cnt[q]);
+    if (lane == 0) sm[warp][q] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x < kSelSegs) {
+    int64_t tot = 0;
+    for (int w = 0; w < 8; ++w) tot += sm[w][threadIdx.x];
+    const int64_t seg = (int64_t)blockIdx.x * kSelSegs + threadIdx.x;
+    if (tot && seg < nseg) atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nseg + seg], (unsigned long long)tot);
+  }
 }
 
 // per column: exclusive scan of the chunk counts (in place), column total -> coltot[c]

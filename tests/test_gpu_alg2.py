@@ -157,3 +157,22 @@ def test_sparse_initial_guess_and_peak_nnz(init_nnz):
         # a positive near zero may flip sign with rounding: allow 1e-4 relative
         assert abs(a["peak_u"] - b["peak_u"]) <= 1e-4 * b["peak_u"] + 1
         assert abs(a["peak_v"] - b["peak_v"]) <= 1e-4 * b["peak_v"] + 1
+
+
+@pytest.mark.parametrize("whole,t", [(True, 3000), (True, 200_000), (False, 6000), (False, 300)])
+def test_selection_with_huge_tie_buckets(whole, t):
+    """Three distinct values only: the threshold bucket holds far more than the
+    4,096 keys sorted on chip, so the exact multi-block radix levels (value,
+    then row bits) decide K*; the result is the oracle's selection exactly
+    (ties -> lower column, then row; per column -> lower row, readings C4 / C17)."""
+    cfg = MEDIUM
+    g = synth.generate(cfg)
+    k = 20
+    s = ESNMF(cfg.n, cfg.m, k, cfg.t, g, seed=cfg.seed)
+    rng = np.random.default_rng(5)
+    U = (rng.random((cfg.n, k)) < 0.3) * rng.choice(np.float32([0.25, 0.5, 1.0]), size=(cfg.n, k))
+    r, c = np.nonzero(U.T)                        # canonical: column, then row
+    s.set_factor(ESNMF_SIDE_U, c.astype(np.int32), r.astype(np.int32), U[c, r].astype(np.float32))
+    s.truncate(ESNMF_SIDE_U, t, whole)
+    got = factor(s, ESNMF_SIDE_U, cfg.n, k)
+    assert np.array_equal(got, oracle.clamp_top_t(U.astype(np.float64), t, whole)[0])
