@@ -297,6 +297,47 @@ def run_sequential(inp: dict, k: int, k2: int, t: int | None, iters: int, seed: 
     return dict(records=recs, U=U, V=V, normA2=normA2)
 
 
+# ------------------------------------------------ NEXT-4: preprocessing, accuracy
+
+def normalize_rows(inp: dict) -> dict:
+    """P:153 "divide each row of the data matrix by the number of nonzero entries
+    in that row": a_ij / nnz(row i of A), rounded to fp32 (the stored data type,
+    reading C24).  Returns a copy of ``inp`` with a_val and at_val (column index =
+    term) replaced."""
+    ln = np.diff(np.asarray(inp["a_ptr"], np.int64)).astype(np.float32)
+    out = dict(inp)
+    out["a_val"] = np.asarray(inp["a_val"], np.float32) / np.repeat(ln, np.diff(inp["a_ptr"]))
+    if inp.get("at_val") is not None:
+        out["at_val"] = np.asarray(inp["at_val"], np.float32) / ln[np.asarray(inp["at_col"], np.int64)]
+    return out
+
+
+def topic_accuracy(V: np.ndarray, labels, n_journals: int) -> np.ndarray:
+    """Eq. (3)-(4) per topic column c of V: the documents "belonging"
+    to the topic are the nonzero entries of column c (n_D of them);
+        Acc = (sum_{i<k} Jnl(i,k)) / (beta - alpha) - alpha / (beta - alpha),
+        alpha = floor(n_D/n_J) (n_J (floor(n_D/n_J) - 1) / 2 + n_D mod n_J),
+        beta = n_D (n_D - 1) / 2,
+    and Acc = 1 for n_D <= 1.  The same-journal pair count is
+    sum_j C(count_j, 2) over the topic's documents of journal j (the pairs
+    grouped by journal); n_J = 1 gives beta = alpha: Acc = 1 (reading C25)."""
+    labels = np.asarray(labels, np.int64)
+    nJ = int(n_journals)
+    acc = np.ones(V.shape[1])
+    for c in range(V.shape[1]):
+        docs = np.nonzero(V[:, c])[0]
+        nD = len(docs)
+        if nD <= 1:
+            continue
+        cnt = np.bincount(labels[docs], minlength=nJ).astype(np.int64)
+        same = int(np.sum(cnt * (cnt - 1) // 2))
+        q = nD // nJ
+        alpha = q * (nJ * (q - 1) + 2 * (nD % nJ)) // 2   # an integer: the pairs of the most even spread
+        beta = nD * (nD - 1) // 2
+        acc[c] = 1.0 if beta == alpha else (same - alpha) / (beta - alpha)
+    return acc
+
+
 # ------------------------------------------------------------- format helpers
 
 def dense_to_coo(F: np.ndarray):

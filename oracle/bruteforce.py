@@ -111,3 +111,19 @@ def sequential_als(A: np.ndarray, U0: np.ndarray, k: int, t_u: int | None, t_v: 
             U[:, b0:b0 + k2] = top(ls_step(R1, V[:, b0:b0 + k2], rho), t_u)
             recs.append((np.linalg.norm(U - Uprev) / np.linalg.norm(U), np.linalg.norm(A - U @ V.T) / nA))
     return U, V, recs
+
+
+def topic_accuracy_pairs(V: np.ndarray, labels, n_journals: int) -> np.ndarray:
+    """Eq. (3)-(4) with the double sum over document pairs written out (tiny only)."""
+    acc = np.ones(V.shape[1])
+    nJ = n_journals
+    for c in range(V.shape[1]):
+        docs = [j for j in range(V.shape[0]) if V[j, c] != 0]
+        nD = len(docs)
+        if nD <= 1:
+            continue
+        same = sum(1 for a in range(nD - 1) for b in range(a + 1, nD) if labels[docs[a]] == labels[docs[b]])
+        alpha = (nD // nJ) * (nJ * ((nD // nJ) - 1) / 2 + nD % nJ)
+        beta = nD * (nD - 1) / 2
+        acc[c] = 1.0 if beta == alpha else same / (beta - alpha) - alpha / (beta - alpha)
+    return acc

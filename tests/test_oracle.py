@@ -422,3 +422,52 @@ def test_sequential_planted_disjoint_topics_recovered():
     # the error drops as each block is appended
     E = [x["E"] for x in r["records"]]
     assert E[29] > E[59] > E[89]
+
+
+# ---- NEXT-4: row normalisation, clustering accuracy Eq. (3)-(4) ----
+
+def test_normalize_rows_divides_by_row_nnz():
+    A = np.array([[2.0, 0, 4.0], [0, 3.0, 0], [0, 0, 0], [1.0, 1.0, 1.0]])
+    inp = _inp(A)
+    out = oracle.normalize_rows(inp)
+    want = np.array([[1.0, 0, 2.0], [0, 3.0, 0], [0, 0, 0], [1 / 3, 1 / 3, 1 / 3]], np.float32)
+    D = bf.dense(out["a_ptr"], out["a_col"], out["a_val"], 3)
+    assert np.array_equal(D.astype(np.float32), want)
+    Dt = bf.dense(out["at_ptr"], out["at_col"], out["at_val"], 4)
+    assert np.array_equal(Dt.T, D)                       # A^T normalised by the same (term) rows
+
+
+def test_accuracy_closed_cases():
+    """1 when all of a topic's documents share a journal, 0 when they are spread as
+    evenly as possible (alpha), 1 for <= 1 document."""
+    nJ = 5
+    labels = np.arange(40) % nJ                         # doc j in journal j mod 5
+    V = np.zeros((40, 5))
+    V[[0, 5, 10, 15], 0] = 1                            # all journal 0
+    V[:10, 1] = 1                                       # 2 per journal: uniform
+    V[:7, 2] = 1                                        # counts (2,2,1,1,1): most even for 7
+    V[3, 3] = 1                                         # one document
+    acc = oracle.topic_accuracy(V, labels, nJ)
+    assert acc[0] == 1.0 and acc[1] == 0.0 and acc[2] == 0.0 and acc[3] == 1.0 and acc[4] == 1.0
+    V2 = np.zeros((40, 1))
+    V2[[0, 5, 1], 0] = 1                                # 1 same pair of 3; alpha = 0, beta = 3
+    assert oracle.topic_accuracy(V2, labels, nJ)[0] == pytest.approx(1 / 3)
+
+
+def test_accuracy_against_pair_loops():
+    rng = np.random.default_rng(31)
+    for nJ in (2, 3, 5):
+        labels = rng.integers(0, nJ, 60)
+        V = (rng.random((60, 6)) < 0.3) * rng.random((60, 6))
+        assert np.allclose(oracle.topic_accuracy(V, labels, nJ), bf.topic_accuracy_pairs(V, labels, nJ),
+                           rtol=1e-12, atol=1e-12)
+
+
+def test_planted_corpus_shape_and_labels():
+    from synth.planted import planted_corpus
+    g = planted_corpus(n_terms=3000, n_docs=600, n_journals=5, tokens=60, topic_terms=300, seed=4)
+    assert np.bincount(g["labels"]).tolist() == [120] * 5
+    A = bf.dense(g["a_ptr"], g["a_col"], g["a_val"], 600)
+    assert np.array_equal(A.T, bf.dense(g["at_ptr"], g["at_col"], g["at_val"], 3000))
+    assert np.all(A.sum(axis=1)[A.sum(axis=1) > 0] >= 2)     # no term occurring once (P:153)
+    assert np.all(A == np.round(A)) and A.min() >= 0         # occurrence counts
