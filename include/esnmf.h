@@ -128,6 +128,11 @@ typedef struct {
      steps 2 and 4 as printed).  Single GPU; U0 must be NULL.  EINVAL otherwise. */
   int32_t seq_k2;
   int32_t seq_iters;
+  /* Row normalisation ("divide each row of the data matrix by the number of
+     nonzero entries in that row"; NEXT-4): 1 = every a_ij is replaced by a_ij / nnz(row i)
+     on the device at create (fp32, correctly rounded; A^T alike), before ||A|| and
+     everything else; 0 (default) = A as given. */
+  int32_t row_normalize;
 } esnmf_options;
 
 typedef struct {
@@ -241,6 +246,17 @@ void esnmf_destroy(esnmf_t* h);
 
 const char* esnmf_strerror(esnmf_status s);
 const char* esnmf_last_error(void);
+
+/* Clustering accuracy of the document topics, Eq. (3)-(4) (NEXT-4).
+ * labels: HOST array of m journal ids in [0, n_journals); acc: HOST array of k
+ * doubles.  For every topic column c of the current V (all k columns, also in
+ * sequential mode) the documents "belonging" to it are its stored entries
+ * (n_D of them); acc[c] = (same-journal pairs - alpha) / (beta - alpha) with
+ * alpha = floor(n_D/n_J) (n_J (floor(n_D/n_J) - 1)/2 + n_D mod n_J) and
+ * beta = n_D (n_D - 1)/2; 1 when n_D <= 1 or beta == alpha (n_J = 1).  Counts are
+ * exact (integer-valued fp64 atomics).  Synchronous.  EINVAL (bad labels),
+ * ESTATE (V not set). */
+esnmf_status esnmf_topic_accuracy(esnmf_t* h, const int32_t* labels, int32_t n_journals, double* acc);
 
 /* Enforce-after: clamp and truncate the CURRENT
  * factor of `side` once, in place -- the t largest entries per column

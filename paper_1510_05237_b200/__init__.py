@@ -33,6 +33,7 @@ from .esnmf import (  # noqa: F401
     esnmf_residual,
     esnmf_set_factor,
     esnmf_truncate,
+    esnmf_topic_accuracy,
     esnmf_version,
     lib,
 )

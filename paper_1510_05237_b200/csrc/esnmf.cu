@@ -1417,6 +1417,7 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->init_nnz = 0;
   o->seq_k2 = 0;
   o->seq_iters = 0;
+  o->row_normalize = 0;
   return ESNMF_OK;
 }
 
@@ -1554,6 +1555,18 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     su.T = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, n0, n1, &aptr);
     h->nnz = hptr[n];
     if (h->nnz < 1) fail(ESNMF_EINVAL, "esnmf_create: nnz must be >= 1");
+    float* rowlen = nullptr;  // row normalisation: nnz of every term row of A
+    if (o.row_normalize) {
+      std::vector<float> rl(n);
+      for (int64_t i = 0; i < n; ++i) rl[i] = (float)(hptr[i + 1] - hptr[i]);
+      rowlen = h->alloc<float>(n);
+      CK(cudaMemcpyAsync(rowlen, rl.data(), sizeof(float) * n, cudaMemcpyHostToDevice, h->stream));
+      ++h->nlaunch;
+      k_norm_rows<<<grid_for(su.rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(su.T.ptr, su.T.ent, su.rows,
+                                                                                        su.row0, rowlen);
+      CK(cudaStreamSynchronize(h->stream));  // rl dies here
+      CKL("norm_rows");
+    }
     // ||A||_F^2 (shard partial, summed over ranks)
     {
       unsigned gb = grid_for(std::max<int64_t>(su.T.nnz, 1), 256, 1024);
@@ -1567,13 +1580,21 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     Side& sv = h->side[ESNMF_SIDE_V];
     sv.row0 = m0;
     sv.rows = m1 - m0;
+    bool at_normalized = false;
     if (o.at_row_ptr && o.at_col_idx && o.at_val) {
       sv.T = upload_csr(h.get(), m, n, o.at_row_ptr, o.at_col_idx, o.at_val, on_dev, m0, m1, nullptr);
     } else if (h->world == 1) {
-      sv.T = build_at(h.get(), su.T, m, 0, m);
+      sv.T = build_at(h.get(), su.T, m, 0, m);  // from the (normalised) A
+      at_normalized = true;
     } else {  // the transpose needs every term row: build it from the full A, keep our documents
       DevCsr full = upload_csr(h.get(), n, m, row_ptr, col_idx, val, on_dev, 0, n, nullptr);
       sv.T = build_at(h.get(), full, m, m0, m1);
+    }
+    if (rowlen && !at_normalized) {
+      ++h->nlaunch;
+      k_norm_cols<<<grid_for(std::max<int64_t>(sv.T.nnz, 1), 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+          sv.T.ent, sv.T.nnz, rowlen);
+      CKL("norm_cols");
     }
     if (h->world == 1 && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
     build_items(h.get(), su, aptr);
@@ -1916,6 +1937,45 @@ esnmf_status esnmf_phase_times(esnmf_t* h, int64_t cap, int64_t* count, esnmf_ph
   });
   if (st == ESNMF_OK && cap < kNumPhases) { g_last_error = "esnmf_phase_times: cap < count"; return ESNMF_ETRUNC; }
   return st;
+}
+
+esnmf_status esnmf_topic_accuracy(esnmf_t* h, const int32_t* labels, int32_t n_journals, double* acc) {
+  if (!h || !labels || !acc || n_journals < 1) { g_last_error = "esnmf_topic_accuracy: bad argument"; return ESNMF_EINVAL; }
+  for (int64_t j = 0; j < h->m; ++j)
+    if (labels[j] < 0 || labels[j] >= n_journals) {
+      g_last_error = "esnmf_topic_accuracy: label " + std::to_string(j) + " out of [0, n_journals)";
+      return ESNMF_EINVAL;
+    }
+  return guarded([&] {
+    set_device(h);
+    join_metrics(h);
+    if (!h->V.has) fail(ESNMF_ESTATE, "V is not set");
+    const int kt = h->ktot ? h->ktot : h->k;
+    struct Tmp {  // per-call scratch, freed on every exit
+      void* p = nullptr;
+      ~Tmp() { if (p) cudaFree(p); }
+    } tl, tc;
+    CK(cudaMalloc(&tl.p, sizeof(int32_t) * h->m));
+    CK(cudaMalloc(&tc.p, sizeof(double) * ((int64_t)kt * n_journals + kt)));
+    int32_t* dl = static_cast<int32_t*>(tl.p);
+    double* cnt = static_cast<double*>(tc.p);
+    double* dacc = cnt + (int64_t)kt * n_journals;
+    CK(cudaMemcpyAsync(dl, labels, sizeof(int32_t) * h->m, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(double) * kt * n_journals, h->stream));
+    const int b0 = h->ktot ? h->seq_b * h->seq_k2 : 0;
+    if (b0 > 0) {
+      ++h->nlaunch;
+      k_acc_count<<<dim3(col_grid_x(h->FV.maxcol), b0), 256, 0, h->stream>>>(h->FV.colptr, h->FV.row, dl,
+                                                                             n_journals, 0, cnt);
+    }
+    h->nlaunch += 2;
+    k_acc_count<<<dim3(col_grid_x(h->V.maxcol), h->k), 256, 0, h->stream>>>(h->V.colptr, h->V.row, dl, n_journals,
+                                                                            b0, cnt);
+    k_acc_final<<<1, 256, 0, h->stream>>>(cnt, kt, n_journals, dacc);
+    CK(cudaMemcpyAsync(acc, dacc, sizeof(double) * kt, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CKL("topic_accuracy");
+  });
 }
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info) {

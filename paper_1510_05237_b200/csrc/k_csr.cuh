@@ -132,3 +132,31 @@ __global__ void __launch_bounds__(256) k_sort_rows(const int64_t* __restrict__ p
 }
 
 }  // namespace esk
+
+namespace esk {
+
+// ---- row normalisation (NEXT-4): a_ij / nnz(row i of A), fp32 correctly rounded ----
+// A's term rows (local rows r = global row0 + r)
+__global__ void k_norm_rows(const int64_t* __restrict__ ptr, int2* __restrict__ ent, int64_t rows, int64_t row0,
+                            const float* __restrict__ rowlen) {
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const float len = rowlen[row0 + r];
+    for (int64_t e = ptr[r] + (threadIdx.x & 31); e < ptr[r + 1]; e += 32) {
+      int2 en = ent[e];
+      en.y = __float_as_int(__fdiv_rn(__int_as_float(en.y), len));
+      ent[e] = en;
+    }
+  }
+}
+
+// A^T's entries: the column index is the term
+__global__ void k_norm_cols(int2* __restrict__ ent, int64_t nnz, const float* __restrict__ rowlen) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    int2 en = ent[e];
+    en.y = __float_as_int(__fdiv_rn(__int_as_float(en.y), rowlen[en.x]));
+    ent[e] = en;
+  }
+}
+
+}  // namespace esk

@@ -192,3 +192,34 @@ __global__ void k_reduce_to(const double* __restrict__ part, int64_t n, double* 
 }
 
 }  // namespace esk
+
+namespace esk {
+
+// ---- clustering accuracy, Eq. (3)-(4) (NEXT-4) ----
+// cnt[(coff + c) * nJ + label[row]] += 1 for every stored entry of column c
+__global__ void k_acc_count(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
+                            const int32_t* __restrict__ label, int nJ, int coff, double* __restrict__ cnt) {
+  const int c = blockIdx.y;
+  for (int64_t e = colptr[c] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < colptr[c + 1];
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[(int64_t)(coff + c) * nJ + label[row[e]]], 1.0);  // integers < 2^53: exact
+}
+
+// Acc_c = (same - alpha) / (beta - alpha); same = sum_j C(n_j, 2), alpha = q (nJ (q-1) + 2 (nD mod nJ)) / 2
+// with q = floor(nD / nJ), beta = nD (nD - 1) / 2; 1 for nD <= 1 or beta == alpha
+__global__ void k_acc_final(const double* __restrict__ cnt, int k, int nJ, double* __restrict__ acc) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    long long nD = 0, same = 0;
+    for (int j = 0; j < nJ; ++j) {
+      const long long x = (long long)cnt[(int64_t)c * nJ + j];
+      nD += x;
+      same += x * (x - 1) / 2;
+    }
+    const long long q = nD / nJ;
+    const long long alpha = q * ((long long)nJ * (q - 1) + 2 * (nD % nJ)) / 2;
+    const long long beta = nD * (nD - 1) / 2;
+    acc[c] = (nD <= 1 || beta == alpha) ? 1.0 : (double)(same - alpha) / (double)(beta - alpha);
+  }
+}
+
+}  // namespace esk

@@ -38,7 +38,7 @@ class esnmf_options(ctypes.Structure):
         ("inputs_on_device", c_i32),
         ("at_row_ptr", c_p), ("at_col_idx", c_p), ("at_val", c_p), ("U0", c_p),
         ("head_terms", c_i32), ("t_u", c_i64), ("t_v", c_i64), ("enforce", c_i32), ("init_nnz", c_i64),
-        ("seq_k2", c_i32), ("seq_iters", c_i32),
+        ("seq_k2", c_i32), ("seq_iters", c_i32), ("row_normalize", c_i32),
     ]
 
 
@@ -94,6 +94,7 @@ SIGNATURES = {
     "esnmf_last_error": (ctypes.c_char_p, []),
     "esnmf_partition_rows": (ctypes.c_int, [c_i64, c_p, c_i32, c_p]),
     "esnmf_truncate": (ctypes.c_int, [c_p, c_i32, c_i64, c_i32]),
+    "esnmf_topic_accuracy": (ctypes.c_int, [c_p, c_p, c_i32, c_p]),
     "esnmf_version": (ctypes.c_char_p, []),
 }
 
@@ -236,6 +237,13 @@ def esnmf_get_gram(h, side: int):
     return G, eps.value
 
 
+def esnmf_topic_accuracy(h, labels, n_journals: int, k: int) -> np.ndarray:
+    lab = np.ascontiguousarray(labels, np.int32)
+    acc = np.empty(k, np.float64)
+    _check(lib().esnmf_topic_accuracy(h, lab.ctypes.data, int(n_journals), acc.ctypes.data), "esnmf_topic_accuracy")
+    return acc
+
+
 def esnmf_get_info(h) -> dict:
     i = esnmf_info()
     _check(lib().esnmf_get_info(h, ctypes.byref(i)), "esnmf_get_info")
@@ -285,11 +293,12 @@ class ESNMF:
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
                  device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None,
                  head_terms: int = -1, t_u="same", t_v="same", whole: bool = False, init_nnz: int = 0,
-                 seq_k2: int = 0, seq_iters: int = 0):
+                 seq_k2: int = 0, seq_iters: int = 0, row_normalize: bool = False):
         """t_u / t_v: separate budgets ("same" = t, None = unlimited); whole: whole-factor
         enforcement (Alg. 2 as printed) instead of per column; init_nnz: sparse U_0
         (reading C18); seq_k2 > 0: sequential ALS (Alg. 3) in blocks of seq_k2 topics,
-        seq_iters iterations per block."""
+        seq_iters iterations per block; row_normalize: divide each row of A by its nnz
+        on the device."""
         o = esnmf_options_init()
         o.head_terms = head_terms
         o.t_u = ESNMF_T_SAME if t_u == "same" else (ESNMF_T_UNLIMITED if t_u is None else int(t_u))
@@ -297,6 +306,7 @@ class ESNMF:
         o.enforce = ESNMF_ENFORCE_MATRIX if whole else ESNMF_ENFORCE_COLUMN
         o.init_nnz = int(init_nnz)
         o.seq_k2, o.seq_iters = int(seq_k2), int(seq_iters)
+        o.row_normalize = 1 if row_normalize else 0
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device
@@ -353,6 +363,10 @@ class ESNMF:
 
     def truncate(self, side: int, t: int, whole: bool = False):
         esnmf_truncate(self.h, side, t, whole)
+
+    def topic_accuracy(self, labels, n_journals: int) -> np.ndarray:
+        """Eq. (3)-(4) per topic column of V (esnmf_topic_accuracy)."""
+        return esnmf_topic_accuracy(self.h, labels, n_journals, self.k)
 
     def info(self) -> dict:
         return esnmf_get_info(self.h)

@@ -7,7 +7,9 @@ belongs to one of ``n_journals`` journals (balanced, shuffled) and draws
 ``tokens`` term occurrences, each with probability ``mix`` from its journal's
 topic distribution (a Zipf law over a journal-specific random subset of
 ``topic_terms`` terms) and otherwise from a shared background Zipf law over the
-whole vocabulary.  Entries are occurrence counts a_ij ("the number of
+``common`` fraction of the vocabulary (the generic words that row normalisation
+is meant to de-emphasise); the topic subsets are drawn from the rest and
+may overlap.  Entries are occurrence counts a_ij ("the number of
 times term i occurs in document j"); terms that occur only once in the corpus
 are dropped, their rows left empty.  Row normalisation is NOT
 applied here: it is a step of the method (esnmf_options.row_normalize,
@@ -33,15 +35,18 @@ def _csr(rows: np.ndarray, cols: np.ndarray, vals: np.ndarray, nrows: int):
 
 
 def planted_corpus(n_terms: int = 20_112, n_docs: int = 7_510, n_journals: int = 5, tokens: int = 120,
-                   topic_terms: int = 2_000, mix: float = 0.5, s: float = 1.05, seed: int = 0) -> dict:
+                   topic_terms: int = 4_000, mix: float = 0.5, common: float = 0.1, s: float = 1.05,
+                   seed: int = 0) -> dict:
     """Returns dict(n, m, a_ptr, a_col, a_val, at_ptr, at_col, at_val, labels, n_journals)."""
     rng = np.random.default_rng(seed)
     labels = rng.permutation(np.arange(n_docs) % n_journals).astype(np.int32)
-    bg_cdf = _zipf_cdf(n_terms, s)
+    n_common = max(1, int(common * n_terms))
+    bg_cdf = _zipf_cdf(n_common, s)
     tp_cdf = _zipf_cdf(topic_terms, s)
-    topic = np.stack([rng.choice(n_terms, topic_terms, replace=False) for _ in range(n_journals)])
+    topic = np.stack([n_common + rng.choice(n_terms - n_common, topic_terms, replace=False)
+                      for _ in range(n_journals)])
     from_topic = rng.random((n_docs, tokens)) < mix
-    bg = np.minimum(np.searchsorted(bg_cdf, rng.random((n_docs, tokens))), n_terms - 1)
+    bg = np.minimum(np.searchsorted(bg_cdf, rng.random((n_docs, tokens))), n_common - 1)
     tr = np.minimum(np.searchsorted(tp_cdf, rng.random((n_docs, tokens))), topic_terms - 1)
     term = np.where(from_topic, topic[labels[:, None], tr], bg)
     doc = np.repeat(np.arange(n_docs), tokens)

@@ -32,7 +32,12 @@ def main():
     ap.add_argument("--config", default="large")
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--pubmed", action="store_true",
+                    help="the paper's timing case (P:398): 100 iterations of a 5-topic NMF of a PubMed-sized "
+                         "planted corpus (synth/planted.py), row-normalised, with clustering accuracy")
     a = ap.parse_args()
+    if a.pubmed:
+        return pubmed(a)
     cfg = synth.CONFIGS[a.config]
     dev = torch.device("cuda", 0)
     g = synth.generate_device(cfg, device=dev)
@@ -73,6 +78,51 @@ def main():
         torch.cuda.empty_cache()
     res = {"config": cfg.name, "variants": out,
            "column_over_seq_k2_1": round(out["alg2_column"]["ms_per_iter"] / out["seq_k2_1"]["ms_per_iter"], 2)}
+    print(json.dumps(res))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+def pubmed(a):
+    """P:398's comparison on a PubMed-sized planted corpus (20,112 terms x 7,510
+    documents, 5 journals): 100 iterations of a 5-topic NMF with whole-matrix,
+    column-wise and sequential (k2 = 1, 20 iterations per topic) enforcement;
+    device time per iteration and the mean clustering accuracy (Eq. (3)-(4))."""
+    import torch
+
+    from synth.planted import planted_corpus
+    from paper_1510_05237_b200 import ESNMF
+
+    g = planted_corpus()
+    k, t, iters = 5, 200, 100
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    variants = {
+        "alg2_whole": dict(whole=True, t_u=k * t, t_v=k * t),
+        "alg2_column": dict(),
+        "seq_k2_1": dict(seq_k2=1, seq_iters=iters // k),
+        "alg2_column_raw_counts": dict(row_normalize=False),
+    }
+    out = {}
+    for name, kw in variants.items():
+        kw = dict(dict(row_normalize=True), **kw)
+        s = ESNMF(g["n"], g["m"], k, t, g, seed=0, stream=stream.cuda_stream, **kw)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.iterate(iters)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        acc = s.topic_accuracy(g["labels"], g["n_journals"])
+        out[name] = {"ms_per_iter": round(ms / iters, 4), "ms_100_iters": round(ms, 2),
+                     "E_last": s.records()[-1]["E"], "accuracy": [round(x, 4) for x in acc],
+                     "accuracy_mean": round(float(acc.mean()), 4)}
+        print(name, json.dumps(out[name]), flush=True)
+        s.close()
+    res = {"config": "pubmed_like 20112x7510, k=5, t=200 per column (1000 per factor), 100 iterations",
+           "variants": out}
     print(json.dumps(res))
     if a.out:
         with open(a.out, "w") as f:
