@@ -111,6 +111,8 @@ struct Side {
   uint64_t* pcand = nullptr;      // [k][pcap]
   int32_t* pfill = nullptr;       // [k] then done [k]
   int pcap = 0;
+  int32_t* npos = nullptr;        // [k] positives per column (fused V-side pass 1)
+  bool fused = false;             // this half-step's pass 1 ran in the head epilogue
   // Gram of the factor this side reads, and its eps
   double* G = nullptr;
   double* eps = nullptr;
@@ -806,10 +808,44 @@ __global__ void k_whole_split(int32_t* __restrict__ idx, const int64_t* __restri
   for (int64_t q = threadIdx.x; q < nnz; q += blockDim.x) idx[q] = (int32_t)((int64_t)(uint32_t)idx[q] % ldx);
 }
 
+// V side after a fused head epilogue: select from the candidates, histogram
+// path only for the columns whose prediction failed
+void select_fused(esnmf_t* h, Side& sd, Factor& out) {
+  const int64_t t = h->tside[ESNMF_SIDE_V];
+  const int k = h->k;
+  int32_t* done = sd.pfill + k;
+  h->nlaunch += 2;
+  k_sel_npos_colptr<<<1, 256, 0, h->stream>>>(sd.npos, k, t, out.colptr, sd.peak);
+  CK(cudaFuncSetAttribute(k_sel_pred_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPredSortSmem));
+  k_sel_pred_sort<<<k, 1024, kPredSortSmem, h->stream>>>(sd.npos, t, sd.pcand, sd.pfill, sd.pcap, out.colptr, out.row,
+                                                         out.val, done, sd.pred);
+  // failed columns: histogram, threshold, collect, final (done columns return at once)
+  const int64_t nch = std::max<int64_t>(1, ceil_div(sd.rows, kSelChunk));
+  dim3 g((unsigned)nch, k);
+  CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
+  CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
+  int32_t* bfill = sd.above_fill + k;
+  h->nlaunch += 4;
+  k_sel_hist<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.hist, nullptr, 0, nullptr, nullptr, 0, done);
+  k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
+  k_sel_collect2<<<g, 256, 0, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(t, 1), sd.above,
+                                           sd.above_fill, sd.bucket, bfill, done);
+  CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
+  k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(sd.X, sd.ldx, sd.rows, sd.row0, sd.sel, std::max<int64_t>(t, 1),
+                                                     sd.above, sd.above_fill, sd.bucket, bfill, out.colptr, out.row,
+                                                     out.val, done, sd.pred);
+  CKL("select_fused");
+}
+
 // clamp + top-t of side s's LS into factor `out` (column-major COO)
 void select_topt(esnmf_t* h, int s, Factor& out) {
   Side& sd = h->side[s];
   const int64_t t = h->tside[s];
+  if (sd.fused) {
+    sd.fused = false;
+    select_fused(h, sd, out);
+    return;
+  }
   if (!h->whole) {
     select_core(h, sd, sd.X, sd.ldx, sd.rows, h->k, sd.row0, t, true, out.colptr, out.row, out.val, sd.peak);
     return;
@@ -834,14 +870,30 @@ template <int ST>
 void vhead_launch_st(esnmf_t* h) {
   Side& sv = h->side[ESNMF_SIDE_V];
   const int smem = ST * head_stage_bytes_host(h->kn) + 1024;
-  auto kern = k_vhead_otf<ST>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, h->num_sms);
   ++h->nlaunch;
+  // selection pass 1 in the epilogue (k_sel_pred_sort) when the V side takes the
+  // predicted-threshold path: per-column top-t, t <= kSelFastT, one GPU.  Opt-in
+  // (ESNMF_FUSED_SELECT=1): the per-element counting costs the epilogue more
+  // (+0.14 ms at Large) than the streaming pass it saves (~0.1 ms)
+  const int64_t t = h->tside[ESNMF_SIDE_V];
+  sv.fused = sv.pred && !h->whole && h->world == 1 && t >= 0 && t <= kSelFastT && t <= sv.above_t &&
+             !(h->ktot && h->seq_b > 0) &&  // Alg. 3 deflates X after this kernel
+             h->kn <= 128 &&                 // <= 4 column chunks per epilogue warp
+             ceil_div(h->head_ntiles, std::min<int64_t>(h->head_ntiles, h->num_sms)) < 65536 &&  // 16-bit counts
+             getenv("ESNMF_FUSED_SELECT");  // opt-in: measured slower
+  SelFuse fz{};
+  if (sv.fused) {
+    CK(cudaMemsetAsync(sv.pfill, 0, sizeof(int32_t) * h->k, h->stream));
+    CK(cudaMemsetAsync(sv.npos, 0, sizeof(int32_t) * h->k, h->stream));
+    fz = SelFuse{sv.pred, sv.npos, sv.pcand, sv.pfill, sv.pcap, sv.row0};
+  }
+  auto kern = sv.fused ? k_vhead_otf<ST, true> : k_vhead_otf<ST, false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
                                                    h->colscale,
                                                    sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
-                                                   h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad);
+                                                   h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad, fz);
   CKL("vhead");
 }
 
@@ -1179,6 +1231,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
       CK(cudaMemsetAsync(sd.pred, 0xFF, sizeof(uint32_t) * k, h->stream));
       sd.pcand = h->alloc<uint64_t>((int64_t)k * sd.pcap);
       sd.pfill = h->alloc<int32_t>(2 * (int64_t)k);
+      sd.npos = h->alloc<int32_t>(k);
     }
   }
   sd.G = h->alloc<double>((int64_t)k * k);

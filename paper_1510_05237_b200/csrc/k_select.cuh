@@ -26,9 +26,11 @@ namespace esk {
 __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, int64_t ldx, int64_t rows,
                                                   uint32_t* __restrict__ hist, const uint32_t* __restrict__ pred = nullptr,
                                                   int64_t row0 = 0, uint64_t* __restrict__ pcand = nullptr,
-                                                  int32_t* __restrict__ pfill = nullptr, int pcap = 0) {
+                                                  int32_t* __restrict__ pfill = nullptr, int pcap = 0,
+                                                  const int32_t* __restrict__ skip = nullptr) {
   __shared__ uint32_t h[kNumBins];
   const int c = blockIdx.y;
+  if (skip && skip[c]) return;  // column already selected (fused path)
   const uint32_t pb = pred ? pred[c] : 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -767,6 +769,96 @@ __global__ void __launch_bounds__(1024) k_sel_pred_final(const ColSel* __restric
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
     done[c] = 1;
     pred_next[c] = s.npos <= t ? 0u : pred_of(m);
+  }
+}
+
+// ---- V side fused with the head kernel's epilogue (k_vhead_otf) -------------
+// The epilogue counted the positives of every column (npos) and appended every
+// positive with value bits >= pred[c] as a candidate, so the LS buffer is not
+// read again in steady state.  colptr (min(t, npos)) and the peak count first:
+__global__ void k_sel_npos_colptr(const int32_t* __restrict__ npos, int k, int64_t t, int64_t* __restrict__ colptr,
+                                  int64_t* __restrict__ peak) {
+  __shared__ int64_t sm[33];
+  int64_t v = 0, np = 0;
+  if (threadIdx.x < k) {
+    np = npos[threadIdx.x];
+    v = t < 0 ? np : min(np, t);
+  }
+  int64_t tot, ptot;
+  const int64_t ex = block_exscan(v, sm, &tot);
+  __syncthreads();
+  block_exscan(np, sm, &ptot);
+  if (threadIdx.x < k) colptr[threadIdx.x] = ex;
+  if (threadIdx.x == 0) {
+    colptr[k] = tot;
+    if (peak) *peak = ptot;
+  }
+}
+
+// ... then per column: if the candidates hold at least min(t, npos) entries (so
+// they contain the column's top min(t, npos): every entry >= the predicted
+// threshold is a candidate), sort them by (value desc, row asc), keep the first
+// min(t, npos), write them in row order and mark the column done; else leave it
+// to the histogram path (k_sel_hist/threshold/collect2/final with `done`).
+constexpr size_t kPredSortSmem = sizeof(uint64_t) * (kPredSort + kSelFastT);
+
+__global__ void __launch_bounds__(1024) k_sel_pred_sort(const int32_t* __restrict__ npos, int64_t t,
+                                                        const uint64_t* __restrict__ pcand,
+                                                        const int32_t* __restrict__ pfill, int pcap,
+                                                        const int64_t* __restrict__ colptr,
+                                                        int32_t* __restrict__ out_row, float* __restrict__ out_val,
+                                                        int32_t* __restrict__ done, uint32_t* __restrict__ pred) {
+  extern __shared__ uint64_t ps[];
+  uint64_t* keys = ps;                // [kPredSort] candidate keys
+  uint64_t* kept = ps + kPredSort;    // [kSelFastT] kept row keys
+  __shared__ uint32_t wmin[32];
+  const int c = blockIdx.x;
+  const int64_t np_c = npos[c];
+  const int64_t need = min(t, np_c);
+  const int nc = pfill[c];
+  if (need == 0) {
+    if (threadIdx.x == 0) {
+      done[c] = 1;
+      pred[c] = t == 0 ? 0xFFFFFFFFu : 0u;
+    }
+    return;
+  }
+  const bool ok = nc <= pcap && nc <= kPredSort && (int64_t)nc >= need && need <= kSelFastT;
+  if (!ok) {
+    if (threadIdx.x == 0) done[c] = 0;
+    return;
+  }
+  int np = 1;
+  while (np < nc) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) keys[i] = i < nc ? pcand[(int64_t)c * pcap + i] : ~0ULL;
+  __syncthreads();
+  bitonic_sort_smem(keys, np);
+  const int nk = (int)need;
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+    const uint64_t key = keys[i];
+    kept[i] = row_key((uint32_t)key, __uint_as_float(0x7FFFFFFFu - (uint32_t)(key >> 32)));
+  }
+  int nq = 1;
+  while (nq < nk) nq <<= 1;
+  for (int i = nk + threadIdx.x; i < nq; i += blockDim.x) kept[i] = ~0ULL;
+  __syncthreads();
+  bitonic_sort_smem(kept, nq);
+  const int64_t o = colptr[c];
+  uint32_t mn = 0xFFFFFFFFu;
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+    const uint64_t key = kept[i];
+    out_row[o + i] = (int32_t)(key >> 32);
+    out_val[o + i] = __uint_as_float((uint32_t)key);
+    mn = min(mn, (uint32_t)key);
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t m = 0xFFFFFFFFu;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
+    done[c] = 1;
+    pred[c] = np_c <= t ? 0u : pred_of(m);
   }
 }
 

@@ -174,6 +174,16 @@ __global__ void k_head_fill(const int64_t* __restrict__ ptr, const int32_t* __re
   }
 }
 
+// fused V-side selection pass 1 (k_sel_pred_sort): pred == nullptr = off
+struct SelFuse {
+  const uint32_t* pred;  // [k] predicted threshold bits
+  int32_t* npos;         // [k] positives per column (+=)
+  uint64_t* pcand;       // [k][pcap] candidate keys
+  int32_t* pfill;        // [k]
+  int pcap;
+  int64_t row0;
+};
+
 constexpr int kHeadProd = 128;                         // producer threads
 constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
@@ -192,15 +202,22 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 // entries and the Z chunk into a stage (TMA engine, STAGES ahead); warps 0-3
 // zero the stage's A block and scatter the run into it; warp 4 (one thread)
 // issues the MMAs; warps 6-13 drain TMEM into X (two per lane quadrant).
-template <int STAGES>
+template <int STAGES, bool FUSE>
 __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
                 const int2* __restrict__ hseg, const unsigned* __restrict__ amax_bits, const uint8_t* __restrict__ zbuf,
                 const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
-                int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad) {
+                int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad,
+                SelFuse fz) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
+  __shared__ int s_npos[256];       // fused selection: positives per column counted by this CTA
+  __shared__ uint32_t s_pred[256];  // ... and the predicted thresholds (0xFFFFFFFF: none)
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+    s_npos[c] = 0;
+    s_pred[c] = (FUSE && c < k) ? fz.pred[c] : 0xFFFFFFFFu;
+  }
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t zhalf = (uint32_t)kn * kHeadK * 2;
@@ -350,6 +367,15 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     const int half = (warp - 6) >> 2;  // the two warps of a quadrant split the columns
     const int cmid = ((kn / 16 + 1) / 2) * 16;
     const int cbeg = half ? cmid : 0, cend = half ? kn : cmid;
+    // fused selection pass 1 (kn <= 128: at most 4 chunks of 16 columns per warp):
+    // per-thread positive counts, two 16-bit counters per register, reduced once
+    // at the end; candidates (value bits >= the predicted threshold) are rare and
+    // take a warp-aggregated slow path
+    uint32_t cnt2[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cnt2[q][j] = 0;
     int acc = 0;
     uint32_t aphase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -357,12 +383,14 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       tc::fence_after();
       const int64_t row = tile * kHeadM + lg * 32 + lane;
       const uint32_t ta = tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16);
-      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+#pragma unroll
+      for (int q = 0; q < (FUSE ? 4 : 1); ++q) {
+      for (int c0 = cbeg + 16 * q; c0 < (FUSE ? min(cend, cbeg + 16 * q + 1) : cend); c0 += 16) {
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();
+        float x[16];
         if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
-          float x[16];
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
             const int c = c0 + 4 * v4;
@@ -373,14 +401,57 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int c = c0 + j;
-            if (c < k) X[(int64_t)c * ldx + row] = fmaf(__uint_as_float(v[j]), colscale[c], x[j]);  // exact 2^-e
+            x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
+            if (c < k) X[(int64_t)c * ldx + row] = x[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = 0.f;
+        }
+        if (FUSE) {  // padding columns c >= k hold x = 0: never counted
+          uint32_t cdm = 0;  // columns j with a candidate in this lane
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
+            cdm |= (uint32_t)(x[j] > 0.f && __float_as_uint(x[j]) >= s_pred[c0 + j]) << j;
+          }
+          uint32_t wm = __reduce_or_sync(kFull, cdm);
+          while (wm) {  // usually one column, one lane
+            const int j = __ffs(wm) - 1;
+            wm &= wm - 1;
+            const int c = c0 + j;
+            const bool cd = (cdm >> j) & 1;
+            const unsigned mc = __ballot_sync(kFull, cd);
+            int b0 = 0;
+            if (lane == 0) b0 = atomicAdd(&fz.pfill[c], __popc(mc));
+            b0 = __shfl_sync(kFull, b0, 0);
+            const int slot = b0 + __popc(mc & ((1u << lane) - 1u));
+            if (cd && slot < fz.pcap) {
+              float xv = 0.f;
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) xv = jj == j ? x[jj] : xv;
+              fz.pcand[(int64_t)c * fz.pcap + slot] = sel_key(xv, (uint32_t)(fz.row0 + row));
+            }
           }
         }
+      }
       }
       tc::fence_before();
       tc::mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
+    }
+    if (FUSE) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c0 = cbeg + 16 * q;
+        if (c0 >= cend) break;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n = warp_sum((int)((cnt2[q][j >> 1] >> (16 * (j & 1))) & 0xFFFFu));
+          if (lane == 0 && n) atomicAdd(&s_npos[c0 + j], n);
+        }
+      }
     }
   }
   tc::fence_before();
@@ -389,6 +460,9 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, 2 * acc_cols);
   }
+  if (FUSE)
+    for (int c = threadIdx.x; c < k; c += blockDim.x)
+      if (s_npos[c]) atomicAdd(&fz.npos[c], s_npos[c]);
 }
 
 }  // namespace esk

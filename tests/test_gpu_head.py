@@ -112,3 +112,35 @@ def test_large_k_paths_medium():
     assert s.info()["head_terms"] >= 64
     s.iterate(2)
     v_side_parity(s, g, cfg, cfg.k, cfg.t)
+
+
+@pytest.mark.parametrize("cfg_name,head", [("tiny", 128), ("medium", 512)])
+def test_fused_selection_in_head_epilogue(cfg_name, head, monkeypatch):
+    """V-side selection pass 1 fused into the head kernel's epilogue (opt-in
+    ESNMF_FUSED_SELECT=1; positives per column + candidates above the predicted
+    threshold; k_sel_pred_sort): the same factors, bit for bit, as the unfused
+    path, and the oracle's trajectory."""
+    cfg = synth.CONFIGS[cfg_name]
+    g = synth.generate(cfg)
+    monkeypatch.setenv("ESNMF_PRED_MIN_ROWS", "1")
+    a = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, head_terms=head)
+    b = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, head_terms=head)
+    iters = 8 if cfg_name == "tiny" else 4
+    monkeypatch.setenv("ESNMF_FUSED_SELECT", "1")   # read at every V side
+    a.iterate(iters)
+    monkeypatch.delenv("ESNMF_FUSED_SELECT")
+    b.iterate(iters)
+    for x, y in zip(a.get_V(), b.get_V()):
+        assert np.array_equal(x, y)
+    for x, y in zip(a.get_U(), b.get_U()):
+        assert np.array_equal(x, y)
+    ra, rb = a.records(), b.records()
+    assert [r["E"] for r in ra] == [r["E"] for r in rb]
+    assert [r["peak_v"] for r in ra] == [r["peak_v"] for r in rb]
+    if cfg_name == "tiny":
+        ref = oracle.run(g, cfg.k, cfg.t, iters, seed=cfg.seed)
+        for x, y in zip(ra, ref["records"]):
+            assert abs(x["E"] - y["E"]) <= 1e-3 * y["E"] and x["nnz_v"] == y["nnz_v"]
+    # and a late (fused) V side against the oracle directly
+    monkeypatch.setenv("ESNMF_FUSED_SELECT", "1")
+    v_side_parity(a, g, cfg, cfg.k, cfg.t)
