@@ -211,6 +211,14 @@ struct esnmf {
   double* normA2_dev = nullptr;
   esnmf_record* rec = nullptr;
   int64_t rec_cap = 0, nrec = 0;
+  int64_t* d_nrec = nullptr;   // device mirror of nrec: k_finalize_record's slot (graph replays)
+  // CUDA graphs of two steady-state iterations (one per parity of ucur), replayed
+  // by esnmf_iterate; any other state change drops them (graph_reset)
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  esnmf_record* grec[2] = {nullptr, nullptr};
+  int64_t glaunch[2] = {0, 0};
+  int steady = 0;              // eager iterations since the last state change
+  bool metrics_pending = false;  // the last iteration's record is not launched yet (flush_metrics)
   double normA2 = 0;
   bool gramU_valid = false;
   int64_t nlaunch = 0;  // kernels enqueued by this handle (esnmf_get_info)
@@ -239,6 +247,8 @@ struct esnmf {
   }
   ~esnmf() {
     if (stream) cudaStreamSynchronize(stream);
+    for (auto& g : gexec)
+      if (g) cudaGraphExecDestroy(g);
     for (auto& r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
@@ -1078,13 +1088,29 @@ void ensure_records(esnmf_t* h, int64_t need) {
   h->rec_cap = cap;
 }
 
+void flush_metrics(esnmf_t* h);
+
+// One iteration.  Its R / E record (a7, a8) is launched at the start of the
+// next iteration (or by esnmf_iterate's final flush): the same stream order as
+// launching it at the end, but every iteration is then a self-contained unit
+// for CUDA-graph capture (the record's aux-stream kernels are joined inside the
+// next V side).
 void iterate_one(esnmf_t* h) {
+  flush_metrics(h);
   if (h->ktot && h->seq_i == h->seq_iters) {
     if ((h->seq_b + 1) * h->seq_k2 >= h->ktot) fail(ESNMF_ESTATE, "sequential ALS: all k / k2 blocks are done");
     seq_next_block(h);
   }
   half_step(h, ESNMF_SIDE_V);
   half_step(h, ESNMF_SIDE_U);
+  h->metrics_pending = true;
+  if (h->ktot) ++h->seq_i;  // after seq_iters: the next iterate appends the block (seq_next_block)
+}
+
+// R, E and the record of the last iteration, and the Gram of its U
+void flush_metrics(esnmf_t* h) {
+  if (!h->metrics_pending) return;
+  h->metrics_pending = false;
   Phase ph(h, kMetrics);
   Factor& Un = h->U[h->ucur];
   Factor& Uo = h->U[1 - h->ucur];
@@ -1145,7 +1171,6 @@ void iterate_one(esnmf_t* h) {
   in.peak_v = h->side[ESNMF_SIDE_V].peak;
   in.normA2 = h->normA2;
   in.k = k;
-  in.it = (int)(h->nrec + 1);
   in.t_reduced = t_red;
   if (h->ktot) {  // whole-factor records: the converged columns' constant terms
     in.seqc = h->seqc;
@@ -1154,11 +1179,69 @@ void iterate_one(esnmf_t* h) {
     in.ktot = h->ktot;
     in.b0 = h->seq_b * h->seq_k2;
   }
-  ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec + h->nrec, h->scal);
+  ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec, h->d_nrec, h->scal);
   CKL("finalize_record");
   h->nrec += 1;
   if (overlap_m) h->aux_pending = true;
-  if (h->ktot) ++h->seq_i;  // after seq_iters: the next iterate appends the block (seq_next_block)
+}
+
+// ---- CUDA graphs of the steady-state iteration ----
+void graph_reset(esnmf_t* h) {
+  for (int p = 0; p < 2; ++p)
+    if (h->gexec[p]) {
+      cudaGraphExecDestroy(h->gexec[p]);
+      h->gexec[p] = nullptr;
+    }
+  h->steady = 0;
+}
+
+// two eager iterations since the last state change: every host-side launch
+// parameter (factor column bounds, selection paths, record slot base) is then
+// the same in every later iteration.  Single GPU, Alg. 2 (sequential ALS has
+// host-side block changes), profiling off.
+bool graph_ok(esnmf_t* h) {
+  return !getenv("ESNMF_NO_GRAPH") && h->world == 1 && !h->ktot && !h->prof_on && h->steady >= 2 &&
+         h->metrics_pending && !h->u_prefork && !h->aux_pending;
+}
+
+// one iteration (with the previous one's record) as one graph launch; one graph
+// per U slot parity (the iteration reads U[ucur] and writes U[1 - ucur]).  The
+// first call per parity captures it (running iterate_one, which advances the
+// host state exactly as a replay does) and launches it.
+void graph_run(esnmf_t* h) {
+  const int p = h->ucur;
+  if (h->gexec[p] && h->grec[p] != h->rec) {
+    cudaGraphExecDestroy(h->gexec[p]);
+    h->gexec[p] = nullptr;
+  }
+  if (!h->gexec[p]) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    const int64_t l0 = h->nlaunch;
+    try {
+      iterate_one(h);
+      if (h->aux_pending || h->u_prefork) fail(ESNMF_ECUDA, "graph capture: unjoined aux-stream work");
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(h->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    CK(cudaStreamEndCapture(h->stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&h->gexec[p], g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    h->grec[p] = h->rec;
+    h->glaunch[p] = h->nlaunch - l0;
+    CK(cudaGraphLaunch(h->gexec[p], h->stream));
+    return;
+  }
+  CK(cudaGraphLaunch(h->gexec[p], h->stream));
+  h->nlaunch += h->glaunch[p];
+  h->nrec += 1;       // the previous iteration's record (device slot counter d_nrec advanced by the graph)
+  h->ucur = 1 - h->ucur;
+  h->gramU_valid = false;
+  h->metrics_pending = true;
 }
 
 void sync_check(esnmf_t* h) {
@@ -1583,6 +1666,8 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->flags = h->alloc<int>(4);
     CK(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
     h->scal = h->alloc<double>(8);
+    h->d_nrec = h->alloc<int64_t>(1);
+    CK(cudaMemsetAsync(h->d_nrec, 0, sizeof(int64_t), h->stream));
     h->normA2_dev = h->alloc<double>(1);
     h->red_cap = 4LL * 2048 * 256 * 2;
     h->red = h->alloc<double>(h->red_cap);
@@ -1744,8 +1829,16 @@ esnmf_status esnmf_iterate(esnmf_t* h, int32_t iters) {
   return guarded([&] {
     set_device(h);
     ensure_records(h, h->nrec + iters);
-    for (int32_t i = 0; i < iters; ++i) iterate_one(h);
-    join_metrics(h);  // everything later on the caller's stream sees the records
+    for (int32_t i = 0; i < iters; ++i) {
+      if (graph_ok(h)) {
+        graph_run(h);
+      } else {
+        iterate_one(h);
+        ++h->steady;
+      }
+    }
+    flush_metrics(h);  // the last iteration's record
+    join_metrics(h);   // everything later on the caller's stream sees the records
   });
 }
 
@@ -1753,6 +1846,7 @@ esnmf_status esnmf_half_step(esnmf_t* h, int32_t side) {
   if (!h || (side != ESNMF_SIDE_V && side != ESNMF_SIDE_U)) { g_last_error = "esnmf_half_step: bad argument"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
+    graph_reset(h);
     half_step(h, side);
     join_metrics(h);
     if (h->u_prefork) join_from_aux(h, h->ev_ujoin);  // callers may read G_V / W next
@@ -1871,6 +1965,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
   if (nnz > f.cap) { g_last_error = "esnmf_set_factor: more entries than the factor capacity"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
+    graph_reset(h);
     CK(cudaStreamSynchronize(h->aux));
     if (side == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, f);
@@ -1899,6 +1994,7 @@ esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce
   if (h->world > 1) { g_last_error = "esnmf_truncate: single GPU only"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
+    graph_reset(h);
     CK(cudaStreamSynchronize(h->aux));
     Factor& f = side == ESNMF_SIDE_U ? h->U[h->ucur] : h->V;
     if (!f.has) fail(ESNMF_ESTATE, "esnmf_truncate: factor not set");

@@ -106,7 +106,6 @@ struct RecordInputs {
   const int64_t* peak_v;
   double normA2;
   int k;
-  int it;
   const double* t_reduced;  // if non-null: T already summed over ranks
   // sequential ALS (Alg. 3): the record covers U = [U_1 U_2 0], V = [V_1 V_2 0]; the
   // pipeline's factors are the block (k columns), U_1 / V_1 the frozen columns
@@ -118,7 +117,12 @@ struct RecordInputs {
 };
 
 // One block: R, E, counts -> rec.  Also stores (Rnum, Rden, T) into scal[0..2].
-__global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ rec, double* __restrict__ scal) {
+// the record goes to rec[*nrec] (then ++*nrec): the slot is found on the device,
+// so a captured iteration (CUDA graph) writes the next record on every replay
+__global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ recs, int64_t* __restrict__ nrec,
+                                  double* __restrict__ scal) {
+  const int64_t slot = *nrec;
+  esnmf_record* rec = recs + slot;
   __shared__ double sm[32];
   const double num = reduce_fixed(in.rnew, in.nrnew, 2, sm) + reduce_fixed(in.rold, in.nrold, 1, sm);
   const double den = reduce_fixed(in.rnew + 1, in.nrnew, 2, sm);
@@ -153,7 +157,7 @@ __global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ re
   dead_v = (int)block_sum((double)dead_v, sm);
   if (threadIdx.x == 0) {
     esnmf_record r;
-    r.it = in.it;
+    r.it = (int)(slot + 1);
     r.R = den + seq_N > 0 ? sqrt(num) / sqrt(den + seq_N) : -1.0;
     double e2 = in.normA2 - 2.0 * (T + seq_T) + S + seq_S;
     if (e2 < 0) e2 = 0;
@@ -167,6 +171,7 @@ __global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ re
     r.peak_u = in.peak_u ? *in.peak_u + fnnz_u : -1;
     r.peak_v = in.peak_v ? *in.peak_v + fnnz_v : -1;
     *rec = r;
+    *nrec = slot + 1;
     scal[0] = num;
     scal[1] = den;
     scal[2] = T;

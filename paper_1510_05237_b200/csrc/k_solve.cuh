@@ -27,6 +27,17 @@ inline bool sweep_packed(int k) { return (int64_t)k * k * 8 + k * 8 > 200 * 1024
 // owners of row p / column p overwrite them with a_pj / d, a_ip / d, -1 / d.
 // Row blocks a with ty + 32a >= k hold only padding and are skipped (warp-
 // uniform).  ~1 DFMA per element and pivot instead of a select chain.
+// 1/d to full fp64 precision: hardware approximation + two Newton steps (the
+// IEEE division's slow path is on the sweep's serial critical path, once per pivot)
+__device__ __forceinline__ double fast_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
 template <int JB>
 __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ G, int k, double rho,
                                                      double* __restrict__ W, double* __restrict__ eps_out,
@@ -66,7 +77,7 @@ __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ 
       bad = true;
       d = 1.0;
     }
-    const double inv = 1.0 / d;
+    const double inv = fast_rcp(d);
     double vj[JB], vi[JB];
 #pragma unroll
     for (int b = 0; b < JB; ++b) vj[b] = v[tx + 32 * b];
@@ -136,7 +147,7 @@ __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict
       if (threadIdx.x == 0) atomicExch(singular, 1);
       d = 1.0;
     }
-    const double inv = 1.0 / d;
+    const double inv = fast_rcp(d);
     double vj[JB];
 #pragma unroll
     for (int b = 0; b < JB; ++b) {
