@@ -5,7 +5,8 @@
 // A dense (n x k) x (k x k) product: 200k x 100 x 100 at Large.  The SIMT
 // register-tiled kernel (k_uside_finish_rt) was bound by instruction issue;
 // here per 128-row tile:
-//   * 4 producer warps (32 rows each, lanes across columns, 4 rows in flight)
+//   * 8 producer warps (16 rows each; lane = 4 consecutive columns, 16-byte
+//     loads, 8-byte shared-memory stores; 8 rows in flight)
 //     convert the tile's fixed-point rows, find each row's maximum, scale the
 //     row by an exact power of two into [2^14, 2^15), split it into fp16 hi/lo
 //     (22 significant bits) in the K-major shared-memory layout, and clear the
@@ -26,8 +27,10 @@
 namespace esk {
 
 constexpr int kUtcM = 128;
-constexpr int kUtcRows = 8;  // rows of a producer warp in flight
-constexpr int kUtcThreads = 128 + 32 + 128;  // producers, MMA, epilogue
+constexpr int kUtcRows = 8;                          // rows of a producer warp in flight
+constexpr int kUtcProdWarps = 8;                     // 16 rows of a tile each
+constexpr int kUtcProd = 32 * kUtcProdWarps;
+constexpr int kUtcThreads = kUtcProd + 32 + 128;     // producers, MMA, epilogue
 
 ESNMF_DEV int utc_exp(double x) {  // e with x 2^e in [2^14, 2^15), 0 for x == 0
   if (!(x > 0.0)) return 0;
@@ -88,21 +91,21 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
   if (threadIdx.x == 0) {
     tc::mbar_init(&wbar, 1);
     for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&afull[s], 128);
+      tc::mbar_init(&afull[s], kUtcProd);
       tc::mbar_init(&aempty[s], 1);
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], 128);
     }
     tc::fence_mbar_init();
   }
-  if (warp == 4) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
+  if (warp == kUtcProdWarps) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
   const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;  // fixed point -> value
 
-  if (warp < 4) {  // ---- producers: warp w converts rows 32w..32w+31 of a tile, lane-parallel per row ----
+  if (warp < kUtcProdWarps) {  // ---- producers: warp w converts rows 16w..16w+15 of a tile ----
     if (threadIdx.x == 0) {
       tc::mbar_arrive_expect_tx(&wbar, wbytes);
       tc::bulk_g2s(ws, wb, wbytes, &wbar);
@@ -110,40 +113,39 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t ahalf = (uint32_t)kUtcM * kk * 2;
+    const int c4 = 4 * lane;  // this lane's 4 consecutive columns
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       tc::mbar_wait(&aempty[stage], phase ^ 1);   // the MMAs of this stage's last tile are done
       tc::mbar_wait(&tempty[stage], phase ^ 1);   // ... and its epilogue (rscale[stage] is free)
       uint8_t* sa = as0 + stage * astride;
-      for (int rr = 0; rr < 32; rr += kUtcRows) {
+      for (int rr = 0; rr < kUtcM / kUtcProdWarps; rr += kUtcRows) {
         // kUtcRows rows in flight: all loads issued before any use (the clearing
         // stores come after, so they cannot serialise the loads)
-        unsigned long long qv[kUtcRows][4];
+        ulonglong2 qv[kUtcRows][2];
 #pragma unroll
         for (int q = 0; q < kUtcRows; ++q) {
-          const int64_t row = tile * kUtcM + warp * 32 + rr + q;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int c = lane + 32 * j;
-            qv[q][j] = (row < rows && c < kpad) ? __ldcs(Yq + row * kpad + c) : 0ull;
-          }
+          const int64_t row = tile * kUtcM + warp * (kUtcM / kUtcProdWarps) + rr + q;
+          const bool live = row < rows && c4 < kpad;  // kpad is a multiple of 4
+          const ulonglong2* src = reinterpret_cast<const ulonglong2*>(Yq + row * kpad + c4);
+          qv[q][0] = live ? __ldcs(src) : make_ulonglong2(0ull, 0ull);
+          qv[q][1] = live ? __ldcs(src + 1) : make_ulonglong2(0ull, 0ull);
         }
 #pragma unroll
         for (int q = 0; q < kUtcRows; ++q) {
-          const int64_t row = tile * kUtcM + warp * 32 + rr + q;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (qv[q][j]) Yq[row * kpad + lane + 32 * j] = 0ull;  // clear for the next half-step
+          const int64_t row = tile * kUtcM + warp * (kUtcM / kUtcProdWarps) + rr + q;
+          ulonglong2* dst = reinterpret_cast<ulonglong2*>(Yq + row * kpad + c4);
+          if (qv[q][0].x | qv[q][0].y) dst[0] = make_ulonglong2(0ull, 0ull);  // clear for the next half-step
+          if (qv[q][1].x | qv[q][1].y) dst[1] = make_ulonglong2(0ull, 0ull);
         }
 #pragma unroll
         for (int q = 0; q < kUtcRows; ++q) {
-          const int r = warp * 32 + rr + q;
+          const int r = warp * (kUtcM / kUtcProdWarps) + rr + q;
           float y[4];
-          float mx = 0.f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            y[j] = (float)((double)qv[q][j] * unit);
-            mx = fmaxf(mx, y[j]);
-          }
+          y[0] = (float)((double)qv[q][0].x * unit);
+          y[1] = (float)((double)qv[q][0].y * unit);
+          y[2] = (float)((double)qv[q][1].x * unit);
+          y[3] = (float)((double)qv[q][1].y * unit);
+          float mx = fmaxf(fmaxf(y[0], y[1]), fmaxf(y[2], y[3]));
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
           int e = 0;
@@ -153,17 +155,17 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
           }
           const float sc = __int_as_float((127 + e) << 23);  // 2^e, exact
           if (lane == 0) rscale[stage][r] = __int_as_float((127 - e) << 23);
+          if (c4 < kk) {  // 4 consecutive K elements of row r: 8 contiguous bytes in the core matrix
+            __half hi[4], lo[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int c = lane + 32 * j;
-            if (c < kk) {
+            for (int j = 0; j < 4; ++j) {
               const float v = y[j] * sc;
-              const __half hi = __float2half_rn(v);
-              const __half lo = __float2half_rn(v - __half2float(hi));
-              const uint32_t off = tc::kmajor_off16(r, c, kk);
-              *reinterpret_cast<__half*>(sa + off) = hi;
-              *reinterpret_cast<__half*>(sa + ahalf + off) = lo;
+              hi[j] = __float2half_rn(v);
+              lo[j] = __float2half_rn(v - __half2float(hi[j]));
             }
+            const uint32_t off = tc::kmajor_off16(r, c4, kk);
+            *reinterpret_cast<uint2*>(sa + off) = *reinterpret_cast<const uint2*>(hi);
+            *reinterpret_cast<uint2*>(sa + ahalf + off) = *reinterpret_cast<const uint2*>(lo);
           }
         }
       }
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
       tc::mbar_arrive(&afull[stage]);
       if (++stage == 2) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == 4) {
+  } else if (warp == kUtcProdWarps) {
     if (lane == 0) {  // ---- MMA issuer ----
       tc::mbar_wait(&wbar, 0);
       const uint32_t idesc = tc::make_idesc_f16(kUtcM, kn);
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
         if (++stage == 2) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp >= 5) {  // ---- epilogue (warps 5-8): thread = row ----
+  } else {  // ---- epilogue (4 warps, one per TMEM lane quadrant): thread = row ----
     const int lg = warp & 3;
     int stage = 0;
     uint32_t phase = 0;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kUtcProdWarps) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 2 * acc_cols);
   }
