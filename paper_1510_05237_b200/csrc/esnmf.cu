@@ -476,8 +476,11 @@ void init_u0(esnmf_t* h, const float* user_u0, bool on_dev);
 
 // block b is done (its seq_iters iterations, reading C12): append U_2, V_2 to
 // U_1, V_1, refresh the record constants, restart from U_2 = U_0
+void graph_reset(esnmf_t* h);
+
 void seq_next_block(esnmf_t* h) {
   join_metrics(h);
+  graph_reset(h);  // new block: b0, the frozen factors' bounds and U_0 change
   const int b0 = h->seq_b * h->seq_k2, k2 = h->k;
   const Factor& U2 = h->U[h->ucur];
   // record constants first (they need the old U_1, V_1): C_U, C_V into seqC / seqM
@@ -1197,11 +1200,11 @@ void graph_reset(esnmf_t* h) {
 
 // two eager iterations since the last state change: every host-side launch
 // parameter (factor column bounds, selection paths, record slot base) is then
-// the same in every later iteration.  Single GPU, Alg. 2 (sequential ALS has
-// host-side block changes), profiling off.
+// the same in every later iteration.  Single GPU, profiling off; in sequential
+// ALS within a block (a block change runs eagerly and drops the graphs).
 bool graph_ok(esnmf_t* h) {
-  return !getenv("ESNMF_NO_GRAPH") && h->world == 1 && !h->ktot && !h->prof_on && h->steady >= 2 &&
-         h->metrics_pending && !h->u_prefork && !h->aux_pending;
+  return !getenv("ESNMF_NO_GRAPH") && h->world == 1 && !h->prof_on && h->steady >= 2 && h->metrics_pending &&
+         !h->u_prefork && !h->aux_pending && !(h->ktot && h->seq_i >= h->seq_iters);
 }
 
 // one iteration (with the previous one's record) as one graph launch; one graph
@@ -1242,6 +1245,7 @@ void graph_run(esnmf_t* h) {
   h->ucur = 1 - h->ucur;
   h->gramU_valid = false;
   h->metrics_pending = true;
+  if (h->ktot) ++h->seq_i;
 }
 
 void sync_check(esnmf_t* h) {

@@ -56,3 +56,21 @@ def test_graph_state_changes_between_calls():
     s.half_step(ESNMF_SIDE_U)
     s.iterate(4)
     assert len(s.records()) == 17
+
+
+def test_graph_replay_sequential_blocks(monkeypatch):
+    """Sequential ALS (Alg. 3) replays graphs inside a block; block changes run
+    eagerly: the same records and factors as without graphs."""
+    cfg = synth.CONFIGS["tiny"]
+    g = synth.generate(cfg)
+    a = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, seq_k2=2, seq_iters=7)
+    monkeypatch.setenv("ESNMF_NO_GRAPH", "1")
+    b = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, seq_k2=2, seq_iters=7)
+    b.iterate(35)
+    monkeypatch.delenv("ESNMF_NO_GRAPH")
+    a.iterate(12)
+    a.iterate(23)
+    for x, y in zip(a.records(), b.records()):
+        assert x == y
+    for x, y in zip(a.get_U(), b.get_U()):
+        assert np.array_equal(x, y)
