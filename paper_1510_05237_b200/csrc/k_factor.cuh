@@ -195,20 +195,28 @@ __global__ void k_scatter_dense(const int64_t* __restrict__ colptr, const int32_
 
 // ---- Gram matrix G = F^T F in fp64 ("U^T U", "V^T V") -----------
 // G[a][b] = sum over the entries (i, u) of column a of u * F[i][b], with F[i]
-// read from the dense row view.  grid = (k columns a, S segments); segment
-// partials are summed in a fixed order by k_gram_reduce (deterministic).
-__global__ void __launch_bounds__(256) k_gram_partial(const int64_t* __restrict__ colptr,
+// read from the dense row view.  grid = (k columns a, S segments); a block is
+// ng groups of gb >= k threads (thread b of a group owns G[a][b]), the groups
+// splitting the segment's entries (long columns -- whole-factor enforcement
+// can put 10^5 entries in one -- are otherwise one long dependent loop);
+// group sums and segment partials are added in a fixed order (k_gram_reduce):
+// deterministic.
+__global__ void __launch_bounds__(512) k_gram_partial(const int64_t* __restrict__ colptr,
                                                       const int32_t* __restrict__ row,
                                                       const float* __restrict__ val,
                                                       const int32_t* __restrict__ rowmap,
                                                       const float* __restrict__ dense, int kpad, int k,
-                                                      int64_t seglen, double* __restrict__ partial) {
+                                                      int64_t seglen, double* __restrict__ partial, int gb) {
+  __shared__ double red[512];
   const int a = blockIdx.x, s = blockIdx.y;
+  const int ng = blockDim.x / gb, g = threadIdx.x / gb, b = threadIdx.x - g * gb;
   const int64_t cb = colptr[a], ce = colptr[a + 1];
-  const int64_t b0 = cb + (int64_t)s * seglen;
-  const int64_t b1 = min(ce, b0 + seglen);
-  for (int b = threadIdx.x; b < k; b += blockDim.x) {
-    double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  const int64_t s0 = cb + (int64_t)s * seglen;
+  const int64_t s1 = min(ce, s0 + seglen);
+  const int64_t sub = (max(s1 - s0, (int64_t)0) + ng - 1) / ng;
+  const int64_t b0 = s0 + g * sub, b1 = min(s1, b0 + sub);
+  double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  if (b < k) {
     int64_t e = b0;
     for (; e + 4 <= b1; e += 4) {
       float u0 = val[e], u1 = val[e + 1], u2 = val[e + 2], u3 = val[e + 3];
@@ -219,7 +227,13 @@ __global__ void __launch_bounds__(256) k_gram_partial(const int64_t* __restrict_
       acc3 += (double)u3 * (double)dense[(int64_t)r3 * kpad + b];
     }
     for (; e < b1; ++e) acc0 += (double)val[e] * (double)dense[(int64_t)rowmap[row[e]] * kpad + b];
-    partial[((int64_t)s * k + a) * k + b] = (acc0 + acc1) + (acc2 + acc3);
+  }
+  red[threadIdx.x] = (acc0 + acc1) + (acc2 + acc3);
+  __syncthreads();
+  if (g == 0 && b < k) {
+    double t = red[b];
+    for (int q = 1; q < ng; ++q) t += red[q * gb + b];
+    partial[((int64_t)s * k + a) * k + b] = t;
   }
 }
 
