@@ -60,6 +60,7 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr int64_t kSplitLen = 4096;   // max stored entries per SpMM work item (A rows)
 constexpr int kMaxGramSeg = 64;
+constexpr int64_t kSelScanMax = 4096;  // flat selection: segment-scan blocks (k * rows < 2^31 needs < 1024)
 
 struct DevCsr {
   int64_t rows = 0, cols = 0, nnz = 0;
@@ -102,6 +103,7 @@ struct Side {
   int64_t* coltot = nullptr;
   uint64_t* kthr = nullptr;
   SelLvl* lvl = nullptr;          // [k] multi-block radix fallback state
+  int64_t* scanbuf = nullptr;     // [kSelScanMax] block sums of the flat view's segment scan
   uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
   int64_t above_t = -1;           // its t capacity per column
   int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
@@ -798,18 +800,28 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
     ++h->nlaunch; k_sel_lvl_count<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.lvl, sd.chunk_cnt, nseg,
                                                             sd.kthr);
   }
-  ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.coltot);
+  if (kc == 1 && nseg > 8 * kScanBlock) {  // one long (flat whole-factor) column: multi-block scan
+    const int64_t nb = ceil_div(nseg, kScanBlock);
+    if (nb > kSelScanMax) fail(ESNMF_EINVAL, "selection: flat view too long");
+    h->nlaunch += 3;
+    k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.scanbuf);
+    k_scan_small<<<1, 1024, 0, h->stream>>>(sd.scanbuf, nb, sd.coltot);
+    k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.scanbuf);
+  } else {
+    ++h->nlaunch; k_sel_scan_cols<<<k, 1024, 0, h->stream>>>(sd.chunk_cnt, nseg, sd.coltot);
+  }
   ++h->nlaunch; k_sel_colptr<<<1, 256, 0, h->stream>>>(sd.coltot, k, colptr_out);
   ++h->nlaunch; k_sel_write<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.kthr, colptr_out,
                                         sd.chunk_cnt, nseg, row_out, val_out);
   CKL("select");
 }
 
-// flat selection indices (c * ldx + row, ascending) -> rows in place + per-column colptr
-__global__ void k_whole_split(int32_t* __restrict__ idx, const int64_t* __restrict__ flat_colptr, int64_t ldx, int k,
-                              int64_t* __restrict__ colptr) {
+// flat selection indices (c * ldx + row, ascending) -> per-column colptr (one
+// binary search per column) ...
+__global__ void k_whole_colptr(const int32_t* __restrict__ idx, const int64_t* __restrict__ flat_colptr,
+                               int64_t ldx, int k, int64_t* __restrict__ colptr) {
   const int64_t nnz = flat_colptr[1];
-  for (int c = threadIdx.x; c <= k; c += blockDim.x) {  // first entry of column c (binary search)
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) {
     int64_t lo = 0, hi = nnz;
     const int64_t key = (int64_t)c * ldx;
     while (lo < hi) {
@@ -818,8 +830,13 @@ __global__ void k_whole_split(int32_t* __restrict__ idx, const int64_t* __restri
     }
     colptr[c] = lo;
   }
-  __syncthreads();
-  for (int64_t q = threadIdx.x; q < nnz; q += blockDim.x) idx[q] = (int32_t)((int64_t)(uint32_t)idx[q] % ldx);
+}
+
+// ... and rows in place (after k_whole_colptr has read the flat indices)
+__global__ void k_whole_rows(int32_t* __restrict__ idx, const int64_t* __restrict__ flat_colptr, int64_t ldx) {
+  const int64_t nnz = flat_colptr[1];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
+    idx[q] = (int32_t)((uint32_t)idx[q] % (uint32_t)ldx);  // k * ldx < 2^31: 32-bit division
 }
 
 // V side after a fused head epilogue: select from the candidates, histogram
@@ -867,8 +884,9 @@ void select_topt(esnmf_t* h, int s, Factor& out) {
   // Alg. 2 as printed: one selection over the flat k x ldx buffer (padding rows are 0)
   select_core(h, sd, sd.X, (int64_t)h->k * sd.ldx, (int64_t)h->k * sd.ldx, 1, 0, t, false, h->wcolptr, out.row,
               out.val, sd.peak);
-  ++h->nlaunch;
-  k_whole_split<<<1, 1024, 0, h->stream>>>(out.row, h->wcolptr, sd.ldx, h->k, out.colptr);
+  h->nlaunch += 2;
+  k_whole_colptr<<<1, 256, 0, h->stream>>>(out.row, h->wcolptr, sd.ldx, h->k, out.colptr);
+  k_whole_rows<<<grid_for(out.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(out.row, h->wcolptr, sd.ldx);
   CKL("whole_split");
 }
 
@@ -1303,6 +1321,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.coltot = h->alloc<int64_t>(k);
   sd.kthr = h->alloc<uint64_t>(k);
   sd.lvl = h->alloc<SelLvl>(k);
+  sd.scanbuf = h->alloc<int64_t>(kSelScanMax);
   const int64_t ts = h->tside[&sd == &h->side[ESNMF_SIDE_V] ? 0 : 1];
   if (ts >= 0 && ts <= kSelFastT) {
     sd.above = h->alloc<uint64_t>((int64_t)k * std::max<int64_t>(ts, 1));
@@ -2015,8 +2034,10 @@ esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce
     } else {
       select_core(h, sd, sd.X, (int64_t)k * sd.ldx, (int64_t)k * sd.ldx, 1, 0, t, false, h->wcolptr, f.row, f.val,
                   nullptr);
-      ++h->nlaunch;
-      k_whole_split<<<1, 1024, 0, h->stream>>>(f.row, h->wcolptr, sd.ldx, k, f.colptr);
+      h->nlaunch += 2;
+      k_whole_colptr<<<1, 256, 0, h->stream>>>(f.row, h->wcolptr, sd.ldx, k, f.colptr);
+      k_whole_rows<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(f.row, h->wcolptr,
+                                                                                        sd.ldx);
     }
     factor_build_rows(h, f, std::min<int64_t>(f.rows, std::max<int64_t>(t, 1)));
     if (side == ESNMF_SIDE_V) vrows_build(h);

@@ -347,13 +347,20 @@ __global__ void __launch_bounds__(256) k_sel_lvl_count(const float* __restrict__
   const float* col = X + (int64_t)c * ldx;
   int32_t cnt[kSelSegs];
 #pragma unroll
-  for (int q = 0; q < kSelSegs; ++q) {
-    cnt[q] = 0;
-    for (int64_t j = r0 + (int64_t)q * kSelSeg + threadIdx.x; j < min(r1, r0 + (int64_t)(q + 1) * kSelSeg);
-         j += blockDim.x) {
-      const float x = col[j];
-      cnt[q] += x > 0.f && sel_digit(x) == digit && sel_key(x, (uint32_t)(row0 + j)) <= kstar;
+  for (int q = 0; q < kSelSegs; ++q) {  // rows r0 + 1024 q + 4 t .. + 3: segment q
+    const int64_t j = r0 + (int64_t)q * kSelSeg + 4 * threadIdx.x;
+    float x[4];
+    if (j + 3 < r1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(col + j));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + u < r1 ? col[j + u] : 0.f;
     }
+    cnt[q] = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      cnt[q] += x[u] > 0.f && sel_digit(x[u]) == digit && sel_key(x[u], (uint32_t)(row0 + j + u)) <= kstar;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -436,10 +443,16 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
     }
   };
   int64_t off = colptr[c] + chunk_off[(int64_t)c * nchunks + seg];
-  for (int64_t base = r0; base < r1; base += 128) {
-    float x[4];
-    unsigned mk;
-    load4(base + 4 * lane, x, mk);
+  // all eight 128-row steps of the segment loaded before any use
+  float xs[kSelSeg / 128][4];
+  unsigned mks[kSelSeg / 128];
+#pragma unroll
+  for (int i = 0; i < kSelSeg / 128; ++i) load4(r0 + 128 * i + 4 * lane, xs[i], mks[i]);
+#pragma unroll
+  for (int i = 0; i < kSelSeg / 128; ++i) {
+    const int64_t base = r0 + 128 * i;
+    const float* x = xs[i];
+    const unsigned mk = mks[i];
     const int mine = __popc(mk);
     int inc = mine;
 #pragma unroll

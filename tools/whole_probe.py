@@ -1,0 +1,9 @@
+import sys, os
+sys.path.insert(0, "/root/repo")
+import torch, synth
+from paper_1510_05237_b200 import ESNMF
+cfg = synth.CONFIGS["large"]
+g = synth.generate_device(cfg, device="cuda"); torch.cuda.synchronize()
+s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, whole=True, t_u=cfg.k*cfg.t, t_v=cfg.k*cfg.t)
+s.iterate(4)
+torch.cuda.synchronize()
