@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -66,6 +67,8 @@ struct DevCsr {
   int64_t rows = 0, cols = 0, nnz = 0;
   int64_t* ptr = nullptr;
   int2* ent = nullptr;
+  RowChunk* chunks = nullptr;  // balanced work units (create-time passes)
+  int64_t nchunks = 0;
 };
 
 struct Factor {
@@ -1384,6 +1387,18 @@ void select_merge(esnmf_t* h, int s, Factor& out) {
 }
 
 // upload (or copy) a CSR and pack it; returns device CSR with local rows [r0, r1)
+// balanced create-time work units over a CSR's rows (host row pointers, local)
+RowChunk* make_chunks(esnmf_t* h, const std::vector<int64_t>& lp, int64_t rows, int64_t* nch_out) {
+  std::vector<RowChunk> v;
+  v.reserve(rows + (lp[rows] / kChunkLen) + 1);
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t b = lp[r]; b < lp[r + 1]; b += kChunkLen) v.push_back(RowChunk{b, std::min(lp[r + 1], b + kChunkLen), (int32_t)r, 0});
+  *nch_out = (int64_t)v.size();
+  RowChunk* d = h->alloc<RowChunk>(std::max<int64_t>(1, (int64_t)v.size()));
+  if (!v.empty()) CK(cudaMemcpy(d, v.data(), sizeof(RowChunk) * v.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
 DevCsr upload_csr(esnmf_t* h, int64_t rows_total, int64_t cols, const int64_t* ptr, const int32_t* col,
                   const float* val, bool on_dev, int64_t r0, int64_t r1, std::vector<int64_t>* host_ptr_local) {
   DevCsr c;
@@ -1427,7 +1442,14 @@ DevCsr upload_csr(esnmf_t* h, int64_t rows_total, int64_t cols, const int64_t* p
       h->bytes -= (int64_t)(sizeof(int32_t) + sizeof(float)) * c.nnz;
     }
   }
-  ++h->nlaunch; k_validate<<<grid_for(c.rows, 8, 148 * 64), 256, 0, h->stream>>>(c.ptr, c.ent, c.rows, cols, c.nnz, h->flags + 1);
+  {
+    int64_t nch = 0;
+    c.chunks = make_chunks(h, lp, c.rows, &nch);
+    c.nchunks = nch;
+    ++h->nlaunch;
+    k_validate_chunks<<<grid_for(nch, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(c.chunks, nch, c.ptr, c.ent,
+                                                                                         cols, h->flags + 1);
+  }
   CKL("validate");
   if (host_ptr_local) *host_ptr_local = std::move(lp);
   return c;
@@ -1447,14 +1469,22 @@ DevCsr build_at(esnmf_t* h, const DevCsr& A, int64_t m, int64_t m0, int64_t m1) 
   launch_scan_inplace(h, T.ptr, m + 1, tot);
   int64_t* cursor = h->alloc<int64_t>(m + 1);
   CK(cudaMemcpyAsync(cursor, T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToDevice, h->stream));
-  ++h->nlaunch; k_transpose_scatter<<<grid_for(A.rows, 8, 148 * 64), 256, 0, h->stream>>>(A.ptr, A.ent, A.rows, cursor, T.ent);
-  ++h->nlaunch; k_sort_rows<<<grid_for(m, 1, 148 * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent, nullptr, 0);
+  if (!A.chunks) fail(ESNMF_EINVAL, "build_at: operator without work units");
+  ++h->nlaunch;
+  k_transpose_chunks<<<grid_for(A.nchunks, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(
+      A.chunks, A.nchunks, A.ent, reinterpret_cast<unsigned long long*>(cursor), T.ent);
+  ++h->nlaunch;
+  k_sort_rows_rank<<<grid_for(m, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent);
   // long rows (> kRowSortCap entries) in a global scratch, one block
   std::vector<int64_t> hp(m + 1);
   CK(cudaMemcpyAsync(hp.data(), T.ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   int64_t maxlen = 0;
   for (int64_t j = 0; j < m; ++j) maxlen = std::max(maxlen, hp[j + 1] - hp[j]);
+  if (maxlen > kRankRow) {  // rows the rank sort skipped: block bitonic sort (shared memory or scratch)
+    ++h->nlaunch;
+    k_sort_rows<<<grid_for(m, 1, 148 * 32), 256, 0, h->stream>>>(T.ptr, m, T.ent, nullptr, 0);
+  }
   if (maxlen > kRowSortCap) {
     int64_t np = 1;
     while (np < maxlen) np <<= 1;
@@ -1599,8 +1629,22 @@ esnmf_status esnmf_partition_rows(int64_t rows, const int64_t* row_ptr, int32_t 
   return ESNMF_OK;
 }
 
+// ESNMF_CREATE_TIMING=1: host wall time of each create stage (synchronised), to stderr
+struct CreateTimer {
+  bool on = getenv("ESNMF_CREATE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(esnmf_t* h, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(h->stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "esnmf_create %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_t t, const int64_t* row_ptr,
                           const int32_t* col_idx, const float* val, const esnmf_options* opt) {
+  CreateTimer ct;
   if (out) *out = nullptr;
   esnmf_options o;
   esnmf_options_init(&o);
@@ -1695,6 +1739,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->normA2_dev = h->alloc<double>(1);
     h->red_cap = 4LL * 2048 * 256 * 2;
     h->red = h->alloc<double>(h->red_cap);
+    ct.mark(h.get(), "setup");
     // ---- row shards: terms nnz-balanced, documents equal ----
     std::vector<int64_t> hptr(n + 1);
     CK(cudaMemcpy(hptr.data(), row_ptr, sizeof(int64_t) * (n + 1),
@@ -1738,6 +1783,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       if (h->world > 1 && h->comm.allreduce_sum_f64(h->comm.ctx, h->normA2_dev, 1, h->stream) != 0)
         fail(ESNMF_ECOMM, "allreduce(||A||^2) failed");
     }
+    ct.mark(h.get(), "upload A + norm");
     // ---- A^T (V side operator, this rank's document rows) ----
     Side& sv = h->side[ESNMF_SIDE_V];
     sv.row0 = m0;
@@ -1759,9 +1805,12 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CKL("norm_cols");
     }
     if (h->world == 1 && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
+    ct.mark(h.get(), "A^T");
     build_items(h.get(), su, aptr);
     side_alloc(h.get(), sv);
+    ct.mark(h.get(), "items + V alloc");
     head_setup(h.get(), hptr, o.head_terms);
+    ct.mark(h.get(), "head setup");
     side_alloc(h.get(), su);
     // ---- factors ----
     const int64_t capU = n * (int64_t)kb;
@@ -1827,7 +1876,9 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     }
     h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * kb * kb);
     if (kb > 224) h->sweep_scratch = h->alloc<double>((int64_t)kb * (kb + 1) / 2);
+    ct.mark(h.get(), "factors + buffers");
     init_u0(h.get(), o.U0, on_dev);
+    ct.mark(h.get(), "U0");
     CK(cudaStreamSynchronize(h->stream));
     int fl[4];
     CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) k_sort_rows(const int64_t* __restrict__ p
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const int64_t s = ptr[r], e = ptr[r + 1];
     const int64_t len = e - s;
-    if (len <= 1) continue;
+    if (len <= 1 || len <= 512) continue;  // rows <= kRankRow: k_sort_rows_rank
     const bool fits = len <= kRowSortCap;
     if (fits == (bool)long_rows_only) continue;
     int64_t np = 1;
@@ -156,6 +156,95 @@ __global__ void k_norm_cols(int2* __restrict__ ent, int64_t nnz, const float* __
     int2 en = ent[e];
     en.y = __float_as_int(__fdiv_rn(__int_as_float(en.y), rowlen[en.x]));
     ent[e] = en;
+  }
+}
+
+}  // namespace esk
+
+namespace esk {
+
+// ---- create-time CSR work in balanced units -----------------------------------
+// A term row of A can hold half a million entries (Zipf head); one warp per row
+// left the create-time passes waiting on the longest rows.  A RowChunk is <=
+// kChunkLen consecutive entries of one row; one warp per chunk.
+constexpr int64_t kChunkLen = 1024;
+struct RowChunk {
+  int64_t begin, end;
+  int32_t row, pad_;
+};
+
+// CSR checks (row_ptr is checked on the host): column in range and strictly
+// increasing within the row, value finite and >= 0
+__global__ void k_validate_chunks(const RowChunk* __restrict__ ch, int64_t nch, const int64_t* __restrict__ ptr,
+                                  const int2* __restrict__ ent, int64_t ncols, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nch; u += nwarps) {
+    const RowChunk c = ch[u];
+    const int64_t rs = ptr[c.row];
+    int flags = 0;
+    for (int64_t q = c.begin + lane; q < c.end; q += 32) {
+      const int2 en = ent[q];
+      if (en.x < 0 || en.x >= ncols) flags |= 2;
+      if (q > rs && ent[q - 1].x >= en.x) flags |= 4;
+      const float v = __int_as_float(en.y);
+      if (!(v >= 0.f) || !isfinite(v)) flags |= 8;
+    }
+    flags = __reduce_or_sync(kFull, flags);
+    if (lane == 0 && flags) atomicOr(bad, flags);
+  }
+}
+
+// transpose scatter: entry (row r, col j, v) -> (r, v) at an atomic slot of row j
+__global__ void k_transpose_chunks(const RowChunk* __restrict__ ch, int64_t nch, const int2* __restrict__ ent,
+                                   unsigned long long* __restrict__ cursor, int2* __restrict__ tent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nch; u += nwarps) {
+    const RowChunk c = ch[u];
+    for (int64_t q = c.begin + lane; q < c.end; q += 32) {
+      const int2 en = ent[q];
+      const int64_t p = (int64_t)atomicAdd(&cursor[en.x], 1ULL);
+      tent[p] = make_int2(c.row, en.y);
+    }
+  }
+}
+
+// order every row of <= kRankRow entries by column: one warp per row, the row
+// staged in shared memory, each entry's slot = the number of smaller columns
+// (columns are distinct within a row); longer rows: k_sort_rows(long_rows_only)
+constexpr int kRankRow = 512;
+__global__ void __launch_bounds__(256) k_sort_rows_rank(const int64_t* __restrict__ ptr, int64_t rows,
+                                                        int2* __restrict__ ent) {
+  __shared__ int2 buf[8][kRankRow];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int2* b = buf[w];
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    const int64_t s = ptr[r];
+    const int len = (int)(ptr[r + 1] - s);
+    if (len <= 1 || len > kRankRow) continue;  // warp-uniform
+    for (int i = lane; i < len; i += 32) b[i] = ent[s + i];
+    __syncwarp();
+    constexpr int kPer = kRankRow / 32;
+    int mine[kPer], rank[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = lane + 32 * q;
+      mine[q] = i < len ? b[i].x : 0x7FFFFFFF;
+      rank[q] = 0;
+    }
+    for (int j = 0; j < len; ++j) {
+      const int cj = b[j].x;  // broadcast
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) rank[q] += cj < mine[q];
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = lane + 32 * q;
+      if (i < len) ent[s + rank[q]] = b[i];
+    }
+    __syncwarp();
   }
 }
 
