@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const bool cd = x[u] > 0.f && f2u(x[u]) >= pb;
-        const unsigned m = __ballot_sync(kFull, cd);
+        const unsigned m = __ballot_sync(kFull, cd);  // (one vote; rare hits)
         if (m) {
           int b0 = 0;
           if (lane == 0) b0 = atomicAdd(&pfill[c], __popc(m));
@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ 
       const int dg = pos ? sel_digit(x[u]) : -1;
       const bool up = pos && dg > s.digit;
       const bool eq = pos && dg == s.digit;
+      if (!__any_sync(kFull, up || eq)) continue;  // most entries sit below the threshold bucket
       const unsigned mu = __ballot_sync(kFull, up), me = __ballot_sync(kFull, eq);
       int bu = 0, be = 0;
       if (lane == 0) {
