@@ -789,19 +789,29 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
     CKL("select2");
     return;
   }
+  // candidate list per column: kSelCap keys (sorted on chip); a flat whole-factor
+  // view (one column) gets the whole buffer, so its bucket usually fits and the
+  // radix levels run over the list instead of over X
+  const int ccap = kc == 1 ? h->k * kSelCap : kSelCap;
   ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
-                                          sd.chunk_cnt, nseg);
+                                          sd.chunk_cnt, nseg, ccap);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
-                                          sd.chunk_cnt, nseg, sd.kthr);
-  {  // columns whose threshold bucket overflowed kSelCap: grid-wide radix levels
+                                          sd.chunk_cnt, nseg, sd.kthr, ccap);
+  {  // columns whose threshold bucket overflowed kSelCap: exact radix levels
     CK(cudaMemsetAsync(sd.hist, 0, sizeof(uint32_t) * k * kNumBins, h->stream));
-    ++h->nlaunch; k_sel_lvl_init<<<1, 256, 0, h->stream>>>(sd.sel, sd.cand_fill, k, sd.lvl);
+    ++h->nlaunch; k_sel_lvl_init<<<1, 256, 0, h->stream>>>(sd.sel, sd.cand_fill, k, sd.lvl, ccap);
     const int shifts[5] = {39, 32, 20, 8, 0}, widths[5] = {12, 7, 12, 12, 8};
+    const dim3 gc((unsigned)ceil_div(ccap, 2048), k);
     for (int lv = 0; lv < 5; ++lv) {
-      h->nlaunch += 2;
+      h->nlaunch += 3;
       k_sel_lvl_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.lvl, shifts[lv], widths[lv], sd.hist);
+      k_sel_lvl_hist_cand<<<gc, 256, 0, h->stream>>>(sd.cand, sd.cand_fill, ccap, sd.lvl, shifts[lv], widths[lv],
+                                                     sd.hist);
       k_sel_lvl_pick<<<k, 256, 0, h->stream>>>(sd.hist, shifts[lv], widths[lv], lv == 4, sd.lvl);
     }
+    ++h->nlaunch;
+    k_sel_cand_count<<<gc, 256, 0, h->stream>>>(sd.cand, sd.cand_fill, ccap, sd.lvl, row0, sd.chunk_cnt, nseg,
+                                               sd.kthr);
     ++h->nlaunch; k_sel_lvl_count<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.lvl, sd.chunk_cnt, nseg,
                                                             sd.kthr);
   }

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(1024) k_sel_threshold(const uint32_t* __restri
 __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X, int64_t ldx, int64_t rows,
                                                      int64_t row0, const ColSel* __restrict__ sel,
                                                      uint64_t* __restrict__ cand, int32_t* __restrict__ cand_fill,
-                                                     int64_t* __restrict__ chunk_cnt, int64_t nseg) {
+                                                     int64_t* __restrict__ chunk_cnt, int64_t nseg, int ccap) {
   // counts of strictly-above entries per kSelSeg-row segment: with 256 threads x
   // float4 one loop iteration covers exactly one segment (1024 rows)
   __shared__ int32_t sm[8][kSelSegs];
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X
         if (lane == leader) b0 = atomicAdd(&cand_fill[c], __popc(m));
         b0 = __shfl_sync(m, b0, leader);
         const int slot = b0 + __popc(m & ((1u << lane) - 1u));
-        if (slot < kSelCap) cand[(int64_t)c * kSelCap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
+        if (slot < ccap) cand[(int64_t)c * ccap + slot] = sel_key(x[u], (uint32_t)(row0 + j + u));
       }
     }
     cnt[q] = above;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
                                                      const uint64_t* __restrict__ cand,
                                                      const int32_t* __restrict__ cand_fill,
                                                      int64_t* __restrict__ chunk_cnt, int64_t nchunks,
-                                                     uint64_t* __restrict__ kthr) {
+                                                     uint64_t* __restrict__ kthr, int ccap) {
   __shared__ uint64_t keys[kSelCap];           // sort buffer (common path)
   uint32_t* h = reinterpret_cast<uint32_t*>(keys);  // histogram (fallback path)
   __shared__ int64_t sm[33];
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
   if (nc <= kSelCap) {
     int np = 1;
     while (np < nc) np <<= 1;
-    for (int i = threadIdx.x; i < np; i += blockDim.x) keys[i] = i < nc ? cand[(int64_t)c * kSelCap + i] : ~0ULL;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) keys[i] = i < nc ? cand[(int64_t)c * ccap + i] : ~0ULL;
     __syncthreads();
     bitonic_sort_smem(keys, np);
     kstar = keys[s.r - 1];
@@ -244,14 +244,17 @@ struct SelLvl {
   uint64_t prefix, mask;
   int64_t r;
   int32_t active, done;
+  int32_t incand, pad_;  // 1: the whole bucket is in the candidate list (levels over it, not over X)
 };
 
 __global__ void k_sel_lvl_init(const ColSel* __restrict__ sel, const int32_t* __restrict__ cand_fill, int k,
-                               SelLvl* __restrict__ lvl) {
+                               SelLvl* __restrict__ lvl, int ccap) {
   for (int c = threadIdx.x; c < k; c += blockDim.x) {
     const ColSel s = sel[c];
     SelLvl L;
     L.active = s.r > 0 && cand_fill[c] > kSelCap;
+    L.incand = L.active && cand_fill[c] <= ccap;
+    L.pad_ = 0;
     L.done = !L.active;
     L.prefix = L.active ? ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51 : 0;
     L.mask = 0xFFFULL << 51;
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(256) k_sel_lvl_hist(const float* __restrict__ 
   __shared__ uint32_t h[kNumBins];
   const int c = blockIdx.y;
   const SelLvl L = lvl[c];
-  if (L.done) return;
+  if (L.done || L.incand) return;
   const int digit = sel[c].digit;
   const int nb = 1 << wd;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(256) k_sel_lvl_count(const float* __restrict__
   __shared__ int32_t sm[8][kSelSegs];
   const int c = blockIdx.y;
   const SelLvl L = lvl[c];
-  if (!L.active) return;
+  if (!L.active || L.incand) return;
   const uint64_t kstar = L.prefix;
   if (blockIdx.x == 0 && threadIdx.x == 0)
     kthr[c] = ((uint64_t)(0x7FFFFFFFu - (uint32_t)(kstar >> 32)) << 32) | (kstar & 0xFFFFFFFFULL);
@@ -374,6 +377,56 @@ __global__ void __launch_bounds__(256) k_sel_lvl_count(const float* __restrict__
     for (int w = 0; w < 8; ++w) tot += sm[w][threadIdx.x];
     const int64_t seg = (int64_t)blockIdx.x * kSelSegs + threadIdx.x;
     if (tot && seg < nseg) atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nseg + seg], (unsigned long long)tot);
+  }
+}
+
+// the same levels over a column's candidate list (every bucket-D key of the
+// column, when it fit the list: incand), 8 keys per thread
+__global__ void __launch_bounds__(256) k_sel_lvl_hist_cand(const uint64_t* __restrict__ cand,
+                                                           const int32_t* __restrict__ cand_fill, int ccap,
+                                                           const SelLvl* __restrict__ lvl, int sh, int wd,
+                                                           uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kNumBins];
+  const int c = blockIdx.y;
+  const SelLvl L = lvl[c];
+  if (L.done || !L.incand) return;
+  const int nc = cand_fill[c];
+  const int64_t b0 = (int64_t)blockIdx.x * 2048;
+  if (b0 >= nc) return;
+  const int nb = 1 << wd;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const uint64_t* cc = cand + (int64_t)c * ccap;
+  for (int64_t i = b0 + threadIdx.x; i < min((int64_t)nc, b0 + 2048); i += blockDim.x) {
+    const uint64_t key = cc[i];
+    if ((key & L.mask) == L.prefix) atomicAdd(&h[(key >> sh) & (nb - 1)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (h[b]) atomicAdd(&ghist[(int64_t)c * kNumBins + b], h[b]);
+}
+
+// per-segment counts of the kept candidates (key <= K*) and kthr, incand columns
+__global__ void __launch_bounds__(256) k_sel_cand_count(const uint64_t* __restrict__ cand,
+                                                        const int32_t* __restrict__ cand_fill, int ccap,
+                                                        const SelLvl* __restrict__ lvl, int64_t row0,
+                                                        int64_t* __restrict__ chunk_cnt, int64_t nseg,
+                                                        uint64_t* __restrict__ kthr) {
+  const int c = blockIdx.y;
+  const SelLvl L = lvl[c];
+  if (!L.incand) return;
+  const uint64_t kstar = L.prefix;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    kthr[c] = ((uint64_t)(0x7FFFFFFFu - (uint32_t)(kstar >> 32)) << 32) | (kstar & 0xFFFFFFFFULL);
+  const int nc = cand_fill[c];
+  const uint64_t* cc = cand + (int64_t)c * ccap;
+  const int64_t b0 = (int64_t)blockIdx.x * 2048;
+  for (int64_t i = b0 + threadIdx.x; i < min((int64_t)nc, b0 + 2048); i += blockDim.x) {
+    const uint64_t key = cc[i];
+    if (key <= kstar) {
+      const int64_t lr = (int64_t)(uint32_t)(key & 0xFFFFFFFFu) - row0;
+      atomicAdd((unsigned long long*)&chunk_cnt[(int64_t)c * nseg + lr / kSelSeg], 1ULL);
+    }
   }
 }
 
