@@ -184,7 +184,12 @@ struct SelFuse {
   int64_t row0;
 };
 
-constexpr int kHeadProd = 128;                         // producer threads
+#ifndef ESNMF_HEAD_PROD_WARPS
+#define ESNMF_HEAD_PROD_WARPS 4
+#endif
+constexpr int kHeadProdWarps = ESNMF_HEAD_PROD_WARPS;   // producer warps
+constexpr int kHeadProd = 32 * kHeadProdWarps;          // producer threads
+constexpr int kHeadMmaWarp = kHeadProdWarps, kHeadLoadWarp = kHeadProdWarps + 1, kHeadEpiWarp = kHeadProdWarps + 2;
 constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
 constexpr int kHeadEpi = 256;                          // epilogue threads (2 warps per TMEM lane quadrant)
@@ -237,13 +242,13 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     }
     tc::fence_mbar_init();
   }
-  if (warp == 4) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
+  if (warp == kHeadMmaWarp) tc::tmem_alloc(&tmem_base, 2 * acc_cols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 5) {
+  if (warp == kHeadLoadWarp) {
     if (lane == 0) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
       int stage = 0;
       uint32_t phase = 0;
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         }
       }
     }
-  } else if (warp < 4) {  // ---- producers: zero + scatter one tile chunk per stage ----
+  } else if (warp < kHeadProdWarps) {  // ---- producers: zero + scatter one tile chunk per stage ----
     const int p = threadIdx.x;
     const int eA = head_exp(__uint_as_float(*amax_bits));
     int stage = 0;
@@ -315,10 +320,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         const int64_t a = sb & ~(int64_t)1;
         const int64_t cap = a + (int64_t)kHeadRaw;  // staged: [a, min(se, cap)); the rest from global
         const int2* raw = reinterpret_cast<const int2*>(sa + raw_off);
-        // zero row p of the A block (8 x 16 B in each of the hi and lo blocks)
+        // zero the A block: row rz, 16-byte chunks j of its 8 (hi and lo blocks)
+        constexpr int kZ = kHeadProd / kHeadM;  // threads per row
 #pragma unroll
-        for (int j = 0; j < kHeadK / 8; ++j) {
-          const uint32_t off = (uint32_t)((p >> 3) * (kHeadK / 8) * 128 + j * 128 + (p & 7) * 16);
+        for (int jj = 0; jj < (kHeadK / 8) / kZ; ++jj) {
+          const int rz = p / kZ, j = (p % kZ) * ((kHeadK / 8) / kZ) + jj;
+          const uint32_t off = (uint32_t)((rz >> 3) * (kHeadK / 8) * 128 + j * 128 + (rz & 7) * 16);
           *reinterpret_cast<uint4*>(sa + off) = make_uint4(0u, 0u, 0u, 0u);
           *reinterpret_cast<uint4*>(sa + kHeadAHalf + off) = make_uint4(0u, 0u, 0u, 0u);
         }
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kHeadMmaWarp) {
     if (lane == 0) {  // ---- MMA issuer ----
       const uint32_t idesc = tc::make_idesc_f16(kHeadM, kn);
       int stage = 0, acc = 0;
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     }
   } else {  // ---- epilogue (warps 6-13): TMEM -> registers -> X += ----
     const int lg = warp & 3;  // TMEM lanes 32*lg .. 32*lg+31
-    const int half = (warp - 6) >> 2;  // the two warps of a quadrant split the columns
+    const int half = (warp - kHeadEpiWarp) >> 2;  // the two warps of a quadrant split the columns
     const int cmid = ((kn / 16 + 1) / 2) * 16;
     const int cbeg = half ? cmid : 0, cend = half ? kn : cmid;
     // fused selection pass 1 (kn <= 128: at most 4 chunks of 16 columns per warp):
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kHeadMmaWarp) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 2 * acc_cols);
   }
