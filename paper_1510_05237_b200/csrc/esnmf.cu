@@ -171,6 +171,7 @@ struct esnmf {
   int ucur = 0;
   Factor V;
   float* Z = nullptr;
+  float* zc = nullptr;          // k = 1: term-indexed z = U W (k_spmv_v)
   int zs = 0;                   // V-side Z row stride (floats), term-indexed rows
   int32_t* zlist = nullptr;     // terms whose Z rows were written last
   int64_t* zcount = nullptr;
@@ -525,6 +526,10 @@ void seq_next_block(esnmf_t* h) {
 // previous call are zeroed first, and the active-term bitmap is rebuilt.
 void form_z(esnmf_t* h, const Factor& f) {
   const int zq = h->zs / 4;
+  if (h->zc) {  // k = 1: the compact z of the previous call is cleared with the same list
+    ++h->nlaunch;
+    k_zc_clear<<<grid_for(f.cap_rows, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount, h->zc);
+  }
   ++h->nlaunch;
   k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
       h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq);
@@ -541,6 +546,11 @@ void form_z(esnmf_t* h, const Factor& f) {
     default: fail(ESNMF_EINVAL, "k too large");
   }
 #undef ESNMF_FZ
+  if (h->zc) {
+    ++h->nlaunch;
+    k_zc_fill<<<grid_for(f.cap_rows, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount, h->Z,
+                                                                                        h->zs, h->zc);
+  }
   CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
   ++h->nlaunch;
   k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits);
@@ -657,6 +667,14 @@ void uside_scatter_launch(esnmf_t* h) {
 }
 
 void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
+  if (s == ESNMF_SIDE_V && h->zc) {  // k = 1: SpMV over A^T (k_spmv_v)
+    Side& sd = h->side[ESNMF_SIDE_V];
+    ++h->nlaunch;
+    k_spmv_v<<<grid_for(sd.rows, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, h->zc,
+                                                                                   sd.X);
+    CKL("spmv_v");
+    return;
+  }
   if (s == ESNMF_SIDE_U && h->world == 1) {
     switch ((h->k + 31) / 32) {
       case 1: uside_scatter_launch<1>(h); break;
@@ -957,6 +975,7 @@ void vhead_launch(esnmf_t* h) {
 // multiple of 64 terms, at most kHeadMax; or `want` terms when want > 0.
 void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (want == 0) return;
+  if (h->k == 1 && h->world == 1 && !getenv("ESNMF_NO_SPMV")) return;  // k = 1: the V side is an SpMV (k_spmv_v)
   const char* env = getenv("ESNMF_HEAD");
   if (env && env[0]) want = atoi(env);
   if (want == 0) return;
@@ -1843,6 +1862,10 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->Z = h->alloc<float>(n * (int64_t)h->zs);
     CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * n * (int64_t)h->zs, h->stream));
     h->zlist = h->alloc<int32_t>(n);
+    if (h->k == 1 && h->world == 1 && !getenv("ESNMF_NO_SPMV")) {
+      h->zc = h->alloc<float>(n);
+      CK(cudaMemsetAsync(h->zc, 0, sizeof(float) * n, h->stream));
+    }
     h->zcount = h->alloc<int64_t>(1);
     CK(cudaMemsetAsync(h->zcount, 0, sizeof(int64_t), h->stream));
     h->tbits = h->alloc<uint32_t>(ceil_div(n, 32));

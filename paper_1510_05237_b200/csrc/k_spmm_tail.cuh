@@ -339,3 +339,41 @@ __global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
 }
 
 }  // namespace esk
+
+namespace esk {
+
+// ---- k = 1 (a one-topic block of sequential ALS, or rank 1) ----------
+// The V side is an SpMV: LS_V[j] = sum over the entries (i, a) of document j of
+// a z_i with z = U W a term-indexed vector (zc).  One warp per document, lanes
+// over its entries, fixed-order warp reduction; z is small (4 n bytes) and the
+// Zipf head of it stays in L1, so the pass streams A^T at HBM speed instead of
+// gathering 64-byte padded Z rows.
+__global__ void __launch_bounds__(256) k_spmv_v(const int64_t* __restrict__ ptr, const int2* __restrict__ ent,
+                                                int64_t rows, const float* __restrict__ zc, float* __restrict__ X) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    float acc = 0.f;
+    for (int64_t q = ptr[r] + lane; q < ptr[r + 1]; q += 32) {
+      const int2 en = __ldcs(ent + q);
+      acc = fmaf(__int_as_float(en.y), __ldg(zc + en.x), acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) X[r] = acc;
+  }
+}
+
+// zc[t] = 0 for the terms of the previous call (before the list is rewritten) ...
+__global__ void k_zc_clear(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
+                           float* __restrict__ zc) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count; q += (int64_t)gridDim.x * blockDim.x)
+    zc[terms[q]] = 0.f;
+}
+// ... and zc[t] = Z[t][0] for this call's terms
+__global__ void k_zc_fill(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
+                          const float* __restrict__ Z, int zs, float* __restrict__ zc) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count; q += (int64_t)gridDim.x * blockDim.x)
+    zc[terms[q]] = Z[(int64_t)terms[q] * zs];
+}
+
+}  // namespace esk
