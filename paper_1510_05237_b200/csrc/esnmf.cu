@@ -2,12 +2,18 @@
 // the enforced-sparse ALS hot path on one B200 (sm_100a) per process.
 //
 // Per iteration (Alg. 2; per-column enforcement P:304):
-//   V side:  G_U = U^T U  -> W = (G_U + eps I)^{-1} -> Z = U W
-//            -> LS_V = A^T Z (k_spmm_tiled) -> clamp + top-t per column -> V
-//   U side:  G_V = V^T V  -> W -> Z = V W -> LS_U = A Z (k_spmm_items)
-//            -> clamp + top-t per column -> U
-//   R (direct difference) and E (trace identity).
-// Everything is enqueued on one stream; iterate never synchronises the host.
+//   V side:  G_U = U^T U -> W = (G_U + eps I)^{-1} (k_sweep_regs) -> Z = U W
+//            -> LS_V = A^T Z: tail terms by row gather (k_spmm_tail), the most
+//               frequent terms on tcgen05 (k_vhead_otf, which also merges the
+//               tail rows); k = 1: an SpMV (k_spmv_v)
+//            -> clamp + top-t per column (k_select.cuh) -> V
+//   U side:  G_V, W on a second stream beside Y = A V (fixed-point scatter from
+//            the active documents, k_uside_scatter) -> LS_U = Y W (k_uside_tc on
+//            tcgen05, or the fp32/fp64 SIMT finish) -> clamp + top-t -> U
+//   R (direct difference) and E (trace identity), launched at the
+//   start of the next iteration on the second stream.
+// Steady-state iterations are replayed as CUDA graphs; the host never
+// synchronises inside esnmf_iterate.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,7 +33,6 @@
 #include "k_metrics.cuh"
 #include "k_select.cuh"
 #include "k_solve.cuh"
-#include "k_spmm.cuh"
 #include "k_spmm_terms.cuh"
 #include "k_uside_scatter.cuh"
 #include "k_vhead.cuh"

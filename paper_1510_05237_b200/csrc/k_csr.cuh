@@ -11,29 +11,6 @@ __global__ void k_pack(const int32_t* __restrict__ col, const float* __restrict_
     ent[e] = make_int2(col[e], __float_as_int(val[e]));
 }
 
-// One warp per row: row_ptr monotone, 0 <= col < ncols strictly increasing,
-// values finite and >= 0.  Sets bits of *bad: 1 ptr, 2 col range, 4 order, 8 value.
-__global__ void k_validate(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
-                           int64_t ncols, int64_t nnz, int* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp0; r < rows; r += nwarps) {
-    const int64_t s = ptr[r], e = ptr[r + 1];
-    if (lane == 0 && (e < s || s < 0 || e > nnz)) atomicOr(bad, 1);
-    if (e < s || s < 0 || e > nnz) continue;
-    int flags = 0;
-    for (int64_t q = s + lane; q < e; q += 32) {
-      const int2 en = ent[q];
-      if (en.x < 0 || en.x >= ncols) flags |= 2;
-      if (q > s && ent[q - 1].x >= en.x) flags |= 4;
-      const float v = __int_as_float(en.y);
-      if (!(v >= 0.f) || !isfinite(v)) flags |= 8;
-    }
-    flags = __reduce_or_sync(kFull, flags);
-    if (lane == 0 && flags) atomicOr(bad, flags);
-  }
-}
 
 // ---- A^T from A on the device (used when the caller gives only CSR(A)) ----
 __global__ void k_col_count(const int2* __restrict__ ent, int64_t nnz, int64_t* __restrict__ cnt) {
@@ -76,20 +53,6 @@ __global__ void k_scan_apply_i64(int64_t* __restrict__ a, int64_t n, const int64
   }
 }
 
-// scatter A's entries into A^T rows (arbitrary order within a row; sorted next)
-__global__ void k_transpose_scatter(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
-                                    int64_t* __restrict__ cursor, int2* __restrict__ tent) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp0; r < rows; r += nwarps) {
-    for (int64_t q = ptr[r] + lane; q < ptr[r + 1]; q += 32) {
-      const int2 en = ent[q];
-      const int64_t p = (int64_t)atomicAdd((unsigned long long*)&cursor[en.x], 1ULL);
-      tent[p] = make_int2((int32_t)r, en.y);
-    }
-  }
-}
 
 // sort every row of A^T by column (terms are distinct within a document):
 // bitonic sort of 64-bit (col << 32 | value bits) keys.  Rows up to

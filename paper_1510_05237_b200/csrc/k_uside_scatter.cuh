@@ -152,7 +152,7 @@ __global__ void k_cond_flag(const double* __restrict__ G, const double* __restri
   }
 }
 
-// W (fp64, k x k) -> fp32 rows of stride kpad (zero padded) for k_uside_finish32
+// W (fp64, k x k) -> fp32 rows of stride kpad (zero padded) for k_uside_finish_rt
 __global__ void k_w_to_f32(const double* __restrict__ W, int k, int kpad, float* __restrict__ W32) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < k * kpad; q += gridDim.x * blockDim.x) {
     const int l = q / kpad, c = q - l * kpad;
@@ -160,96 +160,13 @@ __global__ void k_w_to_f32(const double* __restrict__ W, int k, int kpad, float*
   }
 }
 
-// LS row = (Y row) W in fp32 with W staged in shared memory: lane owns the 4
-// consecutive columns 4(lane + 32 j) .. +3 (float4 loads of W rows); Y is the
-// exact fixed-point row converted once to fp32.  One warp per term row; the
-// nonzero columns of Y are walked in order (deterministic).  The fp32 product
-// keeps the column-relative error ~1e-7.
-template <int CW>
-__global__ void __launch_bounds__(256) k_uside_finish32(int64_t rows, const double* __restrict__ bound,
-                                                        const uint32_t* __restrict__ vmax,
-                                                        const float* __restrict__ W32, int k, int kpad,
-                                                        unsigned long long* __restrict__ Yq, float* __restrict__ X,
-                                                        int64_t ldx, const int* __restrict__ use_fp64) {
-  if (*use_fp64) return;  // ill-conditioned: the fp64 kernel handles it
-  extern __shared__ float4 ws4[];  // [k][kpad/4]
-  const int kq = kpad / 4;
-  for (int q = threadIdx.x; q < k * kq; q += blockDim.x) ws4[q] = reinterpret_cast<const float4*>(W32)[q];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < rows; i += nwarps) {
-    unsigned long long* yr = Yq + i * kpad;
-    float y[CW][4];
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < CW; ++j) {
-      const int ch = lane + 32 * j;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) y[j][e] = 0.f;
-      if (ch < kq) {
-        const ulonglong2 a = reinterpret_cast<const ulonglong2*>(yr)[2 * ch];
-        const ulonglong2 b = reinterpret_cast<const ulonglong2*>(yr)[2 * ch + 1];
-        const unsigned long long q4[4] = {a.x, a.y, b.x, b.y};
-        bool nz = false;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          y[j][e] = (float)((double)q4[e] * unit);
-          nz |= q4[e] != 0ull;
-        }
-        if (nz) {  // clear for the next half-step
-          reinterpret_cast<ulonglong2*>(yr)[2 * ch] = make_ulonglong2(0ull, 0ull);
-          reinterpret_cast<ulonglong2*>(yr)[2 * ch + 1] = make_ulonglong2(0ull, 0ull);
-        }
-        any |= nz;
-      }
-    }
-    float4 o[CW];
-#pragma unroll
-    for (int j = 0; j < CW; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (__any_sync(kFull, any)) {
-#pragma unroll
-      for (int j = 0; j < CW; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          unsigned nz = __ballot_sync(kFull, y[j][e] != 0.f);
-          while (nz) {
-            const int src = __ffs(nz) - 1;
-            nz &= nz - 1;
-            const float yl = __shfl_sync(kFull, y[j][e], src);
-            const float4* wl = ws4 + (4 * (src + 32 * j) + e) * kq;
-#pragma unroll
-            for (int jj = 0; jj < CW; ++jj) {
-              const int ch = lane + 32 * jj;
-              if (ch < kq) {
-                const float4 w = wl[ch];
-                o[jj].x = fmaf(yl, w.x, o[jj].x);
-                o[jj].y = fmaf(yl, w.y, o[jj].y);
-                o[jj].z = fmaf(yl, w.z, o[jj].z);
-                o[jj].w = fmaf(yl, w.w, o[jj].w);
-              }
-            }
-          }
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < CW; ++j) {
-      const int c0 = 4 * (lane + 32 * j);
-      const float v[4] = {o[j].x, o[j].y, o[j].z, o[j].w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (c0 + e < k) X[(int64_t)(c0 + e) * ldx + i] = v[e];
-    }
-  }
-}
-
-// Register-tiled variant of k_uside_finish32: a warp converts RT = 8 rows of
-// the fixed-point Y at a time into shared memory (transposed, ys[l][r]), clears
-// them, and computes the 8 x k block (Y W) with every W row read once from
-// shared memory per 8 rows (the one-row kernel re-read W per row and was bound
-// by shared-memory bandwidth).  Dense in l: Y's zeros are multiplied, not
-// skipped (the same fixed summation order for every row; deterministic).
+// LS row block = (Y rows) W in fp32 (k <= 224, when the tensor-core finish is not
+// used): a warp converts RT = 8 rows of the fixed-point Y at a time into shared
+// memory (transposed, ys[l][r]), clears them, and computes the 8 x k block with
+// every W row read once from shared memory per 8 rows.  Dense in l: Y's zeros
+// are multiplied, not skipped (the same fixed summation order for every row;
+// deterministic).  The fp32 product keeps the column-relative error ~1e-7
+// (DESIGN.md section 4).
 constexpr int kFinRT = 8;
 
 template <int CW>
