@@ -326,3 +326,20 @@ def test_predicted_select_trajectory(tag, cfg, monkeypatch):
     # and a late half-step against the oracle from the same state
     half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_V)
     half_step_parity(s, g, cfg.n, cfg.m, cfg.k, cfg.t, ESNMF_SIDE_U)
+
+
+def test_t_zero_keeps_nothing():
+    """t = 0 (P:134 with an empty budget): every factor is empty after each side,
+    the ridge keeps the solve defined, and E = 1 (U V^T = 0)."""
+    cfg = synth.CONFIGS["tiny"]
+    g = synth.generate(cfg)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, 0, g, seed=cfg.seed)
+    s.iterate(3)
+    for r in s.records():
+        assert r["nnz_u"] == 0 and r["nnz_v"] == 0 and r["dead_u"] == cfg.k
+        assert r["E"] == pytest.approx(1.0, abs=1e-12)
+        assert r["R"] == -1.0                  # ||U_i|| = 0: R undefined (the record's -1)
+    with pytest.raises(ValueError):            # the oracle refuses the same R (S:266)
+        oracle.run(g, cfg.k, 0, 1, seed=cfg.seed)
+    h = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], oracle.u0(cfg.n, cfg.k, cfg.seed), 0)
+    assert not h["F"].any()

@@ -112,7 +112,7 @@ def test_shard_buffer_layout_matches_kernel():
 # ------------------------------------------------------------------ GPU
 
 
-def run_loopback(world, cfg, g, iters, t="cfg"):
+def run_loopback(world, cfg, g, iters, t="cfg", **kw):
     tval = cfg.t if t == "cfg" else t
     grp = pk.comm.LoopbackGroup(world)
     handles = [None] * world
@@ -122,7 +122,7 @@ def run_loopback(world, cfg, g, iters, t="cfg"):
         try:
             stream = torch.cuda.Stream()
             handles[r] = ESNMF(cfg.n, cfg.m, cfg.k, tval, g, seed=cfg.seed, world=world, rank=r,
-                               comm=grp.comms[r], stream=stream.cuda_stream)
+                               comm=grp.comms[r], stream=stream.cuda_stream, **kw)
             handles[r].iterate(iters)
             handles[r].records()
         except Exception as e:  # pragma: no cover
@@ -176,3 +176,23 @@ def test_loopback_two_vs_three_ranks_bitwise():
     for ra, rb in zip(a.records(), b.records()):
         assert ra["R"] == rb["R"]            # computed on the replicated U
         assert ra["E"] == pytest.approx(rb["E"], rel=1e-12)  # T is a sum over ranks
+
+
+@pytest.mark.gpu
+def test_loopback_options_match_single_gpu():
+    """The §8(f) options on the sharded path: row normalisation (each rank scales
+    its term rows and its documents' A^T entries by the global row nnz), separate
+    budgets, sparse U_0; the accuracy of a rank's replicated V equals the single
+    GPU's."""
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    g = synth.generate(TINY)
+    kw = dict(row_normalize=True, t_u=30, t_v=45, init_nnz=400)
+    hs = run_loopback(2, TINY, g, 4, **kw)
+    one = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, **kw)
+    one.iterate(4)
+    for a, b in zip(hs[0].records(), one.records()):
+        assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"]
+        assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"]
+    labels = np.arange(TINY.m) % 3
+    assert np.allclose(hs[1].topic_accuracy(labels, 3), one.topic_accuracy(labels, 3), rtol=0, atol=1e-12)
