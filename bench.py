@@ -45,12 +45,17 @@ def parse():
 
 
 def measured_bf16_tflops():
-    """fp16 dense tensor peak = the measured bf16 one (same rate on B200)."""
+    """fp16 dense tensor peak = the measured bf16 one (same rate on B200).  The head
+    kernel runs inside a long step (one iteration after another), so the sustained
+    figure is its denominator; the burst one is reported beside it."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return d.get("bf16_tflops", 2250.0), "MEASURED_PEAKS.json bf16_tflops (burst; fp16 runs at the bf16 rate)"
-    return 2250.0, "fallback B200_PROFILING.md (2.25 PFLOP/s dense bf16/fp16)"
+        if "bf16_tflops_sustained" in d:
+            return (d["bf16_tflops_sustained"], "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step; "
+                    "fp16 runs at the bf16 rate)", d.get("bf16_tflops"))
+        return d.get("bf16_tflops", 2250.0), "MEASURED_PEAKS.json bf16_tflops (burst; fp16 runs at the bf16 rate)", None
+    return 2250.0, "fallback B200_PROFILING.md (2.25 PFLOP/s dense bf16/fp16)", None
 
 
 def measured_peaks() -> dict:
@@ -315,6 +320,7 @@ def run_ours(args):
         pk = measured_bf16_tflops()
         kernels["V.head.tensor"] = {"bound": "tensor", "achieved": round(tf, 1), "peak": pk[0], "unit": "TFLOP/s",
                                     "frac": round(tf / pk[0], 4), "peak_src": pk[1],
+                                    "frac_of_burst_peak": round(tf / pk[2], 4) if pk[2] else None,
                                     "flops_per_launch": fl, "head_terms": split[0], "head_nnz": split[1]}
     phase_table = {k: {"calls": c, "ms_per_call": round(v / max(c, 1), 4), "share": round(v / prof_ms, 4)}
                    for k, (c, v) in phases.items() if c}
