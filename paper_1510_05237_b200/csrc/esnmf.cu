@@ -934,7 +934,7 @@ void select_merge(esnmf_t* h, int s, Factor& out);
 int head_stage_bytes_host(int kn) {
   return (int)((kHeadABytes + (uint32_t)kn * kHeadK * 4 + kHeadRawBytes + 1023u) & ~1023u);
 }
-int head_stages(int kn) { return std::max(2, std::min(4, (220 * 1024) / head_stage_bytes_host(kn))); }
+int head_stages(int kn) { return std::max(2, std::min(6, (220 * 1024) / head_stage_bytes_host(kn))); }
 
 template <int ST>
 void vhead_launch_st(esnmf_t* h) {
@@ -971,7 +971,9 @@ void vhead_launch(esnmf_t* h) {
   switch (head_stages(h->kn)) {
     case 2: vhead_launch_st<2>(h); break;
     case 3: vhead_launch_st<3>(h); break;
-    default: vhead_launch_st<4>(h); break;
+    case 4: vhead_launch_st<4>(h); break;
+    case 5: vhead_launch_st<5>(h); break;
+    default: vhead_launch_st<6>(h); break;
   }
 }
 
@@ -1042,7 +1044,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   {
     // 8 dense chunks measured best at Large (0.62 ms vs 0.64 for 4, 0.77 for all 16);
     // capped at 4 GB of dense tiles
-    int nd = (int)std::min<int64_t>(8, (int64_t)(4LL << 30) / std::max<int64_t>(1, h->head_ntiles * kHeadABytes));
+    int nd = (int)std::min<int64_t>(512 / kHeadK, (int64_t)(4LL << 30) / std::max<int64_t>(1, h->head_ntiles * kHeadABytes));
     const char* de = getenv("ESNMF_HEAD_DENSE");
     if (de && de[0]) nd = atoi(de);
     h->head_nd = std::max(0, std::min(nd, h->head_nchunks));

@@ -43,7 +43,11 @@
 
 namespace esk {
 
-constexpr int kHeadK = 64;                                   // head terms per chunk
+#ifndef ESNMF_HEAD_K
+#define ESNMF_HEAD_K 64
+#endif
+constexpr int kHeadK = ESNMF_HEAD_K;                         // head terms per chunk (MMA K per stage)
+static_assert(kHeadK == 32 || kHeadK == 64, "chunk entries encode the slot in 6 bits");
 constexpr int kHeadM = 128;                                  // documents per tile (MMA M)
 constexpr uint32_t kHeadABytes = kHeadM * kHeadK * 2 * 2;    // hi + lo fp16 = 32 KB
 constexpr uint32_t kHeadAHalf = kHeadM * kHeadK * 2;         // 16 KB
@@ -190,7 +194,7 @@ struct SelFuse {
 constexpr int kHeadProdWarps = ESNMF_HEAD_PROD_WARPS;   // producer warps
 constexpr int kHeadProd = 32 * kHeadProdWarps;          // producer threads
 constexpr int kHeadMmaWarp = kHeadProdWarps, kHeadLoadWarp = kHeadProdWarps + 1, kHeadEpiWarp = kHeadProdWarps + 2;
-constexpr int kHeadRaw = 1024;                         // entries of a chunk's run staged in smem
+constexpr int kHeadRaw = 16 * kHeadK;                  // entries of a chunk's run staged in smem
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
 constexpr int kHeadEpi = 256;                          // epilogue threads (2 warps per TMEM lane quadrant)
 constexpr int kHeadOtfThreads = kHeadProd + 32 + 32 + kHeadEpi;  // producers, MMA, loader, epilogue
@@ -355,8 +359,9 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
 #pragma unroll
           for (int s = 0; s < kHeadK / 16; ++s) {
             const uint32_t o = s * 256;
-            const uint64_t dah = tc::make_sdesc(ah + o, 128, 1024), dal = tc::make_sdesc(al + o, 128, 1024);
-            const uint64_t dzh = tc::make_sdesc(zh + o, 128, 1024), dzl = tc::make_sdesc(zl + o, 128, 1024);
+            constexpr uint32_t sbo = (kHeadK / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
+            const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
+            const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
             tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
             tc::mma_f16(d, dah, dzl, idesc, 1);
             tc::mma_f16(d, dal, dzh, idesc, 1);
