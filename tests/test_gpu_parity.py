@@ -339,6 +339,9 @@ def test_t_zero_keeps_nothing():
         assert r["nnz_u"] == 0 and r["nnz_v"] == 0 and r["dead_u"] == cfg.k
         assert r["E"] == pytest.approx(1.0, abs=1e-12)
         assert r["R"] == -1.0                  # ||U_i|| = 0: R undefined (the record's -1)
+    with pytest.raises(ESNMFError):            # esnmf_residual: EDEGENERATE
+        s.residual()
+    assert s.error() == pytest.approx(1.0, abs=1e-12)
     with pytest.raises(ValueError):            # the oracle refuses the same R
         oracle.run(g, cfg.k, 0, 1, seed=cfg.seed)
     h = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], oracle.u0(cfg.n, cfg.k, cfg.seed), 0)
