@@ -423,12 +423,15 @@ void gram(esnmf_t* h, const Factor& f, double* G, int kk = 0, int kp = 0, double
   int64_t S = std::min<int64_t>(kMaxGramSeg, std::max<int64_t>(1, ceil_div(f.maxcol, 32)));
   int64_t seglen = std::max<int64_t>(1, ceil_div(f.maxcol, S));
   dim3 g(k, (unsigned)S);
-  const int gb = (k + 31) / 32 * 32;                 // <= 256
-  // entry-splitting groups per block, for long segments only (short ones: the
-  // extra threads cost more than they save)
-  const int ng = seglen >= 256 ? std::max(1, std::min(4, 512 / gb)) : 1;
-  ++h->nlaunch; k_gram_partial<<<g, gb * ng, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k,
-                                                             seglen, partial, gb);
+  const int gb = (k + 31) / 32 * 32;  // <= 256
+  ++h->nlaunch;
+  if (seglen >= 256) {  // long segments: thread groups split the entries
+    const int ng = std::max(1, std::min(4, 512 / gb));
+    k_gram_partial_groups<<<g, gb * ng, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k, seglen,
+                                                        partial, gb);
+  } else {
+    k_gram_partial<<<g, gb, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k, seglen, partial);
+  }
   ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(partial, (int)S, k, G);
   ++h->nlaunch; k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
   CKL("gram");

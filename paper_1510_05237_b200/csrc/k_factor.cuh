@@ -201,7 +201,7 @@ __global__ void k_scatter_dense(const int64_t* __restrict__ colptr, const int32_
 // can put 10^5 entries in one -- are otherwise one long dependent loop);
 // group sums and segment partials are added in a fixed order (k_gram_reduce):
 // deterministic.
-__global__ void __launch_bounds__(512) k_gram_partial(const int64_t* __restrict__ colptr,
+__global__ void __launch_bounds__(512) k_gram_partial_groups(const int64_t* __restrict__ colptr,
                                                       const int32_t* __restrict__ row,
                                                       const float* __restrict__ val,
                                                       const int32_t* __restrict__ rowmap,
@@ -234,6 +234,33 @@ __global__ void __launch_bounds__(512) k_gram_partial(const int64_t* __restrict_
     double t = red[b];
     for (int q = 1; q < ng; ++q) t += red[q * gb + b];
     partial[((int64_t)s * k + a) * k + b] = t;
+  }
+}
+
+// short segments (every column of a per-column factor): thread b owns G[a][b]
+__global__ void __launch_bounds__(256) k_gram_partial(const int64_t* __restrict__ colptr,
+                                                      const int32_t* __restrict__ row,
+                                                      const float* __restrict__ val,
+                                                      const int32_t* __restrict__ rowmap,
+                                                      const float* __restrict__ dense, int kpad, int k,
+                                                      int64_t seglen, double* __restrict__ partial) {
+  const int a = blockIdx.x, s = blockIdx.y;
+  const int64_t cb = colptr[a], ce = colptr[a + 1];
+  const int64_t b0 = cb + (int64_t)s * seglen;
+  const int64_t b1 = min(ce, b0 + seglen);
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {
+    double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    int64_t e = b0;
+    for (; e + 4 <= b1; e += 4) {
+      float u0 = val[e], u1 = val[e + 1], u2 = val[e + 2], u3 = val[e + 3];
+      int32_t r0 = rowmap[row[e]], r1 = rowmap[row[e + 1]], r2 = rowmap[row[e + 2]], r3 = rowmap[row[e + 3]];
+      acc0 += (double)u0 * (double)dense[(int64_t)r0 * kpad + b];
+      acc1 += (double)u1 * (double)dense[(int64_t)r1 * kpad + b];
+      acc2 += (double)u2 * (double)dense[(int64_t)r2 * kpad + b];
+      acc3 += (double)u3 * (double)dense[(int64_t)r3 * kpad + b];
+    }
+    for (; e < b1; ++e) acc0 += (double)val[e] * (double)dense[(int64_t)rowmap[row[e]] * kpad + b];
+    partial[((int64_t)s * k + a) * k + b] = (acc0 + acc1) + (acc2 + acc3);
   }
 }
 
