@@ -223,13 +223,17 @@ __global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
         rc[RG - 1] = cnt - sum;
       }
       // padded layout: row q's entries at [pb[q], pb[q] + rc[q]), zero slots up to a multiple of STEP
-      int pb[RG + 1], shift[RG];
+      // row q's slot shift (padding before it, < 256) packed into byte q of one
+      // register: an indexed array here was placed in local memory
+      static_assert(RG <= 4 && (RG - 1) * (STEP - 1) < 256, "packed row shifts");
+      int pb[RG + 1];
+      uint32_t shp = 0;
       pb[0] = 0;
       {
         int plain = 0;
 #pragma unroll
         for (int q = 0; q < RG; ++q) {
-          shift[q] = pb[q] - plain;
+          shp |= (uint32_t)(pb[q] - plain) << (8 * q);
           plain += rc[q];
           pb[q + 1] = pb[q] + (rc[q] + STEP - 1) / STEP * STEP;
         }
@@ -239,10 +243,7 @@ __global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
 #pragma unroll
       for (int j = 0; j < kTailSub; ++j) {
         if ((act[j] >> lane) & 1u) {
-          int sh = 0;
-#pragma unroll
-          for (int q = 0; q < RG; ++q)
-            if (tg[j] == q) sh = shift[q];
+          const int sh = (int)((shp >> (8 * tg[j])) & 0xFFu);
           st[run + __popc(act[j] & lt_mask) + sh] = make_int2((int)((uint32_t)en[j].x * zrow), en[j].y);
         }
         run += __popc(act[j]);
