@@ -112,6 +112,7 @@ struct Side {
   uint64_t* kthr = nullptr;
   SelLvl* lvl = nullptr;          // [k] multi-block radix fallback state
   int64_t* scanbuf = nullptr;     // [kSelScanMax] block sums of the flat view's segment scan
+  int ccap = 0;                   // candidate list capacity per column (cand)
   uint64_t* above = nullptr;      // two-pass select (t <= kSelFastT): [k][t] row keys
   int64_t above_t = -1;           // its t capacity per column
   int32_t* above_fill = nullptr;  // [k] (followed by bucket_fill [k] in the same allocation)
@@ -818,7 +819,7 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   // candidate list per column: kSelCap keys (sorted on chip); a flat whole-factor
   // view (one column) gets the whole buffer, so its bucket usually fits and the
   // radix levels run over the list instead of over X
-  const int ccap = kc == 1 ? h->k * kSelCap : kSelCap;
+  const int ccap = kc == 1 ? (int)std::min<int64_t>((int64_t)h->k * sd.ccap, INT32_MAX) : sd.ccap;
   ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg, ccap);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
@@ -1359,7 +1360,15 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.nchunks = std::max<int64_t>(1, ceil_div(sd.rows, kSelChunk));
   sd.hist = h->alloc<uint32_t>((int64_t)k * kNumBins);
   sd.sel = h->alloc<ColSel>(k);
-  sd.cand = h->alloc<uint64_t>((int64_t)k * kSelCap);
+  // threshold-bucket candidates per column: kSelCap are sorted on chip; with the
+  // 3-pass path (t > kSelFastT or unlimited) a larger list keeps a big bucket
+  // off the grid-wide radix passes over X (Box: each pass reads 6.4 GB)
+  {
+    const int64_t tt = h->tside[&sd == &h->side[ESNMF_SIDE_V] ? 0 : 1];
+    sd.ccap = (tt < 0 || tt > kSelFastT) ? (int)std::min<int64_t>(65536, std::max<int64_t>(kSelCap, sd.rows / 16))
+                                         : kSelCap;
+  }
+  sd.cand = h->alloc<uint64_t>((int64_t)k * sd.ccap);
   sd.cand_fill = h->alloc<int32_t>(k);
   sd.chunk_cnt = h->alloc<int64_t>((int64_t)k * (sd.nchunks + 1) * kSelSegs);  // (+1: the flat view)
   sd.coltot = h->alloc<int64_t>(k);

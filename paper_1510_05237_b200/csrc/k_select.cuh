@@ -253,7 +253,7 @@ __global__ void k_sel_lvl_init(const ColSel* __restrict__ sel, const int32_t* __
     const ColSel s = sel[c];
     SelLvl L;
     L.active = s.r > 0 && cand_fill[c] > kSelCap;
-    L.incand = L.active && cand_fill[c] <= ccap;
+    L.incand = L.active && cand_fill[c] <= ccap;  // (ccap > kSelCap: the list holds the whole bucket)
     L.pad_ = 0;
     L.done = !L.active;
     L.prefix = L.active ? ((uint64_t)(0x7FFFFFFFu - ((uint32_t)s.digit << kSelShift)) >> kSelShift) << 51 : 0;
