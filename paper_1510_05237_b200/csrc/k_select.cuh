@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(256) k_sel_write(const float* __restrict__ X, 
 // The lists are filled in scheduling order but everything kept is sorted by a
 // total order, so the output is deterministic.  A bucket larger than
 // kSelCap falls back to an exact radix select over the column.
-constexpr int64_t kSelFastT = 4096;
+constexpr int64_t kSelFastT = 8192;
 
 ESNMF_DEV uint64_t row_key(uint32_t row, float x) { return ((uint64_t)row << 32) | (uint64_t)f2u(x); }
 

@@ -97,7 +97,7 @@ def test_medium_whole_matrix_half_steps():
 
 
 def test_whole_matrix_large_budget_uses_three_pass_select():
-    """t > 4096: the exact multi-pass selection over the flat factor."""
+    """t > 8192 (kSelFastT): the exact multi-pass selection over the flat factor."""
     cfg = MEDIUM
     g = synth.generate(cfg)
     s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, t_u=20000, t_v=30000, whole=True)
@@ -159,7 +159,7 @@ def test_sparse_initial_guess_and_peak_nnz(init_nnz):
         assert abs(a["peak_v"] - b["peak_v"]) <= 1e-4 * b["peak_v"] + 1
 
 
-@pytest.mark.parametrize("whole,t", [(True, 3000), (True, 200_000), (False, 6000), (False, 300)])
+@pytest.mark.parametrize("whole,t", [(True, 3000), (True, 200_000), (False, 6000), (False, 9000), (False, 300)])
 def test_selection_with_huge_tie_buckets(whole, t):
     """Three distinct values only: the threshold bucket holds far more than the
     4,096 keys sorted on chip, so the exact multi-block radix levels (value,
