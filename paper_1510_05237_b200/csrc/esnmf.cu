@@ -1187,9 +1187,7 @@ void flush_metrics(esnmf_t* h) {
   double* p_new = h->red;
   double* p_old = p_new + 2 * (int64_t)gxn * k;
   double* p_tr = p_old + (int64_t)gxo * k;
-  ++h->nlaunch; k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
-  ++h->nlaunch; k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
-  // Gram of the new U: S term of E now, and the next V side's G_U
+  // Gram of the new U first (the next V side's solve waits for it): S term of E, G_U
   gram(h, Un, h->side[ESNMF_SIDE_V].G);
   h->gramU_valid = true;
   // a8 error: T = tr(U^T (A V)) from the U side's LS rows.  On one GPU
@@ -1198,6 +1196,9 @@ void flush_metrics(esnmf_t* h) {
   const bool overlap_m = h->world == 1;
   if (overlap_m) fork_to_aux(h, h->ev_mfork);
   OnStream os(h, overlap_m ? h->aux : h->stream);
+  // (on the aux stream: U_{i-1} is overwritten only by the next U side, after the join)
+  ++h->nlaunch; k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
+  ++h->nlaunch; k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
   Side& su = h->side[ESNMF_SIDE_U];
   const unsigned gtr = grid_for(Un.cap_rows, 8, (int64_t)h->num_sms * 8);
   ++h->nlaunch;
