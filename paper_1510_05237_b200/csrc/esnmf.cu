@@ -177,7 +177,7 @@ struct esnmf {
   int ucur = 0;
   Factor V;
   float* Z = nullptr;
-  float* zc = nullptr;          // k = 1: term-indexed z = U W (k_spmv_v)
+  float* zc = nullptr;          // kpad <= 8: compact term-indexed z = U W, kpad per term (k_spmm_narrow)
   int zs = 0;                   // V-side Z row stride (floats), term-indexed rows
   int32_t* zlist = nullptr;     // terms whose Z rows were written last
   int64_t* zcount = nullptr;
@@ -535,9 +535,11 @@ void seq_next_block(esnmf_t* h) {
 // previous call are zeroed first, and the active-term bitmap is rebuilt.
 void form_z(esnmf_t* h, const Factor& f) {
   const int zq = h->zs / 4;
-  if (h->zc) {  // k = 1: the compact z of the previous call is cleared with the same list
+  const int kpz = h->k == 1 ? 1 : h->kpad;  // zc row width
+  if (h->zc) {  // narrow k: the compact z of the previous call is cleared with the same list
     ++h->nlaunch;
-    k_zc_clear<<<grid_for(f.cap_rows, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount, h->zc);
+    k_zc_clear<<<grid_for(f.cap_rows * kpz, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount,
+                                                                                               kpz, h->zc);
   }
   ++h->nlaunch;
   k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
@@ -557,8 +559,8 @@ void form_z(esnmf_t* h, const Factor& f) {
 #undef ESNMF_FZ
   if (h->zc) {
     ++h->nlaunch;
-    k_zc_fill<<<grid_for(f.cap_rows, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount, h->Z,
-                                                                                        h->zs, h->zc);
+    k_zc_fill<<<grid_for(f.cap_rows * kpz, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
+        h->zlist, h->zcount, h->Z, h->zs, kpz, h->zc);
   }
   CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
   ++h->nlaunch;
@@ -676,12 +678,17 @@ void uside_scatter_launch(esnmf_t* h) {
 }
 
 void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
-  if (s == ESNMF_SIDE_V && h->zc) {  // k = 1: SpMV over A^T (k_spmv_v)
+  if (s == ESNMF_SIDE_V && h->zc) {  // narrow k: SpMM over A^T with the compact z (k_spmm_narrow)
     Side& sd = h->side[ESNMF_SIDE_V];
+    const unsigned g = grid_for(sd.rows, 8, (int64_t)h->num_sms * 64);
     ++h->nlaunch;
-    k_spmv_v<<<grid_for(sd.rows, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, h->zc,
-                                                                                   sd.X);
-    CKL("spmv_v");
+    if (h->k == 1)
+      k_spmm_narrow<1><<<g, 256, 0, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, h->zc, h->k, sd.X, sd.ldx);
+    else if (h->kpad == 4)
+      k_spmm_narrow<4><<<g, 256, 0, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, h->zc, h->k, sd.X, sd.ldx);
+    else
+      k_spmm_narrow<8><<<g, 256, 0, h->stream>>>(sd.T.ptr, sd.T.ent, sd.rows, h->zc, h->k, sd.X, sd.ldx);
+    CKL("spmm_narrow");
     return;
   }
   if (s == ESNMF_SIDE_U && h->world == 1) {
@@ -984,9 +991,12 @@ void vhead_launch(esnmf_t* h) {
 // Choose the head (create time): the terms of largest document frequency
 // (row lengths of A, global), at least `min_df` of the documents each, a
 // multiple of 64 terms, at most kHeadMax; or `want` terms when want > 0.
+// kpad <= 8 on one GPU: the V side runs k_spmm_narrow (no head, no padded Z gather)
+bool narrow_v(esnmf_t* h) { return h->kpad <= 8 && h->world == 1 && !getenv("ESNMF_NO_NARROW"); }
+
 void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (want == 0) return;
-  if (h->k == 1 && h->world == 1 && !getenv("ESNMF_NO_SPMV")) return;  // k = 1: the V side is an SpMV (k_spmv_v)
+  if (narrow_v(h)) return;  // narrow k: the V side is an SpMM with a compact z (k_spmm_narrow)
   const char* env = getenv("ESNMF_HEAD");
   if (env && env[0]) want = atoi(env);
   if (want == 0) return;
@@ -1882,9 +1892,10 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->Z = h->alloc<float>(n * (int64_t)h->zs);
     CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * n * (int64_t)h->zs, h->stream));
     h->zlist = h->alloc<int32_t>(n);
-    if (h->k == 1 && h->world == 1 && !getenv("ESNMF_NO_SPMV")) {
-      h->zc = h->alloc<float>(n);
-      CK(cudaMemsetAsync(h->zc, 0, sizeof(float) * n, h->stream));
+    if (narrow_v(h.get())) {
+      const int kpz = h->k == 1 ? 1 : h->kpad;
+      h->zc = h->alloc<float>(n * (int64_t)kpz);
+      CK(cudaMemsetAsync(h->zc, 0, sizeof(float) * n * kpz, h->stream));
     }
     h->zcount = h->alloc<int64_t>(1);
     CK(cudaMemsetAsync(h->zcount, 0, sizeof(int64_t), h->stream));

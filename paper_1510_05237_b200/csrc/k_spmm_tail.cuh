@@ -343,38 +343,60 @@ __global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
 
 namespace esk {
 
-// ---- k = 1 (a one-topic block of sequential ALS, or rank 1) ----------
-// The V side is an SpMV: LS_V[j] = sum over the entries (i, a) of document j of
-// a z_i with z = U W a term-indexed vector (zc).  One warp per document, lanes
-// over its entries, fixed-order warp reduction; z is small (4 n bytes) and the
-// Zipf head of it stays in L1, so the pass streams A^T at HBM speed instead of
-// gathering 64-byte padded Z rows.
-__global__ void __launch_bounds__(256) k_spmv_v(const int64_t* __restrict__ ptr, const int2* __restrict__ ent,
-                                                int64_t rows, const float* __restrict__ zc, float* __restrict__ X) {
+// ---- narrow k (kpad <= 8: small blocks of sequential ALS, or small ranks) ----
+// The V side is an SpMM with a skinny right factor: LS_V[j, :] = sum over the
+// entries (i, a) of document j of a z_i with z = U W held compactly (KP floats
+// per term, zc), instead of 64-byte-padded Z rows and a tensor-core head.  One
+// warp per document, lanes over its entries, fixed-order warp reduction; z is
+// small (4 KP n bytes, its Zipf head L1-resident), so the pass streams A^T.
+template <int KP>
+__global__ void __launch_bounds__(256) k_spmm_narrow(const int64_t* __restrict__ ptr, const int2* __restrict__ ent,
+                                                     int64_t rows, const float* __restrict__ zc, int k,
+                                                     float* __restrict__ X, int64_t ldx) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
-    float acc = 0.f;
+    float acc[KP];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) acc[c] = 0.f;
     for (int64_t q = ptr[r] + lane; q < ptr[r + 1]; q += 32) {
       const int2 en = __ldcs(ent + q);
-      acc = fmaf(__int_as_float(en.y), __ldg(zc + en.x), acc);
+      const float a = __int_as_float(en.y);
+      if constexpr (KP == 1) {
+        acc[0] = fmaf(a, __ldg(zc + en.x), acc[0]);
+      } else {
+#pragma unroll
+        for (int c4 = 0; c4 < KP; c4 += 4) {
+          const float4 z = __ldg(reinterpret_cast<const float4*>(zc + (int64_t)en.x * KP + c4));
+          acc[c4] = fmaf(a, z.x, acc[c4]);
+          acc[c4 + 1] = fmaf(a, z.y, acc[c4 + 1]);
+          acc[c4 + 2] = fmaf(a, z.z, acc[c4 + 2]);
+          acc[c4 + 3] = fmaf(a, z.w, acc[c4 + 3]);
+        }
+      }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) X[r] = acc;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < KP; ++c)
+        if (c < k) X[(int64_t)c * ldx + r] = acc[c];
   }
 }
 
-// zc[t] = 0 for the terms of the previous call (before the list is rewritten) ...
-__global__ void k_zc_clear(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
+// zc[t, :] = 0 for the terms of the previous call (before the list is rewritten) ...
+__global__ void k_zc_clear(const int32_t* __restrict__ terms, const int64_t* __restrict__ count, int kp,
                            float* __restrict__ zc) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count; q += (int64_t)gridDim.x * blockDim.x)
-    zc[terms[q]] = 0.f;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count * kp; q += (int64_t)gridDim.x * blockDim.x)
+    zc[(int64_t)terms[q / kp] * kp + q % kp] = 0.f;
 }
-// ... and zc[t] = Z[t][0] for this call's terms
+// ... and zc[t, :] = Z[t, 0:kp] for this call's terms
 __global__ void k_zc_fill(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
-                          const float* __restrict__ Z, int zs, float* __restrict__ zc) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count; q += (int64_t)gridDim.x * blockDim.x)
-    zc[terms[q]] = Z[(int64_t)terms[q] * zs];
+                          const float* __restrict__ Z, int zs, int kp, float* __restrict__ zc) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < *count * kp; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = terms[q / kp];
+    zc[t * kp + q % kp] = Z[t * zs + q % kp];
+  }
 }
 
 }  // namespace esk

@@ -47,6 +47,7 @@ def main():
         "alg2_column": dict(),
         "alg2_whole": dict(whole=True, t_u=cfg.k * cfg.t, t_v=cfg.k * cfg.t),
         "seq_k2_1": dict(seq_k2=1, seq_iters=2),
+        "seq_k2_4": dict(seq_k2=4, seq_iters=4),
         "seq_k2_10": dict(seq_k2=10, seq_iters=4),
     }
     out = {}
