@@ -5,7 +5,7 @@
 //   V side:  G_U = U^T U -> W = (G_U + eps I)^{-1} (k_sweep_regs) -> Z = U W
 //            -> LS_V = A^T Z: tail terms by row gather (k_spmm_tail), the most
 //               frequent terms on tcgen05 (k_vhead_otf, which also merges the
-//               tail rows); k = 1: an SpMV (k_spmv_v)
+//               tail rows); kpad <= 8: a narrow SpMM (k_spmm_narrow)
 //            -> clamp + top-t per column (k_select.cuh) -> V
 //   U side:  G_V, W on a second stream beside Y = A V (fixed-point scatter from
 //            the active documents, k_uside_scatter) -> LS_U = Y W (k_uside_tc on
