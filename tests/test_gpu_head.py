@@ -144,3 +144,21 @@ def test_fused_selection_in_head_epilogue(cfg_name, head, monkeypatch):
     # and a late (fused) V side against the oracle directly
     monkeypatch.setenv("ESNMF_FUSED_SELECT", "1")
     v_side_parity(a, g, cfg, cfg.k, cfg.t)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8])
+def test_narrow_v_side(k):
+    """kpad <= 8: the V side is the narrow SpMM with a compact z (no head); its LS,
+    selection and trajectory match the oracle."""
+    g = synth.generate(TINY)
+    s = ESNMF(TINY.n, TINY.m, k, 40, g, seed=TINY.seed)
+    assert s.info()["head_terms"] == 0
+    v_side_parity(s, g, TINY, k, 40)
+    s.half_step(ESNMF_SIDE_U)
+    s.iterate(4)
+    v_side_parity(s, g, TINY, k, 40)
+    ref = oracle.run(g, k, 40, 4, seed=TINY.seed)
+    t = ESNMF(TINY.n, TINY.m, k, 40, g, seed=TINY.seed)
+    t.iterate(4)
+    for a, b in zip(t.records(), ref["records"]):
+        assert abs(a["E"] - b["E"]) <= 1e-3 * b["E"] and a["nnz_v"] == b["nnz_v"]
