@@ -152,6 +152,54 @@ __global__ void k_cond_flag(const double* __restrict__ G, const double* __restri
   }
 }
 
+// The same Y = A V driven by V's columns: block (c, chunk) takes kScatDocs
+// entries (doc j, v) of topic column c.  Each document row of A^T stores its
+// head-term entries first (k_reorder_head, nh[j] of them): those accumulate in
+// a per-block shared fixed-point row acc[head slot] (topic c only), flushed
+// once per block; the tail entries go straight to Yq.  Integer atomics in both
+// places: the result is the same exact sum as k_uside_scatter's.
+constexpr int kScatDocs = 64;
+
+__global__ void __launch_bounds__(256) k_uside_scatter_cols(const int64_t* __restrict__ vcolptr,
+                                                            const int32_t* __restrict__ vrow,
+                                                            const float* __restrict__ vval,
+                                                            const int64_t* __restrict__ atptr,
+                                                            const int32_t* __restrict__ nh,
+                                                            const int2* __restrict__ atent,
+                                                            const int32_t* __restrict__ headslot,
+                                                            const int32_t* __restrict__ headterm, int hh,
+                                                            const double* __restrict__ bound,
+                                                            const uint32_t* __restrict__ vmax, int kpad,
+                                                            unsigned long long* __restrict__ Yq) {
+  extern __shared__ unsigned long long acc[];  // [hh]
+  const int c = blockIdx.y;
+  const int64_t cb = vcolptr[c] + (int64_t)blockIdx.x * kScatDocs, ce = min(vcolptr[c + 1], cb + kScatDocs);
+  if (cb >= ce) return;  // block-uniform
+  for (int q = threadIdx.x; q < hh; q += blockDim.x) acc[q] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double B = *bound * (double)__uint_as_float(*vmax);
+  const double S = B > 0 ? 0x1p62 / B : 0.0;
+  for (int64_t e = cb + warp; e < ce; e += blockDim.x >> 5) {
+    const int32_t doc = vrow[e];
+    const double vs = (double)vval[e] * S;
+    const int64_t s = atptr[doc], eh = s + nh[doc], ee = atptr[doc + 1];
+    for (int64_t q = s + lane; q < eh; q += 32) {  // head terms: shared accumulator
+      const int2 en = atent[q];
+      const unsigned long long add = __double2ull_rn((double)__int_as_float(en.y) * vs);
+      if (add) atomicAdd(&acc[headslot[en.x]], add);
+    }
+    for (int64_t q = eh + lane; q < ee; q += 32) {  // tail terms: straight to Yq
+      const int2 en = atent[q];
+      const unsigned long long add = __double2ull_rn((double)__int_as_float(en.y) * vs);
+      if (add) atomicAdd(&Yq[(int64_t)en.x * kpad + c], add);
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < hh; q += blockDim.x)
+    if (acc[q]) atomicAdd(&Yq[(int64_t)headterm[q] * kpad + c], acc[q]);
+}
+
 // W (fp64, k x k) -> fp32 rows of stride kpad (zero padded) for k_uside_finish_rt
 __global__ void k_w_to_f32(const double* __restrict__ W, int k, int kpad, float* __restrict__ W32) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < k * kpad; q += gridDim.x * blockDim.x) {
