@@ -648,9 +648,11 @@ void uside_scatter_launch(esnmf_t* h) {
   if (h->head_h > 0 && !getenv("ESNMF_SCATTER_ROWS")) {  // by V's columns, head terms in shared memory
     const size_t smem = sizeof(unsigned long long) * h->head_h;
     CK(cudaFuncSetAttribute(k_uside_scatter_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const dim3 g((unsigned)ceil_div(std::max<int64_t>(V.maxcol, 1), kScatDocs), h->k);
+    const int nd = kScatDocs;
+    const dim3 g((unsigned)ceil_div(std::max<int64_t>(V.maxcol, 1), nd), h->k);
     k_uside_scatter_cols<<<g, 256, smem, h->stream>>>(V.colptr, V.row, V.val, sv.T.ptr, h->nh, sv.T.ent, h->headslot,
-                                                      h->headterm, h->head_h, h->rsum_max, h->vmax, h->kpad, h->Yq);
+                                                      h->headterm, h->head_h, h->rsum_max, h->vmax, h->kpad, h->Yq,
+                                                      nd);
   } else {
     k_uside_scatter<<<grid_for(V.cap_rows, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
         V.active, V.n_active, h->vmap, h->vent, sv.T.ptr, sv.T.ent, h->rsum_max, h->vmax, h->kpad, h->Yq);
