@@ -120,12 +120,17 @@ __global__ void k_cond_flag(const double* __restrict__ G, const double* __restri
                             double kmax, int* __restrict__ use_fp64) {
   __shared__ double sm[32];
   double g = 0, w = 0;
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+  // one warp per row, lanes across it (coalesced), row sums by warp reduction
+  const double e = *eps;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x >> 5; i < k; i += blockDim.x >> 5) {
     double sg = 0, sw = 0;
-    for (int j = 0; j < k; ++j) {
-      sg += fabs(G[(int64_t)i * k + j] + (i == j ? *eps : 0.0));
+    for (int j = lane; j < k; j += 32) {
+      sg += fabs(G[(int64_t)i * k + j] + (i == j ? e : 0.0));
       sw += fabs(W[(int64_t)i * k + j]);
     }
+    sg = warp_sum(sg);
+    sw = warp_sum(sw);
     g = fmax(g, sg);
     w = fmax(w, sw);
   }
