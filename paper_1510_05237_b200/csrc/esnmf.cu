@@ -434,7 +434,6 @@ void gram(esnmf_t* h, const Factor& f, double* G, int kk = 0, int kp = 0, double
     k_gram_partial<<<g, gb, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k, seglen, partial);
   }
   ++h->nlaunch; k_gram_reduce<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(partial, (int)S, k, G);
-  ++h->nlaunch; k_gram_symmetrize<<<grid_for((int64_t)k * k, 256), 256, 0, h->stream>>>(G, k);
   CKL("gram");
 }
 

@@ -264,21 +264,18 @@ __global__ void __launch_bounds__(256) k_gram_partial(const int64_t* __restrict_
   }
 }
 
+// G[i][j] = G[j][i] = the segment sum of the upper-triangle partial (i <= j):
+// both halves are the same sum, so G is exactly symmetric
 __global__ void k_gram_reduce(const double* __restrict__ partial, int S, int k, double* __restrict__ G) {
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= k * k) return;
+  const int i = q / k, j = q - i * k;
+  const int64_t u = (int64_t)min(i, j) * k + max(i, j);
   double s = 0;
-  for (int j = 0; j < S; ++j) s += partial[(int64_t)j * k * k + q];
+  for (int t = 0; t < S; ++t) s += partial[(int64_t)t * k * k + u];
   G[q] = s;
 }
 
-// symmetrise from the upper triangle (both halves are the same sum in a different order)
-__global__ void k_gram_symmetrize(double* __restrict__ G, int k) {
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= k * k) return;
-  int i = q / k, j = q - i * k;
-  if (j < i) G[q] = G[j * k + i];
-}
 
 // ---- residual R = ||U_i - U_{i-1}||_F / ||U_i||_F, direct difference ----
 // part[2*blk] += sum over new entries (v - old)^2, part[2*blk+1] += v^2
