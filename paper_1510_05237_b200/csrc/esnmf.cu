@@ -246,13 +246,16 @@ struct esnmf {
   int64_t prof_calls[16] = {0};
   std::vector<void*> allocs;
   int64_t bytes = 0;
+  double alloc_ms = 0;  // host time spent in cudaMalloc (ESNMF_CREATE_TIMING)
 
   template <typename T>
   T* alloc(int64_t count) {
     if (count <= 0) count = 1;
     void* p = nullptr;
     size_t b = sizeof(T) * (size_t)count;
+    const auto t0 = std::chrono::steady_clock::now();
     ck(cudaMalloc(&p, b), "cudaMalloc");
+    alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     allocs.push_back(p);
     bytes += (int64_t)b;
     return static_cast<T*>(p);
@@ -1954,6 +1957,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     ct.mark(h.get(), "factors + buffers");
     init_u0(h.get(), o.U0, on_dev);
     ct.mark(h.get(), "U0");
+    if (ct.on) fprintf(stderr, "esnmf_create cudaMalloc total   %8.2f ms (%zu buffers)\n", h->alloc_ms, h->allocs.size());
     CK(cudaStreamSynchronize(h->stream));
     int fl[4];
     CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
