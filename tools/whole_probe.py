@@ -1,5 +1,6 @@
+"""A few whole-factor (Alg. 2 as printed) iterations at Large, for ncu launch lists of the flat selection."""
 import sys, os
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 from paper_1510_05237_b200 import ESNMF
 cfg = synth.CONFIGS["large"]
