@@ -44,6 +44,16 @@ def parse():
     return p.parse_args()
 
 
+# what the ncu captures in profiles/ show each phase's kernel is bound by, when it is
+# not the HBM roofline it is reported against (DESIGN.md sections 5 and 8)
+BINDING = {
+    "V.spmm": "L1/L2 gather of k-wide Z rows (ncu: L1/TEX ~79 %, L2 ~70 %, DRAM ~12 % of peak; "
+              "~48 % of stall samples on the first FMA after each Z-row load)",
+    "V.head": "tcgen05 pipeline latency plus the dense head tiles' HBM reads (see V.head.tensor)",
+    "U.spmm": "64-bit fixed-point atomics of the scatter, then (Y W) on tcgen05",
+}
+
+
 def measured_bf16_tflops():
     """fp16 dense tensor peak = the measured bf16 one (same rate on B200).  The head
     kernel runs inside a long step (one iteration after another), so the sustained
@@ -302,6 +312,8 @@ def run_ours(args):
         if tr:
             r["traffic"] = tr["bytes_per_launch"]
             r["traffic_src"] = tr["source"]
+        if name in BINDING:
+            r["binding_resource"] = BINDING[name]
         return r
 
     dom = max(phases.items(), key=lambda kv: kv[1][1])[0]
