@@ -793,9 +793,8 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
     k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist, sd.pred, row0, sd.pcand, sd.pfill,
                                          sd.pcap);
     ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
-  if (peak_out) { ++h->nlaunch; k_sel_npos_sum<<<1, 256, 0, h->stream>>>(sd.sel, k, peak_out); }
     ++h->nlaunch;
-    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out);
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out, peak_out);
     int32_t* done = sd.pfill + k;
     const size_t psm = sizeof(uint64_t) * (kSelFastT + kSelCap);
     CK(cudaFuncSetAttribute(k_sel_pred_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
@@ -818,15 +817,14 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   }
   ++h->nlaunch; k_sel_hist<<<g, 256, 0, h->stream>>>(X, ldx, rows, sd.hist);
   ++h->nlaunch; k_sel_threshold<<<k, 1024, 0, h->stream>>>(sd.hist, t, sd.sel);
-  if (peak_out) { ++h->nlaunch; k_sel_npos_sum<<<1, 256, 0, h->stream>>>(sd.sel, k, peak_out); }
   if (fast) {  // two passes over X (k_sel_collect2 + k_sel_final)
+    ++h->nlaunch;
+    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out, peak_out);
     CK(cudaMemsetAsync(sd.above_fill, 0, sizeof(int32_t) * 2 * k, h->stream));
     int32_t* bfill = sd.above_fill + k;
     ++h->nlaunch;
     k_sel_collect2<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, std::max<int64_t>(t, 1),
                                              sd.above, sd.above_fill, sd.bucket, bfill);
-    ++h->nlaunch;
-    k_sel_colptr_kept<<<1, 256, 0, h->stream>>>(sd.sel, k, t, colptr_out);
     CK(cudaFuncSetAttribute(k_sel_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelFinalSmem));
     ++h->nlaunch;
     k_sel_final<<<k, 1024, kSelFinalSmem, h->stream>>>(X, ldx, rows, row0, sd.sel,
@@ -839,6 +837,7 @@ void select_core(esnmf_t* h, Side& sd, const float* X, int64_t ldx, int64_t rows
   // view (one column) gets the whole buffer, so its bucket usually fits and the
   // radix levels run over the list instead of over X
   const int ccap = kc == 1 ? (int)std::min<int64_t>((int64_t)h->k * sd.ccap, INT32_MAX) : sd.ccap;
+  if (peak_out) { ++h->nlaunch; k_sel_npos_sum<<<1, 256, 0, h->stream>>>(sd.sel, k, peak_out); }
   ++h->nlaunch; k_sel_collect<<<g, 256, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,
                                           sd.chunk_cnt, nseg, ccap);
   ++h->nlaunch; k_sel_refine<<<k, 1024, 0, h->stream>>>(X, ldx, rows, row0, sd.sel, sd.cand, sd.cand_fill,

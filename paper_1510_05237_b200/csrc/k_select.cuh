@@ -613,17 +613,24 @@ __global__ void k_sel_npos_sum(const ColSel* __restrict__ sel, int kc, int64_t* 
 }
 
 // colptr of the kept entries: min(t, #positive) per column (reading C4/C5)
-__global__ void k_sel_colptr_kept(const ColSel* __restrict__ sel, int k, int64_t t, int64_t* __restrict__ colptr) {
+// (and, when peak != nullptr, the positives of all columns: the record's peak nnz)
+__global__ void k_sel_colptr_kept(const ColSel* __restrict__ sel, int k, int64_t t, int64_t* __restrict__ colptr,
+                                  int64_t* __restrict__ peak = nullptr) {
   __shared__ int64_t sm[33];
-  int64_t v = 0;
+  int64_t v = 0, np = 0;
   if (threadIdx.x < k) {
-    const int64_t np = sel[threadIdx.x].npos;
+    np = sel[threadIdx.x].npos;
     v = t < 0 ? np : min(np, t);
   }
-  int64_t tot;
+  int64_t tot, ptot;
   const int64_t ex = block_exscan(v, sm, &tot);
   if (threadIdx.x < k) colptr[threadIdx.x] = ex;
   if (threadIdx.x == 0) colptr[k] = tot;
+  if (peak) {
+    __syncthreads();
+    block_exscan(np, sm, &ptot);
+    if (threadIdx.x == 0) *peak = ptot;
+  }
 }
 
 constexpr size_t kSelFinalSmem = sizeof(uint64_t) * (kSelCap + kSelFastT);
