@@ -86,3 +86,28 @@ def check_topt_property(ls: np.ndarray, F: np.ndarray, t: int | None):
             tie_kept = np.nonzero(kept & (x == kmin))[0]
             if len(tie_dropped):
                 assert tie_kept.max() < tie_dropped.min(), f"column {c}: tie not broken toward lower rows"
+
+
+def check_topt_property_coo(ls: np.ndarray, row, col, val, t: int | None):
+    """check_topt_property for a factor given as canonical COO (rows x k too large
+    to densify on the host, e.g. Box's 8M x 200 V): the same four conditions."""
+    row = np.asarray(row, np.int64)
+    col = np.asarray(col, np.int64)
+    val = np.asarray(val)
+    order = np.argsort(col, kind="stable")
+    bounds = np.searchsorted(col[order], np.arange(ls.shape[1] + 1))
+    for c in range(ls.shape[1]):
+        sel = order[bounds[c]:bounds[c + 1]]
+        kr, kv = row[sel], val[sel]
+        x = np.ascontiguousarray(ls[:, c])
+        npos = int(np.count_nonzero(x > 0))
+        want = npos if t is None else min(t, npos)
+        assert len(kr) == want, f"column {c}: kept {len(kr)} want {want}"
+        assert np.all(kv == x[kr]) and np.all(kv > 0)
+        if len(kr) and want < npos:
+            kmin = kv.min()
+            x[kr] = -np.inf
+            assert kmin >= x.max(), f"column {c}: dropped positive above the kept minimum"
+            tie_dropped = np.nonzero(x == kmin)[0]
+            if len(tie_dropped):
+                assert kr[kv == kmin].max() < tie_dropped.min(), f"column {c}: tie not broken toward lower rows"

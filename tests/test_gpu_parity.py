@@ -15,7 +15,7 @@ import oracle
 import synth
 from paper_1510_05237_b200 import ESNMF, ESNMF_SIDE_U, ESNMF_SIDE_V, ESNMFError
 from parity import (TRAJ_TOL, check_canonical, check_products, check_selection, check_topt_property,
-                    coo_dense)
+                    check_topt_property_coo, coo_dense)
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -310,6 +310,91 @@ def test_large_sampled_parity():
         out = dense_V(s, cfg.m, cfg.k) if side == ESNMF_SIDE_V else dense_U(s, cfg.n, cfg.k)
         check_topt_property(ls, out, cfg.t)
     del gd
+    torch.cuda.empty_cache()
+
+
+def _rows_restricted(ptr, idx, val, support, dim):
+    """CSR of the rows of T (given as ptr/idx/val) with every column outside
+    `support` (the rows of the sparse factor that hold a nonzero; columns range
+    over [0, dim)) dropped and the rest renumbered into `support` -- input
+    marshalling: the dropped terms multiply exact-zero factor rows, so
+    T F == T' F[support]."""
+    remap = np.full(dim, -1, np.int64)
+    remap[support] = np.arange(len(support))
+    optr, oidx, oval = [0], [], []
+    for r in range(len(ptr) - 1):
+        c = remap[idx[ptr[r]:ptr[r + 1]]]
+        keep = c >= 0
+        oidx.append(c[keep].astype(np.int32))
+        oval.append(val[ptr[r]:ptr[r + 1]][keep])
+        optr.append(optr[-1] + int(keep.sum()))
+    return np.asarray(optr, np.int64), np.concatenate(oidx), np.concatenate(oval)
+
+
+def _support_dense(coo, k):
+    """(support rows, dense fp64 factor restricted to them) from canonical COO."""
+    r, c, v = coo
+    sup = np.unique(np.asarray(r, np.int64))
+    F = np.zeros((len(sup), k), np.float64)
+    F[np.searchsorted(sup, r), c] = v
+    return sup, F
+
+
+@pytest.mark.slow
+def test_box_sampled_parity():
+    """Box (BJ:10: 1M x 8M, 1.6B entries, k = 200, t = 5,000) at full size on one
+    GPU: sampled LS rows of both sides against the oracle row by row (the head term
+    rows included), and the top-t property on every column of both factors.  The
+    sampled rows of A / A^T are read from the seeded device generator's output
+    (the host generator would need ~40 GB for the whole matrix)."""
+    import torch
+
+    cfg = synth.CONFIGS["box"]
+    rng = np.random.default_rng(0)
+    gd = synth.generate_device(cfg)
+    docs = np.sort(rng.choice(cfg.m, 1000, replace=False))
+    terms = np.unique(np.concatenate([np.arange(8), rng.choice(cfg.n, 1000, replace=False)]))
+    d = cfg.d
+    at_idx = gd["at_col"].view(cfg.m, d)[torch.from_numpy(docs).cuda()].cpu().numpy()
+    at_val = gd["at_val"].view(cfg.m, d)[torch.from_numpy(docs).cuda()].cpu().numpy()
+    a_ptr_all = gd["a_ptr"].cpu().numpy()
+    a_rows = [(gd["a_col"][a_ptr_all[i]:a_ptr_all[i + 1]].cpu().numpy(),
+               gd["a_val"][a_ptr_all[i]:a_ptr_all[i + 1]].cpu().numpy()) for i in terms]
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, gd, seed=cfg.seed)
+    del gd
+    torch.cuda.empty_cache()
+    s.iterate(2)
+    # V side: LS_V[docs] = (A^T[docs] U) (G_U + eps I)^-1
+    supU, FU = _support_dense(s.get_U(), cfg.k)
+    L, _ = oracle.cholesky(oracle.gram(FU))
+    ptr = np.arange(len(docs) + 1, dtype=np.int64) * d
+    tptr, tidx, tval = _rows_restricted(ptr, at_idx.ravel(), at_val.ravel(), supU, cfg.n)
+    ref = oracle.solve_rows(L, oracle.spmm_rows(np.arange(len(docs)), tptr, tidx, tval, FU))
+    s.half_step(ESNMF_SIDE_V)
+    _, ls = s.get_ls(ESNMF_SIDE_V)
+    scale = np.abs(ls).max(axis=0).astype(np.float64)
+    assert (np.abs(ls[docs].astype(np.float64) - ref) / scale).max() <= 1e-5
+    Vcoo = s.get_V()
+    check_canonical(Vcoo[0], Vcoo[1], cfg.k)
+    check_topt_property_coo(ls, *Vcoo, cfg.t)
+    del ls
+    # U side: LS_U[terms] = (A[terms] V) (G_V + eps I)^-1
+    supV, FV = _support_dense(Vcoo, cfg.k)
+    L, _ = oracle.cholesky(oracle.gram(FV))
+    rptr = np.zeros(len(terms) + 1, np.int64)
+    rptr[1:] = np.cumsum([len(c) for c, _ in a_rows])
+    ridx = np.concatenate([c for c, _ in a_rows])
+    rval = np.concatenate([v for _, v in a_rows])
+    tptr, tidx, tval = _rows_restricted(rptr, ridx, rval, supV, cfg.m)
+    ref = oracle.solve_rows(L, oracle.spmm_rows(np.arange(len(terms)), tptr, tidx, tval, FV))
+    s.half_step(ESNMF_SIDE_U)
+    _, ls = s.get_ls(ESNMF_SIDE_U)
+    scale = np.abs(ls).max(axis=0).astype(np.float64)
+    assert (np.abs(ls[terms].astype(np.float64) - ref) / scale).max() <= 1e-5
+    Ucoo = s.get_U()
+    check_canonical(Ucoo[0], Ucoo[1], cfg.k)
+    check_topt_property_coo(ls, *Ucoo, cfg.t)
+    s.close()
     torch.cuda.empty_cache()
 
 
