@@ -48,7 +48,8 @@ def parse():
 # not the HBM roofline it is reported against (DESIGN.md sections 5 and 8)
 BINDING = {
     "V.spmm": "L1/L2 gather of k-wide Z rows (ncu: L1/TEX ~79 %, L2 ~70 %, DRAM ~12 % of peak; "
-              "~48 % of stall samples on the first FMA after each Z-row load)",
+              "~48 % of stall samples on the first FMA after each Z-row load; a bare gather of the same "
+              "28.1M 512-B rows, tools/l2_gather_probe.cu, needs >= 0.975 ms on this B200)",
     "V.head": "tcgen05 pipeline latency plus the dense head tiles' HBM reads (see V.head.tensor)",
     "U.spmm": "64-bit fixed-point atomics of the scatter, then (Y W) on tcgen05",
 }
