@@ -188,6 +188,38 @@ def head_split(g, cfg, h: int, nd: int):
     return (h, head_nnz, nd)
 
 
+def gather_roofline(g, cfg, s, h: int, phase):
+    """The tail gather (k_spmm_tail) against its own binding resource: Z-row bytes
+    gathered from L2 per launch (active tail entries of A^T -- term outside the head
+    and its U row nonzero, counted from the last U -- x the zero-padded Z row) over
+    the measured rate of a bare gather of that pattern (tools/l2_gather_probe.cu, best
+    512-B-row line of profiles/r1j_l2_gather_probe.txt; the tail kernel batches its
+    index loads, the probe does not, so frac can exceed 1).  Measurement only."""
+    import re
+
+    import numpy as np
+    import torch
+
+    rows = torch.from_numpy(np.asarray(s.get_U()[0], np.int64)).to(g["at_col"].device)
+    active = torch.bincount(rows, minlength=cfg.n) > 0
+    df = (g["a_ptr"][1:] - g["a_ptr"][:-1]).to(torch.int64)
+    active[torch.argsort(-df, stable=True)[:h]] = False
+    n_act = int(active[g["at_col"].to(torch.int64)].sum().item())
+    kpad = -(-cfg.k // 4) * 4
+    zrow = 512 * -(-kpad // 128)
+    calls, pms = phase
+    ach = n_act * zrow / (pms / max(calls, 1) / 1e3) / 1e12
+    peak, src = None, "profiles/r1j_l2_gather_probe.txt missing"
+    path = os.path.join(ROOT, "profiles", "r1j_l2_gather_probe.txt")
+    if os.path.exists(path):
+        vals = [float(x) for x in re.findall(r"512B\s+blocks\s+\d+\s+[\d.]+ ms\s+([\d.]+) TB/s", open(path).read())]
+        if vals:
+            peak, src = max(vals), "tools/l2_gather_probe.cu on a B200: best 512-B-row gather rate (profiles/r1j_l2_gather_probe.txt)"
+    return {"bound": "l2_gather", "achieved": round(ach, 2), "peak": peak, "unit": "TB/s",
+            "frac": round(ach / peak, 4) if peak else None, "peak_src": src, "active_tail_entries": n_act,
+            "z_row_bytes": zrow}
+
+
 def oracle_sample_step(g, U, V, cfg, frac: float) -> tuple[float, float]:
     """One oracle iteration on a row-strided sample: the V half-step for every
     (1/frac)-th document and the U half-step for every (1/frac)-th term, with the
@@ -335,6 +367,8 @@ def run_ours(args):
                                     "frac": round(tf / pk[0], 4), "peak_src": pk[1],
                                     "frac_of_burst_peak": round(tf / pk[2], 4) if pk[2] else None,
                                     "flops_per_launch": fl, "head_terms": split[0], "head_nnz": split[1]}
+    if split[0] > 0 and "V.spmm" in phases and phases["V.spmm"][0] and world == 1:
+        kernels["V.spmm.gather"] = gather_roofline(g, cfg, s, split[0], phases["V.spmm"])
     phase_table = {k: {"calls": c, "ms_per_call": round(v / max(c, 1), 4), "share": round(v / prof_ms, 4)}
                    for k, (c, v) in phases.items() if c}
     # whole-iteration algorithmic bytes: 16 nnz + 8 (n + m + 2) + 32 k t

@@ -5,9 +5,13 @@
 // tail gather (k_spmm_tail) measured on this B200.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_gather_probe tools/l2_gather_probe.cu
-//   ./l2_gather_probe [rows=12068] [gathers=28105323]
+//   ./l2_gather_probe [rows=12068] [gathers=28105323] [zipf_s=0 [zipf_offset=1024]]
+// zipf_s > 0 draws row r with probability ~ 1 / (offset + r)^s (the tail's active terms
+// are Zipf ranks after the head), else uniformly.
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <cmath>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -62,12 +66,17 @@ void run(const char* name, const float4* z, const int* idx, const float* w, long
 int main(int argc, char** argv) {
   const long rows = argc > 1 ? atol(argv[1]) : 12068;
   const long n = argc > 2 ? atol(argv[2]) : 28105323;
+  const double zs = argc > 3 ? atof(argv[3]) : 0.0;
+  const double zo = argc > 4 ? atof(argv[4]) : 1024.0;
+  std::vector<double> cdf(rows);
+  for (long r = 0; r < rows; ++r) cdf[r] = (r ? cdf[r - 1] : 0.0) + (zs > 0 ? 1.0 / pow(zo + r, zs) : 1.0);
   std::vector<int> hi(n);
   std::vector<float> hw(n);
   unsigned long long s = 88172645463325252ull;
   for (long i = 0; i < n; ++i) {
     s ^= s << 13; s ^= s >> 7; s ^= s << 17;
-    hi[i] = (int)(s % rows);
+    const double u = (double)(s >> 11) * (1.0 / 9007199254740992.0) * cdf[rows - 1];
+    hi[i] = (int)std::min<long>(rows - 1, std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
     hw[i] = 1.0f + (float)(s >> 40) * 1e-7f;
   }
   float4 *z, *out;
@@ -83,7 +92,8 @@ int main(int argc, char** argv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int maxb = sms * 8;
   CK(cudaMalloc(&out, (long)maxb * 256 * 16));
-  printf("table %ld rows (%.1f MB), %ld gathers, %d SMs\n", rows, rows * 512 / 1e6, n, sms);
+  printf("table %ld rows (%.1f MB), %ld gathers, %d SMs, rows %s (s = %.2f, offset %.0f)\n", rows, rows * 512 / 1e6, n, sms,
+         zs > 0 ? "Zipf" : "uniform", zs, zo);
   for (int bps : {3, 4, 6, 8}) {
     run<4, 32>("D=4 512B", z, idx, w, n, out, sms * bps);
     run<4, 25>("D=4 400B (25 lanes)", z, idx, w, n, out, sms * bps);
