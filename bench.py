@@ -49,7 +49,7 @@ def parse():
 BINDING = {
     "V.spmm": "L1/L2 gather of k-wide Z rows (ncu: L1/TEX ~79 %, L2 ~70 %, DRAM ~12 % of peak; "
               "~48 % of stall samples on the first FMA after each Z-row load; a bare gather of the same "
-              "28.1M 512-B rows, tools/l2_gather_probe.cu, needs >= 0.975 ms on this B200)",
+              "28.1M 512-B rows, tools/l2_gather_probe.cu, needs >= 0.972 ms on this B200)",
     "V.head": "tcgen05 pipeline latency plus the dense head tiles' HBM reads (see V.head.tensor)",
     "U.spmm": "64-bit fixed-point atomics of the scatter, then (Y W) on tcgen05",
 }
@@ -369,6 +369,9 @@ def run_ours(args):
                                     "flops_per_launch": fl, "head_terms": split[0], "head_nnz": split[1]}
     if split[0] > 0 and "V.spmm" in phases and phases["V.spmm"][0] and world == 1:
         kernels["V.spmm.gather"] = gather_roofline(g, cfg, s, split[0], phases["V.spmm"])
+        if roof and roof.get("kernel") == "V.spmm":
+            gv = kernels["V.spmm.gather"]
+            roof["binding_view"] = {k: gv[k] for k in ("bound", "achieved", "peak", "unit", "frac")}
     phase_table = {k: {"calls": c, "ms_per_call": round(v / max(c, 1), 4), "share": round(v / prof_ms, 4)}
                    for k, (c, v) in phases.items() if c}
     # whole-iteration algorithmic bytes: 16 nnz + 8 (n + m + 2) + 32 k t
