@@ -203,9 +203,7 @@ __global__ void __launch_bounds__(1024) k_sel_refine(const float* __restrict__ X
                                                      const int32_t* __restrict__ cand_fill,
                                                      int64_t* __restrict__ chunk_cnt, int64_t nchunks,
                                                      uint64_t* __restrict__ kthr, int ccap) {
-  __shared__ uint64_t keys[kSelCap];           // sort buffer (common path)
-  uint32_t* h = reinterpret_cast<uint32_t*>(keys);  // histogram (fallback path)
-  __shared__ int64_t sm[33];
+  __shared__ uint64_t keys[kSelCap];           // sort buffer
   const int c = blockIdx.x;
   const ColSel s = sel[c];
   // kthr[c] = (tb << 32) | tr: keep x > 0 iff bits(x) > tb or (bits(x) == tb and row <= tr)
