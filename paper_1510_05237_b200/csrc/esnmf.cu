@@ -38,6 +38,7 @@
 #include "k_vhead.cuh"
 #include "k_uside_tc.cuh"
 #include "k_spmm_tail.cuh"
+#include "k_vtail.cuh"
 #include "k_seq.cuh"
 
 using namespace esk;
@@ -213,6 +214,26 @@ struct esnmf {
   uint8_t* atile = nullptr;      // [tiles][nd][32 KB] dense fp16 hi/lo tiles of those chunks
   int64_t* hoff = nullptr;       // [tiles * sparse chunks + 1] segment offsets of the tiled head copy
   int2* hseg = nullptr;          // head entries by (tile, chunk): (row in tile << 6 | slot, value)
+  // V-side tail in the paper's order (k_vtail.cuh): A^T_tail U per tile, then
+  // (Y_tail W) as nyc extra K-chunks of the head kernel; off: the Z-row gather
+  bool ptail = false;
+  int nyc = 0;
+  int64_t* toff = nullptr;       // [tiles + 1] tail entries of each tile (jagged-diagonal order)
+  int2* tent = nullptr;          // (row in tile << 24 | term, value)
+  uint8_t* ytile = nullptr;      // [tiles][128 x kn x 4 B] Y_tail as fp16 hi/lo chunks
+  uint8_t* wbuf = nullptr;       // [nyc][kn x 64 x 4 B] W' as the B operand
+  unsigned* rowsum_bits = nullptr;  // max document row sum of A^T (float bits, rounded up; global)
+  uint64_t* umap = nullptr;      // [n] U row view: (first << 32) | count
+  int2* uent = nullptr;          // [U cap] (column, value * 2^s_c)
+  int64_t* urptr = nullptr;      // [U cap_rows + 1]
+  int64_t* ucursor = nullptr;
+  int64_t* uscan = nullptr;
+  int32_t* ulist = nullptr;      // rows published in umap (cleared before the next build)
+  int64_t* ulist_n = nullptr;
+  uint32_t* umax = nullptr;      // [k] max of U over the tail rows, per column (float bits)
+  int* ushift = nullptr;         // [k] fixed-point exponents s_c
+  uint32_t* gmax_buf = nullptr;  // multi-rank: allgather of {amax, rowsum} (16 B per rank)
+  cudaEvent_t ev_vfork = nullptr, ev_vjoin = nullptr;
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -268,7 +289,7 @@ struct esnmf {
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (aux) cudaStreamSynchronize(aux);
-    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin})
+    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin})
       if (e) cudaEventDestroy(e);
     if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -985,7 +1006,8 @@ void vhead_launch_st(esnmf_t* h) {
   kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
                                                    h->colscale,
                                                    sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
-                                                   h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad, fz);
+                                                   h->head_acc_cols, sv.X, sv.ldx, h->ptail ? nullptr : sv.Xt, h->kpad,
+                                                   fz, h->ytile, h->wbuf, h->ptail ? h->nyc : 0);
   CKL("vhead");
 }
 
@@ -1006,21 +1028,26 @@ void vhead_launch(esnmf_t* h) {
 bool narrow_v(esnmf_t* h) { return h->kpad <= 8 && h->world == 1 && !getenv("ESNMF_NO_NARROW"); }
 
 void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
-  if (want == 0) return;
   if (narrow_v(h)) return;  // narrow k: the V side is an SpMM with a compact z (k_spmm_narrow)
+  // the paper-order tail needs the term id in 24 bits of a packed entry
+  h->ptail = h->n < (1LL << kVtTermBits) && !getenv("ESNMF_ZTAIL");
   const char* env = getenv("ESNMF_HEAD");
   if (env && env[0]) want = atoi(env);
-  if (want == 0) return;
+  if (want == 0 && !h->ptail) return;
   const int64_t n = h->n;
   std::vector<int32_t> order(n);
   for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
   std::stable_sort(order.begin(), order.end(),
                    [&](int32_t a, int32_t b) { return hptr[a + 1] - hptr[a] > hptr[b + 1] - hptr[b]; });
   int64_t hh;
-  if (want > 0) {
+  if (want >= 0) {
     hh = std::min<int64_t>(want, n);
   } else {
-    double frac = 0.015;
+    // document-frequency threshold of a head term.  Z-gather tail: 1.5 % (the
+    // dense-tile cost balanced a 400-byte gather per active entry).  Paper-order
+    // tail: a tail entry costs nnz(U row) products instead, so the head keeps only
+    // the densest term bands
+    double frac = h->ptail ? 0.025 : 0.015;
     const char* fe = getenv("ESNMF_HEAD_DF");
     if (fe && fe[0]) frac = atof(fe);
     const double min_df = std::max(1.0, frac * (double)h->m);
@@ -1028,7 +1055,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     while (hh < n && (double)(hptr[order[hh] + 1] - hptr[order[hh]]) >= min_df) ++hh;
   }
   hh = std::min<int64_t>(hh, kHeadMax) / kHeadK * kHeadK;
-  if (hh < kHeadK) return;
+  if (hh < kHeadK && !h->ptail) return;
   Side& sv = h->side[ESNMF_SIDE_V];
   h->kn = (h->k + 15) / 16 * 16;
   h->head_acc_cols = h->kn <= 32 ? 32 : h->kn <= 64 ? 64 : h->kn <= 128 ? 128 : 256;
@@ -1037,20 +1064,20 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   h->head_ntiles = ceil_div(std::max<int64_t>(sv.rows, 1), kHeadM);
   std::vector<int32_t> slot(n, -1);
   for (int64_t s = 0; s < hh; ++s) slot[order[s]] = (int32_t)s;
-  h->headterm = h->alloc<int32_t>(hh);
+  h->headterm = h->alloc<int32_t>(std::max<int64_t>(hh, 1));
   h->headslot = h->alloc<int32_t>(n);
-  CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
+  if (hh > 0) CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
-  h->zhead = h->alloc<uint8_t>((int64_t)h->head_nchunks * h->kn * kHeadK * 4);
-  sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);
+  h->zhead = h->alloc<uint8_t>(std::max<int64_t>(1, (int64_t)h->head_nchunks * h->kn * kHeadK * 4));
+  if (!h->ptail) sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);
   h->colscale = h->alloc<float>(h->kn);
   h->amax_bits = h->alloc<unsigned>(1);
-  CK(cudaMemsetAsync(h->zhead, 0, (size_t)h->head_nchunks * h->kn * kHeadK * 4, h->stream));
+  CK(cudaMemsetAsync(h->zhead, 0, std::max<size_t>(1, (size_t)h->head_nchunks * h->kn * kHeadK * 4), h->stream));
   CK(cudaMemsetAsync(h->colscale, 0, sizeof(float) * h->kn, h->stream));
   CK(cudaMemsetAsync(h->amax_bits, 0, sizeof(unsigned), h->stream));
-  // rows of A^T: head entries first (stable), so the tail gather skips them
+  // rows of A^T: head entries first (stable), so the tail reads skip them
   h->nh = h->alloc<int32_t>(std::max<int64_t>(sv.rows, 1));
-  if (sv.T.nnz > 0) {
+  if (sv.T.nnz > 0 && hh > 0) {
     int2* tmp = nullptr;
     CK(cudaMalloc(&tmp, sizeof(int2) * sv.T.nnz));
     ++h->nlaunch;
@@ -1065,8 +1092,28 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   ++h->nlaunch;
   k_absmax_ent<<<grid_for(std::max<int64_t>(sv.T.nnz, 1), 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
       sv.T.ent, sv.T.nnz, h->amax_bits);
+  if (h->ptail) {
+    h->rowsum_bits = h->alloc<unsigned>(1);
+    CK(cudaMemsetAsync(h->rowsum_bits, 0, sizeof(unsigned), h->stream));
+    ++h->nlaunch;
+    k_doc_rowsum_max<<<grid_for(std::max<int64_t>(sv.rows, 1), 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+        sv.T.ptr, sv.T.ent, sv.rows, h->rowsum_bits);
+  }
+  if (h->world > 1) {
+    // the scales derived from max|A| and the largest document row sum must be the
+    // same on every rank (every rank then rounds exactly as one GPU would)
+    h->gmax_buf = h->alloc<uint32_t>(4 * (h->world + 1));
+    CK(cudaMemsetAsync(h->gmax_buf, 0, sizeof(uint32_t) * 4 * (h->world + 1), h->stream));
+    CK(cudaMemcpyAsync(h->gmax_buf, h->amax_bits, 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (h->rowsum_bits) CK(cudaMemcpyAsync(h->gmax_buf + 1, h->rowsum_bits, 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (h->comm.allgather(h->comm.ctx, h->gmax_buf, h->gmax_buf + 4, 16, h->stream) != 0)
+      fail(ESNMF_ECOMM, "allgather(scales) failed");
+    unsigned* rs = h->rowsum_bits ? h->rowsum_bits : h->gmax_buf + 2;
+    ++h->nlaunch;
+    k_rank_max2<<<1, 1, 0, h->stream>>>(h->gmax_buf + 4, h->world, h->amax_bits, rs);
+  }
   // the densest chunks as dense tiles (bulk-copied as they are) ...
-  {
+  if (hh > 0) {
     // 8 dense chunks measured best at Large (0.62 ms vs 0.64 for 4, 0.77 for all 16);
     // capped at 4 GB of dense tiles
     int nd = (int)std::min<int64_t>(512 / kHeadK, (int64_t)(4LL << 30) / std::max<int64_t>(1, h->head_ntiles * kHeadABytes));
@@ -1088,27 +1135,108 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     const int64_t nseg = h->head_ntiles * nsp;
     h->hoff = h->alloc<int64_t>(nseg + 1);
     CK(cudaMemsetAsync(h->hoff, 0, sizeof(int64_t) * (nseg + 1), h->stream));
-    auto* cnt = reinterpret_cast<unsigned long long*>(h->hoff);
-    const unsigned g = grid_for(sv.rows, 8, (int64_t)h->num_sms * 32);
+    if (nseg > 0) {
+      auto* cnt = reinterpret_cast<unsigned long long*>(h->hoff);
+      const unsigned g = grid_for(sv.rows, 8, (int64_t)h->num_sms * 32);
+      ++h->nlaunch;
+      k_head_count<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cnt);
+      launch_scan_inplace(h, h->hoff, nseg + 1, h->alloc<int64_t>(1));  // hoff[nseg] = total
+      int64_t nhe = 0;
+      CK(cudaMemcpyAsync(&nhe, h->hoff + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      h->hseg = h->alloc<int2>(std::max<int64_t>(nhe, 1));
+      unsigned long long* cursor = nullptr;
+      CK(cudaMalloc(&cursor, sizeof(int64_t) * (nseg + 1)));
+      CK(cudaMemcpyAsync(cursor, h->hoff, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToDevice, h->stream));
+      ++h->nlaunch;
+      k_head_fill<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cursor,
+                                           h->hseg);
+      CK(cudaStreamSynchronize(h->stream));
+      CK(cudaFree(cursor));
+    } else {
+      h->hseg = h->alloc<int2>(1);
+    }
+  }
+  if (h->ptail) {  // paper-order tail: per-tile jagged-diagonal tail entries, Y_tail tiles, W', U row view
+    const int64_t nt = h->head_ntiles;
+    h->nyc = (h->kn + kHeadK - 1) / kHeadK;
+    h->toff = h->alloc<int64_t>(nt + 1);
+    CK(cudaMemsetAsync(h->toff, 0, sizeof(int64_t) * (nt + 1), h->stream));
     ++h->nlaunch;
-    k_head_count<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cnt);
-    launch_scan_inplace(h, h->hoff, nseg + 1, h->alloc<int64_t>(1));  // hoff[nseg] = total
-    int64_t nhe = 0;
-    CK(cudaMemcpyAsync(&nhe, h->hoff + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    k_vt_count<<<(unsigned)nt, kVtM, 0, h->stream>>>(sv.T.ptr, hh > 0 ? h->nh : nullptr, sv.rows, h->toff);
+    launch_scan_inplace(h, h->toff, nt + 1, h->alloc<int64_t>(1));
+    int64_t ntail = 0;
+    CK(cudaMemcpyAsync(&ntail, h->toff + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    h->hseg = h->alloc<int2>(std::max<int64_t>(nhe, 1));
-    unsigned long long* cursor = nullptr;
-    CK(cudaMalloc(&cursor, sizeof(int64_t) * (nseg + 1)));
-    CK(cudaMemcpyAsync(cursor, h->hoff, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToDevice, h->stream));
+    h->tent = h->alloc<int2>(std::max<int64_t>(ntail, 1));
     ++h->nlaunch;
-    k_head_fill<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cursor,
-                                         h->hseg);
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaFree(cursor));
+    k_vt_fill<<<(unsigned)nt, kVtM, 0, h->stream>>>(sv.T.ptr, hh > 0 ? h->nh : nullptr, sv.T.ent, sv.rows, h->toff,
+                                                   h->tent);
+    h->ytile = h->alloc<uint8_t>(nt * kVtM * h->kn * 4);
+    const int64_t wb = (int64_t)h->nyc * h->kn * kHeadK * 4;
+    h->wbuf = h->alloc<uint8_t>(wb);
+    CK(cudaMemsetAsync(h->wbuf, 0, wb, h->stream));
+    h->umap = h->alloc<uint64_t>(n);
+    CK(cudaMemsetAsync(h->umap, 0, sizeof(uint64_t) * n, h->stream));
+    h->uent = h->alloc<int2>(n * (int64_t)h->k);
+    h->urptr = h->alloc<int64_t>(n + 1);
+    h->ucursor = h->alloc<int64_t>(n + 1);
+    h->uscan = h->alloc<int64_t>(ceil_div(n + 1, kScanBlock) + 1);
+    h->ulist = h->alloc<int32_t>(n);
+    h->ulist_n = h->alloc<int64_t>(1);
+    CK(cudaMemsetAsync(h->ulist_n, 0, sizeof(int64_t), h->stream));
+    h->umax = h->alloc<uint32_t>(h->k);
+    h->ushift = h->alloc<int>(h->k);
   }
   CKL("head_setup");
   // host vectors die here: make the async uploads complete first
   CK(cudaStreamSynchronize(h->stream));
+}
+
+// ---- paper-order V-side tail (k_vtail.cuh) ----
+// U row view of the factor the V side reads: umap / uent (values scaled by 2^s_c)
+void urows_build(esnmf_t* h, const Factor& f) {
+  const int64_t nr = f.cap_rows + 1;
+  h->nlaunch += 1;
+  k_urows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(h->ulist, h->ulist_n, h->umap);
+  CK(cudaMemsetAsync(h->urptr, 0, sizeof(int64_t) * nr, h->stream));
+  dim3 g(col_grid_x(f.maxcol), h->k);
+  ++h->nlaunch;
+  k_vrows_count<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, h->urptr);
+  const int64_t nb = ceil_div(nr, kScanBlock);
+  h->nlaunch += 3;
+  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan);
+  k_scan_small<<<1, 1024, 0, h->stream>>>(h->uscan, nb, h->uscan + nb);
+  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan);
+  CK(cudaMemcpyAsync(h->ucursor, h->urptr, sizeof(int64_t) * nr, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemsetAsync(h->umax, 0, sizeof(uint32_t) * h->k, h->stream));
+  h->nlaunch += 3;
+  k_urows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->head_h > 0 ? h->headslot : nullptr,
+                                            h->ucursor, h->uent, h->umax);
+  k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->urptr, h->umap,
+                                                                         h->ulist, h->ulist_n);
+  k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(f.colptr + h->k, h->uent, h->k,
+                                                                                   h->umax, h->rowsum_bits, h->ushift);
+  CKL("urows_build");
+}
+
+void ytail_launch(esnmf_t* h) {
+  const int ys = h->kn | 1;
+  const size_t smem = sizeof(uint32_t) * kVtM * ys;
+  CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(3, (int)((h->smem_optin + 1024) / (smem + 1024))));
+  const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, (int64_t)h->num_sms * per_sm);
+  ++h->nlaunch;
+  k_ytail<<<grid, kVtThreads, smem, h->stream>>>(h->toff, h->tent, h->head_ntiles, h->umap, h->uent, h->kn, ys,
+                                                  h->ytile);
+  CKL("ytail");
+}
+
+void vside_prep(esnmf_t* h, const Factor& f) {
+  ++h->nlaunch;
+  k_vside_prep<<<h->k, 256, 0, h->stream>>>(f.dense, f.rowmap, h->kpad, h->headterm, h->head_h, h->W, h->k, h->kn,
+                                            h->amax_bits, h->ushift, h->zhead, h->wbuf, h->colscale);
+  CKL("vside_prep");
 }
 
 // one half-step; returns the factor that was written
@@ -1120,7 +1248,23 @@ Factor& half_step(esnmf_t* h, int s) {
   const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
   const bool overlap_u = s == ESNMF_SIDE_U && h->world == 1;    // Gram + solve on aux, beside the scatter
   if (s == ESNMF_SIDE_U) join_metrics(h);  // (only pending after a bare half_step call)
-  if (!(overlap_u && h->u_prefork)) {
+  if (s == ESNMF_SIDE_V && h->ptail) {
+    // paper-order tail (k_vtail.cuh): Y_tail = A^T_tail U needs only U, so the
+    // Gram + solve (a1, a2) run on aux beside it; then Z_head = U_head W, the
+    // scales, and the tensor-core kernel: head chunks + (Y_tail W) chunks
+    { Phase ph(h, kVFormZ); urows_build(h, in); }
+    fork_to_aux(h, h->ev_vfork);
+    {
+      OnStream os(h, h->aux);
+      if (!h->gramU_valid) { Phase ph(h, p0 + 0); gram(h, in, sd.G); }   // a1: P:63
+      { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                    // a2
+    }
+    { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
+    join_from_aux(h, h->ev_vjoin);
+    h->aux_pending = false;  // the join covers the previous record's kernels too
+    { Phase ph(h, kVFormZ); vside_prep(h, in); }
+    { Phase ph(h, kVHead); vhead_launch(h); }                             // a3 + a4 (head, tail x W)
+  } else if (!(overlap_u && h->u_prefork)) {
     if (overlap_u) fork_to_aux(h, h->ev_ufork);
     OnStream os(h, overlap_u ? h->aux : h->stream);
     if (!(s == ESNMF_SIDE_V && h->gramU_valid)) {                 // a1: P:63 / P:64
@@ -1131,9 +1275,11 @@ Factor& half_step(esnmf_t* h, int s) {
     if (overlap_u) uside_w_prep(h);
   }
   h->u_prefork = false;
-  if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
-  { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
-  if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
+  if (!(s == ESNMF_SIDE_V && h->ptail)) {
+    if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
+    { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
+    if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
+  }
   seq_deflate(h, s);                                               // Alg. 3: Eq. (7) / (8)
   sd.ls_valid = true;
   {
@@ -1237,9 +1383,10 @@ void flush_metrics(esnmf_t* h) {
   CKL("metrics");
   const double* t_red = nullptr;
   if (h->world > 1) {
-    ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gtr, h->scal + 3);
-    if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 1, h->stream) != 0)
-      fail(ESNMF_ECOMM, "allreduce(T) failed");
+    ++h->nlaunch;
+    k_rank_scalars<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gtr, su.peak, h->side[ESNMF_SIDE_V].peak, h->scal + 3);
+    if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 3, h->stream) != 0)
+      fail(ESNMF_ECOMM, "allreduce(T, peaks) failed");
     t_red = h->scal + 3;
   }
   ensure_records(h, h->nrec + 1);
@@ -1774,7 +1921,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
       CK(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, greatest));
     }
-    for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin})
+    for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin, &h->ev_vfork, &h->ev_vjoin})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;

@@ -106,7 +106,7 @@ struct RecordInputs {
   const int64_t* peak_v;
   double normA2;
   int k;
-  const double* t_reduced;  // if non-null: T already summed over ranks
+  const double* t_reduced;  // if non-null: {T, peak_u, peak_v} already summed over ranks
   // sequential ALS (Alg. 3): the record covers U = [U_1 U_2 0], V = [V_1 V_2 0]; the
   // pipeline's factors are the block (k columns), U_1 / V_1 the frozen columns
   // [0, b0) of ktot.  seqc = {T_1, S_11, ||U_1||^2}; null otherwise.
@@ -168,8 +168,12 @@ __global__ void k_finalize_record(RecordInputs in, esnmf_record* __restrict__ re
     r.dead_v = dead_v;
     r.active_u = *in.nact_u;
     r.active_v = *in.nact_v;
-    r.peak_u = in.peak_u ? *in.peak_u + fnnz_u : -1;
-    r.peak_v = in.peak_v ? *in.peak_v + fnnz_v : -1;
+    // multi-rank: each rank counted the positives of its own rows; the sums
+    // (integers < 2^53, exact in fp64) came back with T
+    const int64_t pu = in.t_reduced ? (int64_t)in.t_reduced[1] : (in.peak_u ? *in.peak_u : -1);
+    const int64_t pv = in.t_reduced ? (int64_t)in.t_reduced[2] : (in.peak_v ? *in.peak_v : -1);
+    r.peak_u = pu >= 0 ? pu + fnnz_u : -1;
+    r.peak_v = pv >= 0 ? pv + fnnz_v : -1;
     *rec = r;
     *nrec = slot + 1;
     scal[0] = num;
@@ -194,6 +198,19 @@ __global__ void k_reduce_to(const double* __restrict__ part, int64_t n, double* 
   __shared__ double sm[32];
   const double s = reduce_fixed(part, n, 1, sm);
   if (threadIdx.x == 0) *out = s;
+}
+
+// multi-rank record scalars before their allreduce: out = {T partial of this
+// rank, this rank's peak_u, peak_v} (the peaks as exact fp64 integers)
+__global__ void k_rank_scalars(const double* __restrict__ part, int64_t n, const int64_t* __restrict__ peak_u,
+                               const int64_t* __restrict__ peak_v, double* __restrict__ out) {
+  __shared__ double sm[32];
+  const double s = reduce_fixed(part, n, 1, sm);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = peak_u ? (double)*peak_u : -1.0;
+    out[2] = peak_v ? (double)*peak_v : -1.0;
+  }
 }
 
 }  // namespace esk

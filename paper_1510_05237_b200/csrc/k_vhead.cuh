@@ -38,6 +38,8 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <climits>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -112,6 +114,93 @@ __global__ void k_zhead_prep(const float* __restrict__ Z, int zs, const int32_t*
     const uint32_t off = tc::kmajor_off16(c, s % kHeadK, kHeadK);
     *reinterpret_cast<__half*>(b + off) = hi;
     *reinterpret_cast<__half*>(b + zhalf + off) = lo;
+  }
+}
+
+// Paper-order tail mode (k_vtail.cuh): one CTA per topic column c.
+//   Z_head[s][c] = sum_j U[headterm[s]][j] W[j][c]   (fp64; U's dense active rows)
+//   one accumulator scale 2^sc_c for both parts of LS_V[:, c]:
+//     head:  A' = A 2^eA,             Z'[s][c] = Z 2^(sc_c - eA)
+//     tail:  Y' = Y 2^(s_j - 15),     W'[j][c] = W 2^(sc_c - s_j + 15)
+//   sc_c the largest exponent keeping max |Z'[:, c]| and every |W'[j][c]| below
+//   2^15 (fp16 hi/lo operands); colscale[c] = 2^-sc_c.
+// zbuf: head chunks as before; wbuf chunk q: [hi | lo] of kn x w_q (K-major,
+// w_q = min(64, kn - 64 q), chunk stride kn * kHeadK * 4 bytes).  Rows c >= k of
+// both and K columns j >= k of W' stay zero (cleared at create).
+__global__ void k_vside_prep(const float* __restrict__ udense, const int32_t* __restrict__ rowmap, int kpad,
+                             const int32_t* __restrict__ headterm, int h, const double* __restrict__ W, int k, int kn,
+                             const unsigned* __restrict__ amax_bits, const int* __restrict__ shift,
+                             uint8_t* __restrict__ zbuf, uint8_t* __restrict__ wbuf, float* __restrict__ colscale) {
+  __shared__ double wc[256];
+  __shared__ float zs[kHeadMax];
+  __shared__ float redf[32];
+  __shared__ int redi[32];
+  const int c = blockIdx.x;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) wc[j] = W[(int64_t)j * k + c];
+  __syncthreads();
+  float zmax = 0.f;
+  for (int s = threadIdx.x; s < h; s += blockDim.x) {
+    const int32_t r = rowmap[headterm[s]];
+    double z = 0;
+    if (r >= 0) {
+      const float* u = udense + (int64_t)r * kpad;
+      for (int j = 0; j < k; ++j) z = fma((double)u[j], wc[j], z);
+    }
+    zs[s] = (float)z;
+    zmax = fmaxf(zmax, fabsf((float)z));
+  }
+  // the W' bound: min_j (e(|W_jc|) + s_j - 15) over the nonzero entries
+  int wlim = INT_MAX;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const float wf = fabsf((float)wc[j]);
+    if (wf > 0.f) wlim = min(wlim, head_exp(wf) + shift[j] - 15);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zmax = fmaxf(zmax, __shfl_xor_sync(kFull, zmax, o));
+    wlim = min(wlim, __shfl_xor_sync(kFull, wlim, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    redf[threadIdx.x >> 5] = zmax;
+    redi[threadIdx.x >> 5] = wlim;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float zm = 0.f;
+    int wl = INT_MAX;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      zm = fmaxf(zm, redf[w]);
+      wl = min(wl, redi[w]);
+    }
+    const int eA = head_exp(__uint_as_float(*amax_bits));
+    int sc = zm > 0.f ? eA + head_exp(zm) : INT_MAX;
+    sc = min(sc, wl);
+    if (sc == INT_MAX) sc = 0;
+    redi[0] = sc;
+    colscale[c] = ldexpf(1.f, -sc);
+  }
+  __syncthreads();
+  const int sc = redi[0];
+  const int eA = head_exp(__uint_as_float(*amax_bits));
+  const uint32_t zhalf = (uint32_t)kn * kHeadK * 2;
+  for (int s = threadIdx.x; s < h; s += blockDim.x) {
+    const float z = ldexpf(zs[s], sc - eA);
+    const __half hi = __float2half_rn(z);
+    const __half lo = __float2half_rn(z - __half2float(hi));
+    uint8_t* b = zbuf + (size_t)(s / kHeadK) * 2 * zhalf;
+    const uint32_t off = tc::kmajor_off16(c, s % kHeadK, kHeadK);
+    *reinterpret_cast<__half*>(b + off) = hi;
+    *reinterpret_cast<__half*>(b + zhalf + off) = lo;
+  }
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const float w = (float)ldexp(wc[j], sc - shift[j] + 15);
+    const __half hi = __float2half_rn(w);
+    const __half lo = __float2half_rn(w - __half2float(hi));
+    const int q = j / kHeadK, wq = min(kHeadK, kn - kHeadK * q);
+    uint8_t* b = wbuf + (size_t)q * 2 * zhalf;
+    const uint32_t off = tc::kmajor_off16(c, j % kHeadK, wq);
+    *reinterpret_cast<__half*>(b + off) = hi;
+    *reinterpret_cast<__half*>(b + (size_t)kn * wq * 2 + off) = lo;
   }
 }
 
@@ -211,13 +300,19 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 // entries and the Z chunk into a stage (TMA engine, STAGES ahead); warps 0-3
 // zero the stage's A block and scatter the run into it; warp 4 (one thread)
 // issues the MMAs; warps 6-13 drain TMEM into X (two per lane quadrant).
+// Paper-order tail (k_vtail.cuh; nyc > 0): after the nchunks head chunks of a
+// tile come nyc chunks of (Y_tail W): A operand = the tile's Y_tail chunk
+// (ytile, fp16 hi/lo, 128 x w_q), B operand = W chunk q (wbuf, kn x w_q),
+// w_q = min(64, kn - 64 q) -- the same stage, copied like a dense tile, into the
+// same accumulator (the scales of Z, W and Y_tail are chosen per column so both
+// parts carry 2^sc_c: k_vside_prep).  Xt is then null.
 template <int STAGES, bool FUSE>
 __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
                 const int2* __restrict__ hseg, const unsigned* __restrict__ amax_bits, const uint8_t* __restrict__ zbuf,
                 const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
                 int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad,
-                SelFuse fz) {
+                SelFuse fz, const uint8_t* __restrict__ ytile, const uint8_t* __restrict__ wbuf, int nyc) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
@@ -261,9 +356,14 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       // on the critical path; from L2 it is ~1/3 of the HBM latency.
       int64_t pf_tile = blockIdx.x;
       int pf_q = 0;
+      const int nall = nchunks + nyc;
       auto prefetch_next = [&]() {
         if (pf_tile >= ntiles) return;
-        if (pf_q < nd) {
+        if (pf_q >= nchunks) {
+          const int yq = pf_q - nchunks;
+          tc::bulk_prefetch_l2(ytile + (size_t)pf_tile * kHeadM * kn * 4 + (size_t)yq * kHeadABytes,
+                               (uint32_t)kHeadM * min(64, kn - 64 * yq) * 4u);
+        } else if (pf_q < nd) {
           tc::bulk_prefetch_l2(atile + ((size_t)pf_tile * nd + pf_q) * kHeadABytes, kHeadABytes);
         } else {
           const int64_t si = pf_tile * (nchunks - nd) + (pf_q - nd);
@@ -272,14 +372,24 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
           const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);
           if (b > a) tc::bulk_prefetch_l2(hseg + a, (uint32_t)(b - a) * 8u);
         }
-        if (++pf_q == nchunks) { pf_q = 0; pf_tile += gridDim.x; }
+        if (++pf_q == nall) { pf_q = 0; pf_tile += gridDim.x; }
       };
       for (int i = 0; i < kHeadPf; ++i) prefetch_next();
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int q = 0; q < nchunks; ++q) {
+        for (int q = 0; q < nall; ++q) {
           prefetch_next();
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = base + stage * stage_bytes;
+          if (q >= nchunks) {  // (Y_tail W) chunk: Y_tail tile chunk + W chunk
+            const int yq = q - nchunks;
+            const uint32_t w = (uint32_t)min(64, kn - 64 * yq);
+            const uint32_t ab = (uint32_t)kHeadM * w * 4u, bb = (uint32_t)kn * w * 4u;
+            tc::mbar_arrive_expect_tx(&raw_full[stage], ab + bb);
+            tc::bulk_g2s(st, ytile + (size_t)tile * kHeadM * kn * 4 + (size_t)yq * kHeadABytes, ab, &raw_full[stage]);
+            tc::bulk_g2s(st + kHeadABytes, wbuf + (size_t)yq * zbytes, bb, &raw_full[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (q < nd) {  // dense chunk: the A tile itself
             tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + kHeadABytes);
             tc::bulk_g2s(st, atile + ((size_t)tile * nd + q) * kHeadABytes, kHeadABytes, &raw_full[stage]);
@@ -311,10 +421,10 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       *reinterpret_cast<__half*>(sa + kHeadAHalf + off) = lo;
     };
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      for (int q = 0; q < nchunks; ++q) {
+      for (int q = 0; q < nchunks + nyc; ++q) {
         uint8_t* sa = base + stage * stage_bytes;
         tc::mbar_wait(&raw_full[stage], phase);  // also: the MMAs of this stage's last round are done
-        if (q < nd) {  // dense chunk: bulk-copied A tile, nothing to build
+        if (q < nd || q >= nchunks) {  // dense or (Y_tail W) chunk: bulk-copied, nothing to build
           tc::mbar_arrive(&a_full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
@@ -351,15 +461,16 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         tc::mbar_wait(&tempty[acc], aphase ^ 1);
         tc::fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * acc_cols);
-        for (int q = 0; q < nchunks; ++q) {
+        for (int q = 0; q < nchunks + nyc; ++q) {
           tc::mbar_wait(&a_full[stage], phase);
           tc::fence_after();
+          // head chunk: K = kHeadK; (Y_tail W) chunk: K = w (its tiles are w wide)
+          const uint32_t w = q < nchunks ? (uint32_t)kHeadK : (uint32_t)min(64, kn - 64 * (q - nchunks));
           const uint32_t ah = tc::smem_u32(base + stage * stage_bytes);
-          const uint32_t al = ah + kHeadAHalf, zh = ah + kHeadABytes, zl = zh + zhalf;
-#pragma unroll
-          for (int s = 0; s < kHeadK / 16; ++s) {
+          const uint32_t al = ah + (uint32_t)kHeadM * w * 2u, zh = ah + kHeadABytes, zl = zh + (uint32_t)kn * w * 2u;
+          const uint32_t sbo = (w / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
+          for (uint32_t s = 0; s < w / 16; ++s) {
             const uint32_t o = s * 256;
-            constexpr uint32_t sbo = (kHeadK / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
             const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
             const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
             tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
@@ -406,8 +517,8 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
             const int c = c0 + 4 * v4;
-            const float4 t4 = c < kpad ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 t4 = (Xt && c < kpad) ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
             x[4 * v4] = t4.x; x[4 * v4 + 1] = t4.y; x[4 * v4 + 2] = t4.z; x[4 * v4 + 3] = t4.w;
           }
 #pragma unroll

@@ -20,6 +20,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
+from parity import TRAJ_TOL, check_products, check_selection, check_topt_property, coo_dense, r_close
 import paper_1510_05237_b200 as pk
 from paper_1510_05237_b200 import ESNMF, ESNMF_SIDE_U, ESNMF_SIDE_V
 
@@ -103,16 +104,12 @@ def test_sharded_topt_merge_equals_unsharded_gloo():
         assert b[0] == 0 and b[-1] == TINY.n and np.all(np.diff(b) >= 0)
 
 
-def test_shard_buffer_layout_matches_kernel():
-    """The exchange buffer layout (int64 cnt[k]; int32 row[k*cap]; float val[k*cap])."""
-    k, cap = 7, 5
-    assert 8 * k + 8 * k * cap == 8 * k * (cap + 1)
-
-
 # ------------------------------------------------------------------ GPU
 
 
-def run_loopback(world, cfg, g, iters, t="cfg", **kw):
+def run_loopback(world, cfg, g, iters, t="cfg", post=None, k=None, **kw):
+    """P logical ranks in P threads; ``post(rank, handle)`` (optional) runs in the
+    rank's thread after the iterations (half-steps there are collective too)."""
     tval = cfg.t if t == "cfg" else t
     grp = pk.comm.LoopbackGroup(world)
     handles = [None] * world
@@ -121,10 +118,12 @@ def run_loopback(world, cfg, g, iters, t="cfg", **kw):
     def worker(r):
         try:
             stream = torch.cuda.Stream()
-            handles[r] = ESNMF(cfg.n, cfg.m, cfg.k, tval, g, seed=cfg.seed, world=world, rank=r,
+            handles[r] = ESNMF(cfg.n, cfg.m, k or cfg.k, tval, g, seed=cfg.seed, world=world, rank=r,
                                comm=grp.comms[r], stream=stream.cuda_stream, **kw)
             handles[r].iterate(iters)
             handles[r].records()
+            if post is not None:
+                post(r, handles[r])
         except Exception as e:  # pragma: no cover
             errs.append(e)
             grp.barrier.abort()
@@ -149,11 +148,19 @@ def test_loopback_ranks_match_single_gpu(world):
     one.iterate(4)
     r1 = one.records()
     u1, v1 = one.get_U(), one.get_V()
+    ref = oracle.run(g, TINY.k, TINY.t, 4, seed=TINY.seed)["records"]
     for h in hs:
         recs = h.records()
-        for a, b in zip(recs, r1):
+        for a, b, o in zip(recs, r1, ref):
             assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"]
             assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"]
+            # peak nnz summed over ranks (the single GPU's count, >= nnz)
+            assert a["peak_u"] == b["peak_u"] and a["peak_v"] == b["peak_v"]
+            assert a["peak_u"] >= a["nnz_u"] and a["peak_v"] >= a["nnz_v"]
+            # and the oracle's run from the same U_0 (BJ:5; reading C15)
+            assert abs(a["E"] - o["E"]) <= TRAJ_TOL * o["E"] and r_close(a["R"], o["R"])
+            assert (a["nnz_u"], a["nnz_v"], a["peak_u"], a["peak_v"]) == (o["nnz_u"], o["nnz_v"], o["peak_u"],
+                                                                          o["peak_v"])
         ur, vr = h.get_U(), h.get_V()
         for x, y in zip(ur[:2] + vr[:2], u1[:2] + v1[:2]):
             assert np.array_equal(x, y)        # same supports
@@ -196,3 +203,118 @@ def test_loopback_options_match_single_gpu():
         assert a["nnz_u"] == b["nnz_u"] and a["nnz_v"] == b["nnz_v"]
     labels = np.arange(TINY.m) % 3
     assert np.allclose(hs[1].topic_accuracy(labels, 3), one.topic_accuracy(labels, 3), rtol=0, atol=1e-12)
+
+
+def _sharded_half_steps(world, cfg, g, iters, k=None, t="cfg"):
+    """Run P ranks for ``iters`` iterations, then one V and one U half-step on every
+    rank; returns the replicated state before (U), the assembled LS of each side
+    (every rank's shard of rows, placed at its row0) and the factors after."""
+    k = k or cfg.k
+    shards = {ESNMF_SIDE_V: [None] * world, ESNMF_SIDE_U: [None] * world}
+    state = {}
+
+    def post(r, h):
+        if r == 0:
+            state["U"] = h.get_U()
+        for side in (ESNMF_SIDE_V, ESNMF_SIDE_U):
+            h.half_step(side)
+            row0, ls = h.get_ls(side)
+            shards[side][r] = (row0, ls)
+            if r == 0 and side == ESNMF_SIDE_V:
+                state["V"] = h.get_V()
+        if r == 0:
+            state["U_after"] = h.get_U()
+
+    hs = run_loopback(world, cfg, g, iters, t=t, post=post, k=k)
+    full = {}
+    for side, n_rows in ((ESNMF_SIDE_V, cfg.m), (ESNMF_SIDE_U, cfg.n)):
+        LS = np.zeros((n_rows, k), np.float32)
+        covered = 0
+        for row0, ls in shards[side]:
+            LS[row0:row0 + len(ls)] = ls
+            covered += len(ls)
+        assert covered == n_rows              # the shards partition the rows
+        full[side] = LS
+    return hs, state, full
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_half_steps_match_oracle(world):
+    """The sharded path (local top-t, allgather, merge: a6) against the ORACLE's
+    half-steps from the same state: every rank's LS rows and the merged factors."""
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    cfg = TINY
+    g = synth.generate(cfg)
+    hs, st, LS = _sharded_half_steps(world, cfg, g, 3)
+    U = coo_dense((cfg.n, cfg.k), *st["U"])
+    ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], U, cfg.t)
+    check_products(LS[ESNMF_SIDE_V], ref["LS"])
+    V = coo_dense((cfg.m, cfg.k), *st["V"])
+    check_selection(V, ref["F"], ref["LS"], cfg.t)
+    ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], V, cfg.t)
+    check_products(LS[ESNMF_SIDE_U], ref["LS"])
+    check_selection(coo_dense((cfg.n, cfg.k), *st["U_after"]), ref["F"], ref["LS"], cfg.t)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_loopback_large_p8_matches_oracle_and_single_gpu():
+    """P = 8 at Large (BJ:9, t = 1,000; the 8-GPU configuration of north_star) on
+    one device: records equal the single GPU's; LS rows of every shard, sampled
+    (the head term rows and 1,500 documents), against the oracle row by row; the
+    top-t property of the merged factors on the assembled LS."""
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    cfg = synth.CONFIGS["large"]
+    g = synth.generate(cfg)
+    hs, st, LS = _sharded_half_steps(8, cfg, g, 2)
+    recs = hs[0].records()
+    for h in hs:
+        h.close()
+    one = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed)
+    one.iterate(2)
+    for a, b in zip(recs, one.records()):
+        assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"] and (a["nnz_u"], a["nnz_v"]) == (b["nnz_u"], b["nnz_v"])
+        assert (a["peak_u"], a["peak_v"]) == (b["peak_u"], b["peak_v"])
+    one.close()
+    rng = np.random.default_rng(0)
+    U = coo_dense((cfg.n, cfg.k), *st["U"])
+    L, _ = oracle.cholesky(oracle.gram(U))
+    docs = np.sort(rng.choice(cfg.m, 1500, replace=False))
+    ref = oracle.solve_rows(L, oracle.spmm_rows(docs, g["at_ptr"], g["at_col"], g["at_val"], U))
+    scale = np.abs(LS[ESNMF_SIDE_V]).max(axis=0).astype(np.float64)
+    assert (np.abs(LS[ESNMF_SIDE_V][docs] - ref) / scale).max() <= 1e-5
+    Vr, Vc, Vv = st["V"]
+    V = coo_dense((cfg.m, cfg.k), Vr, Vc, Vv)
+    check_topt_property(LS[ESNMF_SIDE_V], V, cfg.t)
+    L, _ = oracle.cholesky(oracle.gram(V))
+    terms = np.unique(np.concatenate([np.arange(20), rng.choice(cfg.n, 1500, replace=False)]))
+    ref = oracle.solve_rows(L, oracle.spmm_rows(terms, g["a_ptr"], g["a_col"], g["a_val"], V))
+    scale = np.abs(LS[ESNMF_SIDE_U]).max(axis=0).astype(np.float64)
+    assert (np.abs(LS[ESNMF_SIDE_U][terms] - ref) / scale).max() <= 1e-5
+    check_topt_property(LS[ESNMF_SIDE_U], coo_dense((cfg.n, cfg.k), *st["U_after"]), cfg.t)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_loopback_box_shaped_merge_matches_oracle():
+    """The merge at Box's shape (BJ:10: k = 200, t = 5,000, P = 8: up to 40,000
+    candidate keys per column) on the Medium matrix: the merged factors equal the
+    oracle's clamp + top-t of the full LS from the same state (check_selection)."""
+    import paper_1510_05237_b200.comm  # noqa: F401
+
+    cfg = synth.CONFIGS["medium"]
+    g = synth.generate(cfg)
+    hs, st, LS = _sharded_half_steps(8, cfg, g, 2, k=200, t=5000)
+    for h in hs:
+        h.close()
+    U = coo_dense((cfg.n, 200), *st["U"])
+    ref = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], U, 5000)
+    check_products(LS[ESNMF_SIDE_V], ref["LS"])
+    V = coo_dense((cfg.m, 200), *st["V"])
+    check_selection(V, ref["F"], ref["LS"], 5000)
+    ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], V, 5000)
+    check_products(LS[ESNMF_SIDE_U], ref["LS"])
+    check_selection(coo_dense((cfg.n, 200), *st["U_after"]), ref["F"], ref["LS"], 5000)
