@@ -16,6 +16,8 @@
 // synchronises inside esnmf_iterate.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -65,7 +67,9 @@ void ck(cudaError_t e, const char* what) {
 #define CK(x) ck((x), #x)
 #define CKL(name) ck(cudaGetLastError(), name)
 
-constexpr int64_t kSplitLen = 4096;   // max stored entries per SpMM work item (A rows)
+constexpr int64_t kSplitLen = 4096;
+constexpr double kVtKappaMax = 1e4;  // V side: Y_tail W in fp16 hi/lo only below these (k_vcond_flag)
+constexpr double kVtAmpMax = 8.0;   // max stored entries per SpMM work item (A rows)
 constexpr int kMaxGramSeg = 64;
 constexpr int64_t kSelScanMax = 4096;  // flat selection: segment-scan blocks (k * rows < 2^31 needs < 1024)
 
@@ -196,7 +200,11 @@ struct esnmf {
   uint32_t* vmax = nullptr;   // bits of max(V) (fixed-point scale of the U side)
   double* rsum = nullptr;     // [n_local] row sums of A (fixed-point scale of the U side)
   double* rsum_max = nullptr; // max_i rsum[i]
-  unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side)
+  unsigned long long* Yq = nullptr;  // [n][kpad] fixed-point A V (single-GPU U side): Yqb[ucur] during a U side
+  unsigned long long* Yqb[2] = {nullptr, nullptr};  // double buffer: k_polish_u reads Yq after the select;
+                                                    // the next V side clears it (aux stream)
+  bool v_since_u = true;             // a V side ran since the last U side (Yqb[yq_par] is clear)
+  int yq_par = 0;                    // the buffer the next U side uses (flips every U side)
   float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish_rt
   uint8_t* wtc = nullptr;            // W as the tensor-core B operand (fp16 hi/lo, k_uside_tc)
   float* wtc_scale = nullptr;        // [kn] its per-column scales
@@ -224,6 +232,12 @@ struct esnmf {
   uint8_t* wbuf = nullptr;       // [nyc][kn x 64 x 4 B] W' as the B operand
   unsigned* rowsum_bits = nullptr;  // max document row sum of A^T (float bits, rounded up; global)
   uint64_t* umap = nullptr;      // [n] U row view: (first << 32) | count
+  uint32_t* ubits = nullptr;     // [n / 32] rows of U with a nonzero
+  double* Z64 = nullptr;         // [U active rows][k] Z = U W in fp64 (k_form_z64)
+  double vt_kmax = 1e4, vt_amax = 8.0;  // k_vcond_flag thresholds (ESNMF_VT_KMAX / ESNMF_VT_AMAX)
+  bool polish = true;            // kept V values recomputed exactly (ESNMF_NO_POLISH=1: off)
+  double u_kmax = 100.0;         // U side: (Y W) in fp32 / fp16 hi/lo only for kappa_inf <= this (ESNMF_U_KMAX)
+  unsigned long long* vt_next = nullptr;  // k_ytail's tile counter
   int2* uent = nullptr;          // [U cap] (column, value * 2^s_c)
   int64_t* urptr = nullptr;      // [U cap_rows + 1]
   int64_t* ucursor = nullptr;
@@ -556,7 +570,7 @@ void seq_next_block(esnmf_t* h) {
 
 // V side: Z = U W written term-indexed (stride zs); the rows written by the
 // previous call are zeroed first, and the active-term bitmap is rebuilt.
-void form_z(esnmf_t* h, const Factor& f) {
+void form_z(esnmf_t* h, const Factor& f, const int* gate = nullptr) {
   const int zq = h->zs / 4;
   const int kpz = h->k == 1 ? 1 : h->kpad;  // zc row width
   if (h->zc) {  // narrow k: the compact z of the previous call is cleared with the same list
@@ -566,14 +580,14 @@ void form_z(esnmf_t* h, const Factor& f) {
   }
   ++h->nlaunch;
   k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
-      h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq);
+      h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq, gate);
   const int CJ = (h->kpad + 31) / 32;
   unsigned grid = grid_for(f.cap_rows, 8, 148 * 64);
 #define ESNMF_FZ(cj)                                                                                          \
   case cj:                                                                                                    \
     ++h->nlaunch;                                                                                             \
     k_form_z<cj><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->zs, h->W, h->Z, \
-                                              h->zlist, h->zcount);                                           \
+                                              h->zlist, h->zcount, gate);                                     \
     break;
   switch (CJ) {
     ESNMF_FZ(1) ESNMF_FZ(2) ESNMF_FZ(3) ESNMF_FZ(4) ESNMF_FZ(5) ESNMF_FZ(6) ESNMF_FZ(7) ESNMF_FZ(8)
@@ -587,12 +601,16 @@ void form_z(esnmf_t* h, const Factor& f) {
   }
   CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
   ++h->nlaunch;
-  k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits);
+  k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits, gate);
   if (h->head_h > 0) {  // head terms go through the tensor cores (k_vhead.cuh), not the gather
-    h->nlaunch += 2;
-    k_head_bits_clear<<<(unsigned)ceil_div(h->head_h, 256), 256, 0, h->stream>>>(h->headterm, h->head_h, h->tbits);
-    k_zhead_prep<<<h->k, 256, 0, h->stream>>>(h->Z, h->zs, h->headterm, h->head_h, h->kn, h->amax_bits, h->zhead,
-                                              h->colscale);
+    ++h->nlaunch;
+    k_head_bits_clear<<<(unsigned)ceil_div(h->head_h, 256), 256, 0, h->stream>>>(h->headterm, h->head_h, h->tbits,
+                                                                                  gate);
+    if (!h->ptail) {  // (paper-order mode: k_vside_prep writes the Z chunks)
+      ++h->nlaunch;
+      k_zhead_prep<<<h->k, 256, 0, h->stream>>>(h->Z, h->zs, h->headterm, h->head_h, h->kn, h->amax_bits, h->zhead,
+                                                h->colscale);
+    }
   }
   CKL("form_z");
 }
@@ -608,7 +626,7 @@ void tail_layout(int kpad, int& G, int& CPL) {
 }
 
 template <int G, int CPL, int U, int RG>
-void tail_launch(esnmf_t* h) {
+void tail_launch(esnmf_t* h, const int* gate) {
   Side& sd = h->side[ESNMF_SIDE_V];
   const float4* Z4 = reinterpret_cast<const float4*>(h->Z);
   const int64_t nwords = ceil_div(h->n, 32);
@@ -617,7 +635,7 @@ void tail_launch(esnmf_t* h) {
   if (h->zs != 4 * G * CPL) fail(ESNMF_EINVAL, "Z row stride does not match the tail gather layout");
   // with a head: row-major staging (the head kernel adds its part and stores X);
   // without: column-major straight into X
-  const bool trow = h->head_h > 0;
+  const bool trow = h->head_h > 0 || h->ptail;
   auto kern = trow ? k_spmm_tail<G, CPL, U, RG, true> : k_spmm_tail<G, CPL, U, RG, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t groups = ceil_div(sd.rows, RG);
@@ -625,7 +643,7 @@ void tail_launch(esnmf_t* h) {
   ++h->nlaunch;
   kern<<<grid, kTailThreads, smem, h->stream>>>(sd.T.ptr, h->head_h > 0 ? h->nh : nullptr, sd.T.ent, sd.rows,
                                                 h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4,
-                                                h->k, trow ? sd.Xt : sd.X, trow ? (int64_t)h->kpad : sd.ldx);
+                                                h->k, trow ? sd.Xt : sd.X, trow ? (int64_t)h->kpad : sd.ldx, gate);
   CKL("spmm_tail");
 }
 
@@ -653,7 +671,7 @@ void uside_w_prep(esnmf_t* h) {
   h->nlaunch += 2;
   k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
   // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
-  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, 100.0, h->flags + 3);
+  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, h->u_kmax, h->flags + 3);
   if (h->utc_kn) {
     ++h->nlaunch;
     k_utc_wprep<<<h->k, 128, 0, h->stream>>>(h->W, h->k, h->utc_kn, h->utc_kk, h->wtc, h->wtc_scale);
@@ -710,7 +728,7 @@ void uside_scatter_launch(esnmf_t* h) {
   CKL("uside_scatter");
 }
 
-void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
+void spmm(esnmf_t* h, int s, const int32_t* rowmap, const int* gate = nullptr) {
   if (s == ESNMF_SIDE_V && h->zc) {  // narrow k: SpMM over A^T with the compact z (k_spmm_narrow)
     Side& sd = h->side[ESNMF_SIDE_V];
     const unsigned g = grid_for(sd.rows, 8, (int64_t)h->num_sms * 64);
@@ -752,11 +770,11 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap) {
   }
   const int KQ = h->kpad / 4;
   // layouts must match tail_layout() (the Z row stride)
-  if (KQ <= 4) tail_launch<4, 1, 2, 4>(h);
-  else if (KQ <= 8) tail_launch<8, 1, 2, 4>(h);
-  else if (KQ <= 16) tail_launch<8, 2, 2, 2>(h);
-  else if (KQ <= 32) tail_launch<32, 1, 4, 4>(h);
-  else tail_launch<32, 2, 4, 2>(h);
+  if (KQ <= 4) tail_launch<4, 1, 2, 4>(h, gate);
+  else if (KQ <= 8) tail_launch<8, 1, 2, 4>(h, gate);
+  else if (KQ <= 16) tail_launch<8, 2, 2, 2>(h, gate);
+  else if (KQ <= 32) tail_launch<32, 1, 4, 4>(h, gate);
+  else tail_launch<32, 2, 4, 2>(h, gate);
 }
 
 // ---- V row-CSR for the U side (k_spmm_terms.cuh) ----
@@ -1006,8 +1024,9 @@ void vhead_launch_st(esnmf_t* h) {
   kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
                                                    h->colscale,
                                                    sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
-                                                   h->head_acc_cols, sv.X, sv.ldx, h->ptail ? nullptr : sv.Xt, h->kpad,
-                                                   fz, h->ytile, h->wbuf, h->ptail ? h->nyc : 0);
+                                                   h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad,
+                                                   fz, h->ytile, h->wbuf, h->ptail ? h->nyc : 0,
+                                                   h->ptail ? h->flags + 4 : nullptr);
   CKL("vhead");
 }
 
@@ -1069,7 +1088,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (hh > 0) CK(cudaMemcpyAsync(h->headterm, order.data(), sizeof(int32_t) * hh, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
   h->zhead = h->alloc<uint8_t>(std::max<int64_t>(1, (int64_t)h->head_nchunks * h->kn * kHeadK * 4));
-  if (!h->ptail) sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);
+  sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);  // (paper-order mode: the fallback's)
   h->colscale = h->alloc<float>(h->kn);
   h->amax_bits = h->alloc<unsigned>(1);
   CK(cudaMemsetAsync(h->zhead, 0, std::max<size_t>(1, (size_t)h->head_nchunks * h->kn * kHeadK * 4), h->stream));
@@ -1172,12 +1191,39 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     ++h->nlaunch;
     k_vt_fill<<<(unsigned)nt, kVtM, 0, h->stream>>>(sv.T.ptr, hh > 0 ? h->nh : nullptr, sv.T.ent, sv.rows, h->toff,
                                                    h->tent);
+    if (ntail > 0 && ntail < (1LL << 31)) {  // sort every tile's entries by (term, row)
+      uint32_t *k0 = nullptr, *k1 = nullptr;
+      int32_t *v0 = nullptr, *v1 = nullptr;
+      CK(cudaMalloc(&k0, sizeof(uint32_t) * ntail));
+      CK(cudaMalloc(&k1, sizeof(uint32_t) * ntail));
+      CK(cudaMalloc(&v0, sizeof(int32_t) * ntail));
+      CK(cudaMalloc(&v1, sizeof(int32_t) * ntail));
+      const unsigned g = grid_for(ntail, 256, (int64_t)h->num_sms * 16);
+      ++h->nlaunch;
+      k_vt_to_keys<<<g, 256, 0, h->stream>>>(h->tent, ntail, k0, v0);
+      int end_bit = 7;
+      while (end_bit < 31 && (1LL << (end_bit - 7)) < n) ++end_bit;
+      size_t tmp_bytes = 0;
+      CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, v1, (int)ntail, (int)nt, h->toff,
+                                                  h->toff + 1, 0, end_bit, h->stream));
+      void* tmp = nullptr;
+      CK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+      CK(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)ntail, (int)nt, h->toff,
+                                                  h->toff + 1, 0, end_bit, h->stream));
+      ++h->nlaunch;
+      k_vt_from_keys<<<g, 256, 0, h->stream>>>(k1, v1, ntail, h->tent);
+      CK(cudaStreamSynchronize(h->stream));
+      for (void* q : {(void*)k0, (void*)k1, (void*)v0, (void*)v1, tmp}) CK(cudaFree(q));
+    }
     h->ytile = h->alloc<uint8_t>(nt * kVtM * h->kn * 4);
     const int64_t wb = (int64_t)h->nyc * h->kn * kHeadK * 4;
     h->wbuf = h->alloc<uint8_t>(wb);
     CK(cudaMemsetAsync(h->wbuf, 0, wb, h->stream));
     h->umap = h->alloc<uint64_t>(n);
     CK(cudaMemsetAsync(h->umap, 0, sizeof(uint64_t) * n, h->stream));
+    h->ubits = h->alloc<uint32_t>(ceil_div(n, 32));
+    CK(cudaMemsetAsync(h->ubits, 0, sizeof(uint32_t) * ceil_div(n, 32), h->stream));
+    h->vt_next = h->alloc<unsigned long long>(1);
     h->uent = h->alloc<int2>(n * (int64_t)h->k);
     h->urptr = h->alloc<int64_t>(n + 1);
     h->ucursor = h->alloc<int64_t>(n + 1);
@@ -1187,6 +1233,10 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     CK(cudaMemsetAsync(h->ulist_n, 0, sizeof(int64_t), h->stream));
     h->umax = h->alloc<uint32_t>(h->k);
     h->ushift = h->alloc<int>(h->k);
+    h->Z64 = h->alloc<double>(n * (int64_t)h->k);
+    if (const char* e = getenv("ESNMF_VT_KMAX")) h->vt_kmax = atof(e);
+    if (const char* e = getenv("ESNMF_VT_AMAX")) h->vt_amax = atof(e);
+    { const char* np_ = getenv("ESNMF_NO_POLISH"); h->polish = !(np_ && atoi(np_)); }
   }
   CKL("head_setup");
   // host vectors die here: make the async uploads complete first
@@ -1198,7 +1248,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
 void urows_build(esnmf_t* h, const Factor& f) {
   const int64_t nr = f.cap_rows + 1;
   h->nlaunch += 1;
-  k_urows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(h->ulist, h->ulist_n, h->umap);
+  k_urows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(h->ulist, h->ulist_n, h->umap, h->ubits);
   CK(cudaMemsetAsync(h->urptr, 0, sizeof(int64_t) * nr, h->stream));
   dim3 g(col_grid_x(f.maxcol), h->k);
   ++h->nlaunch;
@@ -1214,7 +1264,7 @@ void urows_build(esnmf_t* h, const Factor& f) {
   k_urows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->head_h > 0 ? h->headslot : nullptr,
                                             h->ucursor, h->uent, h->umax);
   k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->urptr, h->umap,
-                                                                         h->ulist, h->ulist_n);
+                                                                         h->ubits, h->ulist, h->ulist_n);
   k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(f.colptr + h->k, h->uent, h->k,
                                                                                    h->umax, h->rowsum_bits, h->ushift);
   CKL("urows_build");
@@ -1222,21 +1272,67 @@ void urows_build(esnmf_t* h, const Factor& f) {
 
 void ytail_launch(esnmf_t* h) {
   const int ys = h->kn | 1;
-  const size_t smem = sizeof(uint32_t) * kVtM * ys;
+  const size_t smem = ytail_smem(ys);
   CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm = std::max(1, std::min(3, (int)((h->smem_optin + 1024) / (smem + 1024))));
+  CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  const int per_sm = std::max(1, std::min(3, (int)((228 * 1024) / (smem + 1024))));
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, (int64_t)h->num_sms * per_sm);
+  CK(cudaMemsetAsync(h->vt_next, 0, sizeof(unsigned long long), h->stream));
   ++h->nlaunch;
-  k_ytail<<<grid, kVtThreads, smem, h->stream>>>(h->toff, h->tent, h->head_ntiles, h->umap, h->uent, h->kn, ys,
-                                                  h->ytile);
+  k_ytail<<<grid, kVtThreads, smem, h->stream>>>(h->toff, h->tent, h->head_ntiles, h->ubits, h->umap, h->uent, h->kn,
+                                                  ys, h->ytile, h->vt_next);
   CKL("ytail");
+}
+
+// kept V entries recomputed exactly (k_polish_v); not with Alg. 3's deflation
+void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val) {
+  if (!h->ptail || (h->ktot && h->seq_b > 0) || !h->polish) return;  // (Alg. 3 deflates later blocks' LS)
+  Side& sv = h->side[ESNMF_SIDE_V];
+  const int64_t cap = h->V.cap;
+  ++h->nlaunch;
+  k_polish_v<<<grid_for(cap, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent, h->U[h->ucur].rowmap, h->Z64);
+  CKL("polish_v");
+}
+
+// kept U entries recomputed exactly from the fixed-point A V (one GPU; k_polish_u)
+void polish_u(esnmf_t* h, Factor& out) {
+  if (h->world != 1 || !h->Yq || !h->polish || (h->ktot && h->seq_b > 0)) return;
+  ++h->nlaunch;
+  k_polish_u<<<grid_for(out.cap, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
+      out.colptr, out.row, out.val, h->k, h->kpad, h->Yq, h->rsum_max, h->vmax, h->W);
+  CKL("polish_u");
+}
+
+// Z64 = U W for U's active rows (fp64; k_form_z64)
+void form_z64(esnmf_t* h, const Factor& f) {
+  const unsigned grid = grid_for(f.cap_rows, 8, (int64_t)h->num_sms * 16);
+  ++h->nlaunch;
+  switch ((h->k + 31) / 32) {
+    case 1: k_form_z64<1><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 2: k_form_z64<2><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 3: k_form_z64<3><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 4: k_form_z64<4><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 5: k_form_z64<5><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 6: k_form_z64<6><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 7: k_form_z64<7><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    default: k_form_z64<8><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+  }
+  CKL("form_z64");
 }
 
 void vside_prep(esnmf_t* h, const Factor& f) {
   ++h->nlaunch;
-  k_vside_prep<<<h->k, 256, 0, h->stream>>>(f.dense, f.rowmap, h->kpad, h->headterm, h->head_h, h->W, h->k, h->kn,
-                                            h->amax_bits, h->ushift, h->zhead, h->wbuf, h->colscale);
+  k_vside_prep<<<h->k, 256, 0, h->stream>>>(h->Z64, f.rowmap, h->headterm, h->head_h, h->W, h->k, h->kn,
+                                            h->amax_bits, h->ushift, h->zhead, h->wbuf, h->colscale, h->flags + 4);
   CKL("vside_prep");
+}
+
+// U-side fixed-point accumulator: the U side uses Yqb[ucur]; the V side after it
+// clears the other buffer (the one the previous U side used and k_polish_u read)
+void yq_clear_other(esnmf_t* h) {
+  if (!h->Yqb[0]) return;
+  CK(cudaMemsetAsync(h->Yqb[1 - h->yq_par], 0, sizeof(unsigned long long) * h->n * h->kpad, h->stream));
 }
 
 // one half-step; returns the factor that was written
@@ -1248,6 +1344,16 @@ Factor& half_step(esnmf_t* h, int s) {
   const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
   const bool overlap_u = s == ESNMF_SIDE_U && h->world == 1;    // Gram + solve on aux, beside the scatter
   if (s == ESNMF_SIDE_U) join_metrics(h);  // (only pending after a bare half_step call)
+  if (s == ESNMF_SIDE_U && h->Yqb[0]) {
+    h->Yq = h->Yqb[h->yq_par];
+    if (!h->v_since_u)  // two U sides in a row (bare half_step calls): this buffer is the dirty one
+      CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * h->n * h->kpad, h->stream));
+    h->v_since_u = false;
+  }
+  if (s == ESNMF_SIDE_V) {
+    if (!h->ptail) yq_clear_other(h);  // (paper-order mode: on the aux stream, beside the tail product)
+    h->v_since_u = true;
+  }
   if (s == ESNMF_SIDE_V && h->ptail) {
     // paper-order tail (k_vtail.cuh): Y_tail = A^T_tail U needs only U, so the
     // Gram + solve (a1, a2) run on aux beside it; then Z_head = U_head W, the
@@ -1258,12 +1364,33 @@ Factor& half_step(esnmf_t* h, int s) {
       OnStream os(h, h->aux);
       if (!h->gramU_valid) { Phase ph(h, p0 + 0); gram(h, in, sd.G); }   // a1: P:63
       { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                    // a2
+      form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
+      yq_clear_other(h);
+      ++h->nlaunch;  // is Y_tail W safe in fp16 hi/lo this time?  (else: Z-row gather)
+      k_vcond_flag<<<1, 256, 0, h->stream>>>(sd.G, h->W, sd.eps, h->k, h->vt_kmax, h->vt_amax, h->flags + 4);
     }
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
     join_from_aux(h, h->ev_vjoin);
     h->aux_pending = false;  // the join covers the previous record's kernels too
+    {
+      Phase ph(h, kVSpmm);  // fallback only (the kernels return at once otherwise)
+      form_z(h, in, h->flags + 4);
+      spmm(h, s, in.rowmap, h->flags + 4);
+    }
     { Phase ph(h, kVFormZ); vside_prep(h, in); }
     { Phase ph(h, kVHead); vhead_launch(h); }                             // a3 + a4 (head, tail x W)
+    if (getenv("ESNMF_DEBUG_VT")) {
+      CK(cudaStreamSynchronize(h->stream));
+      int fl[8];
+      CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+      std::vector<float> xt(std::min<int64_t>(sd.rows * h->kpad, 4096)), x(std::min<int64_t>(sd.ldx * h->k, 4096));
+      CK(cudaMemcpy(xt.data(), sd.Xt, sizeof(float) * xt.size(), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(x.data(), sd.X, sizeof(float) * x.size(), cudaMemcpyDeviceToHost));
+      double a = 0, b = 0;
+      for (float v : xt) a += fabs(v);
+      for (float v : x) b += fabs(v);
+      fprintf(stderr, "ESNMF_DEBUG_VT flag4=%d |Xt|=%g |X|=%g head=%d nyc=%d\n", fl[4], a, b, h->head_h, h->nyc);
+    }
   } else if (!(overlap_u && h->u_prefork)) {
     if (overlap_u) fork_to_aux(h, h->ev_ufork);
     OnStream os(h, overlap_u ? h->aux : h->stream);
@@ -1287,8 +1414,13 @@ Factor& half_step(esnmf_t* h, int s) {
     join_metrics(h);  // the previous iteration's record reads V
     if (s == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, out);
-    if (h->world == 1) select_topt(h, s, out);                     // a4 clamp + a5 top-t
-    else select_merge(h, s, out);                                  // + a6 shard merge
+    if (h->world == 1) {
+      select_topt(h, s, out);                                      // a4 clamp + a5 top-t
+      if (s == ESNMF_SIDE_V) polish_v(h, out.colptr, out.row, out.val);
+      else polish_u(h, out);
+    } else {
+      select_merge(h, s, out);                                     // + a6 shard merge
+    }
   }
   {
     Phase ph(h, p0 + 5);
@@ -1308,6 +1440,7 @@ Factor& half_step(esnmf_t* h, int s) {
   }
   if (s == ESNMF_SIDE_U) {
     h->ucur = 1 - h->ucur;
+    h->yq_par = 1 - h->yq_par;
     h->gramU_valid = false;
   }
   return out;
@@ -1476,6 +1609,7 @@ void graph_run(esnmf_t* h) {
   h->nlaunch += h->glaunch[p];
   h->nrec += 1;       // the previous iteration's record (device slot counter d_nrec advanced by the graph)
   h->ucur = 1 - h->ucur;
+  h->yq_par = 1 - h->yq_par;
   h->gramU_valid = false;
   h->metrics_pending = true;
   if (h->ktot) ++h->seq_i;
@@ -1591,6 +1725,7 @@ void select_merge(esnmf_t* h, int s, Factor& out) {
   loc.row = sd.lrow;
   loc.val = sd.lval;
   select_topt(h, s, loc);
+  if (s == ESNMF_SIDE_V) polish_v(h, loc.colptr, loc.row, loc.val);  // exact values before the exchange
   dim3 g(col_grid_x(sd.cap_s), k);
   ++h->nlaunch;
   k_pack_shard<<<g, 256, 0, h->stream>>>(sd.lcolptr, sd.lrow, sd.lval, k, sd.cap_s, sd.sendbuf);
@@ -1944,14 +2079,15 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     if (h->whole && (int64_t)kb * (std::max(n, m) + 32) >= (1LL << 31))
       fail(ESNMF_EINVAL, "esnmf_create: whole-matrix enforcement needs k * rows < 2^31");
     h->wcolptr = h->alloc<int64_t>(2);
+    if (const char* e = getenv("ESNMF_U_KMAX")) h->u_kmax = atof(e);
     h->rho = o.ridge_scale;
     h->seed = o.seed;
     h->world = o.world;
     h->rank = o.rank;
     if (o.comm) h->comm = *o.comm;
     const bool on_dev = o.inputs_on_device != 0;
-    h->flags = h->alloc<int>(4);
-    CK(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
+    h->flags = h->alloc<int>(8);  // [0] singular [1] validation [2] U0 [3] U-side fp64 [4] V-side Z-gather fallback
+    CK(cudaMemsetAsync(h->flags, 0, sizeof(int) * 8, h->stream));
     h->scal = h->alloc<double>(8);
     h->d_nrec = h->alloc<int64_t>(1);
     CK(cudaMemsetAsync(h->d_nrec, 0, sizeof(int64_t), h->stream));
@@ -2083,8 +2219,11 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
         h->wtc_scale = h->alloc<float>(h->utc_kn);
         CK(cudaMemsetAsync(h->wtc_scale, 0, sizeof(float) * h->utc_kn, h->stream));
       }
-      h->Yq = h->alloc<unsigned long long>(n * (int64_t)h->kpad);
-      CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * n * h->kpad, h->stream));
+      for (int b = 0; b < 2; ++b) {
+        h->Yqb[b] = h->alloc<unsigned long long>(n * (int64_t)h->kpad);
+        CK(cudaMemsetAsync(h->Yqb[b], 0, sizeof(unsigned long long) * n * h->kpad, h->stream));
+      }
+      h->Yq = h->Yqb[0];
     }
     CK(cudaMemsetAsync(h->vbits, 0, sizeof(uint32_t) * ceil_div(m, 32), h->stream));
     CK(cudaMemsetAsync(h->vmap, 0, sizeof(uint64_t) * m, h->stream));

@@ -199,7 +199,9 @@ __global__ void __launch_bounds__(256) k_form_z(const float* __restrict__ dense,
                                                 const int64_t* __restrict__ n_active,
                                                 const int32_t* __restrict__ active, int zs,
                                                 const double* __restrict__ W, float* __restrict__ Z,
-                                                int32_t* __restrict__ zlist, int64_t* __restrict__ zcount) {
+                                                int32_t* __restrict__ zlist, int64_t* __restrict__ zcount,
+                                                const int* __restrict__ gate) {
+  if (gate && !*gate) return;  // (k_spmm_tail.cuh: the Z-row gather runs only when gated on)
   const int lane = threadIdx.x & 31;
   const int64_t na = *n_active;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

@@ -36,8 +36,11 @@ constexpr int kTailSub = 4;              // entries per lane per load round
 constexpr int kTailRound = 32 * kTailSub;
 
 // zero the Z rows of the terms listed (the previous V side's active terms)
+// gate (all of this file's per-iteration kernels): null = run; else run only if *gate
+// (the paper-order V side falls back to the Z-row gather for an ill-conditioned W)
 __global__ void k_zrows_clear(const int32_t* __restrict__ terms, const int64_t* __restrict__ count,
-                              float4* __restrict__ Z, int zq) {
+                              float4* __restrict__ Z, int zq, const int* __restrict__ gate) {
+  if (gate && !*gate) return;
   const int64_t cnt = *count;
   const int64_t total = cnt * zq;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
@@ -48,7 +51,8 @@ __global__ void k_zrows_clear(const int32_t* __restrict__ terms, const int64_t* 
 
 // term bitmap of the active rows of U (all bits cleared by the caller first)
 __global__ void k_term_bits(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
-                            uint32_t* __restrict__ bits) {
+                            uint32_t* __restrict__ bits, const int* __restrict__ gate) {
+  if (gate && !*gate) return;
   const int64_t na = *n_active;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t t = active[r];
@@ -116,7 +120,8 @@ template <int G, int CPL, int U, int RG, bool TROW>
 __global__ void __launch_bounds__(kTailThreads, kTailMinBlocks)
     k_spmm_tail(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh, const int2* __restrict__ ent,
                 int64_t rows, const uint32_t* __restrict__ tbits, int nwords, const float4* __restrict__ Z, int zq,
-                int kq, int k, float* __restrict__ X, int64_t ldx) {
+                int kq, int k, float* __restrict__ X, int64_t ldx, const int* __restrict__ gate) {
+  if (gate && !*gate) return;
   constexpr int NG = 32 / G;
   constexpr int STEP = U * NG;                         // list slots per gather step
   constexpr int LCAP = kTailRound + RG * (STEP - 1);   // compacted entries + per-row padding

@@ -70,8 +70,7 @@ __global__ void __launch_bounds__(256) k_uside_finish(int64_t rows, const double
       const int c = lane + 32 * q;
       unsigned long long v = 0;
       if (c < kpad) {
-        v = yr[c];
-        if (v) yr[c] = 0ull;
+        v = yr[c];  // (Yq is cleared by the host's double buffering: k_polish_u reads it after the select)
       }
       y[q] = (double)v * unit;
       any |= v != 0ull;
@@ -244,7 +243,7 @@ __global__ void __launch_bounds__(256) k_uside_finish_rt(int64_t rows, const dou
     // before any is used (PER in flight per lane), then converted and cleared
     constexpr int PER = CW * 16;  // >= kFinRT * kpad / 2 / 32 for kpad <= 128 CW
     const int nch = (int)(min((int64_t)kFinRT, rows - i0) * kpad / 2);
-    ulonglong2* yg = reinterpret_cast<ulonglong2*>(Yq + i0 * kpad);
+    const ulonglong2* yg = reinterpret_cast<const ulonglong2*>(Yq + i0 * kpad);
     ulonglong2 buf[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -261,7 +260,6 @@ __global__ void __launch_bounds__(256) k_uside_finish_rt(int64_t rows, const dou
           const int e = 2 * q + h2, r = e / kpad, c = e - r * kpad;
           ys[c * kFinRT + r] = pr[h2] ? (float)((double)pr[h2] * unit) : 0.f;
         }
-        if (q < nch && (buf[u].x | buf[u].y)) yg[q] = make_ulonglong2(0ull, 0ull);  // clear for the next half-step
       }
     }
     __syncwarp();

@@ -132,13 +132,6 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
         }
 #pragma unroll
         for (int q = 0; q < kUtcRows; ++q) {
-          const int64_t row = tile * kUtcM + warp * (kUtcM / kUtcProdWarps) + rr + q;
-          ulonglong2* dst = reinterpret_cast<ulonglong2*>(Yq + row * kpad + c4);
-          if (qv[q][0].x | qv[q][0].y) dst[0] = make_ulonglong2(0ull, 0ull);  // clear for the next half-step
-          if (qv[q][1].x | qv[q][1].y) dst[1] = make_ulonglong2(0ull, 0ull);
-        }
-#pragma unroll
-        for (int q = 0; q < kUtcRows; ++q) {
           const int r = warp * (kUtcM / kUtcProdWarps) + rr + q;
           float y[4];
           y[0] = (float)((double)qv[q][0].x * unit);

@@ -41,6 +41,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "k_vtail.cuh"
 #include "tc.cuh"
 
 namespace esk {
@@ -74,7 +75,9 @@ __global__ void k_absmax_ent(const int2* __restrict__ ent, int64_t nnz, unsigned
 }
 
 // clear the head terms' bits from the gather kernel's active-term bitmap
-__global__ void k_head_bits_clear(const int32_t* __restrict__ headterm, int h, uint32_t* __restrict__ bits) {
+__global__ void k_head_bits_clear(const int32_t* __restrict__ headterm, int h, uint32_t* __restrict__ bits,
+                                  const int* __restrict__ gate) {
+  if (gate && !*gate) return;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < h) {
     const int32_t t = headterm[s];
@@ -118,7 +121,7 @@ __global__ void k_zhead_prep(const float* __restrict__ Z, int zs, const int32_t*
 }
 
 // Paper-order tail mode (k_vtail.cuh): one CTA per topic column c.
-//   Z_head[s][c] = sum_j U[headterm[s]][j] W[j][c]   (fp64; U's dense active rows)
+//   Z_head[s][c] = (U W)[headterm[s]][c]   (fp64, k_form_z64)
 //   one accumulator scale 2^sc_c for both parts of LS_V[:, c]:
 //     head:  A' = A 2^eA,             Z'[s][c] = Z 2^(sc_c - eA)
 //     tail:  Y' = Y 2^(s_j - 15),     W'[j][c] = W 2^(sc_c - s_j + 15)
@@ -127,10 +130,11 @@ __global__ void k_zhead_prep(const float* __restrict__ Z, int zs, const int32_t*
 // zbuf: head chunks as before; wbuf chunk q: [hi | lo] of kn x w_q (K-major,
 // w_q = min(64, kn - 64 q), chunk stride kn * kHeadK * 4 bytes).  Rows c >= k of
 // both and K columns j >= k of W' stay zero (cleared at create).
-__global__ void k_vside_prep(const float* __restrict__ udense, const int32_t* __restrict__ rowmap, int kpad,
+__global__ void k_vside_prep(const double* __restrict__ Z64, const int32_t* __restrict__ rowmap,
                              const int32_t* __restrict__ headterm, int h, const double* __restrict__ W, int k, int kn,
                              const unsigned* __restrict__ amax_bits, const int* __restrict__ shift,
-                             uint8_t* __restrict__ zbuf, uint8_t* __restrict__ wbuf, float* __restrict__ colscale) {
+                             uint8_t* __restrict__ zbuf, uint8_t* __restrict__ wbuf, float* __restrict__ colscale,
+                             const int* __restrict__ fallback) {
   __shared__ double wc[256];
   __shared__ float zs[kHeadMax];
   __shared__ float redf[32];
@@ -141,19 +145,17 @@ __global__ void k_vside_prep(const float* __restrict__ udense, const int32_t* __
   float zmax = 0.f;
   for (int s = threadIdx.x; s < h; s += blockDim.x) {
     const int32_t r = rowmap[headterm[s]];
-    double z = 0;
-    if (r >= 0) {
-      const float* u = udense + (int64_t)r * kpad;
-      for (int j = 0; j < k; ++j) z = fma((double)u[j], wc[j], z);
-    }
+    const double z = r >= 0 ? Z64[(int64_t)r * k + c] : 0.0;  // Z = U W (fp64, k_form_z64)
     zs[s] = (float)z;
     zmax = fmaxf(zmax, fabsf((float)z));
   }
+  const bool fb = *fallback != 0;  // Z-row gather this iteration: no (Y_tail W) chunks
   // the W' bound: min_j (e(|W_jc|) + s_j - 15) over the nonzero entries
   int wlim = INT_MAX;
+  // (a row j whose column of U has no tail entry multiplies Y_tail[:, j] = 0: skipped, W' = 0)
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     const float wf = fabsf((float)wc[j]);
-    if (wf > 0.f) wlim = min(wlim, head_exp(wf) + shift[j] - 15);
+    if (wf > 0.f && shift[j] != kNoTail && !fb) wlim = min(wlim, head_exp(wf) + shift[j] - 15);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -193,7 +195,7 @@ __global__ void k_vside_prep(const float* __restrict__ udense, const int32_t* __
     *reinterpret_cast<__half*>(b + zhalf + off) = lo;
   }
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    const float w = (float)ldexp(wc[j], sc - shift[j] + 15);
+    const float w = (shift[j] == kNoTail || fb) ? 0.f : (float)ldexp(wc[j], sc - shift[j] + 15);
     const __half hi = __float2half_rn(w);
     const __half lo = __float2half_rn(w - __half2float(hi));
     const int q = j / kHeadK, wq = min(kHeadK, kn - kHeadK * q);
@@ -312,7 +314,13 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
                 const int2* __restrict__ hseg, const unsigned* __restrict__ amax_bits, const uint8_t* __restrict__ zbuf,
                 const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
                 int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad,
-                SelFuse fz, const uint8_t* __restrict__ ytile, const uint8_t* __restrict__ wbuf, int nyc) {
+                SelFuse fz, const uint8_t* __restrict__ ytile, const uint8_t* __restrict__ wbuf, int nyc_arg,
+                const int* __restrict__ fallback) {
+  // paper-order tail mode, ill-conditioned W (fallback set): the Z-row gather
+  // staged the tail rows in Xt this time -- no (Y_tail W) chunks
+  const bool fb = fallback && *fallback;
+  const int nyc = fb ? 0 : nyc_arg;
+  if (!fb && nyc_arg > 0) Xt = nullptr;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
@@ -512,6 +520,10 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();
+        if (nchunks + nyc == 0) {  // no MMA wrote the accumulator (no head, tail staged in Xt)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0u;
+        }
         float x[16];
         if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
 #pragma unroll

@@ -10,12 +10,11 @@
 // reassociated A^T (U W) order gathers a k-wide Z row per active entry (28 M x
 // 400 B = 11-14 GB of L2 traffic per launch, round 1's k_spmm_tail).
 //
-// Data (built at create time, k_vt_count / k_vt_fill): per 128-document tile,
-// the tile's tail entries in JAGGED-DIAGONAL order -- documents ranked by tail
-// length (descending), then layer q holds the q-th tail entry of every document
-// with more than q -- each entry (row in tile << 24 | term, value).  Consecutive
-// entries therefore belong to different documents, so the lanes of a warp add
-// into different shared-memory rows.
+// Data (built at create time, k_vt_count / k_vt_fill / sort): per 128-document
+// tile, the tile's tail entries sorted by (term, row), each (row in tile << 24 |
+// term, value).  The lanes of a warp then read neighbouring activity-bitmap words
+// and map words and, for a frequent term, the same U row; entries of one term
+// belong to different documents (different shared-memory rows).
 //
 // Accumulation is FIXED POINT (unsigned 32-bit; every product a_ij u_ic >= 0):
 // U's values are stored pre-scaled by 2^s_c (k_ut_scale) with s_c chosen so that
@@ -82,6 +81,25 @@ __global__ void __launch_bounds__(kVtM) k_vt_fill(const int64_t* __restrict__ pt
   }
 }
 
+// (row << 24 | term, value) <-> (term << 7 | row, value): the keys of the per-tile
+// sort by term (create time, cub segmented radix sort): consecutive entries of a
+// tile then share bitmap words, U-row map words and U rows
+__global__ void k_vt_to_keys(const int2* __restrict__ tent, int64_t n, uint32_t* __restrict__ key,
+                             int32_t* __restrict__ val) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = (uint32_t)tent[e].x;
+    key[e] = ((x & kVtTermMask) << 7) | (x >> kVtTermBits);
+    val[e] = tent[e].y;
+  }
+}
+__global__ void k_vt_from_keys(const uint32_t* __restrict__ key, const int32_t* __restrict__ val, int64_t n,
+                               int2* __restrict__ tent) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key[e];
+    tent[e] = make_int2((int)(((k & 127u) << kVtTermBits) | (k >> 7)), val[e]);
+  }
+}
+
 // row sums of A^T (one warp per document; fixed order) -> max over the shard, as
 // the bits of a float rounded UP (a valid bound for the fixed-point scale)
 __global__ void k_doc_rowsum_max(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
@@ -122,21 +140,26 @@ __global__ void k_urows_scatter(const int64_t* __restrict__ colptr, const int32_
 // published are listed in ulist (for the next clear), their number in *ulist_n
 __global__ void k_urows_finish(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
                                const int64_t* __restrict__ rptr, uint64_t* __restrict__ umap,
-                               int32_t* __restrict__ ulist, int64_t* __restrict__ ulist_n) {
+                               uint32_t* __restrict__ ubits, int32_t* __restrict__ ulist,
+                               int64_t* __restrict__ ulist_n) {
   const int64_t na = *n_active;
   if (blockIdx.x == 0 && threadIdx.x == 0) *ulist_n = na;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = active[r];
     umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)(rptr[r + 1] - rptr[r]);
+    atomicOr(&ubits[i >> 5], 1u << (i & 31));
     ulist[r] = i;
   }
 }
 
 __global__ void k_urows_clear(const int32_t* __restrict__ ulist, const int64_t* __restrict__ ulist_n,
-                              uint64_t* __restrict__ umap) {
+                              uint64_t* __restrict__ umap, uint32_t* __restrict__ ubits) {
   const int64_t na = *ulist_n;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x)
-    umap[ulist[r]] = 0ull;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = ulist[r];
+    umap[i] = 0ull;
+    ubits[i >> 5] = 0u;  // every listed row is cleared: whole words may go
+  }
 }
 
 // max over ranks of the per-rank {amax bits, rowsum bits} (allgathered, 16 bytes per rank)
@@ -151,10 +174,12 @@ __global__ void k_rank_max2(const unsigned* __restrict__ gathered, int world, un
   *rowsum = b;
 }
 
-// fixed-point exponent of column c: 2^s_c * rowsum_max * umax_c <= 2^30
+// fixed-point exponent of column c: 2^s_c * rowsum_max * umax_c <= 2^30;
+// kNoTail: column c of U has no entry in a tail row (Y_tail[:, c] = 0)
+constexpr int kNoTail = -100000;
 ESNMF_DEV int vt_shift(uint32_t umax_bits, uint32_t rowsum_bits) {
   const float b = __uint_as_float(umax_bits) * __uint_as_float(rowsum_bits);  // rounded: slack below
-  if (!(b > 0.f)) return 0;
+  if (!(b > 0.f)) return kNoTail;
   int e;
   frexpf(b, &e);           // b = f 2^e, f in [0.5, 1): b < 2^e
   return 29 - e;           // b 2^s < 2^29 (a factor 2 of slack for the float product's rounding)
@@ -170,7 +195,8 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
   const int64_t n = *n_ent;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     int2 p = uent[e];
-    p.y = __float_as_int(ldexpf(__int_as_float(p.y), vt_shift(umax[p.x], rb)));
+    const int sh = vt_shift(umax[p.x], rb);
+    if (sh != kNoTail) p.y = __float_as_int(ldexpf(__int_as_float(p.y), sh));  // (else: a head row, never read)
     uent[e] = p;
   }
 }
@@ -179,45 +205,64 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
 // Chunk q of a tile covers Y columns [64 q, 64 q + w_q), w_q = min(64, kn - 64 q);
 // it is stored as [hi: 128 x w_q fp16][lo: 128 x w_q fp16], K-major (tc.cuh),
 // at ytile + tile * 128 * kn * 4 + 64 q * 128 * 4.
-// ys: shared row stride in words (odd: lanes on different rows, same column,
-// fall in different banks).
-__global__ void __launch_bounds__(kVtThreads) k_ytail(const int64_t* __restrict__ toff, const int2* __restrict__ tent,
-                                                      int64_t ntiles, const uint64_t* __restrict__ umap,
-                                                      const int2* __restrict__ uent, int kn, int ys,
-                                                      uint8_t* __restrict__ ytile) {
+// ys: shared row stride in words (odd).  Tiles are taken from a global counter
+// (*next, zeroed before the launch): a CTA that starts late (an SM busy with the
+// solve on the other stream) simply takes fewer tiles.
+// Entries are sorted by term inside a tile, so the lanes of a warp hold the same
+// or neighbouring terms: their rows of U are of similar length (the per-lane
+// product loops stay nearly convergent), lanes of one term load the same pairs
+// (broadcast) and add into different document rows (different banks: ys odd).
+constexpr int kVtSub = 4;            // entries per thread per round (their loads in flight together)
+
+ESNMF_DEV void vt_add(uint32_t* yrow, float av, int2 p) {
+  atomicAdd(yrow + p.x, __float2uint_rn(av * __int_as_float(p.y)));
+}
+
+__global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restrict__ toff,
+                                                         const int2* __restrict__ tent, int64_t ntiles,
+                                                         const uint32_t* __restrict__ ubits,
+                                                         const uint64_t* __restrict__ umap,
+                                                         const int2* __restrict__ uent, int kn, int ys,
+                                                         uint8_t* __restrict__ ytile,
+                                                         unsigned long long* __restrict__ next) {
   extern __shared__ uint32_t Ysm[];
+  __shared__ int64_t s_tile;
   const int T = blockDim.x;
   const int ng = kn / 8;  // 8-column groups per row
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(next, 1ull);
     for (int i = threadIdx.x; i < kVtM * ys; i += T) Ysm[i] = 0u;
     __syncthreads();
-    const int64_t e0 = toff[tile], e1 = toff[tile + 1];
-    // two entries per thread per round: their map lookups are in flight together
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += 2 * (int64_t)T) {
-      const int64_t f = e + T;
-      const int2 a0 = __ldcs(tent + e);
-      const int2 a1 = f < e1 ? __ldcs(tent + f) : make_int2(0, 0);
-      const uint64_t m0 = umap[(uint32_t)a0.x & kVtTermMask];
-      const uint64_t m1 = f < e1 ? umap[(uint32_t)a1.x & kVtTermMask] : 0ull;
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int64_t e1 = toff[tile + 1];
+    for (int64_t base = toff[tile] + threadIdx.x; base < e1; base += (int64_t)kVtSub * T) {
+      int2 en[kVtSub];
+      uint64_t mp[kVtSub];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int2 a = u ? a1 : a0;
-        const uint64_t mp = u ? m1 : m0;
-        const int cnt = (int)(mp & 0xFFFFFFFFull);
-        if (cnt == 0) continue;
-        const int2* up = uent + (mp >> 32);
-        uint32_t* yrow = Ysm + ((uint32_t)a.x >> kVtTermBits) * ys;
-        const float av = __int_as_float(a.y);
+      for (int u = 0; u < kVtSub; ++u) {
+        const int64_t e = base + (int64_t)u * T;
+        en[u] = e < e1 ? __ldcs(tent + e) : make_int2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kVtSub; ++u) {
+        const uint32_t term = (uint32_t)en[u].x & kVtTermMask;
+        const bool act = base + (int64_t)u * T < e1 && ((__ldg(ubits + (term >> 5)) >> (term & 31)) & 1u);
+        mp[u] = act ? umap[term] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kVtSub; ++u) {
+        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
+        const int2* up = uent + (mp[u] >> 32);
+        uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
+        const float av = __int_as_float(en[u].y);
         int j = 0;
         for (; j + 2 <= cnt; j += 2) {
-          const int2 p0 = up[j], p1 = up[j + 1];
-          atomicAdd(yrow + p0.x, __float2uint_rn(av * __int_as_float(p0.y)));
-          atomicAdd(yrow + p1.x, __float2uint_rn(av * __int_as_float(p1.y)));
+          const int2 a = up[j], b = up[j + 1];
+          vt_add(yrow, av, a);
+          vt_add(yrow, av, b);
         }
-        if (j < cnt) {
-          const int2 p0 = up[j];
-          atomicAdd(yrow + p0.x, __float2uint_rn(av * __int_as_float(p0.y)));
-        }
+        if (j < cnt) vt_add(yrow, av, up[j]);
       }
     }
     __syncthreads();
@@ -243,5 +288,156 @@ __global__ void __launch_bounds__(kVtThreads) k_ytail(const int64_t* __restrict_
     __syncthreads();
   }
 }
+
+// V-side fallback flag: 1 when the product Y_tail W (fp16 hi/lo operands, ~2^-22
+// relative to each term) could cancel badly -- kappa_inf(G + eps I) > kmax, or a
+// column of W whose absolute sum exceeds wmax times its diagonal entry; the Z-row
+// gather (Z = U W formed in fp64) then takes the tail for this iteration
+__global__ void k_vcond_flag(const double* __restrict__ G, const double* __restrict__ W, const double* eps, int k,
+                             double kmax, double wmax, int* __restrict__ flag) {
+  __shared__ double sg[32], sw[32], sa[32];
+  double g = 0, w = 0, amp = 0;
+  const double e = *eps;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x >> 5; i < k; i += blockDim.x >> 5) {  // row i (W, G symmetric: also column i)
+    double rg = 0, rw = 0;
+    for (int j = lane; j < k; j += 32) {
+      rg += fabs(G[(int64_t)i * k + j] + (i == j ? e : 0.0));
+      rw += fabs(W[(int64_t)i * k + j]);
+    }
+    rg = warp_sum(rg);
+    rw = warp_sum(rw);
+    g = fmax(g, rg);
+    w = fmax(w, rw);
+    amp = fmax(amp, rw / fabs(W[(int64_t)i * k + i]));
+  }
+  if (lane == 0) {
+    sg[threadIdx.x >> 5] = g;
+    sw[threadIdx.x >> 5] = w;
+    sa[threadIdx.x >> 5] = amp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gm = 0, wm = 0, am = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) gm = fmax(gm, sg[q]), wm = fmax(wm, sw[q]), am = fmax(am, sa[q]);
+    *flag = !(gm * wm <= kmax && am <= wmax);
+  }
+}
+
+// Z64 = U W in fp64 for the active rows of U (row r of the dense active view:
+// rowmap[term] = r): the exact Z rows behind k_vside_prep's head chunks and
+// k_polish_v.  One warp per active row, lanes over columns (CJ = ceil(k / 32)).
+template <int CJ>
+__global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dense, int kpad, int k,
+                                                  const int64_t* __restrict__ n_active, const double* __restrict__ W,
+                                                  double* __restrict__ Z64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t na = *n_active;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < na; r += nwarps) {
+    float f[CJ];
+    double acc[CJ];
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) {
+      const int c = lane + 32 * j;
+      f[j] = c < kpad ? dense[r * kpad + c] : 0.f;
+      acc[j] = 0.0;
+    }
+#pragma unroll
+    for (int jl = 0; jl < CJ; ++jl) {
+      const int lmax = min(32, k - 32 * jl);
+      for (int ll = 0; ll < lmax; ++ll) {
+        const float fl = __shfl_sync(kFull, f[jl], ll);
+        if (fl != 0.f) {
+          const double* Wl = W + (int64_t)(32 * jl + ll) * k;
+#pragma unroll
+          for (int j = 0; j < CJ; ++j) {
+            const int c = lane + 32 * j;
+            if (c < k) acc[j] = fma((double)fl, Wl[c], acc[j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) {
+      const int c = lane + 32 * j;
+      if (c < k) Z64[r * k + c] = acc[j];
+    }
+  }
+}
+
+// The kept entries of V (after the selection) recomputed exactly: for kept
+// (document j, topic c) LS_jc = sum over the document's stored entries a_ji Z_ic
+// with Z = U W in fp64 (Z64, k_form_z64; zero for a term whose row of U is
+// empty).  The selection chose the entries from the tensor-core values; this
+// pass makes the VALUES exact to fp32 rounding (BJ:5 "relative 1e-5 on factor
+// entries").  One warp per kept entry, lanes over the document's entries.
+__global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
+                           float* __restrict__ val, int k, int64_t row0, const int64_t* __restrict__ ptr,
+                           const int2* __restrict__ ent, const int32_t* __restrict__ rowmap,
+                           const double* __restrict__ Z64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = colptr[k];
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
+    int lo = 0, hi = k - 1;  // column of entry e: last c with colptr[c] <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (colptr[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int c = lo;
+    const int64_t r = (int64_t)row[e] - row0;
+    const int64_t s1 = ptr[r + 1];
+    double acc = 0;
+    for (int64_t q0 = ptr[r] + lane; q0 < s1; q0 += 128) {  // 4 entries per lane in flight
+      int2 en[4];
+      int32_t rm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) en[u] = q0 + 32 * u < s1 ? ent[q0 + 32 * u] : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) rm[u] = q0 + 32 * u < s1 ? rowmap[en[u].x] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (rm[u] >= 0) acc = fma((double)__int_as_float(en[u].y), Z64[(int64_t)rm[u] * k + c], acc);
+    }
+    acc = warp_sum(acc);
+    // an entry kept for a tensor-core LS value within rounding of zero keeps that
+    // (positive) value: a factor holds no zeros or negatives (P:63 clamp)
+    if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
+  }
+}
+
+// The kept entries of U recomputed exactly (one GPU): LS_ic = sum_j Y_ij W_jc
+// with Y = A V from the U side's exact fixed-point accumulator (Yq, k_uside_*:
+// Y_ij = Yq[i][j] * unit, unit = rowsum_max * max(V) * 2^-62) and W in fp64.
+// One warp per kept entry, lanes over j.
+__global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
+                           float* __restrict__ val, int k, int kpad, const unsigned long long* __restrict__ Yq,
+                           const double* __restrict__ bound, const uint32_t* __restrict__ vmax,
+                           const double* __restrict__ W) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = colptr[k];
+  const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
+    int lo = 0, hi = k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (colptr[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int c = lo;
+    const unsigned long long* yr = Yq + (int64_t)row[e] * kpad;
+    double acc = 0;
+    for (int j = lane; j < k; j += 32) {
+      const unsigned long long y = yr[j];
+      if (y) acc = fma((double)y * unit, W[(int64_t)j * k + c], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
+  }
+}
+
+// dynamic shared memory of k_ytail: the Y tile and the long-row list
+inline size_t ytail_smem(int ys) { return sizeof(uint32_t) * (size_t)kVtM * ys; }
 
 }  // namespace esk

@@ -9,11 +9,20 @@
   absolute error ~1e-7 of its column's scale, reading C15)
 * retained support: identical, except swaps between entries whose oracle
   values differ by <= TIE_TOL * max_j |ref[j,c]| (near-ties)
-* trajectory: |E_gpu - E_ref| <= TRAJ_TOL * E_ref per iteration (BJ:5), and
-  |R_gpu - R_ref| <= TRAJ_TOL * R_ref + 2 * ENTRY_TOL * (1 + R_ref): R (P:160)
-  is a difference of two factors that each carry the per-entry ENTRY_TOL, so
+* trajectory: |E_gpu - E_ref| <= TRAJ_TOL * E_ref per iteration (BJ:5).
+* residual R FROM THE SAME STATE (one iteration from the GPU's factor):
+  |R_gpu - R_ref| <= TRAJ_TOL * R_ref + 2 * ENTRY_TOL * (1 + R_ref): R is a
+  difference of two factors that each carry the per-entry ENTRY_TOL, so
   ||U_i - U_{i-1}|| may move by ENTRY_TOL (||U_i|| + ||U_{i-1}||); late
   iterations have R ~ 1e-4, where that term, not 1e-3 R, is the bound.
+* residual along a whole TRAJECTORY (50 iterations from U_0): not a parity
+  quantity.  The two runs' supports may differ by near-tie swaps (the selection
+  rule above), and late in a run, where R is small, a swapped threshold entry is
+  a large part of ||U_i - U_{i-1}||: the GPU's R differed from the oracle's run
+  by up to 41 % on the Medium sweep (t = 10,000, R ~ 3e-3, iteration 32;
+  DESIGN.md section 4) while E -- BJ:5's trajectory criterion -- stayed within
+  1e-3.  So R_1 (both runs start from U_0) and R one iteration past the end of
+  every trajectory, from the GPU's state, are the R checks (r_close).
 """
 import numpy as np
 
@@ -24,7 +33,7 @@ TRAJ_TOL = 1e-3
 
 
 def r_close(r_gpu: float, r_ref: float) -> bool:
-    """Residual R per iteration against the oracle's (see the module doc)."""
+    """Residual R of one iteration from the same state (module doc)."""
     return abs(r_gpu - r_ref) <= TRAJ_TOL * r_ref + 2 * ENTRY_TOL * (1 + r_ref)
 
 
@@ -79,10 +88,22 @@ def check_selection(gpu_F: np.ndarray, ref_F: np.ndarray, ref_ls: np.ndarray, t:
     return swaps, worst
 
 
+def assert_kept_values(kept_vals, ls_vals, col_scale):
+    """A kept factor entry is its LS entry: bitwise, or -- on the paper-order V
+    side, whose kept values are recomputed exactly after the selection
+    (k_polish_v) -- within the product tolerance of the
+    tensor-core LS value the selection used: the LS value's own tolerance,
+    PROD_TOL of its column's scale."""
+    kv = np.asarray(kept_vals, np.float64)
+    lv = np.asarray(ls_vals, np.float64)
+    assert np.all(np.abs(kv - lv) <= ENTRY_TOL * np.abs(lv) + PROD_TOL * col_scale), "kept value != its LS entry"
+
+
 def check_topt_property(ls: np.ndarray, F: np.ndarray, t: int | None):
     """Selection validity on the GPU's own LS values (any size): exactly
-    min(t, #positive) kept per column, kept values are the LS values, every
-    kept value >= every dropped positive, ties at the threshold -> lower rows."""
+    min(t, #positive) kept per column, kept values are the LS values
+    (assert_kept_values), every kept LS value >= every dropped positive, ties at
+    the threshold -> lower rows."""
     for c in range(ls.shape[1]):
         x = ls[:, c]
         pos = x > 0
@@ -90,11 +111,11 @@ def check_topt_property(ls: np.ndarray, F: np.ndarray, t: int | None):
         npos = int(pos.sum())
         want = npos if t is None else min(t, npos)
         assert kept.sum() == want, f"column {c}: kept {kept.sum()} want {want}"
-        assert np.all(F[kept, c] == x[kept])
+        assert_kept_values(F[kept, c], x[kept], np.abs(x).max())
         dropped = pos & ~kept
         if kept.any() and dropped.any():
             kmin = x[kept].min()
-            assert kmin >= x[dropped].max()
+            assert kmin >= x[dropped].max()     # on the values the selection used
             tie_dropped = np.nonzero(dropped & (x == kmin))[0]
             tie_kept = np.nonzero(kept & (x == kmin))[0]
             if len(tie_dropped):
@@ -116,11 +137,13 @@ def check_topt_property_coo(ls: np.ndarray, row, col, val, t: int | None):
         npos = int(np.count_nonzero(x > 0))
         want = npos if t is None else min(t, npos)
         assert len(kr) == want, f"column {c}: kept {len(kr)} want {want}"
-        assert np.all(kv == x[kr]) and np.all(kv > 0)
+        assert np.all(kv > 0)
+        assert_kept_values(kv, x[kr], np.abs(x).max())
         if len(kr) and want < npos:
-            kmin = kv.min()
+            kl = x[kr]                         # the LS values the selection used
+            kmin = kl.min()
             x[kr] = -np.inf
             assert kmin >= x.max(), f"column {c}: dropped positive above the kept minimum"
             tie_dropped = np.nonzero(x == kmin)[0]
             if len(tie_dropped):
-                assert kr[kv == kmin].max() < tie_dropped.min(), f"column {c}: tie not broken toward lower rows"
+                assert kr[kl == kmin].max() < tie_dropped.min(), f"column {c}: tie not broken toward lower rows"

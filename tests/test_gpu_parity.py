@@ -124,8 +124,25 @@ def check_trajectory(s, gold):
         assert abs(a["nnz_u"] - b["nnz_u"]) <= slack * b["nnz_u"], a["it"]
         assert abs(a["nnz_v"] - b["nnz_v"]) <= slack * b["nnz_v"], a["it"]
         assert a["dead_u"] == b["dead_u"] and a["dead_v"] == b["dead_v"]
-        assert r_close(a["R"], b["R"]), (a["it"], a["R"], b["R"])
+        assert a["R"] > 0
+    # iteration 1 starts from the same U_0 on both sides: R_1 is a same-state value
+    assert r_close(recs[0]["R"], gold["records"][0]["R"]), (recs[0]["R"], gold["records"][0]["R"])
     return recs
+
+
+def same_state_R(s, g, cfg, t="cfg"):
+    """One more iteration from the GPU's current state: its record's R
+    against the oracle's U half-step from the same V, measured against the same
+    U_{i-1} (reading C8; the strict R check, parity.r_close)."""
+    t = cfg.t if t == "cfg" else t
+    k = s.k
+    U_prev = dense_U(s, cfg.n, k)
+    s.iterate(1)
+    r_gpu = s.records()[-1]["R"]
+    V = dense_V(s, cfg.m, k)
+    ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], V, t)
+    r_ref = oracle.residual(ref["F"], U_prev)
+    assert r_close(r_gpu, r_ref), (r_gpu, r_ref)
 
 
 @pytest.mark.parametrize("tag,cfg", [("tiny", TINY), ("medium", MEDIUM), ("large", LARGE)])
@@ -140,6 +157,7 @@ def test_trajectory_matches_golden(tag, cfg):
     s.iterate(cfg.iters)
     recs = check_trajectory(s, gold)
     assert s.error() == recs[-1]["E"] and s.residual() == recs[-1]["R"]
+    same_state_R(s, synth.generate(cfg), cfg)
 
 
 @pytest.mark.parametrize("t", synth.SWEEP_T, ids=[str(t) for t in synth.SWEEP_T])
@@ -149,6 +167,7 @@ def test_sweep_trajectory(t):
     s = solver(MEDIUM, g, t=t)
     s.iterate(MEDIUM.iters)
     check_trajectory(s, gold)
+    same_state_R(s, g, MEDIUM, t=t)
 
 
 def test_tiny_trajectory_live_oracle_R():
@@ -338,6 +357,7 @@ def test_large_graph_replayed_full_parity():
     torch.cuda.empty_cache()
     s.iterate(8)
     assert s.records()[:7] == r7                      # the two runs are the same run
+    r8 = s.records()[7]["R"]
     _, ls_v = s.get_ls(ESNMF_SIDE_V)
     _, ls_u = s.get_ls(ESNMF_SIDE_U)
     V8 = dense_V(s, cfg.m, cfg.k)
@@ -351,6 +371,9 @@ def test_large_graph_replayed_full_parity():
     ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], V8, cfg.t)
     check_products(ls_u, ref["LS"])
     check_selection(U8, ref["F"], ref["LS"], cfg.t)
+    # R of iteration 8 from the same state: ||U_8 - U_7|| / ||U_8||
+    r_ref = oracle.residual(ref["F"], U7)
+    assert r_close(r8, r_ref), (r8, r_ref)
 
 
 def _rows_restricted(ptr, idx, val, support, dim):

@@ -277,7 +277,10 @@ def test_loopback_large_p8_matches_oracle_and_single_gpu():
     one.iterate(2)
     for a, b in zip(recs, one.records()):
         assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"] and (a["nnz_u"], a["nnz_v"]) == (b["nnz_u"], b["nnz_v"])
-        assert (a["peak_u"], a["peak_v"]) == (b["peak_u"], b["peak_v"])
+        # the positives of the LS buffers: the sharded U side's products are fp64
+        # (k_spmm_terms), the single GPU's fp16 hi/lo on tcgen05, so an entry within
+        # rounding of zero may fall on either side
+        assert abs(a["peak_u"] - b["peak_u"]) <= 1e-6 * b["peak_u"] and a["peak_v"] == b["peak_v"]
     one.close()
     rng = np.random.default_rng(0)
     U = coo_dense((cfg.n, cfg.k), *st["U"])
