@@ -225,6 +225,32 @@ typedef struct {
 
 esnmf_status esnmf_get_info(esnmf_t* h, esnmf_info* info);
 
+/* Per-half-step cost model of the last V side, from the compact
+ * factor and the document frequencies df_i of A (O(k t) work per half-step),
+ * plus the U side's product count for the current V.  The V-side tail order
+ * is chosen from it on the device each half-step: the paper's order
+ * (A^T_tail U) W when v_tail_products * ratio <= v_tail_gather_fma (ratio =
+ * the measured cost of one fixed-point shared-memory product over one gathered
+ * FMA, 8), else the reassociated A^T_tail (U W) gather -- and the gather also
+ * whenever W is too ill-conditioned for fp16 hi/lo operands (kappa_inf(G + eps I)
+ * > 1e4, or a column of W whose absolute sum exceeds 8 times its diagonal).
+ * Synchronises.  ESTATE before the first V side; EINVAL for NULL. */
+typedef struct {
+  double v_tail_products;    /* paper order: sum over active tail terms i of df_i * nnz(U row i) */
+  double v_tail_gather_fma;  /* reassociated: sum over active tail terms i of df_i * k */
+  double v_tail_active;      /* active tail entries of A^T (df summed over active tail terms) */
+  double v_head_products;    /* head terms: sum over active head terms of df_i * nnz(U row i) */
+  double v_head_mma_flops;   /* tensor-core flops the head issues (dense 128 x 64 tiles, 3 fp16 passes) */
+  double v_yw_mma_flops;     /* tensor-core flops of the (Y_tail W) chunks (paper order only) */
+  double u_products;         /* U side, paper order: sum over stored entries (d, c) of V of nnz(A^T row d) */
+  int32_t head_terms;        /* h */
+  int32_t v_tail_gather;     /* 1: the last V side ran the Z-row gather */
+  int32_t v_gather_by_cost;  /* ... chosen by the cost model (else by the conditioning) */
+  int32_t paper_order_tail;  /* 1: this handle has the paper-order tail (else always the gather) */
+} esnmf_cost;
+
+esnmf_status esnmf_cost_model(esnmf_t* h, esnmf_cost* out);
+
 /* Per-phase device timing with CUDA events on the handle's stream (the same
  * stream the kernels run on).  esnmf_profile(h, 1) clears the accumulators and
  * starts recording an event pair around every phase of every later half-step;

@@ -235,6 +235,9 @@ struct esnmf {
   uint32_t* ubits = nullptr;     // [n / 32] rows of U with a nonzero
   double* Z64 = nullptr;         // [U active rows][k] Z = U W in fp64 (k_form_z64)
   double vt_kmax = 1e4, vt_amax = 8.0;  // k_vcond_flag thresholds (ESNMF_VT_KMAX / ESNMF_VT_AMAX)
+  double vt_ratio = 8.0;         // cost of a paper-order product / a gathered FMA (ESNMF_VT_RATIO)
+  int32_t* termlen = nullptr;    // [n] stored entries of each term (row lengths of A, global)
+  double* vcost = nullptr;       // [8] the last V side's cost model (k_vt_cost)
   bool polish = true;            // kept V values recomputed exactly (ESNMF_NO_POLISH=1: off)
   double u_kmax = 100.0;         // U side: (Y W) in fp32 / fp16 hi/lo only for kappa_inf <= this (ESNMF_U_KMAX)
   unsigned long long* vt_next = nullptr;  // k_ytail's tile counter
@@ -476,35 +479,35 @@ void gram(esnmf_t* h, const Factor& f, double* G, int kk = 0, int kp = 0, double
 }
 
 template <int JB, bool PACKED>
-void sweep_launch(esnmf_t* h, const double* G, double* eps) {
+void sweep_launch(esnmf_t* h, const double* G, double* eps, SweepCond sc) {
   const bool glob = h->k > 224;
   const size_t smem = sweep_smem_bytes(h->k, glob);
   auto kern = k_sweep_inverse<JB, PACKED>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ++h->nlaunch;
-  kern<<<1, 1024, smem, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, glob ? h->sweep_scratch : nullptr);
+  kern<<<1, 1024, smem, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, glob ? h->sweep_scratch : nullptr, sc);
   CKL("sweep_inverse");
 }
 
-void sweep(esnmf_t* h, const double* G, double* eps) {
+void sweep(esnmf_t* h, const double* G, double* eps, SweepCond sc = SweepCond()) {
   const int JB = (h->k + 31) / 32;
   const bool packed = sweep_packed(h->k);
   if (JB <= 4) {  // register-resident matrix
     ++h->nlaunch;
     switch (JB) {
-      case 1: k_sweep_regs<1><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
-      case 2: k_sweep_regs<2><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
-      case 3: k_sweep_regs<3><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
-      default: k_sweep_regs<4><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags); break;
+      case 1: k_sweep_regs<1><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, sc); break;
+      case 2: k_sweep_regs<2><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, sc); break;
+      case 3: k_sweep_regs<3><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, sc); break;
+      default: k_sweep_regs<4><<<1, 1024, 0, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags, sc); break;
     }
     CKL("sweep_regs");
     return;
   }
   switch (JB) {
-    case 5: packed ? sweep_launch<5, true>(h, G, eps) : sweep_launch<5, false>(h, G, eps); break;
-    case 6: sweep_launch<6, true>(h, G, eps); break;
-    case 7: sweep_launch<7, true>(h, G, eps); break;
-    default: sweep_launch<8, true>(h, G, eps); break;
+    case 5: packed ? sweep_launch<5, true>(h, G, eps, sc) : sweep_launch<5, false>(h, G, eps, sc); break;
+    case 6: sweep_launch<6, true>(h, G, eps, sc); break;
+    case 7: sweep_launch<7, true>(h, G, eps, sc); break;
+    default: sweep_launch<8, true>(h, G, eps, sc); break;
   }
 }
 
@@ -668,10 +671,10 @@ void spmm_terms_launch(esnmf_t* h) {
 // fp32 copy of W and the conditioning flag choosing the fp32 or fp64 (Y W)
 void uside_w_prep(esnmf_t* h) {
   Side& su = h->side[ESNMF_SIDE_U];
-  h->nlaunch += 2;
+  h->nlaunch += 1;
   k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
-  // fp32 (Y W) when kappa(G_V + eps I) <= 100, else fp64 -- decided on the device
-  k_cond_flag<<<1, 256, 0, h->stream>>>(su.G, h->W, su.eps, h->k, h->u_kmax, h->flags + 3);
+  // fp32 / tensor-core (Y W) when kappa(G_V + eps I) <= u_kmax, else fp64 -- decided
+  // on the device by the U side's sweep (SweepCond, flags[3])
   if (h->utc_kn) {
     ++h->nlaunch;
     k_utc_wprep<<<h->k, 128, 0, h->stream>>>(h->W, h->k, h->utc_kn, h->utc_kk, h->wtc, h->wtc_scale);
@@ -1066,7 +1069,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     // dense-tile cost balanced a 400-byte gather per active entry).  Paper-order
     // tail: a tail entry costs nnz(U row) products instead, so the head keeps only
     // the densest term bands
-    double frac = h->ptail ? 0.025 : 0.015;
+    double frac = 0.015;
     const char* fe = getenv("ESNMF_HEAD_DF");
     if (fe && fe[0]) frac = atof(fe);
     const double min_df = std::max(1.0, frac * (double)h->m);
@@ -1236,6 +1239,16 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     h->Z64 = h->alloc<double>(n * (int64_t)h->k);
     if (const char* e = getenv("ESNMF_VT_KMAX")) h->vt_kmax = atof(e);
     if (const char* e = getenv("ESNMF_VT_AMAX")) h->vt_amax = atof(e);
+    if (const char* e = getenv("ESNMF_VT_RATIO")) h->vt_ratio = atof(e);
+    {
+      std::vector<int32_t> tl(n);
+      for (int64_t i = 0; i < n; ++i) tl[i] = (int32_t)(hptr[i + 1] - hptr[i]);
+      h->termlen = h->alloc<int32_t>(n);
+      CK(cudaMemcpyAsync(h->termlen, tl.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    h->vcost = h->alloc<double>(8);
+    CK(cudaMemsetAsync(h->vcost, 0, sizeof(double) * 8, h->stream));
     { const char* np_ = getenv("ESNMF_NO_POLISH"); h->polish = !(np_ && atoi(np_)); }
   }
   CKL("head_setup");
@@ -1280,7 +1293,7 @@ void ytail_launch(esnmf_t* h) {
   CK(cudaMemsetAsync(h->vt_next, 0, sizeof(unsigned long long), h->stream));
   ++h->nlaunch;
   k_ytail<<<grid, kVtThreads, smem, h->stream>>>(h->toff, h->tent, h->head_ntiles, h->ubits, h->umap, h->uent, h->kn,
-                                                  ys, h->ytile, h->vt_next);
+                                                  ys, h->ytile, h->vt_next, h->flags + 5);
   CKL("ytail");
 }
 
@@ -1350,24 +1363,35 @@ Factor& half_step(esnmf_t* h, int s) {
       CK(cudaMemsetAsync(h->Yq, 0, sizeof(unsigned long long) * h->n * h->kpad, h->stream));
     h->v_since_u = false;
   }
-  if (s == ESNMF_SIDE_V) {
-    if (!h->ptail) yq_clear_other(h);  // (paper-order mode: on the aux stream, beside the tail product)
-    h->v_since_u = true;
-  }
+  if (s == ESNMF_SIDE_V) h->v_since_u = true;
   if (s == ESNMF_SIDE_V && h->ptail) {
     // paper-order tail (k_vtail.cuh): Y_tail = A^T_tail U needs only U, so the
     // Gram + solve (a1, a2) run on aux beside it; then Z_head = U_head W, the
     // scales, and the tensor-core kernel: head chunks + (Y_tail W) chunks
-    { Phase ph(h, kVFormZ); urows_build(h, in); }
+    {
+      Phase ph(h, kVFormZ);
+      urows_build(h, in);
+      // cost model: paper order or Z-row gather for the tail this time
+      CK(cudaMemsetAsync(h->vcost, 0, sizeof(double) * 8, h->stream));
+      h->nlaunch += 2;
+      k_vt_cost<<<grid_for(in.cap_rows, 256, (int64_t)h->num_sms * 2), 256, 0, h->stream>>>(
+          in.active, in.n_active, h->umap, h->termlen, h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost);
+      k_vt_choose<<<1, 1, 0, h->stream>>>(h->vcost, h->vt_ratio, h->flags + 5);
+    }
     fork_to_aux(h, h->ev_vfork);
     {
       OnStream os(h, h->aux);
       if (!h->gramU_valid) { Phase ph(h, p0 + 0); gram(h, in, sd.G); }   // a1: P:63
-      { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }                    // a2
+      {  // a2, and: is Y_tail W safe in fp16 hi/lo this time?  (else: Z-row gather; flags[4])
+        Phase ph(h, p0 + 1);
+        SweepCond sc;
+        sc.flag = h->flags + 4;
+        sc.kmax = h->vt_kmax;
+        sc.amax = h->vt_amax;
+        sc.orflag = h->flags + 5;
+        sweep(h, sd.G, sd.eps, sc);
+      }
       form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
-      yq_clear_other(h);
-      ++h->nlaunch;  // is Y_tail W safe in fp16 hi/lo this time?  (else: Z-row gather)
-      k_vcond_flag<<<1, 256, 0, h->stream>>>(sd.G, h->W, sd.eps, h->k, h->vt_kmax, h->vt_amax, h->flags + 4);
     }
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
     join_from_aux(h, h->ev_vjoin);
@@ -1398,7 +1422,12 @@ Factor& half_step(esnmf_t* h, int s) {
       Phase ph(h, p0 + 0);
       gram(h, in, sd.G);
     }
-    { Phase ph(h, p0 + 1); sweep(h, sd.G, sd.eps); }               // a2
+    {  // a2 (U side: is the fp32 / tensor-core (Y W) safe?  flags[3])
+      Phase ph(h, p0 + 1);
+      SweepCond sc;
+      if (s == ESNMF_SIDE_U) sc.flag = h->flags + 3, sc.kmax = h->u_kmax;
+      sweep(h, sd.G, sd.eps, sc);
+    }
     if (overlap_u) uside_w_prep(h);
   }
   h->u_prefork = false;
@@ -1432,7 +1461,14 @@ Factor& half_step(esnmf_t* h, int s) {
       OnStream os(h, h->aux);
       Side& su = h->side[ESNMF_SIDE_U];
       { Phase ph2(h, kUGram); gram(h, out, su.G); }
-      { Phase ph2(h, kUSolve); sweep(h, su.G, su.eps); }
+      {
+        Phase ph2(h, kUSolve);
+        SweepCond sc;
+        sc.flag = h->flags + 3;
+        sc.kmax = h->u_kmax;
+        sweep(h, su.G, su.eps, sc);
+      }
+      yq_clear_other(h);  // the buffer the last U side used (k_polish_u has read it)
       uside_w_prep(h);
       h->u_prefork = true;
     }
@@ -2496,6 +2532,45 @@ esnmf_status esnmf_get_gram(esnmf_t* h, int32_t side, double* G, double* eps) {
       double tr = 0;
       for (int a = 0; a < h->k; ++a) tr += G[a * h->k + a];
       *eps = h->rho * (tr / h->k + 1.0);
+    }
+  });
+}
+
+esnmf_status esnmf_cost_model(esnmf_t* h, esnmf_cost* out) {
+  if (!h || !out) { g_last_error = "esnmf_cost_model: NULL argument"; return ESNMF_EINVAL; }
+  return guarded([&] {
+    set_device(h);
+    if (!h->V.has) fail(ESNMF_ESTATE, "no V side has run");
+    std::memset(out, 0, sizeof(*out));
+    Side& sv = h->side[ESNMF_SIDE_V];
+    out->head_terms = h->head_h;
+    out->paper_order_tail = h->ptail ? 1 : 0;
+    double* d = h->red;  // scratch
+    CK(cudaMemsetAsync(d, 0, sizeof(double), h->stream));
+    ++h->nlaunch;
+    k_u_cost<<<grid_for(h->V.cap, 256, (int64_t)h->num_sms * 4), 256, 0, h->stream>>>(
+        h->V.colptr, h->V.row, h->k, sv.row0, sv.rows, sv.T.ptr, d);
+    CKL("u_cost");
+    sync_check(h);
+    CK(cudaMemcpy(&out->u_products, d, sizeof(double), cudaMemcpyDeviceToHost));
+    if (h->head_ntiles > 0) {
+      const double tiles = (double)h->head_ntiles;
+      out->v_head_mma_flops = tiles * 128.0 * (double)h->head_h * h->kn * 2.0 * 3.0;
+    }
+    if (h->ptail) {
+      double c[8];
+      int fl[8];
+      CK(cudaMemcpy(c, h->vcost, sizeof(c), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+      out->v_tail_products = c[0];
+      out->v_tail_gather_fma = c[1];
+      out->v_tail_active = c[2];
+      out->v_head_products = c[3];
+      out->v_tail_gather = fl[4];
+      out->v_gather_by_cost = fl[5];
+      if (!fl[4]) out->v_yw_mma_flops = (double)h->head_ntiles * 128.0 * h->kn * h->kn * 2.0 * 3.0;
+    } else {
+      out->v_tail_gather = 1;
     }
   });
 }

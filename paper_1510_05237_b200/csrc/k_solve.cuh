@@ -18,6 +18,44 @@ ESNMF_DEV int64_t pk_idx(int i, int j, int k) {  // i <= j, packed upper, row-ma
 
 inline bool sweep_packed(int k) { return (int64_t)k * k * 8 + k * 8 > 200 * 1024; }
 
+// Conditioning of the solve, computed by the sweep kernel itself after W is
+// written (no extra launch): kappa_inf(G + eps I) = ||G + eps I||_inf ||W||_inf and
+// the column amplification max_c sum_j |W_jc| / |W_cc| (W symmetric: row sums).
+// *flag = kappa > kmax || (amax > 0 && amplification > amax) || (orflag && *orflag).
+// Consumers: the U side's fp32 / tensor-core (Y W) (k_uside_*; flag = use fp64) and
+// the V side's paper-order tail (k_vtail.cuh; flag = Z-row gather).
+struct SweepCond {
+  int* flag = nullptr;          // null: not computed
+  double kmax = 0, amax = 0;
+  const int* orflag = nullptr;
+};
+
+__device__ void sweep_cond(const double* __restrict__ G, const double* __restrict__ W, double eps, int k,
+                           const SweepCond& sc) {
+  __shared__ double sg[32], sw[32], sa[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double g = 0, w = 0, amp = 0;
+  for (int i = warp; i < k; i += nw) {
+    double rg = 0, rw = 0;
+    for (int j = lane; j < k; j += 32) {
+      rg += fabs(G[(int64_t)i * k + j] + (i == j ? eps : 0.0));
+      rw += fabs(W[(int64_t)i * k + j]);
+    }
+    rg = warp_sum(rg);
+    rw = warp_sum(rw);
+    g = fmax(g, rg);
+    w = fmax(w, rw);
+    amp = fmax(amp, rw / fabs(W[(int64_t)i * k + i]));
+  }
+  if (lane == 0) sg[warp] = g, sw[warp] = w, sa[warp] = amp;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gm = 0, wm = 0, am = 0;
+    for (int q = 0; q < nw; ++q) gm = fmax(gm, sg[q]), wm = fmax(wm, sw[q]), am = fmax(am, sa[q]);
+    *sc.flag = !(gm * wm <= sc.kmax) || (sc.amax > 0 && !(am <= sc.amax)) || (sc.orflag && *sc.orflag);
+  }
+}
+
 // k <= 128: the whole matrix lives in registers.  Thread (ty = warp, tx = lane)
 // owns elements (i, j) = (ty + 32a, tx + 32b), a, b < JB.  Per pivot the owner
 // warp of row p publishes it to shared memory (double-buffered, so one barrier
@@ -41,7 +79,7 @@ __device__ __forceinline__ double fast_rcp(double d) {
 template <int JB>
 __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ G, int k, double rho,
                                                      double* __restrict__ W, double* __restrict__ eps_out,
-                                                     int* __restrict__ singular) {
+                                                     int* __restrict__ singular, SweepCond sc) {
   __shared__ double vbuf[2][32 * JB];
   __shared__ double red[32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -113,6 +151,10 @@ __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ 
       if (i < k && j < k) W[(int64_t)i * k + j] = -r[a][b];
     }
   if (threadIdx.x == 0) *eps_out = eps;
+  if (sc.flag) {
+    __syncthreads();  // W (global) written by the whole block
+    sweep_cond(G, W, eps, k, sc);
+  }
 }
 
 // 2-D thread layout (32 x 32 warps): warp ty updates rows i = ty + 32 a (so the
@@ -121,7 +163,7 @@ __global__ void __launch_bounds__(1024) k_sweep_regs(const double* __restrict__ 
 template <int JB, bool PACKED>
 __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict__ G, int k, double rho,
                                                         double* __restrict__ W, double* __restrict__ eps_out,
-                                                        int* __restrict__ singular, double* gscratch) {
+                                                        int* __restrict__ singular, double* gscratch, SweepCond sc) {
   extern __shared__ double dsm[];
   __shared__ double red[32];
   double* v = dsm;                              // old pivot row
@@ -178,6 +220,10 @@ __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict
   for (int i = ty; i < k; i += nty)
     for (int j = tx; j < k; j += 32) W[(int64_t)i * k + j] = -P[idx(i, j)];
   if (threadIdx.x == 0) *eps_out = eps;
+  if (sc.flag) {
+    __syncthreads();
+    sweep_cond(G, W, eps, k, sc);
+  }
 }
 
 inline size_t sweep_smem_bytes(int k, bool global_scratch) {

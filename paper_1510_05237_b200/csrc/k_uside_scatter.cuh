@@ -112,50 +112,6 @@ __global__ void __launch_bounds__(256) k_uside_finish(int64_t rows, const double
   }
 }
 
-// kappa_inf(G + eps I) = ||G + eps I||_inf ||W||_inf (one block); *use_fp64 = kappa > kmax.
-// The fp32 product Y W is used only for well-conditioned systems (error ~ kappa * 2^-24);
-// near-singular Grams (e.g. two topics on the same single document) take the fp64 kernel.
-__global__ void k_cond_flag(const double* __restrict__ G, const double* __restrict__ W, const double* eps, int k,
-                            double kmax, int* __restrict__ use_fp64) {
-  __shared__ double sm[32];
-  double g = 0, w = 0;
-  // one warp per row, lanes across it (coalesced), row sums by warp reduction
-  const double e = *eps;
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x >> 5; i < k; i += blockDim.x >> 5) {
-    double sg = 0, sw = 0;
-    for (int j = lane; j < k; j += 32) {
-      sg += fabs(G[(int64_t)i * k + j] + (i == j ? e : 0.0));
-      sw += fabs(W[(int64_t)i * k + j]);
-    }
-    sg = warp_sum(sg);
-    sw = warp_sum(sw);
-    g = fmax(g, sg);
-    w = fmax(w, sw);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    g = fmax(g, __shfl_xor_sync(kFull, g, o));
-    w = fmax(w, __shfl_xor_sync(kFull, w, o));
-  }
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = g;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double gm = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) gm = fmax(gm, sm[q]);
-    sm[0] = gm;
-  }
-  __syncthreads();
-  const double gm = sm[0];
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = w;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double wm = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) wm = fmax(wm, sm[q]);
-    *use_fp64 = !(gm * wm <= kmax);
-  }
-}
-
 // The same Y = A V driven by V's columns: block (c, chunk) takes ndocs
 // entries (doc j, v) of topic column c.  Each document row of A^T stores its
 // head-term entries first (k_reorder_head, nh[j] of them): those accumulate in

@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restri
                                                          const uint64_t* __restrict__ umap,
                                                          const int2* __restrict__ uent, int kn, int ys,
                                                          uint8_t* __restrict__ ytile,
-                                                         unsigned long long* __restrict__ next) {
+                                                         unsigned long long* __restrict__ next,
+                                                         const int* __restrict__ zpath) {
+  if (zpath && *zpath) return;  // the cost model chose the Z-row gather this half-step
   extern __shared__ uint32_t Ysm[];
   __shared__ int64_t s_tile;
   const int T = blockDim.x;
@@ -286,41 +288,6 @@ __global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restri
       *reinterpret_cast<uint4*>(cb + (size_t)kVtM * w * 2 + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
     __syncthreads();
-  }
-}
-
-// V-side fallback flag: 1 when the product Y_tail W (fp16 hi/lo operands, ~2^-22
-// relative to each term) could cancel badly -- kappa_inf(G + eps I) > kmax, or a
-// column of W whose absolute sum exceeds wmax times its diagonal entry; the Z-row
-// gather (Z = U W formed in fp64) then takes the tail for this iteration
-__global__ void k_vcond_flag(const double* __restrict__ G, const double* __restrict__ W, const double* eps, int k,
-                             double kmax, double wmax, int* __restrict__ flag) {
-  __shared__ double sg[32], sw[32], sa[32];
-  double g = 0, w = 0, amp = 0;
-  const double e = *eps;
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x >> 5; i < k; i += blockDim.x >> 5) {  // row i (W, G symmetric: also column i)
-    double rg = 0, rw = 0;
-    for (int j = lane; j < k; j += 32) {
-      rg += fabs(G[(int64_t)i * k + j] + (i == j ? e : 0.0));
-      rw += fabs(W[(int64_t)i * k + j]);
-    }
-    rg = warp_sum(rg);
-    rw = warp_sum(rw);
-    g = fmax(g, rg);
-    w = fmax(w, rw);
-    amp = fmax(amp, rw / fabs(W[(int64_t)i * k + i]));
-  }
-  if (lane == 0) {
-    sg[threadIdx.x >> 5] = g;
-    sw[threadIdx.x >> 5] = w;
-    sa[threadIdx.x >> 5] = amp;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double gm = 0, wm = 0, am = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) gm = fmax(gm, sg[q]), wm = fmax(wm, sw[q]), am = fmax(am, sa[q]);
-    *flag = !(gm * wm <= kmax && am <= wmax);
   }
 }
 
@@ -435,6 +402,64 @@ __global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __
     acc = warp_sum(acc);
     if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
   }
+}
+
+// Per-half-step cost model of the V-side tail, from U's row view
+// and the document frequencies of A (termlen[i] = stored entries of term i):
+//   cost[0] = sum over active tail rows i of termlen_i * r_i   (paper order: products, k_ytail)
+//   cost[1] = sum over active tail rows i of termlen_i * k     (reassociated: FMAs of the Z-row gather)
+//   cost[2] = sum over active tail rows i of termlen_i         (active tail entries of A^T)
+//   cost[3] = sum over active head rows of termlen_i * r_i     (head products, for the report)
+// (integer-valued fp64 sums: exact in any order).  cost[] zeroed by the caller.
+__global__ void k_vt_cost(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
+                          const uint64_t* __restrict__ umap, const int32_t* __restrict__ termlen,
+                          const int32_t* __restrict__ headslot, int k, double* __restrict__ cost) {
+  __shared__ double sm[32];
+  const int64_t na = *n_active;
+  double p = 0, z = 0, a = 0, hp = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = active[r];
+    const double len = (double)termlen[i], cnt = (double)(umap[i] & 0xFFFFFFFFull);
+    if (headslot && headslot[i] >= 0) {
+      hp += len * cnt;
+    } else {
+      p += len * cnt;
+      z += len * k;
+      a += len;
+    }
+  }
+  p = block_sum(p, sm);
+  z = block_sum(z, sm);
+  a = block_sum(a, sm);
+  hp = block_sum(hp, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(&cost[0], p);
+    atomicAdd(&cost[1], z);
+    atomicAdd(&cost[2], a);
+    atomicAdd(&cost[3], hp);
+  }
+}
+
+// the product order of the tail this half-step: Z-row gather (flag = 1) when the
+// paper order's products outweigh the gather's FMAs at the measured relative cost
+// of one smem fixed-point product vs one gathered FMA (ratio)
+__global__ void k_vt_choose(const double* __restrict__ cost, double ratio, int* __restrict__ zpath) {
+  *zpath = cost[0] * ratio > cost[1];
+}
+
+// U side's paper-order products for the current V: sum over V's entries (d, c) of
+// the stored entries of document d (this rank's documents; out zeroed by the caller)
+__global__ void k_u_cost(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row, int k, int64_t row0,
+                         int64_t rows, const int64_t* __restrict__ ptr, double* __restrict__ out) {
+  __shared__ double sm[32];
+  const int64_t total = colptr[k];
+  double p = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = (int64_t)row[e] - row0;
+    if (d >= 0 && d < rows) p += (double)(ptr[d + 1] - ptr[d]);
+  }
+  p = block_sum(p, sm);
+  if (threadIdx.x == 0) atomicAdd(out, p);
 }
 
 // dynamic shared memory of k_ytail: the Y tile and the long-row list

@@ -59,6 +59,16 @@ class esnmf_info(ctypes.Structure):
                 ("ls_cols", c_i32), ("seq_block", c_i32)]
 
 
+class esnmf_cost(ctypes.Structure):
+    _fields_ = [("v_tail_products", c_dbl), ("v_tail_gather_fma", c_dbl), ("v_tail_active", c_dbl),
+                ("v_head_products", c_dbl), ("v_head_mma_flops", c_dbl), ("v_yw_mma_flops", c_dbl),
+                ("u_products", c_dbl), ("head_terms", c_i32), ("v_tail_gather", c_i32),
+                ("v_gather_by_cost", c_i32), ("paper_order_tail", c_i32)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 class esnmf_phase(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("calls", c_i64), ("ms", c_dbl)]
 
@@ -88,6 +98,7 @@ SIGNATURES = {
     "esnmf_get_gram": (ctypes.c_int, [c_p, c_i32, c_p, ctypes.POINTER(c_dbl)]),
     "esnmf_get_info": (ctypes.c_int, [c_p, ctypes.POINTER(esnmf_info)]),
     "esnmf_profile": (ctypes.c_int, [c_p, c_i32]),
+    "esnmf_cost_model": (ctypes.c_int, [c_p, ctypes.POINTER(esnmf_cost)]),
     "esnmf_phase_times": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(esnmf_phase)]),
     "esnmf_destroy": (None, [c_p]),
     "esnmf_strerror": (ctypes.c_char_p, [ctypes.c_int]),
@@ -250,6 +261,14 @@ def esnmf_get_info(h) -> dict:
     return {f: getattr(i, f) for f, _ in i._fields_}
 
 
+def esnmf_cost_model(h) -> dict:
+    """The last V side's cost model and tail order, and the U side's product count
+    (esnmf_cost_model in include/esnmf.h)."""
+    c = esnmf_cost()
+    _check(lib().esnmf_cost_model(h, ctypes.byref(c)), "esnmf_cost_model")
+    return c.as_dict()
+
+
 def esnmf_profile(h, enable: bool):
     _check(lib().esnmf_profile(h, 1 if enable else 0), "esnmf_profile")
 
@@ -370,6 +389,9 @@ class ESNMF:
 
     def info(self) -> dict:
         return esnmf_get_info(self.h)
+
+    def cost_model(self) -> dict:
+        return esnmf_cost_model(self.h)
 
     def profile(self, enable: bool = True):
         esnmf_profile(self.h, enable)

@@ -60,15 +60,16 @@ def test_struct_layouts_match_header(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "esnmf.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(esnmf_options), sizeof(esnmf_record),"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(esnmf_options), sizeof(esnmf_record),"
         " sizeof(esnmf_info), sizeof(esnmf_comm), offsetof(esnmf_options, inputs_on_device),"
-        " offsetof(esnmf_record, active_v), offsetof(esnmf_info, normA2)); return 0;}\n")
+        " offsetof(esnmf_record, active_v), offsetof(esnmf_info, normA2), sizeof(esnmf_cost),"
+        " offsetof(esnmf_cost, v_tail_gather)); return 0;}\n")
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [ctypes.sizeof(B.esnmf_options), ctypes.sizeof(B.esnmf_record), ctypes.sizeof(B.esnmf_info),
             ctypes.sizeof(B.esnmf_comm), B.esnmf_options.inputs_on_device.offset, B.esnmf_record.active_v.offset,
-            B.esnmf_info.normA2.offset]
+            B.esnmf_info.normA2.offset, ctypes.sizeof(B.esnmf_cost), B.esnmf_cost.v_tail_gather.offset]
     assert got == want
 
 
