@@ -1378,9 +1378,10 @@ Factor& half_step(esnmf_t* h, int s) {
           in.active, in.n_active, h->umap, h->termlen, h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost);
       k_vt_choose<<<1, 1, 0, h->stream>>>(h->vcost, h->vt_ratio, h->flags + 5);
     }
-    fork_to_aux(h, h->ev_vfork);
+    const bool vser = getenv("ESNMF_V_SERIAL") != nullptr;  // (measurement: the solve before the tail, one stream)
+    if (!vser) fork_to_aux(h, h->ev_vfork);
     {
-      OnStream os(h, h->aux);
+      OnStream os(h, vser ? h->stream : h->aux);
       if (!h->gramU_valid) { Phase ph(h, p0 + 0); gram(h, in, sd.G); }   // a1: P:63
       {  // a2, and: is Y_tail W safe in fp16 hi/lo this time?  (else: Z-row gather; flags[4])
         Phase ph(h, p0 + 1);
@@ -1394,8 +1395,10 @@ Factor& half_step(esnmf_t* h, int s) {
       form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
     }
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
-    join_from_aux(h, h->ev_vjoin);
-    h->aux_pending = false;  // the join covers the previous record's kernels too
+    if (!vser) {
+      join_from_aux(h, h->ev_vjoin);
+      h->aux_pending = false;  // the join covers the previous record's kernels too
+    }
     {
       Phase ph(h, kVSpmm);  // fallback only (the kernels return at once otherwise)
       form_z(h, in, h->flags + 4);

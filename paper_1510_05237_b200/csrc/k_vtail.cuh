@@ -356,16 +356,18 @@ __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __
     const int64_t r = (int64_t)row[e] - row0;
     const int64_t s1 = ptr[r + 1];
     double acc = 0;
-    for (int64_t q0 = ptr[r] + lane; q0 < s1; q0 += 128) {  // 4 entries per lane in flight
-      int2 en[4];
-      int32_t rm[4];
+    for (int64_t q0 = ptr[r] + lane; q0 < s1; q0 += 256) {  // 8 entries per lane in flight
+      int2 en[8];
+      int32_t rm[8];
+      double z[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) en[u] = q0 + 32 * u < s1 ? ent[q0 + 32 * u] : make_int2(0, 0);
+      for (int u = 0; u < 8; ++u) en[u] = q0 + 32 * u < s1 ? __ldg(ent + q0 + 32 * u) : make_int2(0, 0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) rm[u] = q0 + 32 * u < s1 ? rowmap[en[u].x] : -1;
+      for (int u = 0; u < 8; ++u) rm[u] = q0 + 32 * u < s1 ? __ldg(rowmap + en[u].x) : -1;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (rm[u] >= 0) acc = fma((double)__int_as_float(en[u].y), Z64[(int64_t)rm[u] * k + c], acc);
+      for (int u = 0; u < 8; ++u) z[u] = rm[u] >= 0 ? __ldg(Z64 + (int64_t)rm[u] * k + c) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fma((double)__int_as_float(en[u].y), z[u], acc);
     }
     acc = warp_sum(acc);
     // an entry kept for a tensor-core LS value within rounding of zero keeps that
@@ -394,10 +396,11 @@ __global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __
     }
     const int c = lo;
     const unsigned long long* yr = Yq + (int64_t)row[e] * kpad;
+    const double* wr = W + (int64_t)c * k;  // W symmetric: column c = row c (coalesced)
     double acc = 0;
     for (int j = lane; j < k; j += 32) {
-      const unsigned long long y = yr[j];
-      if (y) acc = fma((double)y * unit, W[(int64_t)j * k + c], acc);
+      const unsigned long long y = __ldg(yr + j);
+      acc = fma((double)y * unit, __ldg(wr + j), acc);
     }
     acc = warp_sum(acc);
     if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
