@@ -333,11 +333,14 @@ def run_ours(args):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     mr = {}
-    if world > 1:  # row-sharded A / A^T, candidates allgathered + T allreduced over NCCL
-        from paper_1510_05237_b200.comm import TorchDistComm
+    nccl = None
+    if world > 1:  # row-sharded A / A^T, candidates allgathered + T allreduced: the library's own NCCL
+        from paper_1510_05237_b200.comm import nccl_comm
 
-        comm = TorchDistComm()
-        mr = dict(world=world, rank=rank, comm=comm.struct)
+        nccl = nccl_comm(local)
+        mr = dict(world=world, rank=rank, comm=nccl.struct)
+        print(f"bench rank {rank}: libesnmf NCCL communicator rank {nccl.rank} of {nccl.world} on cuda:{local}",
+              file=sys.stderr, flush=True)
     s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, stream=stream.cuda_stream, device=local, **mr)
     # iteration 1 (from the dense U_0) timed on its own, then the warm-up
     barrier(world)
@@ -488,7 +491,8 @@ def run_ours(args):
                        "state": f"steady state after {args.warmup} warm-up iterations from U0",
                        "l2": f"inputs larger than L2 (A and A^T {a_bytes / 1e9:.2f} GB each as CSR), no flush",
                        "parallelism": "single GPU" if world == 1 else
-                       f"{world} GPUs: A / A^T row-sharded, top-t candidates allgathered, T allreduced (NCCL)"},
+                       f"{world} GPUs: A / A^T row-sharded, top-t candidates allgathered, T allreduced "
+                       f"(the library's own NCCL communicator, CUDA-graph captured)"},
             "roofline": roof,
             "iteration_roofline": iteration,
             "iteration1_ms": round(it1_ms, 3),
@@ -506,6 +510,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        nccl.close()
         dist.destroy_process_group()
 
 

@@ -81,6 +81,25 @@ typedef struct {
   int (*allreduce_sum_f64)(void* ctx, double* buf, int64_t count, void* stream);
 } esnmf_comm;
 
+/*
+ * Built-in collectives: an NCCL communicator owned by the library (NVLink /
+ * NVSwitch between the GPUs of one box).  The library calls
+ * ncclAllGather / ncclAllReduce on its own stream -- no host callback -- so a
+ * sharded iteration is captured into a CUDA graph like a single-GPU one.
+ * libnccl.so.2 is loaded at run time (dlopen; the one torch loads when present).
+ *   esnmf_nccl_unique_id: rank 0 draws the id (NCCL_UNIQUE_ID_BYTES = 128 bytes
+ *     into `id`); the caller broadcasts it to every rank (any transport).
+ *   esnmf_nccl_comm_create: every rank, collectively, with the same id; `device`
+ *     = this rank's CUDA ordinal.  *out is an esnmf_comm for esnmf_options.comm,
+ *     owned by the library until esnmf_nccl_comm_destroy (after the handles that
+ *     use it are destroyed).
+ * Errors: ECOMM (NCCL missing or failed; esnmf_last_error names the cause),
+ * EINVAL (NULL, world < 1, rank out of range). */
+#define ESNMF_NCCL_ID_BYTES 128
+esnmf_status esnmf_nccl_unique_id(void* id);
+esnmf_status esnmf_nccl_comm_create(int32_t world, int32_t rank, const void* id, int32_t device, esnmf_comm** out);
+void esnmf_nccl_comm_destroy(esnmf_comm* comm);
+
 typedef struct {
   uint64_t seed;        /* U_0 seed (reading C10), default 0 (BJ:7) */
   double ridge_scale;   /* rho of eps = rho (tr G / k + 1), default 1e-10 (C6) */

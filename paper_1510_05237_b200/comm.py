@@ -1,5 +1,10 @@
 """Collective callbacks for multi-rank handles (``esnmf_comm`` in include/esnmf.h).
 
+* ``nccl_comm`` -- the library's OWN NCCL communicator (esnmf_nccl_comm_create):
+  ncclAllGather / ncclAllReduce issued by the library on its stream, no host
+  callback, so sharded iterations are captured into CUDA graphs.  The default
+  for one process per GPU (bench.py --gpus N).
+
 The library calls ``allgather(ctx, send, recv, bytes_per_rank, stream)`` and
 ``allreduce_sum_f64(ctx, buf, count, stream)`` with DEVICE pointers, stream
 ordered on ``stream``.  Two implementations, both plumbing only:
@@ -77,6 +82,31 @@ class TorchDistComm:
         except Exception as e:  # pragma: no cover
             print("esnmf allreduce failed:", e)
             return 1
+
+
+def nccl_comm(device: int, group=None):
+    """The library's own NCCL communicator over a torch.distributed group: rank 0
+    draws the NCCL unique id (esnmf_nccl_unique_id), the group broadcasts it
+    (any backend: gloo on CPU, NCCL on GPUs), every rank creates the communicator
+    collectively.  Returns an ``esnmf.NcclComm`` (``.struct`` for ESNMF(comm=...))."""
+    import torch.distributed as dist
+
+    from .esnmf import NcclComm, esnmf_nccl_unique_id
+
+    uid = [esnmf_nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return NcclComm(dist.get_world_size(group), dist.get_rank(group), uid[0], device)
+
+
+def broadcast_nccl_id(group=None) -> bytes:
+    """Rank 0's NCCL unique id on every rank of the group (host logic of nccl_comm)."""
+    import torch.distributed as dist
+
+    from .esnmf import esnmf_nccl_unique_id
+
+    uid = [esnmf_nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    return uid[0]
 
 
 class LoopbackGroup:

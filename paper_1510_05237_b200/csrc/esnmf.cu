@@ -15,6 +15,8 @@
 // Steady-state iterations are replayed as CUDA graphs; the host never
 // synchronises inside esnmf_iterate.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -145,6 +147,62 @@ struct Side {
   uint64_t* mscratch = nullptr;
 };
 
+// ---- built-in NCCL collectives (esnmf_nccl_*; libnccl.so.2 loaded at run time) ----
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      a.error = std::string("libnccl.so.2 not found: ") + dlerror();
+      return a;
+    }
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(lib, "ncclCommInitRank"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(lib, "ncclAllGather"));
+    a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(lib, "ncclAllReduce"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
+    a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(lib, "ncclGetErrorString"));
+    if (!a.getUniqueId || !a.commInitRank || !a.allGather || !a.allReduce || !a.commDestroy || !a.getErrorString)
+      a.error = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+struct NcclCtx {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+};
+
+int nccl_allgather_cb(void* ctx, const void* send, void* recv, int64_t bytes, void* stream) {
+  auto* c = static_cast<NcclCtx*>(ctx);
+  return nccl_api().allGather(send, recv, (size_t)bytes, ncclUint8, c->comm, (cudaStream_t)stream) == ncclSuccess ? 0
+                                                                                                               : 1;
+}
+
+int nccl_allreduce_cb(void* ctx, double* buf, int64_t count, void* stream) {
+  auto* c = static_cast<NcclCtx*>(ctx);
+  return nccl_api().allReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, c->comm, (cudaStream_t)stream) ==
+                 ncclSuccess
+             ? 0
+             : 1;
+}
+
+// a communicator the library owns: stream-ordered device collectives, CUDA-graph capturable
+bool builtin_nccl(const esnmf_comm& c) { return c.allgather == nccl_allgather_cb && c.allreduce_sum_f64 == nccl_allreduce_cb; }
+
 }  // namespace
 
 struct esnmf {
@@ -176,6 +234,7 @@ struct esnmf {
   double rho = 1e-10;
   uint64_t seed = 0;
   int world = 1, rank = 0;
+  bool sharded = false;        // the multi-rank paths (world > 1; or ESNMF_FORCE_SHARDED=1 with a comm, tests)
   esnmf_comm comm{};
   Side side[2];  // 0: V side (A^T rows = documents), 1: U side (A rows = terms)
   Factor U[2];
@@ -745,7 +804,7 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap, const int* gate = nullptr) {
     CKL("spmm_narrow");
     return;
   }
-  if (s == ESNMF_SIDE_U && h->world == 1) {
+  if (s == ESNMF_SIDE_U && !h->sharded) {
     switch ((h->k + 31) / 32) {
       case 1: uside_scatter_launch<1>(h); break;
       case 2: uside_scatter_launch<2>(h); break;
@@ -1011,7 +1070,7 @@ void vhead_launch_st(esnmf_t* h) {
   // (ESNMF_FUSED_SELECT=1): the per-element counting costs the epilogue more
   // (+0.14 ms at Large) than the streaming pass it saves (~0.1 ms)
   const int64_t t = h->tside[ESNMF_SIDE_V];
-  sv.fused = sv.pred && !h->whole && h->world == 1 && t >= 0 && t <= kSelFastT && t <= sv.above_t &&
+  sv.fused = sv.pred && !h->whole && !h->sharded && t >= 0 && t <= kSelFastT && t <= sv.above_t &&
              !(h->ktot && h->seq_b > 0) &&  // Alg. 3 deflates X after this kernel
              h->kn <= 128 &&                 // <= 4 column chunks per epilogue warp
              ceil_div(h->head_ntiles, std::min<int64_t>(h->head_ntiles, h->num_sms)) < 65536 &&  // 16-bit counts
@@ -1047,7 +1106,7 @@ void vhead_launch(esnmf_t* h) {
 // (row lengths of A, global), at least `min_df` of the documents each, a
 // multiple of 64 terms, at most kHeadMax; or `want` terms when want > 0.
 // kpad <= 8 on one GPU: the V side runs k_spmm_narrow (no head, no padded Z gather)
-bool narrow_v(esnmf_t* h) { return h->kpad <= 8 && h->world == 1 && !getenv("ESNMF_NO_NARROW"); }
+bool narrow_v(esnmf_t* h) { return h->kpad <= 8 && !h->sharded && !getenv("ESNMF_NO_NARROW"); }
 
 void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (narrow_v(h)) return;  // narrow k: the V side is an SpMM with a compact z (k_spmm_narrow)
@@ -1121,7 +1180,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     k_doc_rowsum_max<<<grid_for(std::max<int64_t>(sv.rows, 1), 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
         sv.T.ptr, sv.T.ent, sv.rows, h->rowsum_bits);
   }
-  if (h->world > 1) {
+  if (h->sharded) {
     // the scales derived from max|A| and the largest document row sum must be the
     // same on every rank (every rank then rounds exactly as one GPU would)
     h->gmax_buf = h->alloc<uint32_t>(4 * (h->world + 1));
@@ -1310,7 +1369,7 @@ void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val)
 
 // kept U entries recomputed exactly from the fixed-point A V (one GPU; k_polish_u)
 void polish_u(esnmf_t* h, Factor& out) {
-  if (h->world != 1 || !h->Yq || !h->polish || (h->ktot && h->seq_b > 0)) return;
+  if (h->sharded || !h->Yq || !h->polish || (h->ktot && h->seq_b > 0)) return;
   ++h->nlaunch;
   k_polish_u<<<grid_for(out.cap, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
       out.colptr, out.row, out.val, h->k, h->kpad, h->Yq, h->rsum_max, h->vmax, h->W);
@@ -1355,7 +1414,7 @@ Factor& half_step(esnmf_t* h, int s) {
   Factor& out = (s == ESNMF_SIDE_V) ? h->V : h->U[1 - h->ucur];
   if (!in.has) fail(ESNMF_ESTATE, s == ESNMF_SIDE_V ? "U is not set" : "V is not set (run the V side first)");
   const int p0 = s == ESNMF_SIDE_V ? kVGram : kUGram;
-  const bool overlap_u = s == ESNMF_SIDE_U && h->world == 1;    // Gram + solve on aux, beside the scatter
+  const bool overlap_u = s == ESNMF_SIDE_U && !h->sharded;    // Gram + solve on aux, beside the scatter
   if (s == ESNMF_SIDE_U) join_metrics(h);  // (only pending after a bare half_step call)
   if (s == ESNMF_SIDE_U && h->Yqb[0]) {
     h->Yq = h->Yqb[h->yq_par];
@@ -1446,7 +1505,7 @@ Factor& half_step(esnmf_t* h, int s) {
     join_metrics(h);  // the previous iteration's record reads V
     if (s == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, out);
-    if (h->world == 1) {
+    if (!h->sharded) {
       select_topt(h, s, out);                                      // a4 clamp + a5 top-t
       if (s == ESNMF_SIDE_V) polish_v(h, out.colptr, out.row, out.val);
       else polish_u(h, out);
@@ -1457,7 +1516,7 @@ Factor& half_step(esnmf_t* h, int s) {
   {
     Phase ph(h, p0 + 5);
     factor_build_rows(h, out, steady_maxcol(h, s, out.rows));
-    if (s == ESNMF_SIDE_V && h->world == 1) {
+    if (s == ESNMF_SIDE_V && !h->sharded) {
       // the U side's a1 + a2 need only V's row view: start them now on aux,
       // beside V's row-CSR build and the U side's scatter
       fork_to_aux(h, h->ev_ufork);
@@ -1532,7 +1591,7 @@ void flush_metrics(esnmf_t* h) {
   // a8 error: T = tr(U^T (A V)) from the U side's LS rows.  On one GPU
   // the trace and the record run on the aux stream, beside the next V side
   // (joined before that V side replaces V, join_metrics).
-  const bool overlap_m = h->world == 1;
+  const bool overlap_m = !h->sharded;
   if (overlap_m) fork_to_aux(h, h->ev_mfork);
   OnStream os(h, overlap_m ? h->aux : h->stream);
   // (on the aux stream: U_{i-1} is overwritten only by the next U side, after the join)
@@ -1554,7 +1613,7 @@ void flush_metrics(esnmf_t* h) {
 #undef ESNMF_ET
   CKL("metrics");
   const double* t_red = nullptr;
-  if (h->world > 1) {
+  if (h->sharded) {
     ++h->nlaunch;
     k_rank_scalars<<<1, 256, 0, h->stream>>>(p_tr, (int64_t)gtr, su.peak, h->side[ESNMF_SIDE_V].peak, h->scal + 3);
     if (h->comm.allreduce_sum_f64(h->comm.ctx, h->scal + 3, 3, h->stream) != 0)
@@ -1608,7 +1667,7 @@ void graph_reset(esnmf_t* h) {
 // the same in every later iteration.  Single GPU, profiling off; in sequential
 // ALS within a block (a block change runs eagerly and drops the graphs).
 bool graph_ok(esnmf_t* h) {
-  return !getenv("ESNMF_NO_GRAPH") && h->world == 1 && !h->prof_on && h->steady >= 2 && h->metrics_pending &&
+  return !getenv("ESNMF_NO_GRAPH") && (!h->sharded || builtin_nccl(h->comm)) && !h->prof_on && h->steady >= 2 && h->metrics_pending &&
          !h->u_prefork && !h->aux_pending && !(h->ktot && h->seq_i >= h->seq_iters);
 }
 
@@ -1740,7 +1799,7 @@ void side_alloc(esnmf_t* h, Side& sd) {
   sd.peak = h->alloc<int64_t>(1);
   CK(cudaMemsetAsync(sd.peak, 0, sizeof(int64_t), h->stream));
   sd.eps = h->alloc<double>(1);
-  if (h->world > 1) {
+  if (h->sharded) {
     const int64_t rows_max = (&sd == &h->side[ESNMF_SIDE_V]) ? h->v_rows_max : h->u_rows_max;
     sd.cap_s = std::max<int64_t>(1, ts < 0 ? rows_max : std::min(ts, rows_max));
     sd.lcolptr = h->alloc<int64_t>(k + 1);
@@ -2124,6 +2183,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->world = o.world;
     h->rank = o.rank;
     if (o.comm) h->comm = *o.comm;
+    h->sharded = h->world > 1 || (o.comm && getenv("ESNMF_FORCE_SHARDED"));
     const bool on_dev = o.inputs_on_device != 0;
     h->flags = h->alloc<int>(8);  // [0] singular [1] validation [2] U0 [3] U-side fp64 [4] V-side Z-gather fallback
     CK(cudaMemsetAsync(h->flags, 0, sizeof(int) * 8, h->stream));
@@ -2174,7 +2234,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       ++h->nlaunch; k_frob2<<<gb, 256, 0, h->stream>>>(su.T.ent, su.T.nnz, h->red);
       ++h->nlaunch; k_reduce_to<<<1, 256, 0, h->stream>>>(h->red, gb, h->normA2_dev);
       CKL("frob2");
-      if (h->world > 1 && h->comm.allreduce_sum_f64(h->comm.ctx, h->normA2_dev, 1, h->stream) != 0)
+      if (h->sharded && h->comm.allreduce_sum_f64(h->comm.ctx, h->normA2_dev, 1, h->stream) != 0)
         fail(ESNMF_ECOMM, "allreduce(||A||^2) failed");
     }
     ct.mark(h.get(), "upload A + norm");
@@ -2185,7 +2245,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     bool at_normalized = false;
     if (o.at_row_ptr && o.at_col_idx && o.at_val) {
       sv.T = upload_csr(h.get(), m, n, o.at_row_ptr, o.at_col_idx, o.at_val, on_dev, m0, m1, nullptr);
-    } else if (h->world == 1) {
+    } else if (!h->sharded) {
       sv.T = build_at(h.get(), su.T, m, 0, m);  // from the (normalised) A
       at_normalized = true;
     } else {  // the transpose needs every term row: build it from the full A, keep our documents
@@ -2198,7 +2258,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
           sv.T.ent, sv.T.nnz, rowlen);
       CKL("norm_cols");
     }
-    if (h->world == 1 && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
+    if (!h->sharded && sv.T.nnz != h->nnz) fail(ESNMF_EINVAL, "esnmf_create: nnz(A^T) != nnz(A)");
     ct.mark(h.get(), "A^T");
     build_items(h.get(), su, aptr);
     side_alloc(h.get(), sv);
@@ -2247,7 +2307,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->rsum_max = h->alloc<double>(1);
     ++h->nlaunch;
     k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);
-    if (h->world == 1) {
+    if (!h->sharded) {
       h->W32 = h->alloc<float>((int64_t)kb * h->kpad);
       if (h->kpad <= 128 && !getenv("ESNMF_UTC_OFF")) {  // tensor-core (Y W), k_uside_tc.cuh
         h->utc_kn = (kb + 15) / 16 * 16;
@@ -2469,7 +2529,7 @@ esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce
     g_last_error = "esnmf_truncate: bad argument";
     return ESNMF_EINVAL;
   }
-  if (h->world > 1) { g_last_error = "esnmf_truncate: single GPU only"; return ESNMF_EINVAL; }
+  if (h->sharded) { g_last_error = "esnmf_truncate: single GPU only"; return ESNMF_EINVAL; }
   return guarded([&] {
     set_device(h);
     graph_reset(h);
@@ -2537,6 +2597,56 @@ esnmf_status esnmf_get_gram(esnmf_t* h, int32_t side, double* G, double* eps) {
       *eps = h->rho * (tr / h->k + 1.0);
     }
   });
+}
+
+esnmf_status esnmf_nccl_unique_id(void* id) {
+  if (!id) { g_last_error = "esnmf_nccl_unique_id: NULL"; return ESNMF_EINVAL; }
+  const NcclApi& a = nccl_api();
+  if (!a.error.empty()) { g_last_error = a.error; return ESNMF_ECOMM; }
+  ncclUniqueId u;
+  const ncclResult_t r = a.getUniqueId(&u);
+  if (r != ncclSuccess) { g_last_error = std::string("ncclGetUniqueId: ") + a.getErrorString(r); return ESNMF_ECOMM; }
+  static_assert(sizeof(ncclUniqueId) == ESNMF_NCCL_ID_BYTES, "NCCL unique id size");
+  std::memcpy(id, &u, sizeof(u));
+  return ESNMF_OK;
+}
+
+esnmf_status esnmf_nccl_comm_create(int32_t world, int32_t rank, const void* id, int32_t device, esnmf_comm** out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world) {
+    g_last_error = "esnmf_nccl_comm_create: bad argument";
+    return ESNMF_EINVAL;
+  }
+  *out = nullptr;
+  const NcclApi& a = nccl_api();
+  if (!a.error.empty()) { g_last_error = a.error; return ESNMF_ECOMM; }
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) { g_last_error = "cudaSetDevice failed"; return ESNMF_ECUDA; }
+  auto* ctx = new NcclCtx();
+  ctx->world = world;
+  ctx->rank = rank;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = a.commInitRank(&ctx->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    g_last_error = std::string("ncclCommInitRank: ") + a.getErrorString(r);
+    delete ctx;
+    return ESNMF_ECOMM;
+  }
+  auto* c = new esnmf_comm();
+  c->ctx = ctx;
+  c->allgather = nccl_allgather_cb;
+  c->allreduce_sum_f64 = nccl_allreduce_cb;
+  *out = c;
+  return ESNMF_OK;
+}
+
+void esnmf_nccl_comm_destroy(esnmf_comm* c) {
+  if (!c) return;
+  if (builtin_nccl(*c)) {
+    auto* ctx = static_cast<NcclCtx*>(c->ctx);
+    if (ctx->comm) nccl_api().commDestroy(ctx->comm);
+    delete ctx;
+  }
+  delete c;
 }
 
 esnmf_status esnmf_cost_model(esnmf_t* h, esnmf_cost* out) {

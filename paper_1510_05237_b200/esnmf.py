@@ -99,6 +99,9 @@ SIGNATURES = {
     "esnmf_get_info": (ctypes.c_int, [c_p, ctypes.POINTER(esnmf_info)]),
     "esnmf_profile": (ctypes.c_int, [c_p, c_i32]),
     "esnmf_cost_model": (ctypes.c_int, [c_p, ctypes.POINTER(esnmf_cost)]),
+    "esnmf_nccl_unique_id": (ctypes.c_int, [c_p]),
+    "esnmf_nccl_comm_create": (ctypes.c_int, [c_i32, c_i32, c_p, c_i32, ctypes.POINTER(ctypes.POINTER(esnmf_comm))]),
+    "esnmf_nccl_comm_destroy": (None, [ctypes.POINTER(esnmf_comm)]),
     "esnmf_phase_times": (ctypes.c_int, [c_p, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(esnmf_phase)]),
     "esnmf_destroy": (None, [c_p]),
     "esnmf_strerror": (ctypes.c_char_p, [ctypes.c_int]),
@@ -269,6 +272,36 @@ def esnmf_cost_model(h) -> dict:
     return c.as_dict()
 
 
+ESNMF_NCCL_ID_BYTES = 128
+
+
+def esnmf_nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 draws it; every rank needs the same bytes)."""
+    buf = ctypes.create_string_buffer(ESNMF_NCCL_ID_BYTES)
+    _check(lib().esnmf_nccl_unique_id(buf), "esnmf_nccl_unique_id")
+    return buf.raw
+
+
+class NcclComm:
+    """The library's own NCCL communicator (esnmf_nccl_comm_create): pass ``.struct``
+    as ESNMF(comm=...).  Collective: every rank constructs it with the same id."""
+
+    def __init__(self, world: int, rank: int, uid: bytes, device: int):
+        if len(uid) != ESNMF_NCCL_ID_BYTES:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.world, self.rank = world, rank
+        self._ptr = ctypes.POINTER(esnmf_comm)()
+        buf = ctypes.create_string_buffer(uid, ESNMF_NCCL_ID_BYTES)
+        _check(lib().esnmf_nccl_comm_create(int(world), int(rank), buf, int(device), ctypes.byref(self._ptr)),
+               "esnmf_nccl_comm_create")
+        self.struct = self._ptr.contents
+
+    def close(self):
+        if self._ptr:
+            lib().esnmf_nccl_comm_destroy(self._ptr)
+            self._ptr = ctypes.POINTER(esnmf_comm)()
+
+
 def esnmf_profile(h, enable: bool):
     _check(lib().esnmf_profile(h, 1 if enable else 0), "esnmf_profile")
 
@@ -330,9 +363,9 @@ class ESNMF:
         o.ridge_scale = ridge_scale
         o.device = device
         self._keep = []
-        if world > 1:
-            if comm is None:
-                raise ValueError("world > 1 needs a comm (paper_1510_05237_b200.comm)")
+        if world > 1 and comm is None:
+            raise ValueError("world > 1 needs a comm (paper_1510_05237_b200.comm)")
+        if comm is not None:
             o.world, o.rank = world, rank
             self._keep.append(comm)
             o.comm = ctypes.pointer(comm)

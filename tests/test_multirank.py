@@ -321,3 +321,98 @@ def test_loopback_box_shaped_merge_matches_oracle():
     ref = oracle.half_step(g["a_ptr"], g["a_col"], g["a_val"], V, 5000)
     check_products(LS[ESNMF_SIDE_U], ref["LS"])
     check_selection(coo_dense((cfg.n, 200), *st["U_after"]), ref["F"], ref["LS"], 5000)
+
+
+# ------------------------------------------------------- built-in NCCL
+
+def _nccl_id_worker(rank, world, port, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = pk.comm.broadcast_nccl_id()
+    result[rank] = uid
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_broadcast_gloo():
+    """Host logic of the library's NCCL communicator (no GPU needed): rank 0 draws
+    the 128-byte NCCL unique id through the C ABI (esnmf_nccl_unique_id) and the
+    process group hands every rank the same bytes."""
+    world = 2
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_nccl_id_worker, args=(world, 29553, result), nprocs=world, join=True)
+    ids = [result[r] for r in range(world)]
+    assert len(ids[0]) == 128 and ids[0] == ids[1]
+    assert any(ids[0])  # not all zero
+    assert pk.esnmf.esnmf_nccl_unique_id() != ids[0]  # a fresh id each time
+
+
+def _forced_sharded(cfg, g, iters, **kw):
+    """One rank through the multi-rank code path (local top-t, allgather + merge,
+    the term-row U side, T allreduced) with the library's OWN NCCL communicator of
+    size 1 -- the plumbing of an 8-GPU run exercised on one device."""
+    os.environ["ESNMF_FORCE_SHARDED"] = "1"
+    try:
+        uid = pk.esnmf.esnmf_nccl_unique_id()
+        comm = pk.esnmf.NcclComm(1, 0, uid, 0)
+        s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed, world=1, rank=0, comm=comm.struct, **kw)
+    finally:
+        del os.environ["ESNMF_FORCE_SHARDED"]
+    s.iterate(iters)
+    return s, comm
+
+
+@pytest.mark.gpu
+def test_builtin_nccl_sharded_path_matches_oracle():
+    """The sharded path on the library's NCCL communicator, CUDA graphs on (the
+    collectives are captured with the iteration): the Tiny trajectory against the
+    oracle's golden run (E, nnz, R_1), the factors against the single-GPU path."""
+    import json
+
+    from parity import TRAJ_TOL, r_close
+
+    cfg = TINY
+    g = synth.generate(cfg)
+    s, comm = _forced_sharded(cfg, g, cfg.iters)
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "traj_tiny.json")))["records"]
+    recs = s.records()
+    assert len(recs) == len(gold)
+    for a, b in zip(recs, gold):
+        assert abs(a["E"] - b["E"]) <= TRAJ_TOL * b["E"], (a["it"], a["E"], b["E"])
+        assert (a["nnz_u"], a["nnz_v"]) == (b["nnz_u"], b["nnz_v"])
+    assert r_close(recs[0]["R"], gold[0]["R"])
+    one = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, g, seed=cfg.seed)
+    one.iterate(cfg.iters)
+    for a, b in zip(recs, one.records()):
+        assert abs(a["E"] - b["E"]) <= 1e-6 * b["E"] and (a["nnz_u"], a["nnz_v"]) == (b["nnz_u"], b["nnz_v"])
+    for x, y in zip(s.get_U()[:2] + s.get_V()[:2], one.get_U()[:2] + one.get_V()[:2]):
+        assert np.array_equal(x, y)
+    s.close()
+    one.close()
+    comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_builtin_nccl_sharded_large_half_steps():
+    """Large through the sharded path on the library's NCCL communicator: sampled LS
+    rows of both sides against the oracle row by row, the selection property."""
+    cfg = synth.CONFIGS["large"]
+    g = synth.generate(cfg)
+    s, comm = _forced_sharded(cfg, g, 3)
+    rng = np.random.default_rng(1)
+    for side in (ESNMF_SIDE_V, ESNMF_SIDE_U):
+        F = coo_dense((cfg.n, cfg.k), *s.get_U()) if side == ESNMF_SIDE_V else coo_dense((cfg.m, cfg.k), *s.get_V())
+        ptr, idx, val, rows = ((g["at_ptr"], g["at_col"], g["at_val"], cfg.m) if side == ESNMF_SIDE_V
+                               else (g["a_ptr"], g["a_col"], g["a_val"], cfg.n))
+        L, _ = oracle.cholesky(oracle.gram(F))
+        s.half_step(side)
+        _, ls = s.get_ls(side)
+        sel = np.unique(np.concatenate([np.arange(20), rng.choice(rows, 1500, replace=False)]))
+        ref = oracle.solve_rows(L, oracle.spmm_rows(sel, ptr, idx, val, F))
+        scale = np.abs(ls).max(axis=0).astype(np.float64)
+        assert (np.abs(ls[sel].astype(np.float64) - ref) / scale).max() <= 1e-5
+        out = coo_dense((cfg.m, cfg.k), *s.get_V()) if side == ESNMF_SIDE_V else coo_dense((cfg.n, cfg.k), *s.get_U())
+        check_topt_property(ls, out, cfg.t)
+    s.close()
+    comm.close()
