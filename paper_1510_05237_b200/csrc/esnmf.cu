@@ -213,6 +213,9 @@ struct esnmf {
   // the U side's Gram + solve run beside the active-document scatter, and the
   // error/record kernels of iteration i beside the V side of iteration i+1
   cudaStream_t aux = nullptr;
+  // the previous iteration's record kernels (R, E; a7, a8): lowest priority, so
+  // the solves queued on aux are scheduled first when the V side's tail starts
+  cudaStream_t maux = nullptr;
   cudaEvent_t ev_ufork = nullptr, ev_ujoin = nullptr, ev_mfork = nullptr, ev_mjoin = nullptr;
   bool aux_pending = false;
   bool u_prefork = false;        // the U side's Gram + solve already enqueued on aux (after V's row view)
@@ -368,6 +371,7 @@ struct esnmf {
     for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin})
       if (e) cudaEventDestroy(e);
     if (aux) cudaStreamDestroy(aux);
+    if (maux) cudaStreamSynchronize(maux), cudaStreamDestroy(maux);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -384,20 +388,22 @@ struct OnStream {
   ~OnStream() { h->stream = saved; }
 };
 
-// main -> aux dependency (aux waits for everything enqueued on main so far)
-void fork_to_aux(esnmf_t* h, cudaEvent_t ev) {
+// main -> side-stream dependency (the side stream waits for everything enqueued on main so far)
+void fork_to(esnmf_t* h, cudaStream_t side, cudaEvent_t ev) {
   ck(cudaEventRecord(ev, h->stream), "cudaEventRecord(fork)");
-  ck(cudaStreamWaitEvent(h->aux, ev, 0), "cudaStreamWaitEvent(fork)");
+  ck(cudaStreamWaitEvent(side, ev, 0), "cudaStreamWaitEvent(fork)");
 }
-// aux -> main dependency
-void join_from_aux(esnmf_t* h, cudaEvent_t ev) {
-  ck(cudaEventRecord(ev, h->aux), "cudaEventRecord(join)");
+// side stream -> main dependency
+void join_from(esnmf_t* h, cudaStream_t side, cudaEvent_t ev) {
+  ck(cudaEventRecord(ev, side), "cudaEventRecord(join)");
   ck(cudaStreamWaitEvent(h->stream, ev, 0), "cudaStreamWaitEvent(join)");
 }
+void fork_to_aux(esnmf_t* h, cudaEvent_t ev) { fork_to(h, h->aux, ev); }
+void join_from_aux(esnmf_t* h, cudaEvent_t ev) { join_from(h, h->aux, ev); }
 // the previous iteration's error/record kernels must finish before V is replaced
 void join_metrics(esnmf_t* h) {
   if (!h->aux_pending) return;
-  join_from_aux(h, h->ev_mjoin);
+  join_from(h, h->maux, h->ev_mjoin);
   h->aux_pending = false;
 }
 
@@ -1347,7 +1353,8 @@ void ytail_launch(esnmf_t* h) {
   const size_t smem = ytail_smem(ys);
   CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  const int per_sm = std::max(1, std::min(3, (int)((228 * 1024) / (smem + 1024))));
+  int per_sm = std::max(1, std::min(3, (int)((228 * 1024) / (smem + 1024))));
+  if (const char* e = getenv("ESNMF_YTAIL_PERSM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, (int64_t)h->num_sms * per_sm);
   CK(cudaMemsetAsync(h->vt_next, 0, sizeof(unsigned long long), h->stream));
   ++h->nlaunch;
@@ -1451,13 +1458,10 @@ Factor& half_step(esnmf_t* h, int s) {
         sc.orflag = h->flags + 5;
         sweep(h, sd.G, sd.eps, sc);
       }
-      form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
     }
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
-    if (!vser) {
-      join_from_aux(h, h->ev_vjoin);
-      h->aux_pending = false;  // the join covers the previous record's kernels too
-    }
+    if (!vser) join_from_aux(h, h->ev_vjoin);
+    form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
     {
       Phase ph(h, kVSpmm);  // fallback only (the kernels return at once otherwise)
       form_z(h, in, h->flags + 4);
@@ -1592,8 +1596,8 @@ void flush_metrics(esnmf_t* h) {
   // the trace and the record run on the aux stream, beside the next V side
   // (joined before that V side replaces V, join_metrics).
   const bool overlap_m = !h->sharded;
-  if (overlap_m) fork_to_aux(h, h->ev_mfork);
-  OnStream os(h, overlap_m ? h->aux : h->stream);
+  if (overlap_m) fork_to(h, h->maux, h->ev_mfork);
+  OnStream os(h, overlap_m ? h->maux : h->stream);
   // (on the aux stream: U_{i-1} is overwritten only by the next U side, after the join)
   ++h->nlaunch; k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
   ++h->nlaunch; k_resid_old<<<dim3(gxo, k), 256, 0, h->stream>>>(Uo.colptr, Uo.row, Uo.val, Un.rowmap, Un.dense, h->kpad, p_old);
@@ -2153,6 +2157,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       int least = 0, greatest = 0;
       CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
       CK(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, greatest));
+      CK(cudaStreamCreateWithPriority(&h->maux, cudaStreamNonBlocking, least));
     }
     for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin, &h->ev_vfork, &h->ev_vjoin})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -2505,6 +2510,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
     set_device(h);
     graph_reset(h);
     CK(cudaStreamSynchronize(h->aux));
+    CK(cudaStreamSynchronize(h->maux));
     if (side == ESNMF_SIDE_V) vrows_clear(h);
     factor_clear(h, f);
     CK(cudaMemcpyAsync(f.colptr, cp.data(), sizeof(int64_t) * (h->k + 1), cudaMemcpyHostToDevice, h->stream));
@@ -2520,6 +2526,7 @@ esnmf_status esnmf_set_factor(esnmf_t* h, int32_t side, int64_t nnz, const int32
     if (side == ESNMF_SIDE_U) h->gramU_valid = false;
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaStreamSynchronize(h->aux));
+    CK(cudaStreamSynchronize(h->maux));
   });
 }
 
@@ -2534,6 +2541,7 @@ esnmf_status esnmf_truncate(esnmf_t* h, int32_t side, int64_t t, int32_t enforce
     set_device(h);
     graph_reset(h);
     CK(cudaStreamSynchronize(h->aux));
+    CK(cudaStreamSynchronize(h->maux));
     Factor& f = side == ESNMF_SIDE_U ? h->U[h->ucur] : h->V;
     if (!f.has) fail(ESNMF_ESTATE, "esnmf_truncate: factor not set");
     Side& sd = h->side[side];  // its LS buffer is the scratch

@@ -52,11 +52,15 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (x[u] > 0.f) atomicAdd(&h[sel_digit(x[u])], 1u);
-    if (pred) {
+    // predicted candidates (value bits >= pb: a few per column in a million) --
+    // one vote per four entries, the per-entry votes only when one lane has a hit
+    // (positive floats order like their bit patterns; pb = 0xFFFFFFFF: no prediction)
+    const float xm = fmaxf(fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3])), 0.f);
+    if (pred && __any_sync(kFull, xm > 0.f && f2u(xm) >= pb)) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const bool cd = x[u] > 0.f && f2u(x[u]) >= pb;
-        const unsigned m = __ballot_sync(kFull, cd);  // (one vote; rare hits)
+        const unsigned m = __ballot_sync(kFull, cd);
         if (m) {
           int b0 = 0;
           if (lane == 0) b0 = atomicAdd(&pfill[c], __popc(m));
