@@ -55,7 +55,10 @@ def parse():
 BINDING = {
     "V.head": "tcgen05: dense 128 x 64 fp16 hi/lo tiles, 3 MMA passes, over a 7.6 %-dense head block "
               "(see kernels[\"V.head\"].tensor_issued)",
-    "V.spmm": "shared-memory fixed-point atomics and L1 (k_ytail: ncu L1/TEX ~75 % of peak)",
+    "V.spmm": "the L1 data pipe: shared-memory fixed-point atomics and per-product U-pair loads "
+              "(k_ytail: ncu L1/TEX ~75 % of peak)",
+    "V.gather": "L1/L2 gather of k-wide Z rows (k_spmm_tail; used when the cost model or the conditioning "
+                "rejects the paper order)",
     "U.spmm": "64-bit fixed-point atomics of the scatter, then (Y W) on tcgen05",
 }
 
@@ -172,7 +175,7 @@ def algorithmic_bytes(phase: str, cfg, split, cost, world: int) -> tuple[float |
     kt = cfg.k * (cfg.t if cfg.t is not None else cfg.m)
     if phase == "V.head":   # the head block of A^T (each stored head entry once)
         return 8.0 * head_nnz / world, "8 B x stored A^T entries of the head terms"
-    if phase == "V.spmm":   # the tail of A^T, its row pointers, U's pairs
+    if phase in ("V.spmm", "V.gather"):   # the tail of A^T, its row pointers, U's pairs (or Z rows)
         return (8.0 * (cfg.nnz - head_nnz) + 8.0 * (cfg.m + 1)) / world + 8.0 * kt, \
             "8 B x stored A^T entries of the tail terms + 8 B x row pointers + 8 B x U entries"
     if phase == "U.spmm":   # paper order: the A^T rows of V's documents, once per entry of V
@@ -408,7 +411,7 @@ def run_ours(args):
     dom = max(phases.items(), key=lambda kv: kv[1][1])[0]
     roof = roofline(dom)
     kernels = {}
-    for nm in ("V.head", "V.spmm", "U.spmm", "V.select", "U.select"):
+    for nm in ("V.head", "V.spmm", "V.gather", "U.spmm", "V.select", "U.select"):
         if nm in phases and phases[nm][0]:
             kernels[nm] = roofline(nm)
     if "V.head" in kernels and kernels["V.head"]:

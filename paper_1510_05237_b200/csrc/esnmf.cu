@@ -409,10 +409,10 @@ void join_metrics(esnmf_t* h) {
 
 // ---------------------------------------------------------------- profiling
 enum PhaseId { kVGram, kVSolve, kVFormZ, kVSpmm, kVSelect, kVRows, kUGram, kUSolve, kUFormZ, kUSpmm, kUSelect, kURows,
-               kMetrics, kVHead, kNumPhases };
+               kMetrics, kVHead, kVGather, kNumPhases };
 const char* const kPhaseNames[kNumPhases] = {"V.gram",   "V.solve",  "V.form_z", "V.spmm",   "V.select",
                                              "V.rowview", "U.gram",  "U.solve",  "U.form_z", "U.spmm",
-                                             "U.select", "U.rowview", "iter.metrics", "V.head"};
+                                             "U.select", "U.rowview", "iter.metrics", "V.head", "V.gather"};
 
 cudaEvent_t pool_event(esnmf_t* h) {
   if (!h->ev_pool.empty()) {
@@ -667,6 +667,10 @@ void form_z(esnmf_t* h, const Factor& f, const int* gate = nullptr) {
     k_zc_fill<<<grid_for(f.cap_rows * kpz, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
         h->zlist, h->zcount, h->Z, h->zs, kpz, h->zc);
   }
+  if (h->ptail) {  // the gather reads only tail entries; U's row bitmap (urows_build) marks its active rows
+    CKL("form_z");
+    return;
+  }
   CK(cudaMemsetAsync(h->tbits, 0, sizeof(uint32_t) * ceil_div(h->n, 32), h->stream));
   ++h->nlaunch;
   k_term_bits<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->tbits, gate);
@@ -710,7 +714,8 @@ void tail_launch(esnmf_t* h, const int* gate) {
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(groups, kTailThreads / 32), (int64_t)h->num_sms * kTailMinBlocks);
   ++h->nlaunch;
   kern<<<grid, kTailThreads, smem, h->stream>>>(sd.T.ptr, h->head_h > 0 ? h->nh : nullptr, sd.T.ent, sd.rows,
-                                                h->tbits, smem_bits ? (int)nwords : 0, Z4, h->zs / 4, h->kpad / 4,
+                                                h->ptail ? h->ubits : h->tbits, smem_bits ? (int)nwords : 0, Z4,
+                                                h->zs / 4, h->kpad / 4,
                                                 h->k, trow ? sd.Xt : sd.X, trow ? (int64_t)h->kpad : sd.ldx, gate);
   CKL("spmm_tail");
 }
@@ -1463,7 +1468,7 @@ Factor& half_step(esnmf_t* h, int s) {
     if (!vser) join_from_aux(h, h->ev_vjoin);
     form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
     {
-      Phase ph(h, kVSpmm);  // fallback only (the kernels return at once otherwise)
+      Phase ph(h, kVGather);  // the Z-row gather: fallback only (the kernels return at once otherwise)
       form_z(h, in, h->flags + 4);
       spmm(h, s, in.rowmap, h->flags + 4);
     }

@@ -230,7 +230,6 @@ __global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restri
   extern __shared__ uint32_t Ysm[];
   __shared__ int64_t s_tile;
   const int T = blockDim.x;
-  const int ng = kn / 8;  // 8-column groups per row
   for (;;) {
     if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(next, 1ull);
     for (int i = threadIdx.x; i < kVtM * ys; i += T) Ysm[i] = 0u;
@@ -268,24 +267,22 @@ __global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restri
       }
     }
     __syncthreads();
+    // convert: a thread takes two adjacent columns of one row (lanes on adjacent
+    // pairs of a row: 2-way bank conflicts on the reads), writes 4 + 4 bytes
     uint8_t* tbase = ytile + (size_t)tile * kVtM * kn * 4;
-    for (int i = threadIdx.x; i < kVtM * ng; i += T) {
-      const int r = i / ng, g = i - r * ng;
-      const int c0 = 8 * g, q = c0 >> 6, w = min(64, kn - 64 * q);
-      uint32_t hw[4], lw[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const float y0 = (float)Ysm[r * ys + c0 + 2 * v] * 0x1p-15f;
-        const float y1 = (float)Ysm[r * ys + c0 + 2 * v + 1] * 0x1p-15f;
-        const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
-        const __half l0 = __float2half_rn(y0 - __half2float(h0)), l1 = __float2half_rn(y1 - __half2float(h1));
-        hw[v] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-        lw[v] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-      }
+    const int np = kn / 2;
+    for (int i = threadIdx.x; i < kVtM * np; i += T) {
+      const int r = i / np, c = 2 * (i - r * np);
+      const int q = c >> 6, w = min(64, kn - 64 * q);
+      const float y0 = (float)Ysm[r * ys + c] * 0x1p-15f;
+      const float y1 = (float)Ysm[r * ys + c + 1] * 0x1p-15f;
+      const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
+      const __half l0 = __float2half_rn(y0 - __half2float(h0)), l1 = __float2half_rn(y1 - __half2float(h1));
       uint8_t* cb = tbase + (size_t)64 * q * kVtM * 4;
-      const uint32_t off = tc::kmajor_off16(r, c0 - 64 * q, w);
-      *reinterpret_cast<uint4*>(cb + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(cb + (size_t)kVtM * w * 2 + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      const uint32_t off = tc::kmajor_off16(r, c - 64 * q, w);
+      *reinterpret_cast<uint32_t*>(cb + off) = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      *reinterpret_cast<uint32_t*>(cb + (size_t)kVtM * w * 2 + off) =
+          (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
     }
     __syncthreads();
   }
