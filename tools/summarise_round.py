@@ -58,14 +58,16 @@ for row in rows[2:]:
     lines.append(f"{nm[:44]:44s} read {rd/1e9:8.3f} GB  write {wr/1e9:8.3f} GB  "
                  f"{d['gpu__time_duration.sum']} {u['gpu__time_duration.sum']}  "
                  f"tensor {d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', '')}")
-    key = ("large:V.spmm" if "k_spmm_tail" in nm else "large:V.head" if "k_vhead_otf" in nm else None)
+    key = ("large:V.spmm" if "k_ytail" in nm else "large:V.gather" if "k_spmm_tail" in nm
+           else "large:V.head" if "k_vhead_otf" in nm else "large:U.spmm" if "k_uside_scatter" in nm
+           else "large:V.select" if "k_sel_hist" in nm else None)
     if key and key not in traffic:
         traffic[key] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
                         "source": f"profiles/{tag}_ncu_full_large.txt (ncu --set full, {nm}, Large, steady state)"}
 open(os.path.join(PROF, f"{tag}_ncu_full_large.txt"), "w").write("\n".join(lines) + "\n")
 tp = os.path.join(PROF, "ncu_traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
-old = {k: v for k, v in old.items() if not k.startswith("large:V.")}
+old = {k: v for k, v in old.items() if not k.startswith("large:")}
 old.update(traffic)
 json.dump(old, open(tp, "w"), indent=1)
 print("\n".join(lines[-8:]))
