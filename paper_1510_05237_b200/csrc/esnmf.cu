@@ -1372,19 +1372,22 @@ void ytail_launch(esnmf_t* h) {
 void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val) {
   if (!h->ptail || (h->ktot && h->seq_b > 0) || !h->polish) return;  // (Alg. 3 deflates later blocks' LS)
   Side& sv = h->side[ESNMF_SIDE_V];
-  const int64_t cap = h->V.cap;
+  const int64_t per_col = h->tside[ESNMF_SIDE_V] < 0 ? sv.rows : std::min<int64_t>(h->tside[ESNMF_SIDE_V], sv.rows);
+  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 8), 4096)), h->k);
   ++h->nlaunch;
-  k_polish_v<<<grid_for(cap, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
-      colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent, h->U[h->ucur].rowmap, h->Z64);
+  k_polish_v<<<g, 256, 0, h->stream>>>(colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent,
+                                       h->U[h->ucur].rowmap, h->Z64);
   CKL("polish_v");
 }
 
 // kept U entries recomputed exactly from the fixed-point A V (one GPU; k_polish_u)
 void polish_u(esnmf_t* h, Factor& out) {
   if (h->sharded || !h->Yq || !h->polish || (h->ktot && h->seq_b > 0)) return;
+  const int64_t per_col = h->tside[ESNMF_SIDE_U] < 0 ? h->n : std::min<int64_t>(h->tside[ESNMF_SIDE_U], h->n);
+  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 8), 4096)), h->k);
   ++h->nlaunch;
-  k_polish_u<<<grid_for(out.cap, 8, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(
-      out.colptr, out.row, out.val, h->k, h->kpad, h->Yq, h->rsum_max, h->vmax, h->W);
+  k_polish_u<<<g, 256, 0, h->stream>>>(out.colptr, out.row, out.val, h->k, h->kpad, h->Yq, h->rsum_max, h->vmax,
+                                       h->W);
   CKL("polish_u");
 }
 

@@ -335,21 +335,17 @@ __global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dens
 // with Z = U W in fp64 (Z64, k_form_z64; zero for a term whose row of U is
 // empty).  The selection chose the entries from the tensor-core values; this
 // pass makes the VALUES exact to fp32 rounding (BJ:5 "relative 1e-5 on factor
-// entries").  One warp per kept entry, lanes over the document's entries.
+// entries").  Grid (x, k): one warp per kept entry of column blockIdx.y, lanes
+// over the document's entries.
 __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
                            float* __restrict__ val, int k, int64_t row0, const int64_t* __restrict__ ptr,
                            const int2* __restrict__ ent, const int32_t* __restrict__ rowmap,
                            const double* __restrict__ Z64) {
   const int lane = threadIdx.x & 31;
+  const int c = blockIdx.y;  // grid (x, k): the entries of column c, one warp each
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t total = colptr[k];
-  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
-    int lo = 0, hi = k - 1;  // column of entry e: last c with colptr[c] <= e
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (colptr[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const int c = lo;
+  const int64_t cend = colptr[c + 1];
+  for (int64_t e = colptr[c] + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < cend; e += nw) {
     const int64_t r = (int64_t)row[e] - row0;
     const int64_t s1 = ptr[r + 1];
     double acc = 0;
@@ -376,22 +372,17 @@ __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __
 // The kept entries of U recomputed exactly (one GPU): LS_ic = sum_j Y_ij W_jc
 // with Y = A V from the U side's exact fixed-point accumulator (Yq, k_uside_*:
 // Y_ij = Yq[i][j] * unit, unit = rowsum_max * max(V) * 2^-62) and W in fp64.
-// One warp per kept entry, lanes over j.
+// Grid (x, k): one warp per kept entry of column blockIdx.y, lanes over j.
 __global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
                            float* __restrict__ val, int k, int kpad, const unsigned long long* __restrict__ Yq,
                            const double* __restrict__ bound, const uint32_t* __restrict__ vmax,
                            const double* __restrict__ W) {
   const int lane = threadIdx.x & 31;
+  const int c = blockIdx.y;  // grid (x, k): the entries of column c, one warp each
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t total = colptr[k];
+  const int64_t cend = colptr[c + 1];
   const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
-  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
-    int lo = 0, hi = k - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (colptr[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const int c = lo;
+  for (int64_t e = colptr[c] + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < cend; e += nw) {
     const unsigned long long* yr = Yq + (int64_t)row[e] * kpad;
     const double* wr = W + (int64_t)c * k;  // W symmetric: column c = row c (coalesced)
     double acc = 0;
