@@ -1077,15 +1077,17 @@ void vhead_launch_st(esnmf_t* h) {
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, h->num_sms);
   ++h->nlaunch;
   // selection pass 1 in the epilogue (k_sel_pred_sort) when the V side takes the
-  // predicted-threshold path: per-column top-t, t <= kSelFastT, one GPU.  Opt-in
-  // (ESNMF_FUSED_SELECT=1): the per-element counting costs the epilogue more
-  // (+0.14 ms at Large) than the streaming pass it saves (~0.1 ms)
+  // predicted-threshold path: per-column top-t, t <= kSelFastT, one GPU.  Round 1
+  // measured it slower (+0.14 ms on the head for ~0.1 ms saved); since the head's
+  // epilogue waits on the (Y_tail W) chunks too it fits: head +0.03 ms, select
+  // -0.10 ms at Large (2.19 -> 2.12 ms).  ESNMF_FUSED_SELECT=0 turns it off.
   const int64_t t = h->tside[ESNMF_SIDE_V];
+  const char* fs_env = getenv("ESNMF_FUSED_SELECT");
   sv.fused = sv.pred && !h->whole && !h->sharded && t >= 0 && t <= kSelFastT && t <= sv.above_t &&
              !(h->ktot && h->seq_b > 0) &&  // Alg. 3 deflates X after this kernel
              h->kn <= 128 &&                 // <= 4 column chunks per epilogue warp
              ceil_div(h->head_ntiles, std::min<int64_t>(h->head_ntiles, h->num_sms)) < 65536 &&  // 16-bit counts
-             getenv("ESNMF_FUSED_SELECT");  // opt-in: measured slower
+             !(fs_env && atoi(fs_env) == 0);
   SelFuse fz{};
   if (sv.fused) {
     CK(cudaMemsetAsync(sv.pfill, 0, sizeof(int32_t) * h->k, h->stream));
