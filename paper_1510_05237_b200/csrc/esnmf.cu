@@ -851,9 +851,18 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap, const int* gate = nullptr) {
 }
 
 // ---- V row-CSR for the U side (k_spmm_terms.cuh) ----
+// the single-GPU U side with a head scatters by V's columns (k_uside_scatter_cols):
+// V's row-CSR is only needed by the row-driven scatter and the sharded term kernel.
+// It is built anyway (ESNMF_NO_VROWS=1 skips it): its ~0.04 ms is the gap in which
+// the U side's Gram + solve finish on the aux stream before the scatter needs them
+// (skipped: 2.12 -> 2.17 ms at Large, the U side then waits for the solve)
+bool need_vrows(esnmf_t* h) {
+  return h->sharded || h->head_h == 0 || getenv("ESNMF_SCATTER_ROWS") || !getenv("ESNMF_NO_VROWS");
+}
+
 void vrows_clear(esnmf_t* h) {
   Factor& f = h->V;
-  if (!f.has) return;
+  if (!f.has || !need_vrows(h)) return;
   ++h->nlaunch;
   k_vrows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->vmap, h->vbits);
   CKL("vrows_clear");
@@ -861,6 +870,13 @@ void vrows_clear(esnmf_t* h) {
 
 void vrows_build(esnmf_t* h) {
   Factor& f = h->V;
+  if (!need_vrows(h)) {
+    CK(cudaMemsetAsync(h->vmax, 0, sizeof(uint32_t), h->stream));
+    ++h->nlaunch;
+    k_vmax_only<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 2), 256, 0, h->stream>>>(f.colptr, f.val, h->k, h->vmax);
+    CKL("vmax_only");
+    return;
+  }
   const int64_t nr = f.cap_rows + 1;
   CK(cudaMemsetAsync(h->vrptr, 0, sizeof(int64_t) * nr, h->stream));
   dim3 g(col_grid_x(f.maxcol), h->k);

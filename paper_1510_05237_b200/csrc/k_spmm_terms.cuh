@@ -71,6 +71,17 @@ __global__ void k_vrows_finish(const int32_t* __restrict__ active, const int64_t
   }
 }
 
+// max(V) bits only (the U side's fixed-point scale) when the row-CSR is not needed
+__global__ void k_vmax_only(const int64_t* __restrict__ colptr, const float* __restrict__ val, int k,
+                            uint32_t* __restrict__ vmax) {
+  const int64_t n = colptr[k];
+  uint32_t mx = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, __float_as_uint(val[e]));  // values > 0: bits order like values
+  mx = __reduce_max_sync(kFull, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(vmax, mx);
+}
+
 // clear the previous V's vmap / vbits entries (by its active list)
 __global__ void k_vrows_clear(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
                               uint64_t* __restrict__ vmap, uint32_t* __restrict__ vbits) {
