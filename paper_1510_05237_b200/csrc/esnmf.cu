@@ -557,6 +557,21 @@ void sweep_launch(esnmf_t* h, const double* G, double* eps, SweepCond sc) {
 void sweep(esnmf_t* h, const double* G, double* eps, SweepCond sc = SweepCond()) {
   const int JB = (h->k + 31) / 32;
   const bool packed = sweep_packed(h->k);
+  static const bool scalar = getenv("ESNMF_SWEEP_SCALAR") != nullptr;
+  if (JB >= 2 && h->k <= 256 && !scalar) {  // blocked sweep (k_solve.cuh)
+    bool in_smem = false;
+    const size_t smem = bsweep_smem_bytes(h->k, &in_smem);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_sweep_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = true;
+    }
+    ++h->nlaunch;
+    k_sweep_blocked<<<1, kBsThreads, smem, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags,
+                                                         in_smem ? nullptr : h->sweep_scratch, sc);
+    CKL("sweep_blocked");
+    return;
+  }
   if (JB <= 4) {  // register-resident matrix
     ++h->nlaunch;
     switch (JB) {
@@ -2368,7 +2383,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaMemsetAsync(h->seqc, 0, sizeof(double) * 4, h->stream));
     }
     h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * kb * kb);
-    if (kb > 224) h->sweep_scratch = h->alloc<double>((int64_t)kb * (kb + 1) / 2);
+    if (kb > 128) h->sweep_scratch = h->alloc<double>((int64_t)kb * kb);  // blocked / packed sweep
     ct.mark(h.get(), "factors + buffers");
     init_u0(h.get(), o.U0, on_dev);
     ct.mark(h.get(), "U0");

@@ -226,6 +226,171 @@ __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict
   }
 }
 
+// ---- blocked sweep (k <= 256): the same map A -> -A^{-1}, 32 pivots at a time ----
+// Sweeping the pivot set P of A = [[A_PP, A_PR], [A_RP, A_RR]] at once is the
+// composition of its scalar sweeps:
+//   A_PP <- -A_PP^{-1},  A_PR <- A_PP^{-1} A_PR,  A_RP <- A_PR^T A_PP^{-1},
+//   A_RR <- A_RR - A_RP A_PP^{-1} A_PR.
+// Per block of b <= 32 pivots: four warps sweep the b x b diagonal block D (the
+// scalar sweep above, so its internal pivots are the scalar sweep's and an SPD
+// matrix keeps them positive), giving D^{-1}; the CTA forms C = D^{-1} A_PR and the
+// symmetric rank-b update A_RR -= A_PR^T C on its upper triangle, both as 4 x 4
+// register tiles per thread (fp64 FMA).  ~k^3 / 2 FMAs behind ~4 k / 32 barriers,
+// against k^3 FMAs behind k barriers.  A keeps only its upper triangle (the map
+// preserves symmetry); it lives in shared memory when it fits, else in the global
+// scratch (L2-resident).  fp64 throughout.
+constexpr int kBsThreads = 512;
+
+ESNMF_DEV int bs_ld(int k) { return ((k + 31) / 32) * 32; }  // panel row stride (padded R)
+
+inline size_t bsweep_smem_bytes(int k, bool* a_in_smem) {
+  const size_t ld = (size_t)((k + 31) / 32) * 32;
+  size_t b = sizeof(double) * (32 * 32 + 2 * 32 * ld);
+  const bool fit = b + sizeof(double) * (size_t)k * k <= 220 * 1024;
+  if (a_in_smem) *a_in_smem = fit;
+  return fit ? b + sizeof(double) * (size_t)k * k : b;
+}
+
+__global__ void __launch_bounds__(kBsThreads) k_sweep_blocked(const double* __restrict__ G, int k, double rho,
+                                                              double* __restrict__ W, double* __restrict__ eps_out,
+                                                              int* __restrict__ singular, double* gscratch,
+                                                              SweepCond sc) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double red[32];
+  __shared__ double Drow[2 * 32];
+  const int ld = bs_ld(k);
+  double* Dinv = dsm;           // 32 x 32 (symmetric)
+  double* AP = Dinv + 32 * 32;  // 32 x ld: rows P of A, columns R (compact index r)
+  double* Cp = AP + 32 * ld;    // 32 x ld: D^{-1} A_PR
+  double* A = gscratch ? gscratch : Cp + 32 * ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto up = [k](int i, int j) -> int64_t { return i <= j ? (int64_t)i * k + j : (int64_t)j * k + i; };
+  double tr = 0;
+  for (int i = tid; i < k; i += blockDim.x) tr += G[(int64_t)i * k + i];
+  tr = block_sum(tr, red);
+  const double eps = rho * (tr / k + 1.0);
+  for (int i = warp; i < k; i += nw)
+    for (int j = lane; j < k; j += 32) A[(int64_t)i * k + j] = G[(int64_t)i * k + j] + (i == j ? eps : 0.0);
+  __syncthreads();
+  bool bad = false;
+#pragma unroll 1
+  for (int p0 = 0; p0 < k; p0 += 32) {
+    const int b = min(32, k - p0), nr = k - b;
+    auto ridx = [p0, b](int r) { return r < p0 ? r : r + b; };
+    if (warp < 4) {  // D^{-1}: the scalar sweep of D (padded with the identity) by 4 warps
+      // Thread (warp w, lane j) holds d_ij for rows i = 8w + u in registers.  Per
+      // pivot the owner warp publishes row q (double-buffered, one 128-thread named
+      // barrier per pivot); D stays symmetric, so column q (d_iq) is row q.
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = warp * 8 + u;
+        x[u] = (i < b && lane < b) ? A[up(p0 + i, p0 + lane)] : (i == lane ? 1.0 : 0.0);
+      }
+#pragma unroll 1
+      for (int qb = 0; qb < b; qb += 8) {
+#pragma unroll
+        for (int uq = 0; uq < 8; ++uq) {  // pivot q = qb + uq: its row is register uq of warp qb / 8
+          const int q = qb + uq;
+          if (q < b) {  // block-uniform
+            double* row = Drow + (q & 1) * 32;
+            if (warp == (qb >> 3)) row[lane] = x[uq];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const double rq = row[lane];  // d_qj
+            double d = row[q];
+            if (!(d > 0.0) || !isfinite(d)) {
+              bad = true;
+              d = 1.0;
+            }
+            const double inv = fast_rcp(d);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int i = warp * 8 + u;
+              const double ci = row[i] * inv;  // d_iq / d
+              x[u] = i == q ? (lane == q ? -inv : rq * inv) : (lane == q ? ci : fma(-ci, rq, x[u]));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Dinv[(warp * 8 + u) * 32 + lane] = -x[u];
+    }
+    for (int q = warp; q < 32; q += nw)
+      for (int r = lane; r < ld; r += 32) AP[q * ld + r] = (q < b && r < nr) ? A[up(p0 + q, ridx(r))] : 0.0;
+    __syncthreads();
+    // C = D^{-1} A_PR: thread tile rows q0..q0+3 x columns r0..r0+3 (D^{-1} symmetric:
+    // its column s is row s, read as two 16-byte vectors)
+    for (int t = tid; t < 8 * (ld / 4); t += blockDim.x) {
+      const int q0 = (t & 7) * 4, r0 = (t >> 3) * 4;
+      double acc[4][4] = {};
+#pragma unroll 4
+      for (int s2 = 0; s2 < b; ++s2) {
+        const double2 d01 = *reinterpret_cast<const double2*>(Dinv + s2 * 32 + q0);
+        const double2 d23 = *reinterpret_cast<const double2*>(Dinv + s2 * 32 + q0 + 2);
+        const double2 a01 = *reinterpret_cast<const double2*>(AP + s2 * ld + r0);
+        const double2 a23 = *reinterpret_cast<const double2*>(AP + s2 * ld + r0 + 2);
+        const double dv[4] = {d01.x, d01.y, d23.x, d23.y}, av[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(dv[u], av[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        *reinterpret_cast<double2*>(Cp + (q0 + u) * ld + r0) = make_double2(acc[u][0], acc[u][1]);
+        *reinterpret_cast<double2*>(Cp + (q0 + u) * ld + r0 + 2) = make_double2(acc[u][2], acc[u][3]);
+      }
+    }
+    __syncthreads();
+    // A_RR -= A_PR^T C on the upper triangle: warp tiles of 16 rows x 32 columns
+    const int ti_n = (nr + 15) / 16, tj_n = (nr + 31) / 32;
+    const int ly = lane >> 3, lx = lane & 7;
+    for (int t = warp; t < ti_n * tj_n; t += nw) {
+      const int ti = t / tj_n, tj = t - ti * tj_n;
+      if (ti * 16 > tj * 32 + 31) continue;  // strictly below the diagonal (warp-uniform)
+      const int i0 = ti * 16 + ly * 4, j0 = tj * 32 + lx * 4;
+      double acc[4][4] = {};
+#pragma unroll 4
+      for (int q = 0; q < b; ++q) {
+        const double2 a01 = *reinterpret_cast<const double2*>(AP + q * ld + i0);
+        const double2 a23 = *reinterpret_cast<const double2*>(AP + q * ld + i0 + 2);
+        const double2 c01 = *reinterpret_cast<const double2*>(Cp + q * ld + j0);
+        const double2 c23 = *reinterpret_cast<const double2*>(Cp + q * ld + j0 + 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y}, cv[4] = {c01.x, c01.y, c23.x, c23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], cv[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        if (i >= nr) continue;
+        double* arow = A + (int64_t)ridx(i) * k;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j = j0 + v;
+          if (i <= j && j < nr) arow[ridx(j)] -= acc[u][v];
+        }
+      }
+    }
+    // rows / columns P: C (upper-triangle position) and -D^{-1}; disjoint from A_RR
+    for (int q = warp; q < b; q += nw) {
+      for (int r = lane; r < nr; r += 32) A[up(p0 + q, ridx(r))] = Cp[q * ld + r];
+      if (lane >= q && lane < b) A[(int64_t)(p0 + q) * k + p0 + lane] = -Dinv[q * 32 + lane];
+    }
+    __syncthreads();
+  }
+  if (bad) atomicExch(singular, 1);
+  for (int i = warp; i < k; i += nw)
+    for (int j = lane; j < k; j += 32) W[(int64_t)i * k + j] = -A[up(i, j)];
+  if (tid == 0) *eps_out = eps;
+  if (sc.flag) {
+    __syncthreads();
+    sweep_cond(G, W, eps, k, sc);
+  }
+}
+
 inline size_t sweep_smem_bytes(int k, bool global_scratch) {
   size_t b = sizeof(double) * (size_t)k;
   if (!global_scratch)

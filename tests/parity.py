@@ -8,7 +8,9 @@
   ENTRY_TOL * |ref| + TIE_TOL * max_j |ref[j,c]| (an fp32 LS entry carries an
   absolute error ~1e-7 of its column's scale, reading C15)
 * retained support: identical, except swaps between entries whose oracle
-  values differ by <= TIE_TOL * max_j |ref[j,c]| (near-ties)
+  values differ by <= TIE_TOL * max_j |ref[j,c]| (near-ties); in a column that
+  keeps all its positives the threshold is zero, and an entry within
+  TIE_TOL * max_j |ref[j,c]| of zero may be kept on one side only
 * trajectory: |E_gpu - E_ref| <= TRAJ_TOL * E_ref per iteration (BJ:5).
 * residual R FROM THE SAME STATE (one iteration from the GPU's factor):
   |R_gpu - R_ref| <= TRAJ_TOL * R_ref + 2 * ENTRY_TOL * (1 + R_ref): R is a
@@ -69,6 +71,14 @@ def check_selection(gpu_F: np.ndarray, ref_F: np.ndarray, ref_ls: np.ndarray, t:
         g, r = gpu_F[:, c] > 0, ref_F[:, c] > 0
         if t is not None:
             assert g.sum() <= t
+        keeps_all = t is None or int((ref_ls[:, c] > 0).sum()) <= t
+        if keeps_all:
+            # the threshold is zero: an entry within an fp32 LS entry's error of zero
+            # (TIE_TOL of the column scale, reading C15) may take either sign
+            differ = np.nonzero(g != r)[0]
+            assert np.all(np.abs(ref_ls[differ, c]) <= TIE_TOL * scale), f"column {c}: kept set differs off zero"
+            swaps += len(differ)
+            g = r = g & r
         assert g.sum() == r.sum(), f"column {c}: {g.sum()} kept vs oracle {r.sum()}"
         only_g = np.nonzero(g & ~r)[0]
         only_r = np.nonzero(r & ~g)[0]
@@ -80,7 +90,6 @@ def check_selection(gpu_F: np.ndarray, ref_F: np.ndarray, ref_ls: np.ndarray, t:
             swaps += len(only_g)
         both = g & r
         if both.any():
-            keeps_all = t is None or int((ref_ls[:, c] > 0).sum()) <= t
             slack = (TIE_TOL / ENTRY_TOL) * scale if keeps_all else 0.0
             rel = np.abs(gpu_F[both, c] - ref_F[both, c]) / (ref_F[both, c] + slack)
             worst = max(worst, float(rel.max()))

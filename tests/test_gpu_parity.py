@@ -222,6 +222,18 @@ def test_edge_t_and_k(t, k):
         half_step_parity(s, g, TINY.n, TINY.m, k, t, ESNMF_SIDE_U)
 
 
+@pytest.mark.parametrize("k", [32, 64, 100, 129, 200, 256])
+def test_blocked_sweep_ranks(k):
+    """The k x k solve (k_sweep_blocked: 32 pivots per block, A in shared memory up to
+    k = 128 and in the global scratch above) across its block / storage boundaries:
+    half-steps of both sides against the oracle (whose W is numpy's inverse)."""
+    g = synth.generate(TINY)
+    s = ESNMF(TINY.n, TINY.m, k, None, g, seed=5)
+    for _ in range(2):
+        half_step_parity(s, g, TINY.n, TINY.m, k, None, ESNMF_SIDE_V)
+        half_step_parity(s, g, TINY.n, TINY.m, k, None, ESNMF_SIDE_U)
+
+
 def test_exact_ties_break_to_lower_rows():
     """Duplicated documents give identical LS rows: the kept set must take the lower rows."""
     rng = np.random.default_rng(11)
