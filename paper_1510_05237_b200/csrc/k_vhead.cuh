@@ -54,7 +54,7 @@ static_assert(kHeadK == 32 || kHeadK == 64, "chunk entries encode the slot in 6 
 constexpr int kHeadM = 128;                                  // documents per tile (MMA M)
 constexpr uint32_t kHeadABytes = kHeadM * kHeadK * 2 * 2;    // hi + lo fp16 = 32 KB
 constexpr uint32_t kHeadAHalf = kHeadM * kHeadK * 2;         // 16 KB
-constexpr int kHeadMax = 4096;                               // largest head (terms)
+constexpr int kHeadMax = 31 * ESNMF_HEAD_K;                    // largest head (terms): <= 31 sparse chunks (one run offset per loader lane)
 
 // exponent e such that x * 2^e lies in [2^14, 2^15) (0 for x == 0)
 ESNMF_DEV int head_exp(float x) {
@@ -279,6 +279,22 @@ struct SelFuse {
   int64_t row0;
 };
 
+#ifndef ESNMF_HEAD_EXP
+#define ESNMF_HEAD_EXP 0
+#endif
+// -DESNMF_HEAD_EXP=3 (development): per-role barrier-wait cycles of CTAs 0 and 77,
+// printed at the end of k_vhead_otf (loader: empty, producers: raw_full, MMA:
+// a_full + tempty, epilogue: tfull)
+#if ESNMF_HEAD_EXP == 3
+#define HT_WAIT(bar, ph)                  \
+  {                                       \
+    const long long t0_ = clock64();      \
+    tc::mbar_wait(bar, ph);               \
+    ht_wait += clock64() - t0_;           \
+  }
+#else
+#define HT_WAIT(bar, ph) tc::mbar_wait(bar, ph)
+#endif
 #ifndef ESNMF_HEAD_PROD_WARPS
 #define ESNMF_HEAD_PROD_WARPS 4
 #endif
@@ -289,7 +305,10 @@ constexpr int kHeadRaw = 16 * kHeadK;                  // entries of a chunk's r
 constexpr uint32_t kHeadRawBytes = kHeadRaw * 8 + 16;  // (+1 entry of alignment skew, rounded)
 constexpr int kHeadEpi = 256;                          // epilogue threads (2 warps per TMEM lane quadrant)
 constexpr int kHeadOtfThreads = kHeadProd + 32 + 32 + kHeadEpi;  // producers, MMA, loader, epilogue
-constexpr int kHeadPf = 6;                             // rounds of L2 prefetch ahead of the copies
+#ifndef ESNMF_HEAD_PF
+#define ESNMF_HEAD_PF 6
+#endif
+constexpr int kHeadPf = ESNMF_HEAD_PF;                             // rounds of L2 prefetch ahead of the copies
 
 // stage = [A hi|lo 32 KB][Z chunk hi|lo][raw entries of the chunk's run]
 ESNMF_DEV uint32_t head_stage_bytes(int kn) {
@@ -308,6 +327,74 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 // w_q = min(64, kn - 64 q) -- the same stage, copied like a dense tile, into the
 // same accumulator (the scales of Z, W and Y_tail are chosen per column so both
 // parts carry 2^sc_c: k_vside_prep).  Xt is then null.
+// Epilogue of one 128-row tile (one thread per row: TMEM lane quadrant lg, columns
+// [cbeg, cend) of its warp): X[c][row] = Xt[row][c] + colscale[c] * acc[row][c], and the
+// fused selection pass 1 (positive counts in cnt2, candidate keys to fz.pcand).
+template <bool FUSE>
+__device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, int cbeg, int cend, bool no_mma, int k,
+                                              const float* __restrict__ colscale, int64_t rows, float* __restrict__ X,
+                                              int64_t ldx, const float* __restrict__ Xt, int kpad, const SelFuse& fz,
+                                              const uint32_t* s_pred, uint32_t (&cnt2)[4][8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < (FUSE ? 4 : 1); ++q) {
+    for (int c0 = cbeg + 16 * q; c0 < (FUSE ? min(cend, cbeg + 16 * q + 1) : cend); c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(ta + (uint32_t)c0, v);
+      tc::tmem_wait_ld();
+      if (no_mma) {  // no MMA wrote the accumulator (no head, tail staged in Xt)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      }
+      float x[16];
+      if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          const int c = c0 + 4 * v4;
+          const float4 t4 = (Xt && c < kpad) ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[4 * v4] = t4.x; x[4 * v4 + 1] = t4.y; x[4 * v4 + 2] = t4.z; x[4 * v4 + 3] = t4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = c0 + j;
+          x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
+          if (c < k) X[(int64_t)c * ldx + row] = x[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = 0.f;
+      }
+      if (FUSE) {  // padding columns c >= k hold x = 0: never counted
+        uint32_t cdm = 0;  // columns j with a candidate in this lane
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
+          cdm |= (uint32_t)(x[j] > 0.f && __float_as_uint(x[j]) >= s_pred[c0 + j]) << j;
+        }
+        uint32_t wm = __reduce_or_sync(kFull, cdm);
+        while (wm) {  // usually one column, one lane
+          const int j = __ffs(wm) - 1;
+          wm &= wm - 1;
+          const int c = c0 + j;
+          const bool cd = (cdm >> j) & 1;
+          const unsigned mc = __ballot_sync(kFull, cd);
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&fz.pfill[c], __popc(mc));
+          b0 = __shfl_sync(kFull, b0, 0);
+          const int slot = b0 + __popc(mc & ((1u << lane) - 1u));
+          if (cd && slot < fz.pcap) {
+            float xv = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) xv = jj == j ? x[jj] : xv;
+            fz.pcand[(int64_t)c * fz.pcap + slot] = sel_key(xv, (uint32_t)(fz.row0 + row));
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int STAGES, bool FUSE>
 __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     k_vhead_otf(const uint8_t* __restrict__ atile, int nd, const int64_t* __restrict__ hoff,
@@ -323,6 +410,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   if (!fb && nyc_arg > 0) Xt = nullptr;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t raw_full[STAGES], a_full[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
+  __shared__ int64_t s_run[STAGES][2];  // sparse round: [sb, se) of its run (loader -> producers)
   __shared__ uint32_t tmem_base;
   __shared__ int s_npos[256];       // fused selection: positives per column counted by this CTA
   __shared__ uint32_t s_pred[256];  // ... and the predicted thresholds (0xFFFFFFFF: none)
@@ -354,66 +442,89 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
+  long long ht_wait = 0;
+  const long long ht_t0 = clock64();
 
-  if (warp == kHeadLoadWarp) {
-    if (lane == 0) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
-      int stage = 0;
-      uint32_t phase = 0;
-      // L2 prefetch kHeadPf rounds ahead of the copies: a stage's copy is issued
-      // only when the MMAs of the round STAGES earlier finish, so its latency is
-      // on the critical path; from L2 it is ~1/3 of the HBM latency.
-      int64_t pf_tile = blockIdx.x;
-      int pf_q = 0;
-      const int nall = nchunks + nyc;
-      auto prefetch_next = [&]() {
-        if (pf_tile >= ntiles) return;
-        if (pf_q >= nchunks) {
-          const int yq = pf_q - nchunks;
-          tc::bulk_prefetch_l2(ytile + (size_t)pf_tile * kHeadM * kn * 4 + (size_t)yq * kHeadABytes,
-                               (uint32_t)kHeadM * min(64, kn - 64 * yq) * 4u);
-        } else if (pf_q < nd) {
-          tc::bulk_prefetch_l2(atile + ((size_t)pf_tile * nd + pf_q) * kHeadABytes, kHeadABytes);
-        } else {
-          const int64_t si = pf_tile * (nchunks - nd) + (pf_q - nd);
-          const int64_t sb = hoff[si], se = hoff[si + 1];
-          const int64_t a = sb & ~(int64_t)1;
-          const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);
-          if (b > a) tc::bulk_prefetch_l2(hseg + a, (uint32_t)(b - a) * 8u);
+  if (warp == kHeadLoadWarp) {  // ---- loader: run + Z chunk of each round, STAGES ahead ----
+    // One lane issues the copies.  The run offsets hoff[tile * nsp + j] (j <= nsp) of
+    // a tile are loaded by the whole warp a tile ahead (one per lane) and taken by
+    // shuffle: no dependent global load on the copy path (the producers get a
+    // round's run bounds through s_run[stage]).
+    const int nsp = nchunks - nd;  // sparse chunks per tile (<= 31)
+    const int nall = nchunks + nyc;
+    int stage = 0;
+    uint32_t phase = 0;
+    auto offs_of = [&](int64_t t) -> int64_t {
+      return (t < ntiles && lane <= nsp && nsp > 0) ? hoff[t * nsp + lane] : 0;
+    };
+    int64_t off_cur = offs_of(blockIdx.x);
+    int64_t off_nxt = offs_of(blockIdx.x + gridDim.x);
+    // L2 prefetch kHeadPf rounds ahead of the copies (a stage's copy is issued only
+    // when the MMAs of the round STAGES earlier finish, so its latency is on the
+    // critical path; from L2 it is ~1/3 of the HBM latency).  Rounds ahead of the
+    // current tile belong to the next one (kHeadPf < nchunks + nyc).
+    auto prefetch = [&](int64_t pt, int pq, int64_t offv) {
+      int64_t sb = 0, se = 0;
+      if (pq >= nd && pq < nchunks) {
+        sb = __shfl_sync(kFull, offv, pq - nd);
+        se = __shfl_sync(kFull, offv, pq - nd + 1);
+      }
+      if (lane != 0 || pt >= ntiles) return;
+      if (pq >= nchunks) {
+        const int yq = pq - nchunks;
+        tc::bulk_prefetch_l2(ytile + (size_t)pt * kHeadM * kn * 4 + (size_t)yq * kHeadABytes,
+                             (uint32_t)kHeadM * min(64, kn - 64 * yq) * 4u);
+      } else if (pq < nd) {
+        tc::bulk_prefetch_l2(atile + ((size_t)pt * nd + pq) * kHeadABytes, kHeadABytes);
+      } else {
+        const int64_t a = sb & ~(int64_t)1;
+        const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);
+        if (b > a) tc::bulk_prefetch_l2(hseg + a, (uint32_t)(b - a) * 8u);
+      }
+    };
+    for (int i = 0; i < min(kHeadPf, nall); ++i) prefetch(blockIdx.x, i, off_cur);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int q = 0; q < nall; ++q) {
+        if (kHeadPf > 0) {  // prefetch round (tile, q) + kHeadPf
+          const int pq = q + kHeadPf;
+          if (pq < nall) prefetch(tile, pq, off_cur);
+          else prefetch(tile + gridDim.x, pq - nall, off_nxt);
         }
-        if (++pf_q == nall) { pf_q = 0; pf_tile += gridDim.x; }
-      };
-      for (int i = 0; i < kHeadPf; ++i) prefetch_next();
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int q = 0; q < nall; ++q) {
-          prefetch_next();
-          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+        int64_t sb = 0, se = 0;
+        if (q >= nd && q < nchunks) {
+          sb = __shfl_sync(kFull, off_cur, q - nd);
+          se = __shfl_sync(kFull, off_cur, q - nd + 1);
+        }
+        if (lane == 0) {
+          HT_WAIT(&empty_bar[stage], phase ^ 1);
           uint8_t* st = base + stage * stage_bytes;
+          const int yq = q - nchunks;
           if (q >= nchunks) {  // (Y_tail W) chunk: Y_tail tile chunk + W chunk
-            const int yq = q - nchunks;
             const uint32_t w = (uint32_t)min(64, kn - 64 * yq);
             const uint32_t ab = (uint32_t)kHeadM * w * 4u, bb = (uint32_t)kn * w * 4u;
             tc::mbar_arrive_expect_tx(&raw_full[stage], ab + bb);
             tc::bulk_g2s(st, ytile + (size_t)tile * kHeadM * kn * 4 + (size_t)yq * kHeadABytes, ab, &raw_full[stage]);
             tc::bulk_g2s(st + kHeadABytes, wbuf + (size_t)yq * zbytes, bb, &raw_full[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            continue;
+          } else {
+            if (q < nd) {  // dense chunk: the A tile itself
+              tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + kHeadABytes);
+              tc::bulk_g2s(st, atile + ((size_t)tile * nd + q) * kHeadABytes, kHeadABytes, &raw_full[stage]);
+            } else {         // sparse chunk: its run of entries
+              const int64_t a = sb & ~(int64_t)1;  // 16-byte aligned start
+              const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);  // even, capped
+              const uint32_t rb = (uint32_t)(b - a) * 8u;
+              s_run[stage][0] = sb;
+              s_run[stage][1] = se;
+              tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + rb);
+              if (rb) tc::bulk_g2s(st + raw_off, hseg + a, rb, &raw_full[stage]);
+            }
+            tc::bulk_g2s(st + kHeadABytes, zbuf + (size_t)q * zbytes, zbytes, &raw_full[stage]);
           }
-          if (q < nd) {  // dense chunk: the A tile itself
-            tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + kHeadABytes);
-            tc::bulk_g2s(st, atile + ((size_t)tile * nd + q) * kHeadABytes, kHeadABytes, &raw_full[stage]);
-          } else {         // sparse chunk: its run of entries
-            const int64_t si = tile * (nchunks - nd) + (q - nd);
-            const int64_t sb = hoff[si], se = hoff[si + 1];
-            const int64_t a = sb & ~(int64_t)1;  // 16-byte aligned start
-            const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);  // even, capped
-            const uint32_t rb = (uint32_t)(b - a) * 8u;
-            tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + rb);
-            if (rb) tc::bulk_g2s(st + raw_off, hseg + a, rb, &raw_full[stage]);
-          }
-          tc::bulk_g2s(st + kHeadABytes, zbuf + (size_t)q * zbytes, zbytes, &raw_full[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      off_cur = off_nxt;
+      off_nxt = offs_of(tile + 2 * (int64_t)gridDim.x);
     }
   } else if (warp < kHeadProdWarps) {  // ---- producers: zero + scatter one tile chunk per stage ----
     const int p = threadIdx.x;
@@ -431,14 +542,13 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       for (int q = 0; q < nchunks + nyc; ++q) {
         uint8_t* sa = base + stage * stage_bytes;
-        tc::mbar_wait(&raw_full[stage], phase);  // also: the MMAs of this stage's last round are done
+        HT_WAIT(&raw_full[stage], phase);  // also: the MMAs of this stage's last round are done
         if (q < nd || q >= nchunks) {  // dense or (Y_tail W) chunk: bulk-copied, nothing to build
           tc::mbar_arrive(&a_full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
         }
-        const int64_t si = tile * (nchunks - nd) + (q - nd);
-        const int64_t sb = hoff[si], se = hoff[si + 1];
+        const int64_t sb = s_run[stage][0], se = s_run[stage][1];  // written by the loader before raw_full
         const int64_t a = sb & ~(int64_t)1;
         const int64_t cap = a + (int64_t)kHeadRaw;  // staged: [a, min(se, cap)); the rest from global
         const int2* raw = reinterpret_cast<const int2*>(sa + raw_off);
@@ -463,27 +573,41 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   } else if (warp == kHeadMmaWarp) {
     if (lane == 0) {  // ---- MMA issuer ----
       const uint32_t idesc = tc::make_idesc_f16(kHeadM, kn);
+      // head-chunk descriptors: everything but the 14-bit start address is fixed
+      // (LBO = 128, SBO = (kHeadK / 8) * 128); the stage's addresses are added per round
+      const uint64_t hdesc = tc::make_sdesc(0, 128, (kHeadK / 8) * 128);
+      const uint32_t sbase = tc::smem_u32(base);
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        tc::mbar_wait(&tempty[acc], aphase ^ 1);
+        HT_WAIT(&tempty[acc], aphase ^ 1);
         tc::fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * acc_cols);
         for (int q = 0; q < nchunks + nyc; ++q) {
-          tc::mbar_wait(&a_full[stage], phase);
+          HT_WAIT(&a_full[stage], phase);
           tc::fence_after();
-          // head chunk: K = kHeadK; (Y_tail W) chunk: K = w (its tiles are w wide)
-          const uint32_t w = q < nchunks ? (uint32_t)kHeadK : (uint32_t)min(64, kn - 64 * (q - nchunks));
-          const uint32_t ah = tc::smem_u32(base + stage * stage_bytes);
-          const uint32_t al = ah + (uint32_t)kHeadM * w * 2u, zh = ah + kHeadABytes, zl = zh + (uint32_t)kn * w * 2u;
-          const uint32_t sbo = (w / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
-          for (uint32_t s = 0; s < w / 16; ++s) {
-            const uint32_t o = s * 256;
-            const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
-            const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
-            tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
-            tc::mma_f16(d, dah, dzl, idesc, 1);
-            tc::mma_f16(d, dal, dzh, idesc, 1);
+          const uint32_t ah = sbase + (uint32_t)stage * stage_bytes;
+          if (q < nchunks) {  // head chunk: K = kHeadK, descriptors advance 256 B (16 units) per K-step
+            const uint64_t dah = hdesc | ((ah >> 4) & 0x3FFF), dal = dah + ((kHeadM * kHeadK * 2) >> 4);
+            const uint64_t dzh = dah + (kHeadABytes >> 4), dzl = dzh + (((uint32_t)kn * kHeadK * 2) >> 4);
+#pragma unroll
+            for (uint32_t s = 0; s < kHeadK / 16; ++s) {
+              tc::mma_f16(d, dah + 16 * s, dzh + 16 * s, idesc, (q | s) != 0);
+              tc::mma_f16(d, dah + 16 * s, dzl + 16 * s, idesc, 1);
+              tc::mma_f16(d, dal + 16 * s, dzh + 16 * s, idesc, 1);
+            }
+          } else {  // (Y_tail W) chunk: K = w (its tiles are w wide)
+            const uint32_t w = (uint32_t)min(64, kn - 64 * (q - nchunks));
+            const uint32_t al = ah + (uint32_t)kHeadM * w * 2u, zh = ah + kHeadABytes, zl = zh + (uint32_t)kn * w * 2u;
+            const uint32_t sbo = (w / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
+            for (uint32_t s = 0; s < w / 16; ++s) {
+              const uint32_t o = s * 256;
+              const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
+              const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
+              tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
+              tc::mma_f16(d, dah, dzl, idesc, 1);
+              tc::mma_f16(d, dal, dzh, idesc, 1);
+            }
           }
           tc::mma_commit(&empty_bar[stage]);  // frees the stage when these MMAs finish
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -510,67 +634,10 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      tc::mbar_wait(&tfull[acc], aphase);
+      HT_WAIT(&tfull[acc], aphase);
       tc::fence_after();
-      const int64_t row = tile * kHeadM + lg * 32 + lane;
-      const uint32_t ta = tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16);
-#pragma unroll
-      for (int q = 0; q < (FUSE ? 4 : 1); ++q) {
-      for (int c0 = cbeg + 16 * q; c0 < (FUSE ? min(cend, cbeg + 16 * q + 1) : cend); c0 += 16) {
-        uint32_t v[16];
-        tc::tmem_ld16(ta + (uint32_t)c0, v);
-        tc::tmem_wait_ld();
-        if (nchunks + nyc == 0) {  // no MMA wrote the accumulator (no head, tail staged in Xt)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0u;
-        }
-        float x[16];
-        if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
-#pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4) {
-            const int c = c0 + 4 * v4;
-            const float4 t4 = (Xt && c < kpad) ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-            x[4 * v4] = t4.x; x[4 * v4 + 1] = t4.y; x[4 * v4 + 2] = t4.z; x[4 * v4 + 3] = t4.w;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int c = c0 + j;
-            x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
-            if (c < k) X[(int64_t)c * ldx + row] = x[j];
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) x[j] = 0.f;
-        }
-        if (FUSE) {  // padding columns c >= k hold x = 0: never counted
-          uint32_t cdm = 0;  // columns j with a candidate in this lane
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
-            cdm |= (uint32_t)(x[j] > 0.f && __float_as_uint(x[j]) >= s_pred[c0 + j]) << j;
-          }
-          uint32_t wm = __reduce_or_sync(kFull, cdm);
-          while (wm) {  // usually one column, one lane
-            const int j = __ffs(wm) - 1;
-            wm &= wm - 1;
-            const int c = c0 + j;
-            const bool cd = (cdm >> j) & 1;
-            const unsigned mc = __ballot_sync(kFull, cd);
-            int b0 = 0;
-            if (lane == 0) b0 = atomicAdd(&fz.pfill[c], __popc(mc));
-            b0 = __shfl_sync(kFull, b0, 0);
-            const int slot = b0 + __popc(mc & ((1u << lane) - 1u));
-            if (cd && slot < fz.pcap) {
-              float xv = 0.f;
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj) xv = jj == j ? x[jj] : xv;
-              fz.pcand[(int64_t)c * fz.pcap + slot] = sel_key(xv, (uint32_t)(fz.row0 + row));
-            }
-          }
-        }
-      }
-      }
+      head_epi_tile<FUSE>(tile * kHeadM + lg * 32 + lane, tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16),
+                          cbeg, cend, nchunks + nyc == 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
       tc::fence_before();
       tc::mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -589,6 +656,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       }
     }
   }
+#if ESNMF_HEAD_EXP == 3
+  if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 && (warp == 0 || warp == kHeadMmaWarp || warp == kHeadLoadWarp || warp == kHeadEpiWarp))
+    printf("HT cta %d warp %d wait %lld total %lld\n", blockIdx.x, warp, ht_wait, clock64() - ht_t0);
+#endif
+  (void)ht_wait;
+  (void)ht_t0;
   tc::fence_before();
   __syncthreads();
   if (warp == kHeadMmaWarp) {

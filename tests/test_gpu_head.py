@@ -37,7 +37,7 @@ def v_side_parity(s, g, cfg, k, t):
     return err
 
 
-@pytest.mark.parametrize("head,dense", [(64, 0), (64, 1), (192, 4), (1024, 2), (1024, 0)])
+@pytest.mark.parametrize("head,dense", [(64, 0), (64, 1), (192, 4), (1024, 2), (1024, 0), (1984, 0)])
 def test_tiny_head_sizes_first_and_late(head, dense, monkeypatch):
     """dense = chunks stored as dense tiles (the rest built on chip from entry runs)."""
     monkeypatch.setenv("ESNMF_HEAD_DENSE", str(dense))
