@@ -73,7 +73,8 @@ void ck(cudaError_t e, const char* what) {
 constexpr int64_t kSplitLen = 4096;
 constexpr double kVtKappaMax = 1e4;  // V side: Y_tail W in fp16 hi/lo only below these (k_vcond_flag)
 constexpr double kVtAmpMax = 8.0;   // max stored entries per SpMM work item (A rows)
-constexpr int kMaxGramSeg = 64;
+constexpr int kMaxGramSeg = 64;        // sparse Gram: entry segments per column
+constexpr int kMaxGramSegDense = 296;  // dense Gram: row slabs (2 per SM)
 constexpr int64_t kSelScanMax = 4096;  // flat selection: segment-scan blocks (k * rows < 2^31 needs < 1024)
 
 struct DevCsr {
@@ -547,7 +548,12 @@ void gram(esnmf_t* h, const Factor& f, double* G, int kk = 0, int kp = 0, double
   dim3 g(k, (unsigned)S);
   const int gb = (k + 31) / 32 * 32;  // <= 256
   ++h->nlaunch;
-  if (seglen >= 256) {  // long segments: thread groups split the entries
+  if (f.maxcol * 4 >= f.rows && f.rows >= 256 && !getenv("ESNMF_GRAM_SPARSE")) {
+    // long columns (dense U_0, unlimited t): straight from the dense active rows
+    S = std::min<int64_t>(kMaxGramSegDense, std::max<int64_t>(1, ceil_div(f.rows, 512)));
+    const unsigned nb = (unsigned)ceil_div(kp, 128);
+    k_gram_dense<<<dim3((unsigned)S, nb, nb), 256, 0, h->stream>>>(f.dense, kp, k, f.n_active, partial);
+  } else if (seglen >= 256) {  // long segments: thread groups split the entries
     const int ng = std::max(1, std::min(4, 512 / gb));
     k_gram_partial_groups<<<g, gb * ng, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, f.dense, kp, k, seglen,
                                                         partial, gb);
@@ -2416,7 +2422,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       h->seqc = h->alloc<double>(4);
       CK(cudaMemsetAsync(h->seqc, 0, sizeof(double) * 4, h->stream));
     }
-    h->gram_partial = h->alloc<double>((int64_t)kMaxGramSeg * kb * kb);
+    h->gram_partial = h->alloc<double>((int64_t)std::max(kMaxGramSeg, kMaxGramSegDense) * kb * kb);
     if (kb > 128) h->sweep_scratch = h->alloc<double>((int64_t)kb * kb);  // blocked / packed sweep
     ct.mark(h.get(), "factors + buffers");
     init_u0(h.get(), o.U0, on_dev);

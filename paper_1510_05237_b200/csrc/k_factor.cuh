@@ -264,6 +264,66 @@ __global__ void __launch_bounds__(256) k_gram_partial(const int64_t* __restrict_
   }
 }
 
+// Dense variant (a factor whose columns are long, e.g. the dense U_0 of
+// iteration 1): the same upper-triangle partials straight from the dense active
+// rows, G_ab = sum_r D_ra D_rb (zeros of D contribute nothing; fp32 products are
+// exact in fp64).  Grid (S, nb, nb): slab s of the active rows, output block
+// (bi, bj) of 128 x 128 (bi <= bj); 256 threads, an 8 x 8 fp64 register tile each,
+// rows staged 32 at a time in shared memory.
+constexpr int kGdRows = 32;
+__global__ void __launch_bounds__(256) k_gram_dense(const float* __restrict__ dense, int kpad, int k,
+                                                    const int64_t* __restrict__ n_active, double* __restrict__ partial) {
+  const int bi = blockIdx.y, bj = blockIdx.z;
+  if (bi > bj) return;
+  __shared__ __align__(16) float sa[kGdRows][128], sb[kGdRows][128];
+  const int S = gridDim.x, s = blockIdx.x;
+  const int64_t na = *n_active;
+  const int64_t len = (na + S - 1) / S;
+  const int64_t r0 = (int64_t)s * len, r1 = min(na, r0 + len);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = bi * 128 + ty * 8, j0 = bj * 128 + tx * 8;
+  const bool live = i0 <= j0 + 7 && i0 < k && j0 < k;  // tile touches the upper triangle
+  double acc[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += kGdRows) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGdRows * 128; e += blockDim.x) {
+      const int rr = e >> 7, c = e & 127;
+      const int64_t r = rb + rr;
+      const int ca = bi * 128 + c, cb = bj * 128 + c;
+      sa[rr][c] = (r < r1 && ca < kpad) ? dense[r * kpad + ca] : 0.f;
+      sb[rr][c] = (r < r1 && cb < kpad) ? dense[r * kpad + cb] : 0.f;
+    }
+    __syncthreads();
+    if (live) {
+      const int nr = (int)min((int64_t)kGdRows, r1 - rb);
+      for (int rr = 0; rr < nr; ++rr) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&sa[rr][ty * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&sa[rr][ty * 8 + 4]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&sb[rr][tx * 8]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&sb[rr][tx * 8 + 4]);
+        const double a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const double b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int i = i0 + u, j = j0 + v;
+      if (i <= j && j < k) partial[((int64_t)s * k + i) * k + j] = acc[u][v];
+    }
+}
+
 // G[i][j] = G[j][i] = the segment sum of the upper-triangle partial (i <= j):
 // both halves are the same sum, so G is exactly symmetric
 __global__ void k_gram_reduce(const double* __restrict__ partial, int S, int k, double* __restrict__ G) {
