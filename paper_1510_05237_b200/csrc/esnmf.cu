@@ -70,9 +70,7 @@ void ck(cudaError_t e, const char* what) {
 #define CK(x) ck((x), #x)
 #define CKL(name) ck(cudaGetLastError(), name)
 
-constexpr int64_t kSplitLen = 4096;
-constexpr double kVtKappaMax = 1e4;  // V side: Y_tail W in fp16 hi/lo only below these (k_vcond_flag)
-constexpr double kVtAmpMax = 8.0;   // max stored entries per SpMM work item (A rows)
+constexpr int64_t kSplitLen = 4096;  // max stored entries per SpMM work item (A rows)
 constexpr int kMaxGramSeg = 64;        // sparse Gram: entry segments per column
 constexpr int kMaxGramSegDense = 296;  // dense Gram: row slabs (2 per SM)
 constexpr int64_t kSelScanMax = 4096;  // flat selection: segment-scan blocks (k * rows < 2^31 needs < 1024)
@@ -776,7 +774,6 @@ void spmm_terms_launch(esnmf_t* h) {
 
 // fp32 copy of W and the conditioning flag choosing the fp32 or fp64 (Y W)
 void uside_w_prep(esnmf_t* h) {
-  Side& su = h->side[ESNMF_SIDE_U];
   h->nlaunch += 1;
   k_w_to_f32<<<grid_for((int64_t)h->k * h->kpad, 256, 256), 256, 0, h->stream>>>(h->W, h->k, h->kpad, h->W32);
   // fp32 / tensor-core (Y W) when kappa(G_V + eps I) <= u_kmax, else fp64 -- decided

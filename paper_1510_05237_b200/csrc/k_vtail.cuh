@@ -212,13 +212,19 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
 // or neighbouring terms: their rows of U are of similar length (the per-lane
 // product loops stay nearly convergent), lanes of one term load the same pairs
 // (broadcast) and add into different document rows (different banks: ys odd).
-constexpr int kVtSub = 4;            // entries per thread per round (their loads in flight together)
+#ifndef ESNMF_VT_SUB
+#define ESNMF_VT_SUB 4
+#endif
+#ifndef ESNMF_VT_MINB
+#define ESNMF_VT_MINB 3
+#endif
+constexpr int kVtSub = ESNMF_VT_SUB;  // entries per thread per round (their loads in flight together)
 
 ESNMF_DEV void vt_add(uint32_t* yrow, float av, int2 p) {
   atomicAdd(yrow + p.x, __float2uint_rn(av * __int_as_float(p.y)));
 }
 
-__global__ void __launch_bounds__(kVtThreads, 3) k_ytail(const int64_t* __restrict__ toff,
+__global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64_t* __restrict__ toff,
                                                          const int2* __restrict__ tent, int64_t ntiles,
                                                          const uint32_t* __restrict__ ubits,
                                                          const uint64_t* __restrict__ umap,
