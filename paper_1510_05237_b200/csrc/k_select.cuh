@@ -36,9 +36,10 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
   const unsigned lt = (1u << lane) - 1u;
   for (int b = threadIdx.x; b < kNumBins; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
-  const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
+  // chunks blockIdx.x, + gridDim.x, ... (a full grid takes one chunk per block)
+  for (int64_t r0 = (int64_t)blockIdx.x * kSelChunk; r0 < rows; r0 += (int64_t)gridDim.x * kSelChunk) {
+  const int64_t r1 = min(rows, r0 + kSelChunk);
   for (int64_t base = r0; base < r1; base += 4 * blockDim.x) {  // uniform trip count (ballots below)
     const int64_t j = base + 4 * threadIdx.x;
     float x[4];
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(256) k_sel_hist(const float* __restrict__ X, i
         }
       }
     }
+  }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kNumBins; b += blockDim.x)
@@ -562,14 +564,15 @@ __global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ 
   const ColSel s = sel[c];
   if (s.digit >= kNumBins) return;  // t == 0: nothing kept
   if (done && done[c]) return;      // selected from the predicted candidates
-  const int64_t r0 = (int64_t)blockIdx.x * kSelChunk;
-  const int64_t r1 = min(rows, r0 + kSelChunk);
   const float* col = X + (int64_t)c * ldx;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   uint64_t* ab = above + (int64_t)c * t;
   uint64_t* bk = bucket + (int64_t)c * kSelCap;
-  // every thread runs the same trip count (the ballots need the full warp)
+  // chunks blockIdx.x, + gridDim.x, ...; every thread runs the same trip count (the
+  // ballots need the full warp)
+  for (int64_t r0 = (int64_t)blockIdx.x * kSelChunk; r0 < rows; r0 += (int64_t)gridDim.x * kSelChunk) {
+  const int64_t r1 = min(rows, r0 + kSelChunk);
   for (int64_t base = r0; base < r1; base += 4 * blockDim.x) {
     const int64_t j = base + 4 * threadIdx.x;
     float x[4];
@@ -602,6 +605,7 @@ __global__ void __launch_bounds__(256) k_sel_collect2(const float* __restrict__ 
         if (slot < kSelCap) bk[slot] = sel_key(x[u], gr);
       }
     }
+  }
   }
 }
 
