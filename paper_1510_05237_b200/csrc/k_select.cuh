@@ -186,19 +186,84 @@ __global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ X
 }
 
 // bitonic sort of n (power of two) keys in shared memory, ascending
-__device__ void bitonic_sort_smem(uint64_t* a, int n) {
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        int jx = i ^ stride;
-        if (jx > i) {
-          bool up = (i & size) == 0;
-          uint64_t x = a[i], y = a[jx];
-          if ((x > y) == up) { a[i] = y; a[jx] = x; }
-        }
+// one block-wide compare-exchange stage of the bitonic network (stride >= 128)
+__device__ __forceinline__ void bitonic_stage_smem(uint64_t* a, int n, int size, int stride) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int jx = i ^ stride;
+    if (jx > i) {
+      bool up = (i & size) == 0;
+      uint64_t x = a[i], y = a[jx];
+      if ((x > y) == up) { a[i] = y; a[jx] = x; }
+    }
+  }
+}
+
+// the stages of strides < 128 on a 128-element chunk held 4 per lane (lane l:
+// elements 4l .. 4l+3 of the chunk at global offset b), warp-synchronous
+__device__ __forceinline__ void bitonic_warp_stages(uint64_t (&v)[4], int b, int size, int stride_hi) {
+  const int lane = threadIdx.x & 31;
+  for (int stride = stride_hi; stride > 0; stride >>= 1) {
+    if (stride >= 4) {
+      const int ld = stride >> 2;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t pv = __shfl_xor_sync(kFull, v[j], ld);
+        const int i = b + 4 * lane + j;
+        const bool up = (i & size) == 0, lower = (i & stride) == 0;
+        const uint64_t mn = v[j] < pv ? v[j] : pv, mx = v[j] < pv ? pv : v[j];
+        v[j] = (up == lower) ? mn : mx;
       }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j & stride) continue;
+        const int jp = j | stride;
+        const int i = b + 4 * lane + j;
+        const bool up = (i & size) == 0;
+        if ((v[j] > v[jp]) == up) { const uint64_t t = v[j]; v[j] = v[jp]; v[jp] = t; }
+      }
+    }
+  }
+}
+
+// Ascending bitonic sort of n (a power of two) keys in shared memory by the whole
+// block (blockDim a multiple of 32).  From n = 128 on, every run of stages with
+// strides < 128 is done warp-synchronously on 128-element chunks in registers
+// (shuffles), so only the strides >= 128 cost a block barrier: 15 of the 78 stages
+// at n = 4,096.
+__device__ void bitonic_sort_smem(uint64_t* a, int n) {
+  if (n < 128) {
+    for (int size = 2; size <= n; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        bitonic_stage_smem(a, n, size, stride);
+        __syncthreads();
+      }
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int b = warp * 128; b < n; b += nw * 128) {  // sizes 2 .. 128 inside each chunk
+    uint64_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = a[b + 4 * lane + j];
+    for (int size = 2; size <= 128; size <<= 1) bitonic_warp_stages(v, b, size, size >> 1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[b + 4 * lane + j] = v[j];
+  }
+  __syncthreads();
+  for (int size = 256; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride >= 128; stride >>= 1) {
+      bitonic_stage_smem(a, n, size, stride);
       __syncthreads();
     }
+    for (int b = warp * 128; b < n; b += nw * 128) {
+      uint64_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = a[b + 4 * lane + j];
+      bitonic_warp_stages(v, b, size, 64);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[b + 4 * lane + j] = v[j];
+    }
+    __syncthreads();
   }
 }
 
