@@ -75,11 +75,17 @@ def test_user_u0_is_used():
     assert np.array_equal(dense_U(s, TINY.n, TINY.k).astype(np.float32), U0)
 
 
-def test_gram_matches_oracle():
+@pytest.mark.parametrize("k", [TINY.k, 200], ids=["k20", "k200"])
+@pytest.mark.parametrize("path", ["dense", "sparse"])
+def test_gram_matches_oracle(path, k, monkeypatch):
+    """G_U of the dense U_0 ("U^T U"): the dense-row Gram (k_gram_dense, 128 x 128
+    output blocks: k = 200 has an off-diagonal block) and the entry-gather Gram."""
+    if path == "sparse":
+        monkeypatch.setenv("ESNMF_GRAM_SPARSE", "1")
     g = synth.generate(TINY)
-    s = solver(TINY, g)
+    s = ESNMF(TINY.n, TINY.m, k, TINY.t, g, seed=TINY.seed)
     G, eps = s.get_gram(ESNMF_SIDE_V)
-    Gr = oracle.gram(oracle.u0(TINY.n, TINY.k, TINY.seed).astype(np.float64))
+    Gr = oracle.gram(oracle.u0(TINY.n, k, TINY.seed).astype(np.float64))
     assert np.allclose(G, Gr, rtol=1e-13, atol=0)
     assert np.array_equal(G, G.T)
     _, eps_r = oracle.cholesky(Gr)
@@ -506,3 +512,29 @@ def test_t_zero_keeps_nothing():
         oracle.run(g, cfg.k, 0, 1, seed=cfg.seed)
     h = oracle.half_step(g["at_ptr"], g["at_col"], g["at_val"], oracle.u0(cfg.n, cfg.k, cfg.seed), 0)
     assert not h["F"].any()
+
+
+def test_memory_pool_reuse_and_fallback(monkeypatch):
+    """Device buffers come from the library's stream-ordered pool (esnmf::alloc): handles
+    created and destroyed in turn reuse its pages (device free memory stable from the
+    second cycle on), and ESNMF_NO_POOL=1 (cudaMalloc) gives the bitwise same run."""
+    import torch
+
+    g = synth.generate(TINY)
+    free = []
+    runs = []
+    for _ in range(3):
+        s = solver(TINY, g)
+        s.iterate(3)
+        runs.append((dense_U(s, TINY.n, TINY.k), [r["E"] for r in s.records()]))
+        s.close()
+        torch.cuda.synchronize()
+        free.append(torch.cuda.mem_get_info()[0])
+    assert free[2] == free[1]
+    monkeypatch.setenv("ESNMF_NO_POOL", "1")
+    s = solver(TINY, g)
+    s.iterate(3)
+    U, E = dense_U(s, TINY.n, TINY.k), [r["E"] for r in s.records()]
+    s.close()
+    for Ur, Er in runs:
+        assert np.array_equal(U, Ur) and E == Er
