@@ -267,6 +267,7 @@ struct esnmf {
                                                     // the next V side clears it (aux stream)
   bool v_since_u = true;             // a V side ran since the last U side (Yqb[yq_par] is clear)
   int yq_par = 0;                    // the buffer the next U side uses (flips every U side)
+  bool yq_other_dirty = false;       // Yqb[1 - yq_par] (the last U side's) still holds its sums
   float* W32 = nullptr;              // [k][kpad] fp32 copy of W for k_uside_finish_rt
   uint8_t* wtc = nullptr;            // W as the tensor-core B operand (fp16 hi/lo, k_uside_tc)
   float* wtc_scale = nullptr;        // [kn] its per-column scales
@@ -1474,8 +1475,9 @@ void vside_prep(esnmf_t* h, const Factor& f) {
 // U-side fixed-point accumulator: the U side uses Yqb[ucur]; the V side after it
 // clears the other buffer (the one the previous U side used and k_polish_u read)
 void yq_clear_other(esnmf_t* h) {
-  if (!h->Yqb[0]) return;
+  if (!h->Yqb[0] || !h->yq_other_dirty) return;
   CK(cudaMemsetAsync(h->Yqb[1 - h->yq_par], 0, sizeof(unsigned long long) * h->n * h->kpad, h->stream));
+  h->yq_other_dirty = false;
 }
 
 // one half-step; returns the factor that was written
@@ -1598,7 +1600,7 @@ Factor& half_step(esnmf_t* h, int s) {
         sc.kmax = h->u_kmax;
         sweep(h, su.G, su.eps, sc);
       }
-      yq_clear_other(h);  // the buffer the last U side used (k_polish_u has read it)
+      yq_clear_other(h);  // the buffer the last U side used, unless the record cleared it
       uside_w_prep(h);
       h->u_prefork = true;
     }
@@ -1607,6 +1609,7 @@ Factor& half_step(esnmf_t* h, int s) {
   if (s == ESNMF_SIDE_U) {
     h->ucur = 1 - h->ucur;
     h->yq_par = 1 - h->yq_par;
+    if (h->Yqb[0]) h->yq_other_dirty = true;
     h->gramU_valid = false;
   }
   return out;
@@ -1716,6 +1719,10 @@ void flush_metrics(esnmf_t* h) {
   }
   ++h->nlaunch; k_finalize_record<<<1, 256, 0, h->stream>>>(in, h->rec, h->d_nrec, h->scal);
   CKL("finalize_record");
+  // the last U side's fixed-point buffer (k_polish_u has read it) is cleared here, on
+  // the low-priority stream beside the next V side, instead of on the aux stream
+  // ahead of the next U side's W preparation (n x kpad x 8 bytes: 166 MB at Large)
+  if (overlap_m) yq_clear_other(h);
   h->nrec += 1;
   if (overlap_m) h->aux_pending = true;
 }
