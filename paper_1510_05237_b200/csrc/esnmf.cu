@@ -296,7 +296,7 @@ struct esnmf {
   unsigned* rowsum_bits = nullptr;  // max document row sum of A^T (float bits, rounded up; global)
   uint64_t* umap = nullptr;      // [n] U row view: (first << 32) | count
   uint32_t* ubits = nullptr;     // [n / 32] rows of U with a nonzero
-  double* Z64 = nullptr;         // [U active rows][k] Z = U W in fp64 (k_form_z64)
+  double* Z64 = nullptr;         // [n terms][k] Z = U W in fp64 for U's active rows (k_form_z64); others stale
   double vt_kmax = 1e4, vt_amax = 8.0;  // k_vcond_flag thresholds (ESNMF_VT_KMAX / ESNMF_VT_AMAX)
   double vt_ratio = 8.0;         // cost of a paper-order product / a gathered FMA (ESNMF_VT_RATIO)
   int32_t* termlen = nullptr;    // [n] stored entries of each term (row lengths of A, global)
@@ -1432,8 +1432,7 @@ void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val)
   const int64_t per_col = h->tside[ESNMF_SIDE_V] < 0 ? sv.rows : std::min<int64_t>(h->tside[ESNMF_SIDE_V], sv.rows);
   const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 8), 4096)), h->k);
   ++h->nlaunch;
-  k_polish_v<<<g, 256, 0, h->stream>>>(colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent,
-                                       h->U[h->ucur].rowmap, h->Z64);
+  k_polish_v<<<g, 256, 0, h->stream>>>(colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent, h->ubits, h->Z64);
   CKL("polish_v");
 }
 
@@ -1448,19 +1447,19 @@ void polish_u(esnmf_t* h, Factor& out) {
   CKL("polish_u");
 }
 
-// Z64 = U W for U's active rows (fp64; k_form_z64)
+// Z64 = U W for U's active rows (fp64; k_form_z64), term-indexed
 void form_z64(esnmf_t* h, const Factor& f) {
   const unsigned grid = grid_for(f.cap_rows, 8, (int64_t)h->num_sms * 16);
   ++h->nlaunch;
   switch ((h->k + 31) / 32) {
-    case 1: k_form_z64<1><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 2: k_form_z64<2><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 3: k_form_z64<3><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 4: k_form_z64<4><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 5: k_form_z64<5><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 6: k_form_z64<6><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    case 7: k_form_z64<7><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
-    default: k_form_z64<8><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, h->W, h->Z64); break;
+    case 1: k_form_z64<1><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 2: k_form_z64<2><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 3: k_form_z64<3><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 4: k_form_z64<4><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 5: k_form_z64<5><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 6: k_form_z64<6><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    case 7: k_form_z64<7><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
+    default: k_form_z64<8><<<grid, 256, 0, h->stream>>>(f.dense, h->kpad, h->k, f.n_active, f.active, h->W, h->Z64); break;
   }
   CKL("form_z64");
 }

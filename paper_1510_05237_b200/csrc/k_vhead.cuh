@@ -144,8 +144,8 @@ __global__ void k_vside_prep(const double* __restrict__ Z64, const int32_t* __re
   __syncthreads();
   float zmax = 0.f;
   for (int s = threadIdx.x; s < h; s += blockDim.x) {
-    const int32_t r = rowmap[headterm[s]];
-    const double z = r >= 0 ? Z64[(int64_t)r * k + c] : 0.0;  // Z = U W (fp64, k_form_z64)
+    const int32_t term = headterm[s];
+    const double z = rowmap[term] >= 0 ? Z64[(int64_t)term * k + c] : 0.0;  // Z = U W (fp64, k_form_z64)
     zs[s] = (float)z;
     zmax = fmaxf(zmax, fabsf((float)z));
   }

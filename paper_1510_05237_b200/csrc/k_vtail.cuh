@@ -294,12 +294,15 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
   }
 }
 
-// Z64 = U W in fp64 for the active rows of U (row r of the dense active view:
-// rowmap[term] = r): the exact Z rows behind k_vside_prep's head chunks and
-// k_polish_v.  One warp per active row, lanes over columns (CJ = ceil(k / 32)).
+// Z64 = U W in fp64 for the active rows of U (row r of the dense active view,
+// written at its term: Z64[active[r]][c]; rows of inactive terms are stale and
+// never read): the exact Z rows behind k_vside_prep's head chunks and k_polish_v
+// (term-indexed, so the polish needs no rowmap lookup).  One warp per active row,
+// lanes over columns (CJ = ceil(k / 32)).
 template <int CJ>
 __global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dense, int kpad, int k,
-                                                  const int64_t* __restrict__ n_active, const double* __restrict__ W,
+                                                  const int64_t* __restrict__ n_active,
+                                                  const int32_t* __restrict__ active, const double* __restrict__ W,
                                                   double* __restrict__ Z64) {
   const int lane = threadIdx.x & 31;
   const int64_t na = *n_active;
@@ -328,24 +331,25 @@ __global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dens
         }
       }
     }
+    double* zr = Z64 + (int64_t)active[r] * k;  // term-indexed: the readers skip inactive terms
 #pragma unroll
     for (int j = 0; j < CJ; ++j) {
       const int c = lane + 32 * j;
-      if (c < k) Z64[r * k + c] = acc[j];
+      if (c < k) zr[c] = acc[j];
     }
   }
 }
 
 // The kept entries of V (after the selection) recomputed exactly: for kept
 // (document j, topic c) LS_jc = sum over the document's stored entries a_ji Z_ic
-// with Z = U W in fp64 (Z64, k_form_z64; zero for a term whose row of U is
-// empty).  The selection chose the entries from the tensor-core values; this
+// with Z = U W in fp64 (Z64, k_form_z64, term-indexed; a term whose row of U
+// is empty -- its bit in ubits clear -- contributes zero).  The selection chose the entries from the tensor-core values; this
 // pass makes the VALUES exact to fp32 rounding (BJ:5 "relative 1e-5 on factor
 // entries").  Grid (x, k): one warp per kept entry of column blockIdx.y, lanes
 // over the document's entries.
 __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
                            float* __restrict__ val, int k, int64_t row0, const int64_t* __restrict__ ptr,
-                           const int2* __restrict__ ent, const int32_t* __restrict__ rowmap,
+                           const int2* __restrict__ ent, const uint32_t* __restrict__ ubits,
                            const double* __restrict__ Z64) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.y;  // grid (x, k): the entries of column c, one warp each
@@ -357,14 +361,15 @@ __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __
     double acc = 0;
     for (int64_t q0 = ptr[r] + lane; q0 < s1; q0 += 256) {  // 8 entries per lane in flight
       int2 en[8];
-      int32_t rm[8];
+      bool act[8];
       double z[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) en[u] = q0 + 32 * u < s1 ? __ldg(ent + q0 + 32 * u) : make_int2(0, 0);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) rm[u] = q0 + 32 * u < s1 ? __ldg(rowmap + en[u].x) : -1;
+      for (int u = 0; u < 8; ++u)  // the term's row of U is non-empty (U's bitmap, L1-resident)
+        act[u] = q0 + 32 * u < s1 && ((__ldg(ubits + ((uint32_t)en[u].x >> 5)) >> (en[u].x & 31)) & 1u);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) z[u] = rm[u] >= 0 ? __ldg(Z64 + (int64_t)rm[u] * k + c) : 0.0;
+      for (int u = 0; u < 8; ++u) z[u] = act[u] ? __ldg(Z64 + (int64_t)en[u].x * k + c) : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc = fma((double)__int_as_float(en[u].y), z[u], acc);
     }
