@@ -581,11 +581,7 @@ void sweep(esnmf_t* h, const double* G, double* eps, SweepCond sc = SweepCond())
   if (JB >= 2 && h->k <= 256 && !scalar) {  // blocked sweep (k_solve.cuh)
     bool in_smem = false;
     const size_t smem = bsweep_smem_bytes(h->k, &in_smem);
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_sweep_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-      attr = true;
-    }
+    CK(cudaFuncSetAttribute(k_sweep_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     ++h->nlaunch;
     k_sweep_blocked<<<1, kBsThreads, smem, h->stream>>>(G, h->k, h->rho, h->W, eps, h->flags,
                                                          in_smem ? nullptr : h->sweep_scratch, sc);
