@@ -677,11 +677,15 @@ void form_z(esnmf_t* h, const Factor& f, const int* gate = nullptr) {
     k_zc_clear<<<grid_for(f.cap_rows * kpz, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->zlist, h->zcount,
                                                                                                kpz, h->zc);
   }
+  // gated launches (the Z-row gather as the paper-order tail's fallback) take
+  // grid-stride grids of 4 blocks per SM: when the gate is off they cost a few
+  // microseconds instead of thousands of blocks that exit at once
+  const int64_t gcap = gate ? 4 : 32;
   ++h->nlaunch;
-  k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
+  k_zrows_clear<<<grid_for(f.cap_rows * zq, 256, (int64_t)h->num_sms * gcap), 256, 0, h->stream>>>(
       h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq, gate);
   const int CJ = (h->kpad + 31) / 32;
-  unsigned grid = grid_for(f.cap_rows, 8, 148 * 64);
+  unsigned grid = grid_for(f.cap_rows, 8, (int64_t)h->num_sms * (gate ? 4 : 64));
 #define ESNMF_FZ(cj)                                                                                          \
   case cj:                                                                                                    \
     ++h->nlaunch;                                                                                             \
