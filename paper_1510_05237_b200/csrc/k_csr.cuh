@@ -177,6 +177,29 @@ __global__ void k_transpose_chunks(const RowChunk* __restrict__ ch, int64_t nch,
 // staged in shared memory, each entry's slot = the number of smaller columns
 // (columns are distinct within a row); longer rows: k_sort_rows(long_rows_only)
 constexpr int kRankRow = 512;
+// the rank sort of one row held in shared memory (b[0..len), len <= 32 * PER):
+// entry i goes to position #{j : b[j].x < b[i].x} (the columns are distinct)
+template <int PER>
+__device__ __forceinline__ void rank_row(const int2* __restrict__ b, int len, int2* __restrict__ out, int lane) {
+  int mine[PER], rank[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int i = lane + 32 * q;
+    mine[q] = i < len ? b[i].x : 0x7FFFFFFF;
+    rank[q] = 0;
+  }
+  for (int j = 0; j < len; ++j) {
+    const int cj = b[j].x;  // broadcast
+#pragma unroll
+    for (int q = 0; q < PER; ++q) rank[q] += cj < mine[q];
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int i = lane + 32 * q;
+    if (i < len) out[rank[q]] = b[i];
+  }
+}
+
 __global__ void __launch_bounds__(256) k_sort_rows_rank(const int64_t* __restrict__ ptr, int64_t rows,
                                                         int2* __restrict__ ent) {
   __shared__ int2 buf[8][kRankRow];
@@ -189,24 +212,14 @@ __global__ void __launch_bounds__(256) k_sort_rows_rank(const int64_t* __restric
     if (len <= 1 || len > kRankRow) continue;  // warp-uniform
     for (int i = lane; i < len; i += 32) b[i] = ent[s + i];
     __syncwarp();
-    constexpr int kPer = kRankRow / 32;
-    int mine[kPer], rank[kPer];
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int i = lane + 32 * q;
-      mine[q] = i < len ? b[i].x : 0x7FFFFFFF;
-      rank[q] = 0;
-    }
-    for (int j = 0; j < len; ++j) {
-      const int cj = b[j].x;  // broadcast
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) rank[q] += cj < mine[q];
-    }
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int i = lane + 32 * q;
-      if (i < len) ent[s + rank[q]] = b[i];
-    }
+    // as many entries per lane as the row needs (the compare loop is len x PER)
+    if (len <= 64) rank_row<2>(b, len, ent + s, lane);
+    else if (len <= 96) rank_row<3>(b, len, ent + s, lane);
+    else if (len <= 128) rank_row<4>(b, len, ent + s, lane);
+    else if (len <= 160) rank_row<5>(b, len, ent + s, lane);
+    else if (len <= 192) rank_row<6>(b, len, ent + s, lane);
+    else if (len <= 256) rank_row<8>(b, len, ent + s, lane);
+    else rank_row<kRankRow / 32>(b, len, ent + s, lane);
     __syncwarp();
   }
 }
