@@ -371,6 +371,23 @@ struct esnmf {
     if (pool) ck(cudaFreeAsync(p, stream), "cudaFreeAsync");
     else ck(cudaFree(p), "cudaFree");
   }
+  // create-time scratch: stream-ordered from the pool (freed without a host sync),
+  // else cudaMalloc / synchronize + cudaFree
+  void* tmp_get(size_t b) {
+    void* p = nullptr;
+    if (pool) ck(cudaMallocFromPoolAsync(&p, std::max<size_t>(b, 16), pool, stream), "cudaMallocFromPoolAsync");
+    else ck(cudaMalloc(&p, std::max<size_t>(b, 16)), "cudaMalloc");
+    return p;
+  }
+  void tmp_put(void* p) {
+    if (!p) return;
+    if (pool) {
+      ck(cudaFreeAsync(p, stream), "cudaFreeAsync");
+    } else {
+      ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+      ck(cudaFree(p), "cudaFree");
+    }
+  }
   ~esnmf() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& g : gexec)
@@ -1184,13 +1201,21 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (env && env[0]) want = atoi(env);
   if (want == 0 && !h->ptail) return;
   const int64_t n = h->n;
-  std::vector<int32_t> order(n);
-  for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t a, int32_t b) { return hptr[a + 1] - hptr[a] > hptr[b + 1] - hptr[b]; });
+  // terms by document frequency, descending, ties to the lower term id; only the
+  // first hh (<= kHeadMax) are ever used, so only those are put in order
+  auto df_of = [&](int32_t t) { return hptr[t + 1] - hptr[t]; };
+  auto by_df = [&](int32_t a, int32_t b) {
+    const int64_t da = df_of(a), db = df_of(b);
+    return da != db ? da > db : a < b;
+  };
+  std::vector<int32_t> order;
   int64_t hh;
   if (want >= 0) {
     hh = std::min<int64_t>(want, n);
+    order.resize(n);
+    for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+    const int64_t top = std::min<int64_t>(hh, kHeadMax);
+    std::partial_sort(order.begin(), order.begin() + top, order.end(), by_df);
   } else {
     // document-frequency threshold of a head term.  Z-gather tail: 1.5 % (the
     // dense-tile cost balanced a 400-byte gather per active entry).  Paper-order
@@ -1200,8 +1225,10 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     const char* fe = getenv("ESNMF_HEAD_DF");
     if (fe && fe[0]) frac = atof(fe);
     const double min_df = std::max(1.0, frac * (double)h->m);
-    hh = 0;
-    while (hh < n && (double)(hptr[order[hh] + 1] - hptr[order[hh]]) >= min_df) ++hh;
+    for (int64_t i = 0; i < n; ++i)
+      if ((double)df_of((int32_t)i) >= min_df) order.push_back((int32_t)i);
+    std::sort(order.begin(), order.end(), by_df);
+    hh = (int64_t)order.size();
   }
   hh = std::min<int64_t>(hh, kHeadMax) / kHeadK * kHeadK;
   if (hh < kHeadK && !h->ptail) return;
@@ -1227,14 +1254,12 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   // rows of A^T: head entries first (stable), so the tail reads skip them
   h->nh = h->alloc<int32_t>(std::max<int64_t>(sv.rows, 1));
   if (sv.T.nnz > 0 && hh > 0) {
-    int2* tmp = nullptr;
-    CK(cudaMalloc(&tmp, sizeof(int2) * sv.T.nnz));
+    int2* tmp = static_cast<int2*>(h->tmp_get(sizeof(int2) * sv.T.nnz));
     ++h->nlaunch;
     k_reorder_head<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
         sv.T.ptr, sv.T.ent, sv.rows, h->headslot, tmp, h->nh);
     CK(cudaMemcpyAsync(sv.T.ent, tmp, sizeof(int2) * sv.T.nnz, cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaFree(tmp));
+    h->tmp_put(tmp);
   } else {
     CK(cudaMemsetAsync(h->nh, 0, sizeof(int32_t) * std::max<int64_t>(sv.rows, 1), h->stream));
   }
@@ -1294,14 +1319,12 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
       CK(cudaMemcpyAsync(&nhe, h->hoff + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));
       h->hseg = h->alloc<int2>(std::max<int64_t>(nhe, 1));
-      unsigned long long* cursor = nullptr;
-      CK(cudaMalloc(&cursor, sizeof(int64_t) * (nseg + 1)));
+      auto* cursor = static_cast<unsigned long long*>(h->tmp_get(sizeof(int64_t) * (nseg + 1)));
       CK(cudaMemcpyAsync(cursor, h->hoff, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToDevice, h->stream));
       ++h->nlaunch;
       k_head_fill<<<g, 256, 0, h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->head_nd, nsp, cursor,
                                            h->hseg);
-      CK(cudaStreamSynchronize(h->stream));
-      CK(cudaFree(cursor));
+      h->tmp_put(cursor);
     } else {
       h->hseg = h->alloc<int2>(1);
     }
@@ -1322,12 +1345,10 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     k_vt_fill<<<(unsigned)nt, kVtM, 0, h->stream>>>(sv.T.ptr, hh > 0 ? h->nh : nullptr, sv.T.ent, sv.rows, h->toff,
                                                    h->tent);
     if (ntail > 0 && ntail < (1LL << 31)) {  // sort every tile's entries by (term, row)
-      uint32_t *k0 = nullptr, *k1 = nullptr;
-      int32_t *v0 = nullptr, *v1 = nullptr;
-      CK(cudaMalloc(&k0, sizeof(uint32_t) * ntail));
-      CK(cudaMalloc(&k1, sizeof(uint32_t) * ntail));
-      CK(cudaMalloc(&v0, sizeof(int32_t) * ntail));
-      CK(cudaMalloc(&v1, sizeof(int32_t) * ntail));
+      auto* k0 = static_cast<uint32_t*>(h->tmp_get(sizeof(uint32_t) * ntail));
+      auto* k1 = static_cast<uint32_t*>(h->tmp_get(sizeof(uint32_t) * ntail));
+      auto* v0 = static_cast<int32_t*>(h->tmp_get(sizeof(int32_t) * ntail));
+      auto* v1 = static_cast<int32_t*>(h->tmp_get(sizeof(int32_t) * ntail));
       const unsigned g = grid_for(ntail, 256, (int64_t)h->num_sms * 16);
       ++h->nlaunch;
       k_vt_to_keys<<<g, 256, 0, h->stream>>>(h->tent, ntail, k0, v0);
@@ -1336,14 +1357,12 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
       size_t tmp_bytes = 0;
       CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, v1, (int)ntail, (int)nt, h->toff,
                                                   h->toff + 1, 0, end_bit, h->stream));
-      void* tmp = nullptr;
-      CK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+      void* tmp = h->tmp_get(tmp_bytes);
       CK(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)ntail, (int)nt, h->toff,
                                                   h->toff + 1, 0, end_bit, h->stream));
       ++h->nlaunch;
       k_vt_from_keys<<<g, 256, 0, h->stream>>>(k1, v1, ntail, h->tent);
-      CK(cudaStreamSynchronize(h->stream));
-      for (void* q : {(void*)k0, (void*)k1, (void*)v0, (void*)v1, tmp}) CK(cudaFree(q));
+      for (void* q : {(void*)k0, (void*)k1, (void*)v0, (void*)v1, tmp}) h->tmp_put(q);
     }
     h->ytile = h->alloc<uint8_t>(nt * kVtM * h->kn * 4);
     const int64_t wb = (int64_t)h->nyc * h->kn * kHeadK * 4;
@@ -2396,8 +2415,8 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
     h->vmax = h->alloc<uint32_t>(1);
     h->rsum = h->alloc<double>(su.rows);
     ++h->nlaunch;
-    k_rowsum<<<grid_for(su.rows, 8, (int64_t)h->num_sms * 64), 256, 0, h->stream>>>(su.T.ptr, su.T.ent, su.rows,
-                                                                                   h->rsum);
+    k_rowsum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(su.rows, (int64_t)h->num_sms * 8)), 256, 0,
+               h->stream>>>(su.T.ptr, su.T.ent, su.rows, h->rsum);
     h->rsum_max = h->alloc<double>(1);
     ++h->nlaunch;
     k_max_to<<<1, 1024, 0, h->stream>>>(h->rsum, su.rows, h->rsum_max);

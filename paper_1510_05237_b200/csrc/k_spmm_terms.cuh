@@ -93,16 +93,17 @@ __global__ void k_vrows_clear(const int32_t* __restrict__ active, const int64_t*
   }
 }
 
-// row sums of A (fp64) for the fixed-point scales, one warp per row
-__global__ void k_rowsum(const int64_t* __restrict__ ptr, const int2* __restrict__ ent, int64_t rows,
-                         double* __restrict__ rsum) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+// row sums of A (fp64) for the fixed-point scales, one block per row (grid-stride):
+// A's term rows are Zipf-long (the top ones hold most documents), which left a
+// warp per row running one long row alone; the block sum is a fixed tree
+__global__ void __launch_bounds__(256) k_rowsum(const int64_t* __restrict__ ptr, const int2* __restrict__ ent,
+                                                int64_t rows, double* __restrict__ rsum) {
+  __shared__ double sm[32];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     double s = 0;
-    for (int64_t q = ptr[r] + lane; q < ptr[r + 1]; q += 32) s += (double)__int_as_float(ent[q].y);
-    s = warp_sum(s);
-    if (lane == 0) rsum[r] = s;
+    for (int64_t q = ptr[r] + threadIdx.x; q < ptr[r + 1]; q += blockDim.x) s += (double)__int_as_float(ent[q].y);
+    s = block_sum(s, sm);
+    if (threadIdx.x == 0) rsum[r] = s;
   }
 }
 
