@@ -703,6 +703,13 @@ void form_z(esnmf_t* h, const Factor& f, const int* gate = nullptr) {
       h->zlist, h->zcount, reinterpret_cast<float4*>(h->Z), zq, gate);
   const int CJ = (h->kpad + 31) / 32;
   unsigned grid = grid_for(f.cap_rows, 8, (int64_t)h->num_sms * (gate ? 4 : 64));
+  if (h->ptail && !h->zc) {  // Z64 = U W is already there (form_z64): convert it
+    ++h->nlaunch;
+    k_form_z_from64<<<grid, 256, 0, h->stream>>>(f.n_active, f.active, h->k, h->zs, h->Z64, h->Z, h->zlist, h->zcount,
+                                                 gate);
+    CKL("form_z");
+    return;
+  }
 #define ESNMF_FZ(cj)                                                                                          \
   case cj:                                                                                                    \
     ++h->nlaunch;                                                                                             \

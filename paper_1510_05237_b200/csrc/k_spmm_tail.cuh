@@ -49,6 +49,28 @@ __global__ void k_zrows_clear(const int32_t* __restrict__ terms, const int64_t* 
   }
 }
 
+// Z rows for the gather from the fp64 Z64 = U W already formed (paper-order mode,
+// k_form_z64, term-indexed): Z[term][c] = fp32(Z64[term][c]) -- the rounding
+// k_form_z applies to the same fp64 sums -- instead of a second k x k product per
+// row.  One warp per active row; the rows' terms go to zlist for the next clear.
+__global__ void k_form_z_from64(const int64_t* __restrict__ n_active, const int32_t* __restrict__ active, int k,
+                                int zs, const double* __restrict__ Z64, float* __restrict__ Z,
+                                int32_t* __restrict__ zlist, int64_t* __restrict__ zcount,
+                                const int* __restrict__ gate) {
+  if (gate && !*gate) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t na = *n_active;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < na; r += nwarps) {
+    const int32_t term = active[r];
+    const double* zr64 = Z64 + (int64_t)term * k;
+    float* zr = Z + (int64_t)term * zs;
+    for (int c = lane; c < zs; c += 32) zr[c] = c < k ? (float)zr64[c] : 0.f;
+    if (lane == 0) zlist[r] = term;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *zcount = na;
+}
+
 // term bitmap of the active rows of U (all bits cleared by the caller first)
 __global__ void k_term_bits(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
                             uint32_t* __restrict__ bits, const int* __restrict__ gate) {
