@@ -4,7 +4,7 @@
 The product is ``libesnmf.so`` (CUDA, sm_100a) behind the C ABI in
 ``include/esnmf.h``; this package is its ctypes binding.  See DESIGN.md.
 """
-from . import comm  # noqa: F401
+from . import checkpoint, comm  # noqa: F401
 from .esnmf import (  # noqa: F401
     ESNMF,
     ESNMFError,

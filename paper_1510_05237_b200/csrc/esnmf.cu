@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -458,11 +459,14 @@ cudaEvent_t pool_event(esnmf_t* h) {
 }
 
 // RAII event pair around one phase, recorded on the handle's stream
+// Also an NVTX range named after the phase (host side: the launches of the phase,
+// visible in Nsight Systems / Nsight Compute's NVTX filters; no cost without a tool)
 struct Phase {
   esnmf_t* h;
   int id;
   cudaEvent_t a = nullptr;
   Phase(esnmf_t* h_, int id_) : h(h_), id(id_) {
+    nvtxRangePushA(kPhaseNames[id]);
     if (h->prof_on) {
       a = pool_event(h);
       ck(cudaEventRecord(a, h->stream), "cudaEventRecord");
@@ -474,6 +478,7 @@ struct Phase {
       cudaEventRecord(b, h->stream);
       h->prof.push_back({id, a, b});
     }
+    nvtxRangePop();
   }
 };
 
