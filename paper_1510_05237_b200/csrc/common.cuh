@@ -3,8 +3,32 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #define ESNMF_DEV __device__ __forceinline__
+
+// Device bounds checks (compute-sanitizer is not available on the GPU pool):
+// built with -DESNMF_DEBUG_CHECKS=1 (tools/debug_checks.sh) every ESNMF_CHECK
+// prints the failing condition with its block / thread and traps, so the test
+// suite run on the debug library stops at the first out-of-range index; in the
+// product build it compiles to nothing.
+#ifndef ESNMF_DEBUG_CHECKS
+#define ESNMF_DEBUG_CHECKS 0
+#endif
+#if ESNMF_DEBUG_CHECKS
+#define ESNMF_CHECK(cond)                                                                                 \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("ESNMF_CHECK failed: %s at %s:%d block %d thread %d\n", #cond, __FILE__, __LINE__,         \
+             (int)blockIdx.x, (int)threadIdx.x);                                                        \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define ESNMF_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 namespace esk {
 

@@ -359,6 +359,7 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, int cbeg
         for (int j = 0; j < 16; ++j) {
           const int c = c0 + j;
           x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
+          ESNMF_CHECK(row < ldx);
           if (c < k) X[(int64_t)c * ldx + row] = x[j];
         }
       } else {
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   }
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ESNMF_CHECK((uint32_t)(base - smem_raw) + STAGES * head_stage_bytes(kn) <= tc::dyn_smem_bytes());
   const uint32_t zhalf = (uint32_t)kn * kHeadK * 2;
   const uint32_t zbytes = 2 * zhalf;
   const uint32_t stage_bytes = head_stage_bytes(kn);
@@ -502,6 +504,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
           if (q >= nchunks) {  // (Y_tail W) chunk: Y_tail tile chunk + W chunk
             const uint32_t w = (uint32_t)min(64, kn - 64 * yq);
             const uint32_t ab = (uint32_t)kHeadM * w * 4u, bb = (uint32_t)kn * w * 4u;
+            ESNMF_CHECK(ab <= kHeadABytes && bb <= zbytes);
             tc::mbar_arrive_expect_tx(&raw_full[stage], ab + bb);
             tc::bulk_g2s(st, ytile + (size_t)tile * kHeadM * kn * 4 + (size_t)yq * kHeadABytes, ab, &raw_full[stage]);
             tc::bulk_g2s(st + kHeadABytes, wbuf + (size_t)yq * zbytes, bb, &raw_full[stage]);
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
               const int64_t a = sb & ~(int64_t)1;  // 16-byte aligned start
               const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);  // even, capped
               const uint32_t rb = (uint32_t)(b - a) * 8u;
+              ESNMF_CHECK(rb <= kHeadRawBytes && raw_off + rb <= stage_bytes);
               s_run[stage][0] = sb;
               s_run[stage][1] = se;
               tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + rb);
@@ -535,6 +539,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       const float a = ldexpf(__int_as_float(en.y), eA);
       const __half hi = __float2half_rn(a);
       const __half lo = __float2half_rn(a - __half2float(hi));
+      ESNMF_CHECK((en.x >> 6) < kHeadM && (en.x & 63) < kHeadK);
       const uint32_t off = tc::kmajor_off16(en.x >> 6, en.x & 63, kHeadK);
       *reinterpret_cast<__half*>(sa + off) = hi;
       *reinterpret_cast<__half*>(sa + kHeadAHalf + off) = lo;
@@ -563,6 +568,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kHeadProd) : "memory");
         const int64_t se_s = min(se, cap);
+        ESNMF_CHECK(sb >= a && se_s - a <= kHeadRaw);
         for (int64_t i = sb + p; i < se_s; i += kHeadProd) put(sa, raw[i - a]);
         for (int64_t i = cap + p; i < se; i += kHeadProd) put(sa, __ldcs(hseg + i));  // long runs only
         tc::fence_async_smem();  // generic-proxy writes -> visible to the tensor core

@@ -221,6 +221,7 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
 constexpr int kVtSub = ESNMF_VT_SUB;  // entries per thread per round (their loads in flight together)
 
 ESNMF_DEV void vt_add(uint32_t* yrow, float av, int2 p) {
+  ESNMF_CHECK(p.x >= 0 && p.x < 256);
   atomicAdd(yrow + p.x, __float2uint_rn(av * __int_as_float(p.y)));
 }
 
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
       for (int u = 0; u < kVtSub; ++u) {
         const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
         const int2* up = uent + (mp[u] >> 32);
+        ESNMF_CHECK(((uint32_t)en[u].x >> kVtTermBits) < (uint32_t)kVtM && cnt <= kn);
         uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
         const float av = __int_as_float(en[u].y);
         int j = 0;
