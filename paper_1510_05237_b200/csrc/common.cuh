@@ -32,6 +32,13 @@
 
 namespace esk {
 
+// dynamic shared memory of the running launch, bytes (bounds checks)
+ESNMF_DEV uint32_t dyn_smem_bytes() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 

@@ -241,12 +241,6 @@ __global__ void __launch_bounds__(1024) k_sweep_inverse(const double* __restrict
 // scratch (L2-resident).  fp64 throughout.
 constexpr int kBsThreads = 512;
 
-ESNMF_DEV uint32_t tc_dyn_smem() {  // dynamic shared memory of the launch (bounds checks)
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
-  return r;
-}
-
 ESNMF_DEV int bs_ld(int k) { return ((k + 31) / 32) * 32; }  // panel row stride (padded R)
 
 inline size_t bsweep_smem_bytes(int k, bool* a_in_smem) {
@@ -269,7 +263,7 @@ __global__ void __launch_bounds__(kBsThreads) k_sweep_blocked(const double* __re
   double* AP = Dinv + 32 * 32;  // 32 x ld: rows P of A, columns R (compact index r)
   double* Cp = AP + 32 * ld;    // 32 x ld: D^{-1} A_PR
   double* A = gscratch ? gscratch : Cp + 32 * ld;
-  ESNMF_CHECK(k <= 256 && (size_t)(32 * 32 + 2 * 32 * ld + (gscratch ? 0 : k * k)) * 8 <= tc_dyn_smem());
+  ESNMF_CHECK(k <= 256 && (size_t)(32 * 32 + 2 * 32 * ld + (gscratch ? 0 : k * k)) * 8 <= dyn_smem_bytes());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   auto up = [k](int i, int j) -> int64_t { return i <= j ? (int64_t)i * k + j : (int64_t)j * k + i; };
   double tr = 0;

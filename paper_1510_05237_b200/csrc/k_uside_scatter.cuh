@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(256) k_uside_scatter_cols(const int64_t* __res
   const int c = blockIdx.y;
   const int64_t cb = vcolptr[c] + (int64_t)blockIdx.x * ndocs, ce = min(vcolptr[c + 1], cb + ndocs);
   if (cb >= ce) return;  // block-uniform
+  ESNMF_CHECK(c < kpad && (uint32_t)hh * 8u <= dyn_smem_bytes());
   for (int q = threadIdx.x; q < hh; q += blockDim.x) acc[q] = 0ull;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(256) k_uside_scatter_cols(const int64_t* __res
     for (int64_t q = s + lane; q < eh; q += 32) {  // head terms: shared accumulator
       const int2 en = atent[q];
       const unsigned long long add = __double2ull_rn((double)__int_as_float(en.y) * vs);
+      ESNMF_CHECK(headslot[en.x] >= 0 && headslot[en.x] < hh);
       if (add) atomicAdd(&acc[headslot[en.x]], add);
     }
     for (int64_t q = eh + lane; q < ee; q += 32) {  // tail terms: straight to Yq

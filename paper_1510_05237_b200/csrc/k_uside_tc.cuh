@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
               lo[j] = __float2half_rn(v - __half2float(hi[j]));
             }
             const uint32_t off = tc::kmajor_off16(r, c4, kk);
+            ESNMF_CHECK(r < kUtcM && off + 8 <= ahalf && (uint32_t)(sa - smem_raw) + 2 * ahalf <= dyn_smem_bytes());
             *reinterpret_cast<uint2*>(sa + off) = *reinterpret_cast<const uint2*>(hi);
             *reinterpret_cast<uint2*>(sa + ahalf + off) = *reinterpret_cast<const uint2*>(lo);
           }

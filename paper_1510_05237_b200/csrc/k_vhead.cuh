@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   }
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  ESNMF_CHECK((uint32_t)(base - smem_raw) + STAGES * head_stage_bytes(kn) <= tc::dyn_smem_bytes());
+  ESNMF_CHECK((uint32_t)(base - smem_raw) + STAGES * head_stage_bytes(kn) <= dyn_smem_bytes());
   const uint32_t zhalf = (uint32_t)kn * kHeadK * 2;
   const uint32_t zbytes = 2 * zhalf;
   const uint32_t stage_bytes = head_stage_bytes(kn);

@@ -19,13 +19,6 @@ namespace tc {
 
 ESNMF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// dynamic shared memory of the launch, bytes (bounds checks)
-ESNMF_DEV uint32_t dyn_smem_bytes() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
-  return r;
-}
-
 // tile byte offset of element (r, k) in the K-major no-swizzle layout above
 ESNMF_DEV uint32_t kmajor_off(int r, int k, int K) {
   return (uint32_t)((r >> 3) * (K / 4) * 128 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
