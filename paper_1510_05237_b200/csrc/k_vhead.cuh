@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       if (pq >= nchunks) {
         const int yq = pq - nchunks;
         tc::bulk_prefetch_l2(ytile + (size_t)pt * kHeadM * kn * 4 + (size_t)yq * kHeadABytes,
-                             (uint32_t)kHeadM * min(64, kn - 64 * yq) * 4u);
+                             (uint32_t)kHeadM * min(kHeadK, kn - kHeadK * yq) * 4u);
       } else if (pq < nd) {
         tc::bulk_prefetch_l2(atile + ((size_t)pt * nd + pq) * kHeadABytes, kHeadABytes);
       } else {
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
           uint8_t* st = base + stage * stage_bytes;
           const int yq = q - nchunks;
           if (q >= nchunks) {  // (Y_tail W) chunk: Y_tail tile chunk + W chunk
-            const uint32_t w = (uint32_t)min(64, kn - 64 * yq);
+            const uint32_t w = (uint32_t)min(kHeadK, kn - kHeadK * yq);
             const uint32_t ab = (uint32_t)kHeadM * w * 4u, bb = (uint32_t)kn * w * 4u;
             ESNMF_CHECK(ab <= kHeadABytes && bb <= zbytes);
             tc::mbar_arrive_expect_tx(&raw_full[stage], ab + bb);
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
               tc::mma_f16(d, dal + 16 * s, dzh + 16 * s, idesc, 1);
             }
           } else {  // (Y_tail W) chunk: K = w (its tiles are w wide)
-            const uint32_t w = (uint32_t)min(64, kn - 64 * (q - nchunks));
+            const uint32_t w = (uint32_t)min(kHeadK, kn - kHeadK * (q - nchunks));
             const uint32_t al = ah + (uint32_t)kHeadM * w * 2u, zh = ah + kHeadABytes, zl = zh + (uint32_t)kn * w * 2u;
             const uint32_t sbo = (w / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
             for (uint32_t s = 0; s < w / 16; ++s) {

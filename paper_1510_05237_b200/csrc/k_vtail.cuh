@@ -202,9 +202,13 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
 }
 
 // ---- Y_tail per tile, written as fp16 hi/lo K-major chunks ----
-// Chunk q of a tile covers Y columns [64 q, 64 q + w_q), w_q = min(64, kn - 64 q);
+// Chunk q of a tile covers Y columns [K q, K q + w_q), w_q = min(K, kn - K q), K = kHeadK;
 // it is stored as [hi: 128 x w_q fp16][lo: 128 x w_q fp16], K-major (tc.cuh),
-// at ytile + tile * 128 * kn * 4 + 64 q * 128 * 4.
+// at ytile + tile * 128 * kn * 4 + K q * 128 * 4.
+#ifndef ESNMF_HEAD_K
+#define ESNMF_HEAD_K 64
+#endif
+constexpr int kVtYChunk = ESNMF_HEAD_K;  // Y chunk width K: the head kernel's K per stage
 // ys: shared row stride in words (odd).  Tiles are taken from a global counter
 // (*next, zeroed before the launch): a CTA that starts late (an SM busy with the
 // solve on the other stream) simply takes fewer tiles.
@@ -281,13 +285,13 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
     const int np = kn / 2;
     for (int i = threadIdx.x; i < kVtM * np; i += T) {
       const int r = i / np, c = 2 * (i - r * np);
-      const int q = c >> 6, w = min(64, kn - 64 * q);
+      const int q = c / kVtYChunk, w = min(kVtYChunk, kn - kVtYChunk * q);
       const float y0 = (float)Ysm[r * ys + c] * 0x1p-15f;
       const float y1 = (float)Ysm[r * ys + c + 1] * 0x1p-15f;
       const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
       const __half l0 = __float2half_rn(y0 - __half2float(h0)), l1 = __float2half_rn(y1 - __half2float(h1));
-      uint8_t* cb = tbase + (size_t)64 * q * kVtM * 4;
-      const uint32_t off = tc::kmajor_off16(r, c - 64 * q, w);
+      uint8_t* cb = tbase + (size_t)kVtYChunk * q * kVtM * 4;
+      const uint32_t off = tc::kmajor_off16(r, c - kVtYChunk * q, w);
       *reinterpret_cast<uint32_t*>(cb + off) = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
       *reinterpret_cast<uint32_t*>(cb + (size_t)kVtM * w * 2 + off) =
           (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
