@@ -264,6 +264,35 @@ def test_without_transpose_input():
     assert s1.records() == s2.records()
 
 
+def test_device_transpose_row_lengths():
+    """A^T built on the device (k_transpose_chunks + the per-row sorts: the rank sort
+    sized to ceil(len / 32) entries per lane up to 512, the bitonic sort beyond) equals
+    the given A^T for documents of every length class: the runs match bit for bit."""
+    rng = np.random.default_rng(12)
+    n, m = 2000, 240
+    lens = [1, 2, 31, 32, 33, 64, 65, 96, 97, 128, 129, 160, 161, 192, 193, 256, 257, 511, 512, 513, 700, 1500]
+    docs = []
+    for j in range(m):
+        L = lens[j % len(lens)] if j < 3 * len(lens) else int(rng.integers(1, 300))
+        terms = np.sort(rng.choice(n, L, replace=False)).astype(np.int32)
+        docs.append((terms, rng.lognormal(0.0, 1.0, L).astype(np.float32)))
+    at_ptr = np.cumsum([0] + [len(t) for t, _ in docs]).astype(np.int64)
+    at_col = np.concatenate([t for t, _ in docs]).astype(np.int32)
+    at_val = np.concatenate([v for _, v in docs]).astype(np.float32)
+    doc_of = np.repeat(np.arange(m, dtype=np.int32), np.diff(at_ptr))
+    order = np.lexsort((doc_of, at_col))  # by term, then document
+    a_ptr = np.concatenate([[0], np.cumsum(np.bincount(at_col, minlength=n))]).astype(np.int64)
+    a_col, a_val = doc_of[order].astype(np.int32), at_val[order]
+    inp = dict(a_ptr=a_ptr, a_col=a_col, a_val=a_val, at_ptr=at_ptr, at_col=at_col, at_val=at_val)
+    s1 = ESNMF(n, m, 5, 40, inp, use_at=False, seed=2)
+    s2 = ESNMF(n, m, 5, 40, inp, seed=2)
+    s1.iterate(3)
+    s2.iterate(3)
+    assert s1.records() == s2.records()
+    for a, b in zip(s1.get_V() + s1.get_U(), s2.get_V() + s2.get_U()):
+        assert np.array_equal(a, b)
+
+
 def test_planted_fixed_point_on_gpu():
     rng = np.random.default_rng(4)
     n, m, k, t = 40, 30, 3, 6
