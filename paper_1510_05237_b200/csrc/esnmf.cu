@@ -1309,10 +1309,12 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     if (h->head_nd > 0) {
       const size_t ab = (size_t)h->head_ntiles * h->head_nd * kHeadABytes;
       h->atile = h->alloc<uint8_t>((int64_t)ab);
-      CK(cudaMemsetAsync(h->atile, 0, ab, h->stream));
+      const int smem = kHeadDenseG * (int)kHeadABytes;
+      CK(cudaFuncSetAttribute(k_head_dense_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       ++h->nlaunch;
-      k_head_dense<<<grid_for(sv.rows, 8, (int64_t)h->num_sms * 32), 256, 0, h->stream>>>(
-          sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nd, h->atile);
+      k_head_dense_tiles<<<dim3((unsigned)h->head_ntiles, (unsigned)ceil_div(h->head_nd, kHeadDenseG)), 512, smem,
+                           h->stream>>>(sv.T.ptr, h->nh, sv.T.ent, sv.rows, h->headslot, h->amax_bits, h->head_nd,
+                                        h->atile);
     }
   }
   // ... and the others as a tiled copy of their entries: one run per (tile, chunk)

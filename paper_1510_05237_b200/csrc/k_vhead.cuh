@@ -206,30 +206,47 @@ __global__ void k_vside_prep(const double* __restrict__ Z64, const int32_t* __re
   }
 }
 
-// dense A^T head tiles for the first nd chunks (the densest slots, where a run
-// would hold more entries than a stage can stage); warp per document
-__global__ void k_head_dense(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nh,
-                             const int2* __restrict__ ent, int64_t rows, const int32_t* __restrict__ headslot,
-                             const unsigned* __restrict__ amax_bits, int nd, uint8_t* __restrict__ atile) {
+// Dense A^T head tiles for the first nd chunks (the densest slots, where a run
+// would hold more entries than a stage can stage), built per (tile, group of
+// kHeadDenseG chunks) in shared memory and written out whole (coalesced, no memset
+// of the tiles first): 16 warps, a warp per document row of the tile scatters the
+// row's entries of the group's chunks (distinct terms: distinct cells), then the
+// block copies the tiles out.
+constexpr int kHeadDenseG = 4;
+__global__ void __launch_bounds__(512) k_head_dense_tiles(const int64_t* __restrict__ ptr,
+                                                          const int32_t* __restrict__ nh,
+                                                          const int2* __restrict__ ent, int64_t rows,
+                                                          const int32_t* __restrict__ headslot,
+                                                          const unsigned* __restrict__ amax_bits, int nd,
+                                                          uint8_t* __restrict__ atile) {
+  extern __shared__ __align__(16) uint8_t dt[];  // [kHeadDenseG][kHeadABytes]
+  const int64_t tile = blockIdx.x;
+  const int g0 = blockIdx.y * kHeadDenseG, ng = min(kHeadDenseG, nd - g0);
   const int eA = head_exp(__uint_as_float(*amax_bits));
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-    const int64_t s = ptr[row], e = s + nh[row], tile = row / kHeadM;
-    const int r = (int)(row % kHeadM);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < ng * (int)(kHeadABytes / 16); i += blockDim.x)
+    reinterpret_cast<uint4*>(dt)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  for (int r = warp; r < kHeadM; r += nw) {
+    const int64_t row = tile * kHeadM + r;
+    if (row >= rows) break;  // warp-uniform
+    const int64_t s = ptr[row], e = s + nh[row];
     for (int64_t q = s + lane; q < e; q += 32) {
       const int2 en = ent[q];
-      const int sl = headslot[en.x];
-      if (sl >= nd * kHeadK) continue;
+      const int sl = headslot[en.x], ch = sl / kHeadK - g0;
+      if (ch < 0 || ch >= ng) continue;
       const float a = ldexpf(__int_as_float(en.y), eA);
       const __half hi = __float2half_rn(a);
       const __half lo = __float2half_rn(a - __half2float(hi));
-      uint8_t* b = atile + ((size_t)tile * nd + sl / kHeadK) * kHeadABytes;
+      uint8_t* b = dt + (size_t)ch * kHeadABytes;
       const uint32_t off = tc::kmajor_off16(r, sl % kHeadK, kHeadK);
       *reinterpret_cast<__half*>(b + off) = hi;
       *reinterpret_cast<__half*>(b + kHeadAHalf + off) = lo;
     }
   }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(atile + ((size_t)tile * nd + g0) * kHeadABytes);
+  for (int i = threadIdx.x; i < ng * (int)(kHeadABytes / 16); i += blockDim.x) dst[i] = reinterpret_cast<uint4*>(dt)[i];
 }
 
 // per (tile, chunk) counts of head entries (warp per document; head entries
