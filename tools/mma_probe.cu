@@ -260,6 +260,7 @@ void run_rot() {
 
 int main() {
   run<112, 0>(148); run<112, 1>(148); run<128, 0>(148); run<64, 0>(148); run<256, 0>(148); run<208, 0>(148);
+  run<104, 0>(148); run<96, 0>(148); run<88, 0>(148); run<80, 0>(148); run<120, 0>(148);
   run<112, 0>(1);
   uint8_t* g;
   cudaMalloc(&g, 64 << 20);
