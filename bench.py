@@ -448,7 +448,7 @@ def run_ours(args):
         del g
         torch.cuda.empty_cache()
         times, d2h = [], 0
-        for _ in range(2):
+        for _ in range(3):  # best of 3: the first job also maps the library pool's pages
             torch.cuda.synchronize()
             barrier(world)
             t0 = time.perf_counter()
@@ -466,7 +466,7 @@ def run_ours(args):
         e2e = {"value": round(cfg.iters / best, 3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / cfg.iters), "d2h_bytes_per_step": int(d2h / cfg.iters),
                "job": f"esnmf_create(host CSR(A), A^T built on device) + esnmf_iterate({cfg.iters}) + records + "
-                      f"get_U + get_V; best of 2 jobs, {best:.3f} s",
+                      f"get_U + get_V; best of 3 jobs, {best:.3f} s",
                "unit_note": "iterations/s of the whole job; bytes per step = job bytes / iterations"}
     else:
         del g
