@@ -112,10 +112,12 @@ def cholesky(G: np.ndarray, rho: float = RHO_DEFAULT):
     return L, eps.value
 
 
-def solve_rows(L: np.ndarray, Y: np.ndarray) -> np.ndarray:
-    """X = Y (L L^T)^{-1}, row by row (two triangular solves)."""
+def solve_rows(L: np.ndarray, Y: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+    """X = Y (L L^T)^{-1}, row by row (two triangular solves).  out=Y solves in
+    place (each row's solve reads y_i before it writes x_i: or_solve_row)."""
     Y = _c(Y, np.float64)
-    X = np.empty_like(Y)
+    X = np.empty_like(Y) if out is None else out
+    assert X.shape == Y.shape and X.dtype == np.float64 and X.flags.c_contiguous
     _lib().or_solve_rows(Y.shape[0], Y.shape[1], _p(_c(L, np.float64)), _p(Y), _p(X))
     return X
 
@@ -146,12 +148,16 @@ def spmm_rows(sel, ptr, idx, val, F: np.ndarray) -> np.ndarray:
     return Y
 
 
-def clamp_top_t(X: np.ndarray, t: int | None, whole: bool = False):
+def clamp_top_t(X: np.ndarray, t: int | None, whole: bool = False, inplace: bool = False):
     """Projection + enforcement (P:63 clamp; P:134,146 keep t largest).
     whole=False: per column (C4 ties -> lower row); returns (X', kept per column).
     whole=True: of the whole matrix, Alg. 2 as printed (C17 ties ->
-    lower column, then row); returns (X', [kept total])."""
-    X = np.array(X, dtype=np.float64, order="C", copy=True)
+    lower column, then row); returns (X', [kept total]).  inplace=True overwrites
+    X (fp64, C order) instead of a copy."""
+    if inplace:
+        assert X.dtype == np.float64 and X.flags.c_contiguous
+    else:
+        X = np.array(X, dtype=np.float64, order="C", copy=True)
     rows, k = X.shape
     if whole:
         kept = np.empty(1, np.int64)
@@ -185,18 +191,27 @@ def frob2(val) -> float:
 
 # ------------------------------------------------------------------ the method
 
-def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFAULT, whole: bool = False) -> dict:
+def half_step(ptr, idx, val, F: np.ndarray, t: int | None, rho: float = RHO_DEFAULT, whole: bool = False,
+              lean: bool = False) -> dict:
     """One ALS half-step in the paper's order (P:133-134 for the V side with
     T = A^T and F = U; P:135-136 for the U side with T = A and F = V):
         G = F^T F; L L^T = G + eps I; Y = T F; LS = Y (G + eps I)^{-1};
         F' = keep_top_t_per_column(max(LS, 0)).
-    All dense fp64."""
+    All dense fp64.  peak = positives of LS (SPEC peak_nnz).  lean=True (memory
+    only, the same operations in the same order): LS overwrites Y and F'
+    overwrites LS in one buffer; Y and LS are not returned (the Box golden,
+    whose 8M x 200 fp64 buffers would not fit three at a time)."""
     G = gram(F)
     L, eps = cholesky(G, rho)
     Y = spmm(ptr, idx, val, F)
+    if lean:
+        LS = solve_rows(L, Y, out=Y)
+        peak = int(np.count_nonzero(LS > 0))
+        Fn, kept = clamp_top_t(LS, t, whole, inplace=True)
+        return dict(G=G, eps=eps, L=L, Y=None, LS=None, F=Fn, kept=kept, peak=peak)
     LS = solve_rows(L, Y)
     Fn, kept = clamp_top_t(LS, t, whole)
-    return dict(G=G, eps=eps, L=L, Y=Y, LS=LS, F=Fn, kept=kept)
+    return dict(G=G, eps=eps, L=L, Y=Y, LS=LS, F=Fn, kept=kept, peak=int(np.count_nonzero(LS > 0)))
 
 
 _SAME = object()
@@ -204,21 +219,26 @@ _SAME = object()
 
 def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float = RHO_DEFAULT,
         U_init: np.ndarray | None = None, keep_states: bool = False, t_u=_SAME, t_v=_SAME,
-        whole: bool = False, init_nnz: int = 0) -> dict:
+        whole: bool = False, init_nnz: int = 0, lean: bool = False, on_record=None) -> dict:
     """Alg. 2 for ``iters`` iterations: per-column enforcement
     (BJ:5) or, whole=True, of the whole matrix (Alg. 2 as printed).
     t_u / t_v (default t; None = unlimited) are the separate budgets of P:124
     (U-only / V-only enforcement).  Returns the per-iteration records
     {it, R, E, nnz_u, nnz_v, dead_u, dead_v} (IterationRecord, S:226-229) and
-    the final dense U, V."""
+    the final dense U, V.  lean=True: the V side in one buffer (half_step lean)
+    and the previous V freed before the next V side -- memory only; on_record
+    is called with each record as it is made (long runs)."""
     tu = t if t_u is _SAME else t_u
     tv = t if t_v is _SAME else t_v
     n, m = inp["n"], inp["m"]
     U = (u0(n, k, seed, init_nnz) if U_init is None else U_init).astype(np.float64)
     normA2 = frob2(inp["a_val"])
     recs, states = [], []
+    V = hv = None
     for it in range(1, iters + 1):
-        hv = half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, tv, rho, whole)  # P:133-134
+        if lean:
+            V = hv = None  # freed before the next V side's buffer is made
+        hv = half_step(inp["at_ptr"], inp["at_col"], inp["at_val"], U, tv, rho, whole, lean)  # P:133-134
         V = hv["F"]
         hu = half_step(inp["a_ptr"], inp["a_col"], inp["a_val"], V, tu, rho, whole)     # P:135-136
         Un = hu["F"]
@@ -227,7 +247,9 @@ def run(inp: dict, k: int, t: int | None, iters: int, seed: int = 0, rho: float 
         E = error(Un, hu["Y"], GU, hu["G"], normA2)
         recs.append(dict(it=it, R=R, E=E, nnz_u=int(np.count_nonzero(Un)), nnz_v=int(np.count_nonzero(V)),
                          dead_u=int(np.sum(~Un.any(axis=0))), dead_v=int(np.sum(~V.any(axis=0))),
-                         peak_u=int(np.sum(hu["LS"] > 0)), peak_v=int(np.sum(hv["LS"] > 0))))
+                         peak_u=hu["peak"], peak_v=hv["peak"]))
+        if on_record is not None:
+            on_record(recs[-1])
         if keep_states:
             states.append(dict(U_prev=U, V=V, U=Un, LS_V=hv["LS"], LS_U=hu["LS"], G_U=hv["G"], G_V=hu["G"]))
         U = Un

@@ -166,6 +166,28 @@ def test_trajectory_matches_golden(tag, cfg):
     same_state_R(s, synth.generate(cfg), cfg)
 
 
+@pytest.mark.slow
+def test_box_trajectory_matches_golden():
+    """Box (BJ:10: 1M x 8M, 1.6B entries, k = 200, t = 5,000) at full size on one
+    GPU: E, R_1, nnz and dead columns of every iteration against the oracle's
+    trajectory from the same U_0 (tests/golden/traj_box.json, as many iterations
+    as the host oracle ran: ~5 min per iteration on 8 cores, the lean memory
+    mode), graph replays from the third iteration on like the bench."""
+    import torch
+
+    cfg = synth.CONFIGS["box"]
+    gold = golden("box")
+    assert gold["t"] == cfg.t and gold["k"] == cfg.k and gold["iters"] >= 3
+    gd = synth.generate_device(cfg)
+    s = solver(cfg, gd)
+    del gd
+    torch.cuda.empty_cache()
+    s.iterate(gold["iters"])
+    check_trajectory(s, gold)
+    s.close()
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("t", synth.SWEEP_T, ids=[str(t) for t in synth.SWEEP_T])
 def test_sweep_trajectory(t):
     gold = golden(f"sweep_t{'inf' if t is None else t}")

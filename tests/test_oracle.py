@@ -257,6 +257,33 @@ def test_oracle_run_matches_bruteforce(t):
             assert rec["nnz_u"] <= k * t and rec["nnz_v"] <= k * t
 
 
+@pytest.mark.parametrize("t", [None, 4])
+def test_oracle_lean_mode_is_the_same_run(t):
+    """run(lean=True) (the Box golden's memory mode: LS and the new factor
+    overwrite Y in place) makes the same records and factors as the plain run,
+    and on_record sees every record; pinned by the brute-force twin above."""
+    rng = np.random.default_rng(8)
+    n, m, k = 40, 30, 3
+    A = rand_sparse(rng, n, m, 0.25)
+    p, i, v = csr(A)
+    pt, it, vt = csr(A.T)
+    inp = dict(n=n, m=m, a_ptr=p, a_col=i, a_val=v, at_ptr=pt, at_col=it, at_val=vt)
+    seen = []
+    a = oracle.run(inp, k, t, 6, seed=3)
+    b = oracle.run(inp, k, t, 6, seed=3, lean=True, on_record=seen.append)
+    assert seen == b["records"]
+    # (or_gram sums its per-thread partials in arrival order: equal to rounding)
+    for F in ("U", "V"):
+        assert np.array_equal(a[F] != 0, b[F] != 0)
+        assert np.allclose(a[F], b[F], rtol=1e-12, atol=0)
+    for x, y in zip(a["records"], b["records"]):
+        assert {q: x[q] for q in x if q not in ("R", "E")} == {q: y[q] for q in y if q not in ("R", "E")}
+        assert x["R"] == pytest.approx(y["R"], rel=1e-12) and x["E"] == pytest.approx(y["E"], rel=1e-12)
+    U0 = oracle.u0(n, k, 3)
+    U, V, _ = bf.projected_als(A, U0, t, 6, 1e-10)
+    assert np.allclose(b["V"], V, rtol=1e-9, atol=1e-12 * np.abs(V).max())
+
+
 def test_oracle_tiny_config_records_sane():
     cfg = synth.CONFIGS["tiny"]
     g = synth.generate(cfg)
