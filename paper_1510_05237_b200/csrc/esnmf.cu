@@ -1246,7 +1246,10 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   if (hh < kHeadK && !h->ptail) return;
   Side& sv = h->side[ESNMF_SIDE_V];
   h->kn = (h->k + 15) / 16 * 16;
-  h->head_acc_cols = h->kn <= 32 ? 32 : h->kn <= 64 ? 64 : h->kn <= 128 ? 128 : 256;
+  {  // TMEM columns per accumulator (two): kn, or 2 kn when wide (head_wide)
+    const int cols = head_wide(h->kn) ? 2 * h->kn : h->kn;
+    h->head_acc_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
+  }
   h->head_h = (int)hh;
   h->head_nchunks = (int)(hh / kHeadK);
   h->head_ntiles = ceil_div(std::max<int64_t>(sv.rows, 1), kHeadM);

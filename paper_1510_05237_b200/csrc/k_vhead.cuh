@@ -327,6 +327,13 @@ constexpr int kHeadOtfThreads = kHeadProd + 32 + 32 + kHeadEpi;  // producers, M
 #endif
 constexpr int kHeadPf = ESNMF_HEAD_PF;                             // rounds of L2 prefetch ahead of the copies
 
+// wide accumulators (2 kn TMEM columns each, the a_hi z_lo part beside the rest):
+// 2 MMAs per K-step (tensor-core operand reads from shared memory: A_hi once)
+#ifndef ESNMF_HEAD_WIDE
+#define ESNMF_HEAD_WIDE 1
+#endif
+__host__ __device__ __forceinline__ bool head_wide(int kn) { return ESNMF_HEAD_WIDE && 2 * kn <= 256; }
+
 // stage = [A hi|lo 32 KB][Z chunk hi|lo][raw entries of the chunk's run]
 ESNMF_DEV uint32_t head_stage_bytes(int kn) {
   return (kHeadABytes + (uint32_t)kn * kHeadK * 4 + kHeadRawBytes + 1023u) & ~1023u;
@@ -348,7 +355,8 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 // [cbeg, cend) of its warp): X[c][row] = Xt[row][c] + colscale[c] * acc[row][c], and the
 // fused selection pass 1 (positive counts in cnt2, candidate keys to fz.pcand).
 template <bool FUSE>
-__device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, int cbeg, int cend, bool no_mma, int k,
+__device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t lo_off, int cbeg, int cend,
+                                              bool no_mma, int k,
                                               const float* __restrict__ colscale, int64_t rows, float* __restrict__ X,
                                               int64_t ldx, const float* __restrict__ Xt, int kpad, const SelFuse& fz,
                                               const uint32_t* s_pred, uint32_t (&cnt2)[4][8]) {
@@ -358,6 +366,13 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, int cbeg
     for (int c0 = cbeg + 16 * q; c0 < (FUSE ? min(cend, cbeg + 16 * q + 1) : cend); c0 += 16) {
       uint32_t v[16];
       tc::tmem_ld16(ta + (uint32_t)c0, v);
+      if (lo_off) {  // wide accumulator: columns [kn, 2 kn) hold the a_hi z_lo part
+        uint32_t v2[16];
+        tc::tmem_ld16(ta + lo_off + (uint32_t)c0, v2);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
+      }
       tc::tmem_wait_ld();
       if (no_mma) {  // no MMA wrote the accumulator (no head, tail staged in Xt)
 #pragma unroll
@@ -443,6 +458,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   const uint32_t zbytes = 2 * zhalf;
   const uint32_t stage_bytes = head_stage_bytes(kn);
   const uint32_t raw_off = kHeadABytes + zbytes;
+  const bool wide = head_wide(kn);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -596,6 +612,11 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   } else if (warp == kHeadMmaWarp) {
     if (lane == 0) {  // ---- MMA issuer ----
       const uint32_t idesc = tc::make_idesc_f16(kHeadM, kn);
+      // wide (2 kn <= 256): one MMA of A_hi against [Z_hi; Z_lo] (the lo block follows
+      // the hi block as row groups kn/8.. of one K-major operand) into columns
+      // [0, 2 kn), then A_lo Z_hi into [0, kn): 2 MMAs per K-step instead of 3, and
+      // A_hi is read from shared memory once
+      const uint32_t idesc_w = tc::make_idesc_f16(kHeadM, wide ? 2 * kn : kn);
       // head-chunk descriptors: everything but the 14-bit start address is fixed
       // (LBO = 128, SBO = (kHeadK / 8) * 128); the stage's addresses are added per round
       const uint64_t hdesc = tc::make_sdesc(0, 128, (kHeadK / 8) * 128);
@@ -615,8 +636,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
             const uint64_t dzh = dah + (kHeadABytes >> 4), dzl = dzh + (((uint32_t)kn * kHeadK * 2) >> 4);
 #pragma unroll
             for (uint32_t s = 0; s < kHeadK / 16; ++s) {
-              tc::mma_f16(d, dah + 16 * s, dzh + 16 * s, idesc, (q | s) != 0);
-              tc::mma_f16(d, dah + 16 * s, dzl + 16 * s, idesc, 1);
+              if (wide) {
+                tc::mma_f16(d, dah + 16 * s, dzh + 16 * s, idesc_w, (q | s) != 0);
+              } else {
+                tc::mma_f16(d, dah + 16 * s, dzh + 16 * s, idesc, (q | s) != 0);
+                tc::mma_f16(d, dah + 16 * s, dzl + 16 * s, idesc, 1);
+              }
               tc::mma_f16(d, dal + 16 * s, dzh + 16 * s, idesc, 1);
             }
           } else {  // (Y_tail W) chunk: K = w (its tiles are w wide)
@@ -627,8 +652,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
               const uint32_t o = s * 256;
               const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
               const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
-              tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
-              tc::mma_f16(d, dah, dzl, idesc, 1);
+              if (wide) {
+                tc::mma_f16(d, dah, dzh, idesc_w, (q | s) != 0);
+              } else {
+                tc::mma_f16(d, dah, dzh, idesc, (q | s) != 0);
+                tc::mma_f16(d, dah, dzl, idesc, 1);
+              }
               tc::mma_f16(d, dal, dzh, idesc, 1);
             }
           }
@@ -660,7 +689,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       HT_WAIT(&tfull[acc], aphase);
       tc::fence_after();
       head_epi_tile<FUSE>(tile * kHeadM + lg * 32 + lane, tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16),
-                          cbeg, cend, nchunks + nyc == 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
+                          wide ? (uint32_t)kn : 0u, cbeg, cend, nchunks + nyc == 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
       tc::fence_before();
       tc::mbar_arrive(&tempty[acc]);
       acc ^= 1;
