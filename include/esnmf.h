@@ -152,6 +152,13 @@ typedef struct {
      on the device at create (fp32, correctly rounded; A^T alike), before ||A|| and
      everything else; 0 (default) = A as given. */
   int32_t row_normalize;
+  /* The V side's pre-clamp least-squares buffer (esnmf_get_ls).  0 (default): when
+     the V side's selection runs from the candidates the head kernel's epilogue
+     collects (per-column top-t with a predicted threshold, one GPU), esnmf_iterate
+     writes the LS buffer only if some column's prediction failed (its exact path
+     reads it): 400 MB of stores per iteration at Large saved; esnmf_get_ls(V) then
+     fails with ESTATE.  1: every V side writes it.  esnmf_half_step always does. */
+  int32_t keep_ls;
 } esnmf_options;
 
 typedef struct {

@@ -132,6 +132,9 @@ struct Side {
   int pcap = 0;
   int32_t* npos = nullptr;        // [k] positives per column (fused V-side pass 1)
   bool fused = false;             // this half-step's pass 1 ran in the head epilogue
+  bool xdeferred = false;         // ... and the head did not write X (written only if a prediction fails)
+  bool ls_stored = true;          // X holds this side's last LS (esnmf_get_ls)
+  int* xneed = nullptr;           // [1] device: some column's prediction failed (gates the head re-run)
   // Gram of the factor this side reads, and its eps
   double* G = nullptr;
   double* eps = nullptr;
@@ -275,6 +278,8 @@ struct esnmf {
   int utc_kn = 0, utc_kk = 0;        // 0: k_uside_tc not used (kpad > 128)
   // V-side tensor-core head (k_vhead.cuh): h most frequent terms, dense fp16 hi/lo tiles
   int head_h = 0, head_nchunks = 0, kn = 0, head_acc_cols = 0;
+  bool keep_ls = false;   // esnmf_options.keep_ls: every V side writes its LS buffer
+  bool force_ls = false;  // esnmf_half_step in progress: write it
   int64_t head_ntiles = 0;
   int32_t* headterm = nullptr;   // [h] term of head slot s
   int32_t* headslot = nullptr;   // [n] head slot of term i, -1 if not in the head
@@ -1093,6 +1098,8 @@ __global__ void k_whole_rows(int32_t* __restrict__ idx, const int64_t* __restric
     idx[q] = (int32_t)((uint32_t)idx[q] % (uint32_t)ldx);  // k * ldx < 2^31: 32-bit division
 }
 
+void vhead_launch(esnmf_t* h, bool rerun);
+
 // V side after a fused head epilogue: select from the candidates, histogram
 // path only for the columns whose prediction failed
 void select_fused(esnmf_t* h, Side& sd, Factor& out) {
@@ -1104,6 +1111,12 @@ void select_fused(esnmf_t* h, Side& sd, Factor& out) {
   CK(cudaFuncSetAttribute(k_sel_pred_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPredSortSmem));
   k_sel_pred_sort<<<k, 1024, kPredSortSmem, h->stream>>>(sd.npos, t, sd.pcand, sd.pfill, sd.pcap, out.colptr, out.row,
                                                          out.val, done, sd.pred);
+  if (sd.xdeferred) {  // the head wrote no X: write it now if a column needs its exact path
+    sd.xdeferred = false;
+    ++h->nlaunch;
+    k_any_undone<<<1, 256, 0, h->stream>>>(done, k, sd.xneed);
+    vhead_launch(h, true);
+  }
   // failed columns: histogram, threshold, collect, final (done columns return at
   // once; 16 blocks per column loop over the chunks, so the usual all-done case costs
   // a few microseconds per launch instead of a full grid of empty blocks)
@@ -1154,12 +1167,25 @@ int head_stage_bytes_host(int kn) {
 }
 int head_stages(int kn) { return std::max(2, std::min(6, (220 * 1024) / head_stage_bytes_host(kn))); }
 
+// rerun: the gated second launch of select_fused (no fused pass, X written, all
+// CTAs return at once unless sv.xneed is set)
 template <int ST>
-void vhead_launch_st(esnmf_t* h) {
+void vhead_launch_st(esnmf_t* h, bool rerun) {
   Side& sv = h->side[ESNMF_SIDE_V];
   const int smem = ST * head_stage_bytes_host(h->kn) + 1024;
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, h->num_sms);
   ++h->nlaunch;
+  if (rerun) {
+    auto kern = k_vhead_otf<ST, false>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
+                                                     h->colscale, sv.rows, h->head_ntiles, h->head_nchunks, h->k,
+                                                     h->kn, h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad, SelFuse{},
+                                                     h->ytile, h->wbuf, h->ptail ? h->nyc : 0,
+                                                     h->ptail ? h->flags + 4 : nullptr, 1, sv.xneed);
+    CKL("vhead_rerun");
+    return;
+  }
   // selection pass 1 in the epilogue (k_sel_pred_sort) when the V side takes the
   // predicted-threshold path: per-column top-t, t <= kSelFastT, one GPU.  Round 1
   // measured it slower (+0.14 ms on the head for ~0.1 ms saved); since the head's
@@ -1178,6 +1204,9 @@ void vhead_launch_st(esnmf_t* h) {
     CK(cudaMemsetAsync(sv.npos, 0, sizeof(int32_t) * h->k, h->stream));
     fz = SelFuse{sv.pred, sv.npos, sv.pcand, sv.pfill, sv.pcap, sv.row0};
   }
+  // the LS buffer is written later, and only if needed (esnmf_options.keep_ls)
+  sv.xdeferred = sv.fused && !h->keep_ls && !h->force_ls;
+  sv.ls_stored = !sv.xdeferred;
   auto kern = sv.fused ? k_vhead_otf<ST, true> : k_vhead_otf<ST, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, kHeadOtfThreads, smem, h->stream>>>(h->atile, h->head_nd, h->hoff, h->hseg, h->amax_bits, h->zhead,
@@ -1185,17 +1214,17 @@ void vhead_launch_st(esnmf_t* h) {
                                                    sv.rows, h->head_ntiles, h->head_nchunks, h->k, h->kn,
                                                    h->head_acc_cols, sv.X, sv.ldx, sv.Xt, h->kpad,
                                                    fz, h->ytile, h->wbuf, h->ptail ? h->nyc : 0,
-                                                   h->ptail ? h->flags + 4 : nullptr);
+                                                   h->ptail ? h->flags + 4 : nullptr, sv.xdeferred ? 0 : 1, nullptr);
   CKL("vhead");
 }
 
-void vhead_launch(esnmf_t* h) {
+void vhead_launch(esnmf_t* h, bool rerun) {
   switch (head_stages(h->kn)) {
-    case 2: vhead_launch_st<2>(h); break;
-    case 3: vhead_launch_st<3>(h); break;
-    case 4: vhead_launch_st<4>(h); break;
-    case 5: vhead_launch_st<5>(h); break;
-    default: vhead_launch_st<6>(h); break;
+    case 2: vhead_launch_st<2>(h, rerun); break;
+    case 3: vhead_launch_st<3>(h, rerun); break;
+    case 4: vhead_launch_st<4>(h, rerun); break;
+    case 5: vhead_launch_st<5>(h, rerun); break;
+    default: vhead_launch_st<6>(h, rerun); break;
   }
 }
 
@@ -1261,6 +1290,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
   CK(cudaMemcpyAsync(h->headslot, slot.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
   h->zhead = h->alloc<uint8_t>(std::max<int64_t>(1, (int64_t)h->head_nchunks * h->kn * kHeadK * 4));
   sv.Xt = h->alloc<float>(std::max<int64_t>(sv.rows, 1) * h->kpad);  // (paper-order mode: the fallback's)
+  sv.xneed = h->alloc<int>(1);
   h->colscale = h->alloc<float>(h->kn);
   h->amax_bits = h->alloc<unsigned>(1);
   CK(cudaMemsetAsync(h->zhead, 0, std::max<size_t>(1, (size_t)h->head_nchunks * h->kn * kHeadK * 4), h->stream));
@@ -1451,7 +1481,7 @@ void ytail_launch(esnmf_t* h) {
   const size_t smem = ytail_smem(ys);
   CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(k_ytail, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  int per_sm = std::max(1, std::min(3, (int)((228 * 1024) / (smem + 1024))));
+  int per_sm = std::max(1, std::min(kVtMinB, (int)((228 * 1024) / (smem + 1024))));
   if (const char* e = getenv("ESNMF_YTAIL_PERSM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
   const unsigned grid = (unsigned)std::min<int64_t>(h->head_ntiles, (int64_t)h->num_sms * per_sm);
   CK(cudaMemsetAsync(h->vt_next, 0, sizeof(unsigned long long), h->stream));
@@ -1569,7 +1599,7 @@ Factor& half_step(esnmf_t* h, int s) {
       spmm(h, s, in.rowmap, h->flags + 4);
     }
     { Phase ph(h, kVFormZ); vside_prep(h, in); }
-    { Phase ph(h, kVHead); vhead_launch(h); }                             // a3 + a4 (head, tail x W)
+    { Phase ph(h, kVHead); vhead_launch(h, false); }                      // a3 + a4 (head, tail x W)
     if (getenv("ESNMF_DEBUG_VT")) {
       CK(cudaStreamSynchronize(h->stream));
       int fl[8];
@@ -1601,7 +1631,7 @@ Factor& half_step(esnmf_t* h, int s) {
   if (!(s == ESNMF_SIDE_V && h->ptail)) {
     if (s == ESNMF_SIDE_V) { Phase ph(h, p0 + 2); form_z(h, in); }   // Z = U W (V side only)
     { Phase ph(h, p0 + 3); spmm(h, s, in.rowmap); }                  // a3 (+a4 scale); V: tail terms
-    if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h); }  // V: head terms (TC)
+    if (s == ESNMF_SIDE_V && h->head_h > 0) { Phase ph(h, kVHead); vhead_launch(h, false); }  // V: head terms (TC)
   }
   seq_deflate(h, s);                                               // Alg. 3: Eq. (7) / (8)
   sd.ls_valid = true;
@@ -2188,6 +2218,7 @@ esnmf_status esnmf_options_init(esnmf_options* o) {
   o->seq_k2 = 0;
   o->seq_iters = 0;
   o->row_normalize = 0;
+  o->keep_ls = 0;
   return ESNMF_OK;
 }
 
@@ -2288,6 +2319,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
+    h->keep_ls = o.keep_ls != 0;
     h->k = o.seq_k2 ? o.seq_k2 : k;  // sequential ALS: the pipeline works on one block
     h->kpad = (h->k + 3) / 4 * 4;
     const int32_t kb = h->k;  // columns of the pipeline (k, or k2 in sequential mode)
@@ -2515,7 +2547,9 @@ esnmf_status esnmf_half_step(esnmf_t* h, int32_t side) {
   return guarded([&] {
     set_device(h);
     graph_reset(h);
+    h->force_ls = true;  // explicit half-steps always materialise the LS buffer
     half_step(h, side);
+    h->force_ls = false;
     join_metrics(h);
     if (h->u_prefork) join_from_aux(h, h->ev_ujoin);  // callers may read G_V / W next
   });
@@ -2704,6 +2738,9 @@ esnmf_status esnmf_get_ls(esnmf_t* h, int32_t side, int64_t* row0, int64_t* rows
   return guarded([&] {
     set_device(h);
     if (!sd.ls_valid) fail(ESNMF_ESTATE, "no half-step of this side has run");
+    if (!sd.ls_stored)
+      fail(ESNMF_ESTATE, "the V side's LS buffer was not written by esnmf_iterate (esnmf_options.keep_ls = 1, "
+                         "or esnmf_half_step)");
     sync_check(h);
     std::vector<float> buf((size_t)h->k * sd.ldx);
     CK(cudaMemcpy(buf.data(), sd.X, sizeof(float) * buf.size(), cudaMemcpyDeviceToHost));

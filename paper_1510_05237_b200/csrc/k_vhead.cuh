@@ -286,6 +286,15 @@ __global__ void k_head_fill(const int64_t* __restrict__ ptr, const int32_t* __re
   }
 }
 
+// *need = some column's predicted selection failed (done[c] == 0): the deferred
+// LS buffer must be written after all (the gated head re-run)
+__global__ void k_any_undone(const int32_t* __restrict__ done, int k, int* __restrict__ need) {
+  int any = 0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) any |= done[c] == 0;
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) *need = any;
+}
+
 // fused V-side selection pass 1 (k_sel_pred_sort): pred == nullptr = off
 struct SelFuse {
   const uint32_t* pred;  // [k] predicted threshold bits
@@ -312,6 +321,23 @@ struct SelFuse {
 #else
 #define HT_WAIT(bar, ph) tc::mbar_wait(bar, ph)
 #endif
+// waits off the critical path (the epilogue has a whole tile of slack) suspend
+// instead of polling; ESNMF_HEAD_SLEEP_ALL=1 makes every role's wait suspend
+#ifndef ESNMF_HEAD_SLEEP_NS
+#define ESNMF_HEAD_SLEEP_NS 20000
+#endif
+#ifndef ESNMF_HEAD_SLEEP_ALL
+#define ESNMF_HEAD_SLEEP_ALL 0
+#endif
+#if ESNMF_HEAD_EXP == 3
+#define HT_WAIT_SLOW(bar, ph) HT_WAIT(bar, ph)
+#else
+#define HT_WAIT_SLOW(bar, ph) tc::mbar_wait_sleep(bar, ph, ESNMF_HEAD_SLEEP_NS)
+#if ESNMF_HEAD_SLEEP_ALL
+#undef HT_WAIT
+#define HT_WAIT(bar, ph) tc::mbar_wait_sleep(bar, ph, ESNMF_HEAD_SLEEP_NS)
+#endif
+#endif
 #ifndef ESNMF_HEAD_PROD_WARPS
 #define ESNMF_HEAD_PROD_WARPS 4
 #endif
@@ -326,6 +352,27 @@ constexpr int kHeadOtfThreads = kHeadProd + 32 + 32 + kHeadEpi;  // producers, M
 #define ESNMF_HEAD_PF 6
 #endif
 constexpr int kHeadPf = ESNMF_HEAD_PF;                             // rounds of L2 prefetch ahead of the copies
+
+// one arrival per warp (after __syncwarp: the lanes' shared-memory writes and
+// fences are ordered before lane 0's arrive) instead of one per thread: 4 / 8
+// arrivals on the producers' and the epilogue's barriers instead of 128 / 256
+#ifndef ESNMF_HEAD_WARP_ARRIVE
+#define ESNMF_HEAD_WARP_ARRIVE 1
+#endif
+constexpr bool kHeadWarpArrive = ESNMF_HEAD_WARP_ARRIVE != 0;
+// -DESNMF_HEAD_SKIP=bits (timing experiments only, results wrong): 1 no sparse
+// build, 2 no dense A copies, 4 no MMAs, 8 no epilogue work, 16 no run copies
+#ifndef ESNMF_HEAD_SKIP
+#define ESNMF_HEAD_SKIP 0
+#endif
+ESNMF_DEV void head_arrive(uint64_t* bar) {
+  if (kHeadWarpArrive) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
+  } else {
+    tc::mbar_arrive(bar);
+  }
+}
 
 // wide accumulators (2 kn TMEM columns each, the a_hi z_lo part beside the rest):
 // 2 MMAs per K-step (tensor-core operand reads from shared memory: A_hi once)
@@ -356,7 +403,7 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 // fused selection pass 1 (positive counts in cnt2, candidate keys to fz.pcand).
 template <bool FUSE>
 __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t lo_off, int cbeg, int cend,
-                                              bool no_mma, int k,
+                                              bool no_mma, bool xstore, int k,
                                               const float* __restrict__ colscale, int64_t rows, float* __restrict__ X,
                                               int64_t ldx, const float* __restrict__ Xt, int kpad, const SelFuse& fz,
                                               const uint32_t* s_pred, uint32_t (&cnt2)[4][8]) {
@@ -365,6 +412,10 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
   for (int q = 0; q < (FUSE ? 4 : 1); ++q) {
     for (int c0 = cbeg + 16 * q; c0 < (FUSE ? min(cend, cbeg + 16 * q + 1) : cend); c0 += 16) {
       uint32_t v[16];
+      if (ESNMF_HEAD_SKIP & 64) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint((float)(j + c0) * 1e-30f);
+      } else {
       tc::tmem_ld16(ta + (uint32_t)c0, v);
       if (lo_off) {  // wide accumulator: columns [kn, 2 kn) hold the a_hi z_lo part
         uint32_t v2[16];
@@ -374,6 +425,7 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
         for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
       }
       tc::tmem_wait_ld();
+      }
       if (no_mma) {  // no MMA wrote the accumulator (no head, tail staged in Xt)
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0u;
@@ -392,7 +444,7 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
           const int c = c0 + j;
           x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
           ESNMF_CHECK(row < ldx);
-          if (c < k) X[(int64_t)c * ldx + row] = x[j];
+          if (c < k && xstore && !(ESNMF_HEAD_SKIP & 32)) X[(int64_t)c * ldx + row] = x[j];
         }
       } else {
 #pragma unroll
@@ -402,10 +454,10 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
         uint32_t cdm = 0;  // columns j with a candidate in this lane
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
+          if (!(ESNMF_HEAD_SKIP & 256)) cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
           cdm |= (uint32_t)(x[j] > 0.f && __float_as_uint(x[j]) >= s_pred[c0 + j]) << j;
         }
-        uint32_t wm = __reduce_or_sync(kFull, cdm);
+        uint32_t wm = (ESNMF_HEAD_SKIP & 128) ? 0u : __reduce_or_sync(kFull, cdm);
         while (wm) {  // usually one column, one lane
           const int j = __ffs(wm) - 1;
           wm &= wm - 1;
@@ -435,7 +487,10 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
                 const float* __restrict__ colscale, int64_t rows, int64_t ntiles, int nchunks, int k, int kn,
                 int acc_cols, float* __restrict__ X, int64_t ldx, const float* __restrict__ Xt, int kpad,
                 SelFuse fz, const uint8_t* __restrict__ ytile, const uint8_t* __restrict__ wbuf, int nyc_arg,
-                const int* __restrict__ fallback) {
+                const int* __restrict__ fallback, int xstore, const int* __restrict__ gate) {
+  // gate (the re-run after a fused selection whose prediction failed for some
+  // column: the LS buffer is needed after all): nothing to do when *gate == 0
+  if (gate && *gate == 0) return;
   // paper-order tail mode, ill-conditioned W (fallback set): the Z-row gather
   // staged the tail rows in Xt this time -- no (Y_tail W) chunks
   const bool fb = fallback && *fallback;
@@ -463,12 +518,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&raw_full[s], 1);
-      tc::mbar_init(&a_full[s], kHeadProd);
+      tc::mbar_init(&a_full[s], kHeadWarpArrive ? kHeadProdWarps : kHeadProd);
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], kHeadEpi);
+      tc::mbar_init(&tempty[a], kHeadWarpArrive ? kHeadEpi / 32 : kHeadEpi);
     }
     tc::fence_mbar_init();
   }
@@ -543,8 +598,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
             tc::bulk_g2s(st + kHeadABytes, wbuf + (size_t)yq * zbytes, bb, &raw_full[stage]);
           } else {
             if (q < nd) {  // dense chunk: the A tile itself
+              if (ESNMF_HEAD_SKIP & 2) {
+                tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes);
+              } else {
               tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + kHeadABytes);
               tc::bulk_g2s(st, atile + ((size_t)tile * nd + q) * kHeadABytes, kHeadABytes, &raw_full[stage]);
+              }
             } else {         // sparse chunk: its run of entries
               const int64_t a = sb & ~(int64_t)1;  // 16-byte aligned start
               const int64_t b = min((int64_t)((se + 1) & ~(int64_t)1), a + (int64_t)kHeadRaw);  // even, capped
@@ -552,8 +611,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
               ESNMF_CHECK(rb <= kHeadRawBytes && raw_off + rb <= stage_bytes);
               s_run[stage][0] = sb;
               s_run[stage][1] = se;
+              if (ESNMF_HEAD_SKIP & 16) {
+                tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes);
+              } else {
               tc::mbar_arrive_expect_tx(&raw_full[stage], zbytes + rb);
               if (rb) tc::bulk_g2s(st + raw_off, hseg + a, rb, &raw_full[stage]);
+              }
             }
             tc::bulk_g2s(st + kHeadABytes, zbuf + (size_t)q * zbytes, zbytes, &raw_full[stage]);
           }
@@ -581,8 +644,8 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       for (int q = 0; q < nchunks + nyc; ++q) {
         uint8_t* sa = base + stage * stage_bytes;
         HT_WAIT(&raw_full[stage], phase);  // also: the MMAs of this stage's last round are done
-        if (q < nd || q >= nchunks) {  // dense or (Y_tail W) chunk: bulk-copied, nothing to build
-          tc::mbar_arrive(&a_full[stage]);
+        if (q < nd || q >= nchunks || (ESNMF_HEAD_SKIP & 1)) {  // dense or (Y_tail W) chunk: bulk-copied, nothing to build
+          head_arrive(&a_full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
         }
@@ -605,7 +668,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
         for (int64_t i = sb + p; i < se_s; i += kHeadProd) put(sa, raw[i - a]);
         for (int64_t i = cap + p; i < se; i += kHeadProd) put(sa, __ldcs(hseg + i));  // long runs only
         tc::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
-        tc::mbar_arrive(&a_full[stage]);
+        head_arrive(&a_full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -636,6 +699,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
             const uint64_t dzh = dah + (kHeadABytes >> 4), dzl = dzh + (((uint32_t)kn * kHeadK * 2) >> 4);
 #pragma unroll
             for (uint32_t s = 0; s < kHeadK / 16; ++s) {
+              if (ESNMF_HEAD_SKIP & 4) break;
               if (wide) {
                 tc::mma_f16(d, dah + 16 * s, dzh + 16 * s, idesc_w, (q | s) != 0);
               } else {
@@ -649,6 +713,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
             const uint32_t al = ah + (uint32_t)kHeadM * w * 2u, zh = ah + kHeadABytes, zl = zh + (uint32_t)kn * w * 2u;
             const uint32_t sbo = (w / 8) * 128;  // K-major, no swizzle: 8-row core-matrix groups
             for (uint32_t s = 0; s < w / 16; ++s) {
+              if (ESNMF_HEAD_SKIP & 4) break;
               const uint32_t o = s * 256;
               const uint64_t dah = tc::make_sdesc(ah + o, 128, sbo), dal = tc::make_sdesc(al + o, 128, sbo);
               const uint64_t dzh = tc::make_sdesc(zh + o, 128, sbo), dzl = tc::make_sdesc(zl + o, 128, sbo);
@@ -686,12 +751,13 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      HT_WAIT(&tfull[acc], aphase);
+      HT_WAIT_SLOW(&tfull[acc], aphase);
       tc::fence_after();
+      if (!(ESNMF_HEAD_SKIP & 8))
       head_epi_tile<FUSE>(tile * kHeadM + lg * 32 + lane, tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16),
-                          wide ? (uint32_t)kn : 0u, cbeg, cend, nchunks + nyc == 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
+                          wide ? (uint32_t)kn : 0u, cbeg, cend, nchunks + nyc == 0, xstore != 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
       tc::fence_before();
-      tc::mbar_arrive(&tempty[acc]);
+      head_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }

@@ -223,6 +223,11 @@ constexpr int kVtYChunk = ESNMF_HEAD_K;  // Y chunk width K: the head kernel's K
 #define ESNMF_VT_MINB 3
 #endif
 constexpr int kVtSub = ESNMF_VT_SUB;  // entries per thread per round (their loads in flight together)
+#ifndef ESNMF_VT_PRE
+#define ESNMF_VT_PRE 0
+#endif
+constexpr int kVtPre = ESNMF_VT_PRE > 0 ? ESNMF_VT_PRE : 1;  // U pairs per entry loaded up front
+constexpr int kVtMinB = ESNMF_VT_MINB;                      // resident CTAs per SM the launch asks for
 
 ESNMF_DEV void vt_add(uint32_t* yrow, float av, int2 p) {
   ESNMF_CHECK(p.x >= 0 && p.x < 256);
@@ -262,6 +267,45 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
         const bool act = base + (int64_t)u * T < e1 && ((__ldg(ubits + (term >> 5)) >> (term & 31)) & 1u);
         mp[u] = act ? umap[term] : 0ull;
       }
+#if ESNMF_VT_PRE > 0
+      // the first kVtPre pairs of every entry's U row loaded before any product
+      // (one round trip to L2 for most rows instead of one per two products)
+      int2 pr[kVtSub][kVtPre];
+#pragma unroll
+      for (int u = 0; u < kVtSub; ++u) {
+        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
+        const int2* up = uent + (mp[u] >> 32);
+#pragma unroll
+        for (int j = 0; j < kVtPre; ++j) pr[u][j] = j < cnt ? __ldg(up + j) : make_int2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kVtSub; ++u) {
+        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
+        ESNMF_CHECK(((uint32_t)en[u].x >> kVtTermBits) < (uint32_t)kVtM && cnt <= kn);
+        uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
+        const float av = __int_as_float(en[u].y);
+#pragma unroll
+        for (int j = 0; j < kVtPre; ++j)
+          if (j < cnt) vt_add(yrow, av, pr[u][j]);
+      }
+#pragma unroll
+      for (int u = 0; u < kVtSub; ++u) {
+        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
+        if (cnt <= kVtPre) continue;
+        const int2* up = uent + (mp[u] >> 32);
+        uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
+        const float av = __int_as_float(en[u].y);
+        int j = kVtPre;
+        for (; j + 4 <= cnt; j += 4) {
+          const int2 a = up[j], b = up[j + 1], c2 = up[j + 2], d = up[j + 3];
+          vt_add(yrow, av, a);
+          vt_add(yrow, av, b);
+          vt_add(yrow, av, c2);
+          vt_add(yrow, av, d);
+        }
+        for (; j < cnt; ++j) vt_add(yrow, av, up[j]);
+      }
+#else
 #pragma unroll
       for (int u = 0; u < kVtSub; ++u) {
         const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
@@ -277,6 +321,7 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
         }
         if (j < cnt) vt_add(yrow, av, up[j]);
       }
+#endif
     }
     __syncthreads();
     // convert: a thread takes two adjacent columns of one row (lanes on adjacent

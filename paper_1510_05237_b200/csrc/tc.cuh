@@ -95,6 +95,19 @@ ESNMF_DEV void mbar_wait(uint64_t* mbar, uint32_t phase) {
       : "memory");
 }
 
+// the same wait, but the warp may be suspended in hardware (up to `ns`
+// nanoseconds per try) until the phase completes instead of re-polling: waits
+// that are not latency-critical no longer take issue slots from the other warps
+// of their SM sub-partition (the head's epilogue spun ~220 times per tile)
+ESNMF_DEV void mbar_wait_sleep(uint64_t* mbar, uint32_t phase, uint32_t ns) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(mbar)),
+      "r"(phase), "r"(ns)
+      : "memory");
+}
+
 // 8 consecutive fp32 columns of this thread's TMEM lane (warp w: lanes 32(w%4)..)
 ESNMF_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];

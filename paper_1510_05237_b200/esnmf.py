@@ -38,7 +38,7 @@ class esnmf_options(ctypes.Structure):
         ("inputs_on_device", c_i32),
         ("at_row_ptr", c_p), ("at_col_idx", c_p), ("at_val", c_p), ("U0", c_p),
         ("head_terms", c_i32), ("t_u", c_i64), ("t_v", c_i64), ("enforce", c_i32), ("init_nnz", c_i64),
-        ("seq_k2", c_i32), ("seq_iters", c_i32), ("row_normalize", c_i32),
+        ("seq_k2", c_i32), ("seq_iters", c_i32), ("row_normalize", c_i32), ("keep_ls", c_i32),
     ]
 
 
@@ -345,12 +345,13 @@ class ESNMF:
     def __init__(self, n, m, k, t, inputs: dict, seed: int = 0, ridge_scale: float = 1e-10, stream=None,
                  device: int = -1, use_at: bool = True, U0=None, world: int = 1, rank: int = 0, comm=None,
                  head_terms: int = -1, t_u="same", t_v="same", whole: bool = False, init_nnz: int = 0,
-                 seq_k2: int = 0, seq_iters: int = 0, row_normalize: bool = False):
+                 seq_k2: int = 0, seq_iters: int = 0, row_normalize: bool = False, keep_ls: bool = False):
         """t_u / t_v: separate budgets ("same" = t, None = unlimited); whole: whole-factor
         enforcement (Alg. 2 as printed) instead of per column; init_nnz: sparse U_0
         (reading C18); seq_k2 > 0: sequential ALS (Alg. 3) in blocks of seq_k2 topics,
         seq_iters iterations per block; row_normalize: divide each row of A by its nnz
-        on the device."""
+        on the device; keep_ls: esnmf_iterate always writes the V side's LS buffer
+        (esnmf_get_ls after esnmf_iterate; esnmf_half_step always writes it)."""
         o = esnmf_options_init()
         o.head_terms = head_terms
         o.t_u = ESNMF_T_SAME if t_u == "same" else (ESNMF_T_UNLIMITED if t_u is None else int(t_u))
@@ -359,6 +360,7 @@ class ESNMF:
         o.init_nnz = int(init_nnz)
         o.seq_k2, o.seq_iters = int(seq_k2), int(seq_iters)
         o.row_normalize = 1 if row_normalize else 0
+        o.keep_ls = 1 if keep_ls else 0
         o.seed = seed
         o.ridge_scale = ridge_scale
         o.device = device

@@ -94,12 +94,39 @@ def test_head_deterministic():
     g = synth.generate(TINY)
     outs = []
     for _ in range(2):
-        s = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, head_terms=192)
+        s = ESNMF(TINY.n, TINY.m, TINY.k, TINY.t, g, seed=TINY.seed, head_terms=192, keep_ls=True)
         s.iterate(4)
         _, ls = s.get_ls(ESNMF_SIDE_V)
         outs.append((ls, s.get_U()))
     assert np.array_equal(outs[0][0], outs[1][0])
     for x, y in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(x, y)
+
+
+def test_deferred_ls_buffer_same_run(monkeypatch):
+    """esnmf_iterate without keep_ls: the head kernel's epilogue selects from its
+    candidates and writes no LS buffer; the buffer is written by a gated re-run of
+    the head only when a column's predicted threshold fails (iteration 1 always:
+    no prediction yet; graph replays later).  The run is bitwise the run that
+    writes the buffer every time, and esnmf_get_ls(V) refuses the stale buffer."""
+    monkeypatch.setenv("ESNMF_PRED_MIN_ROWS", "1")  # the predicted path at Medium's size
+    g = synth.generate(MEDIUM)
+    runs = []
+    for keep in (False, True):
+        s = ESNMF(MEDIUM.n, MEDIUM.m, MEDIUM.k, MEDIUM.t, g, seed=MEDIUM.seed, keep_ls=keep)
+        s.iterate(8)
+        if keep:
+            s.get_ls(ESNMF_SIDE_V)
+        else:
+            with pytest.raises(RuntimeError, match="keep_ls"):
+                s.get_ls(ESNMF_SIDE_V)
+        s.get_ls(ESNMF_SIDE_U)  # the U side's buffer is always written (E reads it)
+        runs.append((s.records(), s.get_U(), s.get_V()))
+        s.half_step(ESNMF_SIDE_V)  # explicit half-steps always write it
+        s.get_ls(ESNMF_SIDE_V)
+        s.close()
+    assert runs[0][0] == runs[1][0]
+    for x, y in zip(runs[0][1] + runs[0][2], runs[1][1] + runs[1][2]):
         assert np.array_equal(x, y)
 
 

@@ -421,7 +421,7 @@ def test_large_graph_replayed_full_parity():
     U7 = dense_U(s7, cfg.n, cfg.k)
     r7 = s7.records()
     s7.close()
-    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, gd, seed=cfg.seed)
+    s = ESNMF(cfg.n, cfg.m, cfg.k, cfg.t, gd, seed=cfg.seed, keep_ls=True)  # LS buffers written
     del gd
     torch.cuda.empty_cache()
     s.iterate(8)
