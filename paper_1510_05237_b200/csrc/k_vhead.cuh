@@ -404,7 +404,7 @@ ESNMF_DEV uint32_t head_stage_bytes(int kn) {
 template <bool FUSE>
 __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t lo_off, int cbeg, int cend,
                                               bool no_mma, bool xstore, int k,
-                                              const float* __restrict__ colscale, int64_t rows, float* __restrict__ X,
+                                              const float* s_cs, int64_t rows, float* __restrict__ X,
                                               int64_t ldx, const float* __restrict__ Xt, int kpad, const SelFuse& fz,
                                               const uint32_t* s_pred, uint32_t (&cnt2)[4][8]) {
   const int lane = threadIdx.x & 31;
@@ -431,31 +431,54 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
         for (int j = 0; j < 16; ++j) v[j] = 0u;
       }
       float x[16];
-      if (row < rows) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
+      const bool live = row < rows;
+      if (Xt && live) {  // X = tail part (row-major staging, k_spmm_tail<TROW>) + head part
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4) {
           const int c = c0 + 4 * v4;
-          const float4 t4 = (Xt && c < kpad) ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 t4 = c < kpad ? *reinterpret_cast<const float4*>(Xt + row * kpad + c)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
           x[4 * v4] = t4.x; x[4 * v4 + 1] = t4.y; x[4 * v4 + 2] = t4.z; x[4 * v4 + 3] = t4.w;
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = c0 + j;
-          x[j] = fmaf(__uint_as_float(v[j]), c < k ? colscale[c] : 0.f, x[j]);  // exact 2^-e
-          ESNMF_CHECK(row < ldx);
-          if (c < k && xstore && !(ESNMF_HEAD_SKIP & 32)) X[(int64_t)c * ldx + row] = x[j];
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = 0.f;
       }
+      {  // column scales from shared memory (0 for padding columns c >= k): exact 2^-e
+        const float4* cs4 = reinterpret_cast<const float4*>(s_cs + c0);
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          const float4 cs = cs4[v4];
+          x[4 * v4] = fmaf(__uint_as_float(v[4 * v4]), cs.x, x[4 * v4]);
+          x[4 * v4 + 1] = fmaf(__uint_as_float(v[4 * v4 + 1]), cs.y, x[4 * v4 + 1]);
+          x[4 * v4 + 2] = fmaf(__uint_as_float(v[4 * v4 + 2]), cs.z, x[4 * v4 + 2]);
+          x[4 * v4 + 3] = fmaf(__uint_as_float(v[4 * v4 + 3]), cs.w, x[4 * v4 + 3]);
+        }
+      }
+      if (!live) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = 0.f;
+      }
+      if (xstore && live && !(ESNMF_HEAD_SKIP & 32)) {
+        ESNMF_CHECK(row < ldx);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < k) X[(int64_t)(c0 + j) * ldx + row] = x[j];
+      }
       if (FUSE) {  // padding columns c >= k hold x = 0: never counted
         uint32_t cdm = 0;  // columns j with a candidate in this lane
+        const uint4* p4 = reinterpret_cast<const uint4*>(s_pred + c0);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (!(ESNMF_HEAD_SKIP & 256)) cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
-          cdm |= (uint32_t)(x[j] > 0.f && __float_as_uint(x[j]) >= s_pred[c0 + j]) << j;
+        for (int v4 = 0; v4 < 4; ++v4) {
+          const uint4 pr = p4[v4];
+          const uint32_t pj[4] = {pr.x, pr.y, pr.z, pr.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = 4 * v4 + i;
+            const bool pos = x[j] > 0.f;
+            if (!(ESNMF_HEAD_SKIP & 256)) cnt2[q][j >> 1] += (uint32_t)pos << (16 * (j & 1));
+            cdm |= (uint32_t)(pos && __float_as_uint(x[j]) >= pj[i]) << j;
+          }
         }
         uint32_t wm = (ESNMF_HEAD_SKIP & 128) ? 0u : __reduce_or_sync(kFull, cdm);
         while (wm) {  // usually one column, one lane
@@ -501,10 +524,12 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   __shared__ int64_t s_run[STAGES][2];  // sparse round: [sb, se) of its run (loader -> producers)
   __shared__ uint32_t tmem_base;
   __shared__ int s_npos[256];       // fused selection: positives per column counted by this CTA
-  __shared__ uint32_t s_pred[256];  // ... and the predicted thresholds (0xFFFFFFFF: none)
+  __shared__ __align__(16) uint32_t s_pred[256];  // ... and the predicted thresholds (0xFFFFFFFF: none)
+  __shared__ __align__(16) float s_cs[256];       // the epilogue's column scales (0: padding)
   for (int c = threadIdx.x; c < 256; c += blockDim.x) {
     s_npos[c] = 0;
     s_pred[c] = (FUSE && c < k) ? fz.pred[c] : 0xFFFFFFFFu;
+    s_cs[c] = c < k ? colscale[c] : 0.f;
   }
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -755,7 +780,7 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
       tc::fence_after();
       if (!(ESNMF_HEAD_SKIP & 8))
       head_epi_tile<FUSE>(tile * kHeadM + lg * 32 + lane, tmem + (uint32_t)(acc * acc_cols) + ((uint32_t)(lg * 32) << 16),
-                          wide ? (uint32_t)kn : 0u, cbeg, cend, nchunks + nyc == 0, xstore != 0, k, colscale, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
+                          wide ? (uint32_t)kn : 0u, cbeg, cend, nchunks + nyc == 0, xstore != 0, k, s_cs, rows, X, ldx, Xt, kpad, fz, s_pred, cnt2);
       tc::fence_before();
       head_arrive(&tempty[acc]);
       acc ^= 1;
