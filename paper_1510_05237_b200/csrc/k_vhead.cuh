@@ -475,9 +475,8 @@ __device__ __forceinline__ void head_epi_tile(int64_t row, uint32_t ta, uint32_t
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int j = 4 * v4 + i;
-            const bool pos = x[j] > 0.f;
-            if (!(ESNMF_HEAD_SKIP & 256)) cnt2[q][j >> 1] += (uint32_t)pos << (16 * (j & 1));
-            cdm |= (uint32_t)(pos && __float_as_uint(x[j]) >= pj[i]) << j;
+            if (!(ESNMF_HEAD_SKIP & 256)) cnt2[q][j >> 1] += (uint32_t)(x[j] > 0.f) << (16 * (j & 1));
+            cdm |= (uint32_t)(__float_as_int(x[j]) >= (int)pj[i]) << j;
           }
         }
         uint32_t wm = (ESNMF_HEAD_SKIP & 128) ? 0u : __reduce_or_sync(kFull, cdm);
@@ -528,7 +527,10 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   __shared__ __align__(16) float s_cs[256];       // the epilogue's column scales (0: padding)
   for (int c = threadIdx.x; c < 256; c += blockDim.x) {
     s_npos[c] = 0;
-    s_pred[c] = (FUSE && c < k) ? fz.pred[c] : 0xFFFFFFFFu;
+    // thresholds as signed bit patterns: a candidate is (int)bits(x) >= s_pred, which
+    // also excludes x <= 0 (threshold >= 1) and, with 0x7FFFFFFF, every finite x
+    const uint32_t pu = (FUSE && c < k) ? fz.pred[c] : 0xFFFFFFFFu;
+    s_pred[c] = pu == 0u ? 1u : (pu > 0x7F800000u ? 0x7FFFFFFFu : pu);
     s_cs[c] = c < k ? colscale[c] : 0.f;
   }
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
