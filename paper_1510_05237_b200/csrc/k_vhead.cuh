@@ -656,10 +656,13 @@ __global__ void __launch_bounds__(kHeadOtfThreads, 1)
   } else if (warp < kHeadProdWarps) {  // ---- producers: zero + scatter one tile chunk per stage ----
     const int p = threadIdx.x;
     const int eA = head_exp(__uint_as_float(*amax_bits));
+    // 2^eA as a float (a product by it rounds like ldexpf: both are correctly rounded)
+    const bool fastA = eA >= -126 && eA <= 127;
+    const float sA = fastA ? __int_as_float((127 + eA) << 23) : 1.f;
     int stage = 0;
     uint32_t phase = 0;
     auto put = [&](uint8_t* sa, int2 en) {
-      const float a = ldexpf(__int_as_float(en.y), eA);
+      const float a = fastA ? __int_as_float(en.y) * sA : ldexpf(__int_as_float(en.y), eA);
       const __half hi = __float2half_rn(a);
       const __half lo = __float2half_rn(a - __half2float(hi));
       ESNMF_CHECK((en.x >> 6) < kHeadM && (en.x & 63) < kHeadK);
