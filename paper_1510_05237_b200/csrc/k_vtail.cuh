@@ -228,6 +228,13 @@ constexpr int kVtSub = ESNMF_VT_SUB;  // entries per thread per round (their loa
 #endif
 constexpr int kVtPre = ESNMF_VT_PRE > 0 ? ESNMF_VT_PRE : 1;  // U pairs per entry loaded up front
 constexpr int kVtMinB = ESNMF_VT_MINB;                      // resident CTAs per SM the launch asks for
+#ifndef ESNMF_VT_NOBITS
+#define ESNMF_VT_NOBITS 0
+#endif
+#ifndef ESNMF_VT_PF
+#define ESNMF_VT_PF 1
+#endif
+constexpr bool kVtPf = ESNMF_VT_PF != 0;                     // L2 prefetch of the next tile's entries
 
 ESNMF_DEV void vt_add(uint32_t* yrow, float av, int2 p) {
   ESNMF_CHECK(p.x >= 0 && p.x < 256);
@@ -244,10 +251,26 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
                                                          const int* __restrict__ zpath) {
   if (zpath && *zpath) return;  // the cost model chose the Z-row gather this half-step
   extern __shared__ uint32_t Ysm[];
-  __shared__ int64_t s_tile;
+  __shared__ int64_t s_tile, s_next;
   const int T = blockDim.x;
+  // tiles are claimed one ahead: the next tile's entries are prefetched into L2
+  // (one bulk prefetch) while this one is processed, so the first link of the
+  // entry -> bitmap -> map -> pairs chain is an L2 hit instead of an HBM read
+  auto claim = [&]() -> int64_t {
+    const int64_t t = (int64_t)atomicAdd(next, 1ull);
+    if (kVtPf && t < ntiles) {
+      const int64_t a = toff[t] & ~(int64_t)1;  // 16-byte aligned, inside the array
+      const int64_t b = min((toff[t + 1] + 1) & ~(int64_t)1, toff[ntiles] & ~(int64_t)1);
+      if (b > a) tc::bulk_prefetch_l2(tent + a, (uint32_t)((b - a) * 8));
+    }
+    return t;
+  };
+  if (threadIdx.x == 0) s_next = claim();
   for (;;) {
-    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(next, 1ull);
+    if (threadIdx.x == 0) {
+      s_tile = s_next;
+      s_next = s_tile < ntiles ? claim() : ntiles;
+    }
     for (int i = threadIdx.x; i < kVtM * ys; i += T) Ysm[i] = 0u;
     __syncthreads();
     const int64_t tile = s_tile;
@@ -264,8 +287,12 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
 #pragma unroll
       for (int u = 0; u < kVtSub; ++u) {
         const uint32_t term = (uint32_t)en[u].x & kVtTermMask;
+#if ESNMF_VT_NOBITS
+        mp[u] = base + (int64_t)u * T < e1 ? umap[term] : 0ull;  // 0 for an inactive term
+#else
         const bool act = base + (int64_t)u * T < e1 && ((__ldg(ubits + (term >> 5)) >> (term & 31)) & 1u);
         mp[u] = act ? umap[term] : 0ull;
+#endif
       }
 #if ESNMF_VT_PRE > 0
       // the first kVtPre pairs of every entry's U row loaded before any product
