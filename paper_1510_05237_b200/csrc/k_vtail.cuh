@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
                                                          unsigned long long* __restrict__ next,
                                                          const int* __restrict__ zpath) {
   if (zpath && *zpath) return;  // the cost model chose the Z-row gather this half-step
-  extern __shared__ uint32_t Ysm[];
+  extern __shared__ __align__(16) uint32_t Ysm[];
   __shared__ int64_t s_tile, s_next;
   const int T = blockDim.x;
   // tiles are claimed one ahead: the next tile's entries are prefetched into L2
@@ -271,7 +271,12 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
       s_tile = s_next;
       s_next = s_tile < ntiles ? claim() : ntiles;
     }
-    for (int i = threadIdx.x; i < kVtM * ys; i += T) Ysm[i] = 0u;
+    {  // zero the Y tile, 16 bytes per store (the tile is 16-byte aligned, ys odd: its rows are not)
+      const int nz = kVtM * ys;
+      uint4* z4 = reinterpret_cast<uint4*>(Ysm);
+      for (int i = threadIdx.x; i < nz / 4; i += T) z4[i] = make_uint4(0u, 0u, 0u, 0u);
+      for (int i = (nz & ~3) + threadIdx.x; i < nz; i += T) Ysm[i] = 0u;
+    }
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
@@ -355,8 +360,12 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
     // pairs of a row: 2-way bank conflicts on the reads), writes 4 + 4 bytes
     uint8_t* tbase = ytile + (size_t)tile * kVtM * kn * 4;
     const int np = kn / 2;
-    for (int i = threadIdx.x; i < kVtM * np; i += T) {
-      const int r = i / np, c = 2 * (i - r * np);
+    // pair i = (row r, columns c, c + 1), i = r np + c / 2, stepped by T without a division per step
+    const int dr = T / np, dc = T - dr * np;
+    int r = threadIdx.x / np, cp = threadIdx.x - r * np;
+    for (; r < kVtM; r += dr, cp += dc) {
+      if (cp >= np) { cp -= np; ++r; if (r >= kVtM) break; }
+      const int c = 2 * cp;
       const int q = c / kVtYChunk, w = min(kVtYChunk, kn - kVtYChunk * q);
       const float y0 = (float)Ysm[r * ys + c] * 0x1p-15f;
       const float y1 = (float)Ysm[r * ys + c + 1] * 0x1p-15f;
