@@ -1496,7 +1496,7 @@ void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val)
   if (!h->ptail || (h->ktot && h->seq_b > 0) || !h->polish) return;  // (Alg. 3 deflates later blocks' LS)
   Side& sv = h->side[ESNMF_SIDE_V];
   const int64_t per_col = h->tside[ESNMF_SIDE_V] < 0 ? sv.rows : std::min<int64_t>(h->tside[ESNMF_SIDE_V], sv.rows);
-  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 8), 4096)), h->k);
+  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 16), 4096)), h->k);  // 2 per warp
   ++h->nlaunch;
   k_polish_v<<<g, 256, 0, h->stream>>>(colptr, row, val, h->k, sv.row0, sv.T.ptr, sv.T.ent, h->ubits, h->Z64);
   CKL("polish_v");

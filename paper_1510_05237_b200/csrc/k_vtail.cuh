@@ -432,38 +432,49 @@ __global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dens
 // with Z = U W in fp64 (Z64, k_form_z64, term-indexed; a term whose row of U
 // is empty -- its bit in ubits clear -- contributes zero).  The selection chose the entries from the tensor-core values; this
 // pass makes the VALUES exact to fp32 rounding (BJ:5 "relative 1e-5 on factor
-// entries").  Grid (x, k): one warp per kept entry of column blockIdx.y, lanes
-// over the document's entries.
+// entries").  Grid (x, k): half a warp per kept entry of column blockIdx.y,
+// lanes over the document's entries.
+constexpr int kPolHalf = 16;  // lanes per kept entry (two entries per warp)
+constexpr int kPolIn = 10;    // document entries per lane in flight (16 x 10 >= a typical row)
 __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
                            float* __restrict__ val, int k, int64_t row0, const int64_t* __restrict__ ptr,
                            const int2* __restrict__ ent, const uint32_t* __restrict__ ubits,
                            const double* __restrict__ Z64) {
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.y;  // grid (x, k): the entries of column c, one warp each
+  const int lane = threadIdx.x & 31, hl = lane & (kPolHalf - 1), hw = lane / kPolHalf;
+  const int c = blockIdx.y;  // grid (x, k): the entries of column c, two per warp
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t cend = colptr[c + 1];
-  for (int64_t e = colptr[c] + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < cend; e += nw) {
-    const int64_t r = (int64_t)row[e] - row0;
-    const int64_t s1 = ptr[r + 1];
-    double acc = 0;
-    for (int64_t q0 = ptr[r] + lane; q0 < s1; q0 += 256) {  // 8 entries per lane in flight
-      int2 en[8];
-      bool act[8];
-      double z[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) en[u] = q0 + 32 * u < s1 ? __ldg(ent + q0 + 32 * u) : make_int2(0, 0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)  // the term's row of U is non-empty (U's bitmap, L1-resident)
-        act[u] = q0 + 32 * u < s1 && ((__ldg(ubits + ((uint32_t)en[u].x >> 5)) >> (en[u].x & 31)) & 1u);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) z[u] = act[u] ? __ldg(Z64 + (int64_t)en[u].x * k + c) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc = fma((double)__int_as_float(en[u].y), z[u], acc);
+  for (int64_t e0 = colptr[c] + 2 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e0 < cend;
+       e0 += 2 * nw) {  // warp-uniform
+    const int64_t e = e0 + hw;
+    const bool valid = e < cend;
+    int64_t s0 = 0, s1 = 0;
+    if (valid) {
+      const int64_t r = (int64_t)row[e] - row0;
+      s0 = ptr[r];
+      s1 = ptr[r + 1];
     }
-    acc = warp_sum(acc);
+    double acc = 0;
+    for (int64_t q0 = s0 + hl; q0 < s1; q0 += kPolHalf * kPolIn) {
+      int2 en[kPolIn];
+      bool act[kPolIn];
+      double z[kPolIn];
+#pragma unroll
+      for (int u = 0; u < kPolIn; ++u)
+        en[u] = q0 + kPolHalf * u < s1 ? __ldg(ent + q0 + kPolHalf * u) : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < kPolIn; ++u)  // the term's row of U is non-empty (U's bitmap, L1-resident)
+        act[u] = q0 + kPolHalf * u < s1 && ((__ldg(ubits + ((uint32_t)en[u].x >> 5)) >> (en[u].x & 31)) & 1u);
+#pragma unroll
+      for (int u = 0; u < kPolIn; ++u) z[u] = act[u] ? __ldg(Z64 + (int64_t)en[u].x * k + c) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kPolIn; ++u) acc = fma((double)__int_as_float(en[u].y), z[u], acc);
+    }
+#pragma unroll
+    for (int o = kPolHalf / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // within the half
     // an entry kept for a tensor-core LS value within rounding of zero keeps that
     // (positive) value: a factor holds no zeros or negatives (P:63 clamp)
-    if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
+    if (valid && hl == 0 && (float)acc > 0.f) val[e] = (float)acc;
   }
 }
 
