@@ -1506,7 +1506,7 @@ void polish_v(esnmf_t* h, const int64_t* colptr, const int32_t* row, float* val)
 void polish_u(esnmf_t* h, Factor& out) {
   if (h->sharded || !h->Yq || !h->polish || (h->ktot && h->seq_b > 0)) return;
   const int64_t per_col = h->tside[ESNMF_SIDE_U] < 0 ? h->n : std::min<int64_t>(h->tside[ESNMF_SIDE_U], h->n);
-  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 8), 4096)), h->k);
+  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(per_col, 16), 4096)), h->k);  // 2 per warp
   ++h->nlaunch;
   k_polish_u<<<g, 256, 0, h->stream>>>(out.colptr, out.row, out.val, h->k, h->kpad, h->Yq, h->rsum_max, h->vmax,
                                        h->W);

@@ -481,26 +481,39 @@ __global__ void k_polish_v(const int64_t* __restrict__ colptr, const int32_t* __
 // The kept entries of U recomputed exactly (one GPU): LS_ic = sum_j Y_ij W_jc
 // with Y = A V from the U side's exact fixed-point accumulator (Yq, k_uside_*:
 // Y_ij = Yq[i][j] * unit, unit = rowsum_max * max(V) * 2^-62) and W in fp64.
-// Grid (x, k): one warp per kept entry of column blockIdx.y, lanes over j.
+// Grid (x, k): half a warp per kept entry of column blockIdx.y, lanes over j
+// (4 loads per lane in flight).
 __global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __restrict__ row,
                            float* __restrict__ val, int k, int kpad, const unsigned long long* __restrict__ Yq,
                            const double* __restrict__ bound, const uint32_t* __restrict__ vmax,
                            const double* __restrict__ W) {
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.y;  // grid (x, k): the entries of column c, one warp each
+  const int lane = threadIdx.x & 31, hl = lane & (kPolHalf - 1), hw = lane / kPolHalf;
+  const int c = blockIdx.y;  // grid (x, k): the entries of column c, two per warp
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t cend = colptr[c + 1];
   const double unit = *bound * (double)__uint_as_float(*vmax) * 0x1p-62;
-  for (int64_t e = colptr[c] + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < cend; e += nw) {
-    const unsigned long long* yr = Yq + (int64_t)row[e] * kpad;
-    const double* wr = W + (int64_t)c * k;  // W symmetric: column c = row c (coalesced)
+  const double* wr = W + (int64_t)c * k;  // W symmetric: column c = row c (coalesced)
+  for (int64_t e0 = colptr[c] + 2 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e0 < cend;
+       e0 += 2 * nw) {  // warp-uniform
+    const int64_t e = e0 + hw;
+    const bool valid = e < cend;
+    const unsigned long long* yr = Yq + (int64_t)(valid ? row[e] : 0) * kpad;
     double acc = 0;
-    for (int j = lane; j < k; j += 32) {
-      const unsigned long long y = __ldg(yr + j);
-      acc = fma((double)y * unit, __ldg(wr + j), acc);
+    for (int j0 = valid ? hl : k; j0 < k; j0 += 4 * kPolHalf) {
+      unsigned long long y[4];
+      double w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + kPolHalf * u;
+        y[u] = j < k ? __ldg(yr + j) : 0ull;
+        w[u] = j < k ? __ldg(wr + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma((double)y[u] * unit, w[u], acc);
     }
-    acc = warp_sum(acc);
-    if (lane == 0 && (float)acc > 0.f) val[e] = (float)acc;
+#pragma unroll
+    for (int o = kPolHalf / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // within the half
+    if (valid && hl == 0 && (float)acc > 0.f) val[e] = (float)acc;
   }
 }
 
