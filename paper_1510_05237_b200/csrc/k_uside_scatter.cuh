@@ -141,20 +141,46 @@ __global__ void __launch_bounds__(256) k_uside_scatter_cols(const int64_t* __res
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double B = *bound * (double)__uint_as_float(*vmax);
   const double S = B > 0 ? 0x1p62 / B : 0.0;
-  for (int64_t e = cb + warp; e < ce; e += blockDim.x >> 5) {
-    const int32_t doc = vrow[e];
-    const double vs = (double)vval[e] * S;
-    const int64_t s = atptr[doc], eh = s + nh[doc], ee = atptr[doc + 1];
-    for (int64_t q = s + lane; q < eh; q += 32) {  // head terms: shared accumulator
-      const int2 en = atent[q];
-      const unsigned long long add = __double2ull_rn((double)__int_as_float(en.y) * vs);
-      ESNMF_CHECK(headslot[en.x] >= 0 && headslot[en.x] < hh);
-      if (add) atomicAdd(&acc[headslot[en.x]], add);
+  // half a warp per entry of V (two documents per warp), 4 document entries per
+  // lane in flight: the chain entry -> document row -> A^T entries -> head slot
+  // is latency-bound, so more independent chains per warp
+  const int hl = lane & 15, hw = lane >> 4;
+  for (int64_t e0 = cb + 2 * warp; e0 < ce; e0 += 2 * (blockDim.x >> 5)) {  // warp-uniform
+    const int64_t e = e0 + hw;
+    int64_t s = 0, eh = 0, ee = 0;
+    double vs = 0;
+    if (e < ce) {
+      const int32_t doc = vrow[e];
+      vs = (double)vval[e] * S;
+      s = atptr[doc];
+      eh = s + nh[doc];
+      ee = atptr[doc + 1];
     }
-    for (int64_t q = eh + lane; q < ee; q += 32) {  // tail terms: straight to Yq
-      const int2 en = atent[q];
-      const unsigned long long add = __double2ull_rn((double)__int_as_float(en.y) * vs);
-      if (add) atomicAdd(&Yq[(int64_t)en.x * kpad + c], add);
+    for (int64_t q0 = s + hl; q0 < eh; q0 += 64) {  // head terms: shared accumulator
+      int2 en[4];
+      int sl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) en[u] = q0 + 16 * u < eh ? atent[q0 + 16 * u] : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sl[u] = q0 + 16 * u < eh ? headslot[en[u].x] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (sl[u] < 0) continue;
+        ESNMF_CHECK(sl[u] < hh);
+        const unsigned long long add = __double2ull_rn((double)__int_as_float(en[u].y) * vs);
+        if (add) atomicAdd(&acc[sl[u]], add);
+      }
+    }
+    for (int64_t q0 = eh + hl; q0 < ee; q0 += 64) {  // tail terms: straight to Yq
+      int2 en[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) en[u] = q0 + 16 * u < ee ? atent[q0 + 16 * u] : make_int2(-1, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (en[u].x < 0) continue;
+        const unsigned long long add = __double2ull_rn((double)__int_as_float(en[u].y) * vs);
+        if (add) atomicAdd(&Yq[(int64_t)en[u].x * kpad + c], add);
+      }
     }
   }
   __syncthreads();
