@@ -406,15 +406,18 @@ __global__ void __launch_bounds__(256) k_form_z64(const float* __restrict__ dens
 #pragma unroll
     for (int jl = 0; jl < CJ; ++jl) {
       const int lmax = min(32, k - 32 * jl);
-      for (int ll = 0; ll < lmax; ++ll) {
+      // the row's nonzeros only, in ascending l (the same sum as a loop over every l
+      // that skips zeros): most active rows of U hold a few entries
+      unsigned m = __ballot_sync(kFull, f[jl] != 0.f) & (lmax >= 32 ? ~0u : lmax <= 0 ? 0u : (1u << lmax) - 1u);
+      while (m) {
+        const int ll = __ffs(m) - 1;
+        m &= m - 1u;
         const float fl = __shfl_sync(kFull, f[jl], ll);
-        if (fl != 0.f) {
-          const double* Wl = W + (int64_t)(32 * jl + ll) * k;
+        const double* Wl = W + (int64_t)(32 * jl + ll) * k;
 #pragma unroll
-          for (int j = 0; j < CJ; ++j) {
-            const int c = lane + 32 * j;
-            if (c < k) acc[j] = fma((double)fl, Wl[c], acc[j]);
-          }
+        for (int j = 0; j < CJ; ++j) {
+          const int c = lane + 32 * j;
+          if (c < k) acc[j] = fma((double)fl, Wl[c], acc[j]);
         }
       }
     }
