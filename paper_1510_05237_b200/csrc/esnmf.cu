@@ -1593,12 +1593,17 @@ Factor& half_step(esnmf_t* h, int s) {
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
     if (!vser) join_from_aux(h, h->ev_vjoin);
     form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
+    // the Z-row gather (fallback only: its kernels return at once otherwise) on aux,
+    // beside the head's operand prep: its launches leave the critical path
+    if (!vser) fork_to_aux(h, h->ev_vfork);
     {
-      Phase ph(h, kVGather);  // the Z-row gather: fallback only (the kernels return at once otherwise)
+      OnStream os(h, vser ? h->stream : h->aux);
+      Phase ph(h, kVGather);
       form_z(h, in, h->flags + 4);
       spmm(h, s, in.rowmap, h->flags + 4);
     }
     { Phase ph(h, kVFormZ); vside_prep(h, in); }
+    if (!vser) join_from_aux(h, h->ev_vjoin);
     { Phase ph(h, kVHead); vhead_launch(h, false); }                      // a3 + a4 (head, tail x W)
     if (getenv("ESNMF_DEBUG_VT")) {
       CK(cudaStreamSynchronize(h->stream));

@@ -34,7 +34,10 @@
 namespace esk {
 
 constexpr int kVtM = 128;           // documents per tile (= the head kernel's MMA M)
-constexpr int kVtThreads = 512;     // k_ytail block
+#ifndef ESNMF_VT_THREADS
+#define ESNMF_VT_THREADS 512
+#endif
+constexpr int kVtThreads = ESNMF_VT_THREADS;  // k_ytail block
 constexpr int kVtTermBits = 24;     // term id bits of a packed tail entry (n < 2^24)
 constexpr uint32_t kVtTermMask = (1u << kVtTermBits) - 1u;
 
