@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
   __shared__ __align__(8) uint64_t wbar, afull[2], aempty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ float rscale[2][kUtcM];
+  __shared__ __align__(16) float s_ws[256];  // the epilogue's column scales (0: padding)
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) s_ws[c] = c < k ? wscale[c] : 0.f;
   uint8_t* base = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t wbytes = (uint32_t)kn * kk * 4;               // hi + lo
   const uint32_t abytes = (uint32_t)kUtcM * kk * 4;            // hi + lo
@@ -210,11 +212,21 @@ __global__ void __launch_bounds__(kUtcThreads, 1)
         uint32_t v[16];
         tc::tmem_ld16(ta + (uint32_t)c0, v);
         tc::tmem_wait_ld();
-        if (row < rows) {
+        if (row < rows) {  // exact powers of two: row scale, column scale (shared memory)
+          float ws[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int c = c0 + j;
-            if (c < k) X[(int64_t)c * ldx + row] = __uint_as_float(v[j]) * rs * wscale[c];  // exact powers of two
+          for (int v4 = 0; v4 < 4; ++v4) {
+            const float4 w4 = reinterpret_cast<const float4*>(s_ws + c0)[v4];
+            ws[4 * v4] = w4.x; ws[4 * v4 + 1] = w4.y; ws[4 * v4 + 2] = w4.z; ws[4 * v4 + 3] = w4.w;
+          }
+          float* xr = X + (int64_t)c0 * ldx + row;
+          if (c0 + 16 <= k) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xr[(int64_t)j * ldx] = __uint_as_float(v[j]) * rs * ws[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < k) xr[(int64_t)j * ldx] = __uint_as_float(v[j]) * rs * ws[j];
           }
         }
       }
