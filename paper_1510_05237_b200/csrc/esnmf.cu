@@ -320,6 +320,8 @@ struct esnmf {
   int* ushift = nullptr;         // [k] fixed-point exponents s_c
   uint32_t* gmax_buf = nullptr;  // multi-rank: allgather of {amax, rowsum} (16 B per rank)
   cudaEvent_t ev_vfork = nullptr, ev_vjoin = nullptr;
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;  // the record's Gram of U on aux
+  bool gram_on_aux = false;  // G_U was last computed on aux (a main-stream reader joins first)
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
   int num_sms = 148;
   int smem_optin = 227 * 1024;
@@ -406,7 +408,7 @@ struct esnmf {
       cudaMemPoolTrimTo(pool, (size_t)24 << 30);
     }
     if (aux) cudaStreamSynchronize(aux);
-    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin})
+    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin, ev_gfork, ev_gjoin})
       if (e) cudaEventDestroy(e);
     if (aux) cudaStreamDestroy(aux);
     if (maux) cudaStreamSynchronize(maux), cudaStreamDestroy(maux);
@@ -1561,6 +1563,11 @@ Factor& half_step(esnmf_t* h, int s) {
     h->v_since_u = false;
   }
   if (s == ESNMF_SIDE_V) h->v_since_u = true;
+  if (h->gram_on_aux) {  // G_U on aux: only the paper-order V side's solve (on aux) is ordered after it
+    const bool solve_on_aux = s == ESNMF_SIDE_V && h->ptail && !getenv("ESNMF_V_SERIAL");
+    if (!solve_on_aux) join_from_aux(h, h->ev_gjoin);
+    h->gram_on_aux = false;
+  }
   if (s == ESNMF_SIDE_V && h->ptail) {
     // paper-order tail (k_vtail.cuh): Y_tail = A^T_tail U needs only U, so the
     // Gram + solve (a1, a2) run on aux beside it; then Z_head = U_head W, the
@@ -1726,14 +1733,23 @@ void flush_metrics(esnmf_t* h) {
   double* p_new = h->red;
   double* p_old = p_new + 2 * (int64_t)gxn * k;
   double* p_tr = p_old + (int64_t)gxo * k;
-  // Gram of the new U first (the next V side's solve waits for it): S term of E, G_U
-  gram(h, Un, h->side[ESNMF_SIDE_V].G);
+  // Gram of the new U first (the next V side's solve waits for it): S term of E, G_U.
+  // On one GPU it runs on aux (ahead of that solve, beside the next V side's U row
+  // view on main) and the record's stream starts after it.
+  const bool overlap_m = !h->sharded;
+  if (overlap_m) {
+    fork_to(h, h->aux, h->ev_gfork);
+    OnStream og(h, h->aux);
+    gram(h, Un, h->side[ESNMF_SIDE_V].G);
+    fork_to(h, h->maux, h->ev_mfork);  // maux: after main's state (via aux) and the Gram
+    h->gram_on_aux = true;
+  } else {
+    gram(h, Un, h->side[ESNMF_SIDE_V].G);
+  }
   h->gramU_valid = true;
   // a8 error: T = tr(U^T (A V)) from the U side's LS rows.  On one GPU
   // the trace and the record run on the aux stream, beside the next V side
   // (joined before that V side replaces V, join_metrics).
-  const bool overlap_m = !h->sharded;
-  if (overlap_m) fork_to(h, h->maux, h->ev_mfork);
   OnStream os(h, overlap_m ? h->maux : h->stream);
   // (on the aux stream: U_{i-1} is overwritten only by the next U side, after the join)
   ++h->nlaunch; k_resid_new<<<dim3(gxn, k), 256, 0, h->stream>>>(Un.colptr, Un.row, Un.val, Uo.rowmap, Uo.dense, h->kpad, p_new);
@@ -2320,7 +2336,8 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, greatest));
       CK(cudaStreamCreateWithPriority(&h->maux, cudaStreamNonBlocking, least));
     }
-    for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin, &h->ev_vfork, &h->ev_vjoin})
+    for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin, &h->ev_vfork, &h->ev_vjoin,
+                           &h->ev_gfork, &h->ev_gjoin})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
