@@ -1547,6 +1547,23 @@ void yq_clear_other(esnmf_t* h) {
   h->yq_other_dirty = false;
 }
 
+// the V side's operands after the solve: Z = U W (fp64; the head's Z chunks and the
+// exact kept values), the Z-row gather (the paper-order tail's fallback: its kernels
+// return at once otherwise) and the head's operand prep
+// (gather_aux: the gather's launches on aux beside the prep)
+void vside_ops(esnmf_t* h, const Factor& in, bool gather_aux) {
+  form_z64(h, in);
+  if (gather_aux) fork_to_aux(h, h->ev_vfork);
+  {
+    OnStream os(h, gather_aux ? h->aux : h->stream);
+    Phase ph(h, kVGather);
+    form_z(h, in, h->flags + 4);
+    spmm(h, ESNMF_SIDE_V, in.rowmap, h->flags + 4);
+  }
+  { Phase ph(h, kVFormZ); vside_prep(h, in); }
+  if (gather_aux) join_from_aux(h, h->ev_vjoin);
+}
+
 // one half-step; returns the factor that was written
 Factor& half_step(esnmf_t* h, int s) {
   Side& sd = h->side[s];
@@ -1583,6 +1600,7 @@ Factor& half_step(esnmf_t* h, int s) {
       k_vt_choose<<<1, 1, 0, h->stream>>>(h->vcost, h->vt_ratio, h->flags + 5);
     }
     const bool vser = getenv("ESNMF_V_SERIAL") != nullptr;  // (measurement: the solve before the tail, one stream)
+    static const bool prep_aux = getenv("ESNMF_VPREP_MAIN") == nullptr;
     if (!vser) fork_to_aux(h, h->ev_vfork);
     {
       OnStream os(h, vser ? h->stream : h->aux);
@@ -1596,21 +1614,16 @@ Factor& half_step(esnmf_t* h, int s) {
         sc.orflag = h->flags + 5;
         sweep(h, sd.G, sd.eps, sc);
       }
+      // everything else the head needs depends on U and W only, so it follows the
+      // solve on aux beside the tail product instead of between the tail and the
+      // head: Z = U W (fp64; the head's Z chunks and the exact kept values), the
+      // Z-row gather (fallback only: its kernels return at once otherwise) and the
+      // head's operand prep
+      if (prep_aux) vside_ops(h, in, false);
     }
     { Phase ph(h, kVSpmm); ytail_launch(h); }                             // a3 (tail, paper order)
     if (!vser) join_from_aux(h, h->ev_vjoin);
-    form_z64(h, in);  // Z = U W (fp64): the head's Z chunks and the exact kept values
-    // the Z-row gather (fallback only: its kernels return at once otherwise) on aux,
-    // beside the head's operand prep: its launches leave the critical path
-    if (!vser) fork_to_aux(h, h->ev_vfork);
-    {
-      OnStream os(h, vser ? h->stream : h->aux);
-      Phase ph(h, kVGather);
-      form_z(h, in, h->flags + 4);
-      spmm(h, s, in.rowmap, h->flags + 4);
-    }
-    { Phase ph(h, kVFormZ); vside_prep(h, in); }
-    if (!vser) join_from_aux(h, h->ev_vjoin);
+    if (!prep_aux) vside_ops(h, in, !vser);
     { Phase ph(h, kVHead); vhead_launch(h, false); }                      // a3 + a4 (head, tail x W)
     if (getenv("ESNMF_DEBUG_VT")) {
       CK(cudaStreamSynchronize(h->stream));
