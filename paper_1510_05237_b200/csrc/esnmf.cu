@@ -320,6 +320,7 @@ struct esnmf {
   int* ushift = nullptr;         // [k] fixed-point exponents s_c
   uint32_t* gmax_buf = nullptr;  // multi-rank: allgather of {amax, rowsum} (16 B per rank)
   cudaEvent_t ev_vfork = nullptr, ev_vjoin = nullptr;
+  cudaEvent_t ev_ugram = nullptr;  // the U side's Gram done on aux (the scatter waits on it)
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;  // the record's Gram of U on aux
   bool gram_on_aux = false;  // G_U was last computed on aux (a main-stream reader joins first)
   int64_t u_rows_max = 0, v_rows_max = 0;  // largest shard over ranks
@@ -408,7 +409,8 @@ struct esnmf {
       cudaMemPoolTrimTo(pool, (size_t)24 << 30);
     }
     if (aux) cudaStreamSynchronize(aux);
-    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin, ev_gfork, ev_gjoin})
+    for (cudaEvent_t e : {ev_ufork, ev_ujoin, ev_mfork, ev_mjoin, ev_vfork, ev_vjoin, ev_gfork, ev_gjoin,
+                          ev_ugram})
       if (e) cudaEventDestroy(e);
     if (aux) cudaStreamDestroy(aux);
     if (maux) cudaStreamSynchronize(maux), cudaStreamDestroy(maux);
@@ -923,11 +925,14 @@ void spmm(esnmf_t* h, int s, const int32_t* rowmap, const int* gate = nullptr) {
 // ---- V row-CSR for the U side (k_spmm_terms.cuh) ----
 // the single-GPU U side with a head scatters by V's columns (k_uside_scatter_cols):
 // V's row-CSR is only needed by the row-driven scatter and the sharded term kernel.
-// It is built anyway (ESNMF_NO_VROWS=1 skips it): its ~0.04 ms is the gap in which
-// the U side's Gram + solve finish on the aux stream before the scatter needs them
-// (skipped: 2.12 -> 2.17 ms at Large, the U side then waits for the solve)
+// Without it the scatter waits on an event after the U side's Gram (on aux) instead:
+// launched beside the scatter's full grid, the one-CTA solve found no SM until the
+// scatter drained (2.12 -> 2.17 ms at Large when the row-CSR build was simply
+// skipped); released together, the solve's higher-priority CTA is placed first.
+// ESNMF_VROWS=1 builds the row-CSR anyway (the old ~0.04 ms gap, for measurement).
 bool need_vrows(esnmf_t* h) {
-  return h->sharded || h->head_h == 0 || getenv("ESNMF_SCATTER_ROWS") || !getenv("ESNMF_NO_VROWS");
+  static const bool force = getenv("ESNMF_VROWS") != nullptr;
+  return h->sharded || h->head_h == 0 || getenv("ESNMF_SCATTER_ROWS") || force;
 }
 
 void vrows_clear(esnmf_t* h) {
@@ -1683,6 +1688,7 @@ Factor& half_step(esnmf_t* h, int s) {
       OnStream os(h, h->aux);
       Side& su = h->side[ESNMF_SIDE_U];
       { Phase ph2(h, kUGram); gram(h, out, su.G); }
+      if (!need_vrows(h)) CK(cudaEventRecord(h->ev_ugram, h->stream));
       {
         Phase ph2(h, kUSolve);
         SweepCond sc;
@@ -1694,7 +1700,10 @@ Factor& half_step(esnmf_t* h, int s) {
       uside_w_prep(h);
       h->u_prefork = true;
     }
-    if (s == ESNMF_SIDE_V) vrows_build(h);
+    if (s == ESNMF_SIDE_V) {
+      vrows_build(h);
+      if (!h->sharded && !need_vrows(h)) CK(cudaStreamWaitEvent(h->stream, h->ev_ugram, 0));
+    }
   }
   if (s == ESNMF_SIDE_U) {
     h->ucur = 1 - h->ucur;
@@ -2350,7 +2359,7 @@ esnmf_status esnmf_create(esnmf_t** out, int64_t n, int64_t m, int32_t k, int64_
       CK(cudaStreamCreateWithPriority(&h->maux, cudaStreamNonBlocking, least));
     }
     for (cudaEvent_t* e : {&h->ev_ufork, &h->ev_ujoin, &h->ev_mfork, &h->ev_mjoin, &h->ev_vfork, &h->ev_vjoin,
-                           &h->ev_gfork, &h->ev_gjoin})
+                           &h->ev_gfork, &h->ev_gjoin, &h->ev_ugram})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     h->n = n;
     h->m = m;
