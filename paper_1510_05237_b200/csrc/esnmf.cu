@@ -306,7 +306,8 @@ struct esnmf {
   double vt_kmax = 1e4, vt_amax = 8.0;  // k_vcond_flag thresholds (ESNMF_VT_KMAX / ESNMF_VT_AMAX)
   double vt_ratio = 8.0;         // cost of a paper-order product / a gathered FMA (ESNMF_VT_RATIO)
   int32_t* termlen = nullptr;    // [n] stored entries of each term (row lengths of A, global)
-  double* vcost = nullptr;       // [8] the last V side's cost model (k_vt_cost)
+  double* vcost = nullptr;       // [8] the last V side's cost model (k_urows_finish)
+  unsigned* vt_ticket = nullptr; // [1] k_urows_finish's last-block ticket (zero between launches)
   bool polish = true;            // kept V values recomputed exactly (ESNMF_NO_POLISH=1: off)
   double u_kmax = 100.0;         // U side: (Y W) in fp32 / fp16 hi/lo only for kappa_inf <= this (ESNMF_U_KMAX)
   unsigned long long* vt_next = nullptr;  // k_ytail's tile counter
@@ -1449,6 +1450,8 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     }
     h->vcost = h->alloc<double>(8);
     CK(cudaMemsetAsync(h->vcost, 0, sizeof(double) * 8, h->stream));
+    h->vt_ticket = h->alloc<unsigned>(1);
+    CK(cudaMemsetAsync(h->vt_ticket, 0, sizeof(unsigned), h->stream));
     { const char* np_ = getenv("ESNMF_NO_POLISH"); h->polish = !(np_ && atoi(np_)); }
   }
   CKL("head_setup");
@@ -1461,7 +1464,8 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
 void urows_build(esnmf_t* h, const Factor& f) {
   const int64_t nr = f.cap_rows + 1;
   h->nlaunch += 1;
-  k_urows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(h->ulist, h->ulist_n, h->umap, h->ubits);
+  k_urows_clear<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(h->ulist, h->ulist_n, h->umap, h->ubits,
+                                                                        h->vcost);
   CK(cudaMemsetAsync(h->urptr, 0, sizeof(int64_t) * nr, h->stream));
   dim3 g(col_grid_x(f.maxcol), h->k);
   ++h->nlaunch;
@@ -1476,8 +1480,9 @@ void urows_build(esnmf_t* h, const Factor& f) {
   h->nlaunch += 3;
   k_urows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->head_h > 0 ? h->headslot : nullptr,
                                             h->ucursor, h->uent, h->umax);
-  k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(f.active, f.n_active, h->urptr, h->umap,
-                                                                         h->ubits, h->ulist, h->ulist_n);
+  k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(
+      f.active, f.n_active, h->urptr, h->umap, h->ubits, h->ulist, h->ulist_n, h->termlen,
+      h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost, h->vt_ticket, h->vt_ratio, h->flags + 5);
   k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(f.colptr + h->k, h->uent, h->k,
                                                                                    h->umax, h->rowsum_bits, h->ushift);
   CKL("urows_build");
@@ -1596,13 +1601,8 @@ Factor& half_step(esnmf_t* h, int s) {
     // scales, and the tensor-core kernel: head chunks + (Y_tail W) chunks
     {
       Phase ph(h, kVFormZ);
+      // + the cost model: paper order or Z-row gather for the tail this time
       urows_build(h, in);
-      // cost model: paper order or Z-row gather for the tail this time
-      CK(cudaMemsetAsync(h->vcost, 0, sizeof(double) * 8, h->stream));
-      h->nlaunch += 2;
-      k_vt_cost<<<grid_for(in.cap_rows, 256, (int64_t)h->num_sms * 2), 256, 0, h->stream>>>(
-          in.active, in.n_active, h->umap, h->termlen, h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost);
-      k_vt_choose<<<1, 1, 0, h->stream>>>(h->vcost, h->vt_ratio, h->flags + 5);
     }
     const bool vser = getenv("ESNMF_V_SERIAL") != nullptr;  // (measurement: the solve before the tail, one stream)
     static const bool prep_aux = getenv("ESNMF_VPREP_MAIN") == nullptr;

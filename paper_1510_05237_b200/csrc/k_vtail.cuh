@@ -140,23 +140,66 @@ __global__ void k_urows_scatter(const int64_t* __restrict__ colptr, const int32_
 }
 
 // publish umap[row] = (first << 32) | count for every active row of U; the rows
-// published are listed in ulist (for the next clear), their number in *ulist_n
+// published are listed in ulist (for the next clear), their number in *ulist_n.
+// The same pass sums the per-half-step cost model of the V-side tail
+// from the document frequencies of A (termlen[i] = stored entries of term i):
+//   cost[0] = sum over active tail rows i of termlen_i * r_i   (paper order: products, k_ytail)
+//   cost[1] = sum over active tail rows i of termlen_i * k     (reassociated: FMAs of the Z-row gather)
+//   cost[2] = sum over active tail rows i of termlen_i         (active tail entries of A^T)
+//   cost[3] = sum over active head rows of termlen_i * r_i     (head products, for the report)
+// (integer-valued fp64 sums: exact in any order; cost[] zeroed by k_urows_clear), and
+// its last block (a ticket, reset by that block) takes the product order of the
+// tail: Z-row gather (*zpath = 1) when the paper order's products outweigh the
+// gather's FMAs at the measured relative cost of one shared-memory fixed-point
+// product vs one gathered FMA (ratio).
 __global__ void k_urows_finish(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
                                const int64_t* __restrict__ rptr, uint64_t* __restrict__ umap,
                                uint32_t* __restrict__ ubits, int32_t* __restrict__ ulist,
-                               int64_t* __restrict__ ulist_n) {
+                               int64_t* __restrict__ ulist_n, const int32_t* __restrict__ termlen,
+                               const int32_t* __restrict__ headslot, int k, double* __restrict__ cost,
+                               unsigned* __restrict__ ticket, double ratio, int* __restrict__ zpath) {
+  __shared__ double sm[32];
+  __shared__ bool last;
   const int64_t na = *n_active;
   if (blockIdx.x == 0 && threadIdx.x == 0) *ulist_n = na;
+  double p = 0, z = 0, a = 0, hp = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = active[r];
-    umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)(rptr[r + 1] - rptr[r]);
+    const int64_t cnt = rptr[r + 1] - rptr[r];
+    umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)cnt;
     atomicOr(&ubits[i >> 5], 1u << (i & 31));
     ulist[r] = i;
+    const double len = (double)termlen[i];
+    if (headslot && headslot[i] >= 0) {
+      hp += len * (double)cnt;
+    } else {
+      p += len * (double)cnt;
+      z += len * k;
+      a += len;
+    }
+  }
+  p = block_sum(p, sm);
+  z = block_sum(z, sm);
+  a = block_sum(a, sm);
+  hp = block_sum(hp, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(&cost[0], p);
+    atomicAdd(&cost[1], z);
+    atomicAdd(&cost[2], a);
+    atomicAdd(&cost[3], hp);
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (last) {
+      __threadfence();
+      *zpath = __ldcg(cost) * ratio > __ldcg(cost + 1);
+      *ticket = 0u;
+    }
   }
 }
 
 __global__ void k_urows_clear(const int32_t* __restrict__ ulist, const int64_t* __restrict__ ulist_n,
-                              uint64_t* __restrict__ umap, uint32_t* __restrict__ ubits) {
+                              uint64_t* __restrict__ umap, uint32_t* __restrict__ ubits, double* __restrict__ cost) {
+  if (blockIdx.x == 0 && threadIdx.x < 8) cost[threadIdx.x] = 0.0;
   const int64_t na = *ulist_n;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = ulist[r];
@@ -521,49 +564,6 @@ __global__ void k_polish_u(const int64_t* __restrict__ colptr, const int32_t* __
     for (int o = kPolHalf / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // within the half
     if (valid && hl == 0 && (float)acc > 0.f) val[e] = (float)acc;
   }
-}
-
-// Per-half-step cost model of the V-side tail, from U's row view
-// and the document frequencies of A (termlen[i] = stored entries of term i):
-//   cost[0] = sum over active tail rows i of termlen_i * r_i   (paper order: products, k_ytail)
-//   cost[1] = sum over active tail rows i of termlen_i * k     (reassociated: FMAs of the Z-row gather)
-//   cost[2] = sum over active tail rows i of termlen_i         (active tail entries of A^T)
-//   cost[3] = sum over active head rows of termlen_i * r_i     (head products, for the report)
-// (integer-valued fp64 sums: exact in any order).  cost[] zeroed by the caller.
-__global__ void k_vt_cost(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
-                          const uint64_t* __restrict__ umap, const int32_t* __restrict__ termlen,
-                          const int32_t* __restrict__ headslot, int k, double* __restrict__ cost) {
-  __shared__ double sm[32];
-  const int64_t na = *n_active;
-  double p = 0, z = 0, a = 0, hp = 0;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t i = active[r];
-    const double len = (double)termlen[i], cnt = (double)(umap[i] & 0xFFFFFFFFull);
-    if (headslot && headslot[i] >= 0) {
-      hp += len * cnt;
-    } else {
-      p += len * cnt;
-      z += len * k;
-      a += len;
-    }
-  }
-  p = block_sum(p, sm);
-  z = block_sum(z, sm);
-  a = block_sum(a, sm);
-  hp = block_sum(hp, sm);
-  if (threadIdx.x == 0) {
-    atomicAdd(&cost[0], p);
-    atomicAdd(&cost[1], z);
-    atomicAdd(&cost[2], a);
-    atomicAdd(&cost[3], hp);
-  }
-}
-
-// the product order of the tail this half-step: Z-row gather (flag = 1) when the
-// paper order's products outweigh the gather's FMAs at the measured relative cost
-// of one smem fixed-point product vs one gathered FMA (ratio)
-__global__ void k_vt_choose(const double* __restrict__ cost, double ratio, int* __restrict__ zpath) {
-  *zpath = cost[0] * ratio > cost[1];
 }
 
 // U side's paper-order products for the current V: sum over V's entries (d, c) of
