@@ -1,5 +1,5 @@
 """Hot SASS lines of one kernel in an ncu report (needs -lineinfo / --import-source).
-usage: python tools_ncu_source.py REPORT BLOCK_INDEX [threshold]"""
+usage: python tools/ncu_source.py REPORT BLOCK_INDEX [threshold]"""
 import csv, subprocess, sys, io
 rep, blk = sys.argv[1], int(sys.argv[2])
 thr = float(sys.argv[3]) if len(sys.argv) > 3 else 0.004

@@ -19,7 +19,7 @@ line = open(os.path.join(OUT, "bench_default.log")).read().strip().splitlines()[
 json.loads(line)
 open(os.path.join(PROF, f"{tag}_bench_large.json"), "w").write(line + "\n")
 
-agg = subprocess.run([sys.executable, os.path.join(ROOT, "tools_launches.py"), os.path.join(OUT, "launches.csv")],
+agg = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launches.py"), os.path.join(OUT, "launches.csv")],
                      capture_output=True, text=True).stdout
 open(os.path.join(PROF, f"{tag}_launches_steady_large.txt"), "w").write(
     "# ncu --metrics gpu__time_duration.sum --clock-control none, steady state (Large), per kernel; ns\n" + agg)
