@@ -1428,7 +1428,7 @@ void head_setup(esnmf_t* h, const std::vector<int64_t>& hptr, int32_t want) {
     h->ubits = h->alloc<uint32_t>(ceil_div(n, 32));
     CK(cudaMemsetAsync(h->ubits, 0, sizeof(uint32_t) * ceil_div(n, 32), h->stream));
     h->vt_next = h->alloc<unsigned long long>(1);
-    h->uent = h->alloc<int2>(n * (int64_t)h->k);
+    h->uent = h->alloc<int2>(n * (int64_t)(h->k + 1));  // rows padded to an even length
     h->urptr = h->alloc<int64_t>(n + 1);
     h->ucursor = h->alloc<int64_t>(n + 1);
     h->uscan = h->alloc<int64_t>(ceil_div(n + 1, kScanBlock) + 1);
@@ -1472,18 +1472,20 @@ void urows_build(esnmf_t* h, const Factor& f) {
   k_vrows_count<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.rowmap, h->urptr);
   const int64_t nb = ceil_div(nr, kScanBlock);
   h->nlaunch += 3;
-  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan);
+  // rows at even offsets (counts rounded up to even): k_ytail loads two pairs at a time
+  k_blocksum_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan, 1);
   k_scan_small<<<1, 1024, 0, h->stream>>>(h->uscan, nb, h->uscan + nb);
-  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan);
+  k_scan_apply_i64<<<(unsigned)nb, 256, 0, h->stream>>>(h->urptr, nr, h->uscan, 1);
   CK(cudaMemcpyAsync(h->ucursor, h->urptr, sizeof(int64_t) * nr, cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemsetAsync(h->umax, 0, sizeof(uint32_t) * h->k, h->stream));
   h->nlaunch += 3;
   k_urows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->head_h > 0 ? h->headslot : nullptr,
                                             h->ucursor, h->uent, h->umax);
   k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(
-      f.active, f.n_active, h->urptr, h->umap, h->ubits, h->ulist, h->ulist_n, h->termlen,
+      f.active, f.n_active, h->urptr, h->ucursor, h->uent, h->umap, h->ubits, h->ulist, h->ulist_n, h->termlen,
       h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost, h->vt_ticket, h->vt_ratio, h->flags + 5);
-  k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(f.colptr + h->k, h->uent, h->k,
+  // (every slot up to the padded total, uscan[nb]: the pads are (0, 0))
+  k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->uscan + nb, h->uent, h->k,
                                                                                    h->umax, h->rowsum_bits, h->ushift);
   CKL("urows_build");
 }

@@ -20,20 +20,23 @@ __global__ void k_col_count(const int2* __restrict__ ent, int64_t nnz, int64_t* 
 
 constexpr int kScanBlock = 2048;
 
-__global__ void k_blocksum_i64(const int64_t* __restrict__ a, int64_t n, int64_t* __restrict__ bsum) {
+// (rmask = 1: every count rounded up to even first -- 16-byte aligned pair rows)
+__global__ void k_blocksum_i64(const int64_t* __restrict__ a, int64_t n, int64_t* __restrict__ bsum,
+                               int64_t rmask = 0) {
   __shared__ int64_t sm[32];
   int64_t s = 0;
   const int64_t base = blockIdx.x * (int64_t)kScanBlock;
   for (int q = threadIdx.x; q < kScanBlock; q += blockDim.x) {
     const int64_t i = base + q;
-    if (i < n) s += a[i];
+    if (i < n) s += (a[i] + rmask) & ~rmask;
   }
   s = block_sum(s, sm);
   if (threadIdx.x == 0) bsum[blockIdx.x] = s;
 }
 
 // in place exclusive scan of a[0..n) given exclusive block offsets; 256 threads x 8
-__global__ void k_scan_apply_i64(int64_t* __restrict__ a, int64_t n, const int64_t* __restrict__ boff) {
+__global__ void k_scan_apply_i64(int64_t* __restrict__ a, int64_t n, const int64_t* __restrict__ boff,
+                                 int64_t rmask = 0) {
   __shared__ int64_t sm[33];
   constexpr int per = kScanBlock / 256;
   const int64_t base = blockIdx.x * (int64_t)kScanBlock + threadIdx.x * per;
@@ -41,7 +44,7 @@ __global__ void k_scan_apply_i64(int64_t* __restrict__ a, int64_t n, const int64
   int64_t s = 0;
 #pragma unroll
   for (int q = 0; q < per; ++q) {
-    v[q] = base + q < n ? a[base + q] : 0;
+    v[q] = base + q < n ? (a[base + q] + rmask) & ~rmask : 0;
     s += v[q];
   }
   int64_t tot;

@@ -153,7 +153,8 @@ __global__ void k_urows_scatter(const int64_t* __restrict__ colptr, const int32_
 // gather's FMAs at the measured relative cost of one shared-memory fixed-point
 // product vs one gathered FMA (ratio).
 __global__ void k_urows_finish(const int32_t* __restrict__ active, const int64_t* __restrict__ n_active,
-                               const int64_t* __restrict__ rptr, uint64_t* __restrict__ umap,
+                               const int64_t* __restrict__ rptr, const int64_t* __restrict__ cursor,
+                               int2* __restrict__ uent, uint64_t* __restrict__ umap,
                                uint32_t* __restrict__ ubits, int32_t* __restrict__ ulist,
                                int64_t* __restrict__ ulist_n, const int32_t* __restrict__ termlen,
                                const int32_t* __restrict__ headslot, int k, double* __restrict__ cost,
@@ -165,7 +166,8 @@ __global__ void k_urows_finish(const int32_t* __restrict__ active, const int64_t
   double p = 0, z = 0, a = 0, hp = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = active[r];
-    const int64_t cnt = rptr[r + 1] - rptr[r];
+    const int64_t cnt = cursor[r] - rptr[r];  // (rows start at even offsets: an odd row ends in a (0, 0) pad)
+    if (cnt & 1) uent[rptr[r] + cnt] = make_int2(0, 0);
     umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)cnt;
     atomicOr(&ubits[i >> 5], 1u << (i & 31));
     ulist[r] = i;
@@ -391,13 +393,12 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
         ESNMF_CHECK(((uint32_t)en[u].x >> kVtTermBits) < (uint32_t)kVtM && cnt <= kn);
         uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
         const float av = __int_as_float(en[u].y);
-        int j = 0;
-        for (; j + 2 <= cnt; j += 2) {
-          const int2 a = up[j], b = up[j + 1];
-          vt_add(yrow, av, a);
-          vt_add(yrow, av, b);
+        // a row starts at an even pair offset (16-byte aligned; k_urows_*): two pairs per load
+        for (int j = 0; j < cnt; j += 2) {
+          const int4 q = __ldg(reinterpret_cast<const int4*>(up + j));
+          vt_add(yrow, av, make_int2(q.x, q.y));
+          if (j + 1 < cnt) vt_add(yrow, av, make_int2(q.z, q.w));
         }
-        if (j < cnt) vt_add(yrow, av, up[j]);
       }
 #endif
     }
