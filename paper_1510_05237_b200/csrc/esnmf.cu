@@ -1481,12 +1481,12 @@ void urows_build(esnmf_t* h, const Factor& f) {
   h->nlaunch += 3;
   k_urows_scatter<<<g, 256, 0, h->stream>>>(f.colptr, f.row, f.val, f.rowmap, h->head_h > 0 ? h->headslot : nullptr,
                                             h->ucursor, h->uent, h->umax);
+  // (every slot up to the padded total, uscan[nb]; the pads, written next, are skipped)
+  k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->uscan + nb, h->uent, h->k,
+                                                                                   h->umax, h->rowsum_bits, h->ushift);
   k_urows_finish<<<grid_for(f.cap_rows, 256, 4096), 256, 0, h->stream>>>(
       f.active, f.n_active, h->urptr, h->ucursor, h->uent, h->umap, h->ubits, h->ulist, h->ulist_n, h->termlen,
       h->head_h > 0 ? h->headslot : nullptr, h->k, h->vcost, h->vt_ticket, h->vt_ratio, h->flags + 5);
-  // (every slot up to the padded total, uscan[nb]: the pads are (0, 0))
-  k_ut_scale<<<grid_for(f.cap, 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(h->uscan + nb, h->uent, h->k,
-                                                                                   h->umax, h->rowsum_bits, h->ushift);
   CKL("urows_build");
 }
 

@@ -139,7 +139,9 @@ __global__ void k_urows_scatter(const int64_t* __restrict__ colptr, const int32_
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(&umax[c_], mx);
 }
 
-// publish umap[row] = (first << 32) | count for every active row of U; the rows
+// publish umap[row] = (first << 32) | count for every active row of U -- or, for a
+// row with one pair (most rows past rank ~2k), the pair itself (bit 63 set), which
+// spares k_ytail a dependent load per entry; runs after k_ut_scale.  The rows
 // published are listed in ulist (for the next clear), their number in *ulist_n.
 // The same pass sums the per-half-step cost model of the V-side tail
 // from the document frequencies of A (termlen[i] = stored entries of term i):
@@ -166,9 +168,14 @@ __global__ void k_urows_finish(const int32_t* __restrict__ active, const int64_t
   double p = 0, z = 0, a = 0, hp = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < na; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = active[r];
-    const int64_t cnt = cursor[r] - rptr[r];  // (rows start at even offsets: an odd row ends in a (0, 0) pad)
-    if (cnt & 1) uent[rptr[r] + cnt] = make_int2(0, 0);
-    umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)cnt;
+    const int64_t cnt = cursor[r] - rptr[r];
+    if (cnt == 1) {  // the (scaled) pair itself: bit 63, column in bits 32-39, value bits below
+      const int2 p = uent[rptr[r]];
+      umap[i] = (1ull << 63) | ((uint64_t)(uint32_t)p.x << 32) | (uint64_t)(uint32_t)p.y;
+    } else {  // (rows start at even offsets: an odd row ends in a (0, 0) pad)
+      if (cnt & 1) uent[rptr[r] + cnt] = make_int2(0, 0);
+      umap[i] = ((uint64_t)rptr[r] << 32) | (uint64_t)cnt;
+    }
     atomicOr(&ubits[i >> 5], 1u << (i & 31));
     ulist[r] = i;
     const double len = (double)termlen[i];
@@ -243,6 +250,7 @@ __global__ void k_ut_scale(const int64_t* __restrict__ n_ent, int2* __restrict__
   const int64_t n = *n_ent;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     int2 p = uent[e];
+    if ((unsigned)p.x >= (unsigned)k) continue;  // a pad slot not yet written (k_urows_finish writes it)
     const int sh = vt_shift(umax[p.x], rb);
     if (sh != kNoTail) p.y = __float_as_int(ldexpf(__int_as_float(p.y), sh));  // (else: a head row, never read)
     uent[e] = p;
@@ -271,10 +279,6 @@ constexpr int kVtYChunk = ESNMF_HEAD_K;  // Y chunk width K: the head kernel's K
 #define ESNMF_VT_MINB 3
 #endif
 constexpr int kVtSub = ESNMF_VT_SUB;  // entries per thread per round (their loads in flight together)
-#ifndef ESNMF_VT_PRE
-#define ESNMF_VT_PRE 0
-#endif
-constexpr int kVtPre = ESNMF_VT_PRE > 0 ? ESNMF_VT_PRE : 1;  // U pairs per entry loaded up front
 constexpr int kVtMinB = ESNMF_VT_MINB;                      // resident CTAs per SM the launch asks for
 #ifndef ESNMF_VT_NOBITS
 #define ESNMF_VT_NOBITS 0
@@ -347,52 +351,18 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
         mp[u] = act ? umap[term] : 0ull;
 #endif
       }
-#if ESNMF_VT_PRE > 0
-      // the first kVtPre pairs of every entry's U row loaded before any product
-      // (one round trip to L2 for most rows instead of one per two products)
-      int2 pr[kVtSub][kVtPre];
 #pragma unroll
       for (int u = 0; u < kVtSub; ++u) {
-        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
-        const int2* up = uent + (mp[u] >> 32);
-#pragma unroll
-        for (int j = 0; j < kVtPre; ++j) pr[u][j] = j < cnt ? __ldg(up + j) : make_int2(0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < kVtSub; ++u) {
-        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
-        ESNMF_CHECK(((uint32_t)en[u].x >> kVtTermBits) < (uint32_t)kVtM && cnt <= kn);
+        const uint64_t m = mp[u];
         uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
         const float av = __int_as_float(en[u].y);
-#pragma unroll
-        for (int j = 0; j < kVtPre; ++j)
-          if (j < cnt) vt_add(yrow, av, pr[u][j]);
-      }
-#pragma unroll
-      for (int u = 0; u < kVtSub; ++u) {
-        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
-        if (cnt <= kVtPre) continue;
-        const int2* up = uent + (mp[u] >> 32);
-        uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
-        const float av = __int_as_float(en[u].y);
-        int j = kVtPre;
-        for (; j + 4 <= cnt; j += 4) {
-          const int2 a = up[j], b = up[j + 1], c2 = up[j + 2], d = up[j + 3];
-          vt_add(yrow, av, a);
-          vt_add(yrow, av, b);
-          vt_add(yrow, av, c2);
-          vt_add(yrow, av, d);
+        if (m >> 63) {  // a one-pair row, inline in its map word (k_urows_finish): no pair load
+          vt_add(yrow, av, make_int2((int)((m >> 32) & 0xFFu), (int)(uint32_t)m));
+          continue;
         }
-        for (; j < cnt; ++j) vt_add(yrow, av, up[j]);
-      }
-#else
-#pragma unroll
-      for (int u = 0; u < kVtSub; ++u) {
-        const int cnt = (int)(mp[u] & 0xFFFFFFFFull);
-        const int2* up = uent + (mp[u] >> 32);
+        const int cnt = (int)(m & 0xFFFFFFFFull);
+        const int2* up = uent + (m >> 32);
         ESNMF_CHECK(((uint32_t)en[u].x >> kVtTermBits) < (uint32_t)kVtM && cnt <= kn);
-        uint32_t* yrow = Ysm + ((uint32_t)en[u].x >> kVtTermBits) * ys;
-        const float av = __int_as_float(en[u].y);
         // a row starts at an even pair offset (16-byte aligned; k_urows_*): two pairs per load
         for (int j = 0; j < cnt; j += 2) {
           const int4 q = __ldg(reinterpret_cast<const int4*>(up + j));
@@ -400,7 +370,6 @@ __global__ void __launch_bounds__(kVtThreads, ESNMF_VT_MINB) k_ytail(const int64
           if (j + 1 < cnt) vt_add(yrow, av, make_int2(q.z, q.w));
         }
       }
-#endif
     }
     __syncthreads();
     // convert: a thread takes two adjacent columns of one row (lanes on adjacent
